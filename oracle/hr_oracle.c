@@ -1,0 +1,341 @@
+/*
+ * hr_oracle.c — plain, slow, single-threaded CPU oracle for the racy-address
+ * set of an access trace.
+ *
+ * TEST INFRASTRUCTURE.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code with the CUDA path (paper_2401_04701_b200/): it decodes the trace
+ * records itself and never looks at an FSM.
+ *
+ * What it computes (the plain definition, §II-A "Data Races"):
+ *   "A parallel program has a data race if multiple threads access the same
+ *    memory location, at least one of the accesses is a write, and the
+ *    accesses are concurrent (more precisely, are not ordered by some
+ *    happens-before relation)."
+ * with the happens-before relation of CUDA barriers (PAPER.md:261-264,
+ * §II-B: __syncthreads orders a block, __syncwarp orders a warp) and kernel
+ * boundaries.  Atomics are "a third class of memory action"
+ * (PAPER.md:565); reading R1 in DESIGN.md: atomic–atomic pairs do not
+ * conflict, atomic–read and atomic–write pairs do, atomics create no
+ * happens-before edges.
+ *
+ * Per access a we derive (SPEC.md:69-77 materialize_threads):
+ *   kernel, space, address block (shared memory: one instance per block),
+ *   word, thread (block, warp, lane), bc = #__syncthreads before a in its
+ *   thread, wc = #__syncwarp before a in its thread, kind.
+ * Two accesses a, b of distinct threads in the same kernel are UNORDERED iff
+ *   block(a) != block(b), or
+ *   block equal ∧ bc equal ∧ (warp differs ∨ wc equal)
+ * (SPEC.md:410 static_hb_races: ordered by block-epoch order — same block,
+ *  different bc — or by warp-epoch order — same warp, different wc).
+ * A RACE PAIR is: same address ∧ distinct threads ∧ conflict ∧ unordered.
+ * Output 1: the sorted set of racy addresses (kernel, space, block, word).
+ * Output 2: scope per racy address — GRID if some race pair has its two
+ *   threads in different blocks, BLOCK otherwise (reading R4 in DESIGN.md).
+ *
+ * Two modes:
+ *   HRO_PAIRWISE  — the literal O(n^2) loop over pairs of each address.
+ *   HRO_BUCKETED  — the same predicate evaluated per group of the sort key
+ *                   (block, bc, warp, wc, lane) with kind-set counts; needed
+ *                   for hub addresses with 10^5..10^6 accesses.
+ *   tests/test_oracle_pins.py checks both modes equal on random traces.
+ *
+ * Clock overflow (PAPER.md:540 footnote: "race detection is discontinued with
+ * a warning if a clock overflows (after reporting any previously identified
+ * races)"): reading R6 — a thread whose bc (wc) would exceed bc_max (wc_max)
+ * latches HRO_F_CLOCK_OVERFLOW and its later accesses are not checked.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define HRO_PAIRWISE 0
+#define HRO_BUCKETED 1
+
+#define HRO_F_CLOCK_OVERFLOW 1u
+#define HRO_F_MODEL_VIOLATION 4u
+#define HRO_F_BARRIER_DIVERGENCE 8u
+
+#define K_READ 0
+#define K_WRITE 1
+#define K_ATOMIC 2
+
+#define GLOBAL_BLOCK 0xFFFFFFFFu
+
+typedef struct {
+    uint64_t word;
+    uint32_t kernel;
+    uint32_t ablock;   /* address instance: simulated block for shared, GLOBAL_BLOCK for global */
+    uint32_t tblock;   /* accessing thread: block, warp, lane */
+    uint32_t bc;       /* __syncthreads crossed by the thread before this access */
+    uint32_t wc;       /* __syncwarp crossed by the thread before this access */
+    uint16_t twarp;
+    uint8_t tlane;
+    uint8_t space;
+    uint8_t kind;
+    uint8_t pad[3];
+} acc_t;
+
+typedef struct {
+    uint64_t word;
+    uint32_t kernel;
+    uint32_t block;
+    uint8_t space;
+    uint8_t scope;   /* 1 = BLOCK, 2 = GRID */
+    uint8_t pad[6];
+} hro_race;
+
+/* ---- step 1: materialise per-access (thread, bc, wc) from the records ---- */
+
+static int materialize(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_kernels,
+                       const uint64_t *warp_off, uint32_t bc_max, uint32_t wc_max,
+                       acc_t **out, uint64_t *n_out, uint32_t *flags)
+{
+    uint64_t cap = 1024, n = 0;
+    acc_t *a = (acc_t *)malloc(cap * sizeof(acc_t));
+    if (!a) return -2;
+    for (uint64_t k = 0; k < n_kernels; k++) {
+        const uint64_t *kd = kdesc + 8 * k;
+        uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], woi = kd[4];
+        if (lanes < 1 || lanes > 32) { free(a); return -1; }
+        for (uint64_t b = 0; b < blocks; b++) {
+            int64_t block_sync_count = -1;
+            for (uint64_t w = 0; w < warps; w++) {
+                uint64_t gw = b * warps + w;
+                uint64_t r0 = warp_off[woi + gw], r1 = warp_off[woi + gw + 1];
+                uint32_t bc[32], wc[32];
+                int dead[32];
+                memset(bc, 0, sizeof bc); memset(wc, 0, sizeof wc); memset(dead, 0, sizeof dead);
+                for (uint64_t r = r0; r < r1; r++) {
+                    const uint64_t *row = rec + r * 32;
+                    /* barrier uniformity within the warp */
+                    int nbar = 0, same = 1;
+                    uint64_t first_bar = 0;
+                    for (uint64_t l = 0; l < lanes; l++) {
+                        uint64_t x = row[l];
+                        if ((x >> 62) == 3 && (x & ((1ull << 61) - 1)) != 0) {
+                            if (nbar == 0) first_bar = x; else if (x != first_bar) same = 0;
+                            nbar++;
+                        }
+                    }
+                    if (nbar != 0 && (nbar != (int)lanes || !same)) *flags |= HRO_F_BARRIER_DIVERGENCE;
+                    for (uint64_t l = 0; l < lanes; l++) {
+                        uint64_t x = row[l];
+                        uint32_t op = (uint32_t)(x >> 62);
+                        uint32_t space = (uint32_t)((x >> 61) & 1);
+                        uint64_t word = x & ((1ull << 61) - 1);
+                        if (op == 3) {
+                            if (word == 1) {            /* __syncthreads: bc + 1 */
+                                if (bc[l] + 1 > bc_max) { dead[l] = 1; *flags |= HRO_F_CLOCK_OVERFLOW; }
+                                else bc[l]++;
+                            } else if (word == 2) {     /* __syncwarp: wc + 1 */
+                                if (wc[l] + 1 > wc_max) { dead[l] = 1; *flags |= HRO_F_CLOCK_OVERFLOW; }
+                                else wc[l]++;
+                            } else if (word != 0) {
+                                *flags |= HRO_F_MODEL_VIOLATION;
+                            }
+                            continue;
+                        }
+                        if (dead[l]) continue;
+                        if (n == cap) {
+                            cap *= 2;
+                            acc_t *t = (acc_t *)realloc(a, cap * sizeof(acc_t));
+                            if (!t) { free(a); return -2; }
+                            a = t;
+                        }
+                        acc_t *e = &a[n++];
+                        memset(e, 0, sizeof *e);
+                        e->word = word;
+                        e->kernel = (uint32_t)k;
+                        e->space = (uint8_t)space;
+                        e->ablock = space ? (uint32_t)b : GLOBAL_BLOCK;
+                        e->tblock = (uint32_t)b;
+                        e->twarp = (uint16_t)w;
+                        e->tlane = (uint8_t)l;
+                        e->bc = bc[l];
+                        e->wc = wc[l];
+                        e->kind = (uint8_t)op;
+                    }
+                }
+                /* every thread of a block crosses the same number of __syncthreads */
+                for (uint64_t l = 0; l < lanes; l++) {
+                    if (dead[l]) continue;
+                    if (block_sync_count < 0) block_sync_count = bc[l];
+                    else if ((int64_t)bc[l] != block_sync_count) *flags |= HRO_F_BARRIER_DIVERGENCE;
+                }
+            }
+        }
+    }
+    *out = a;
+    *n_out = n;
+    return 0;
+}
+
+/* ---- the race predicate, written out ---- */
+
+static int conflict(int k1, int k2)
+{
+    /* at least one write; atomics conflict with plain accesses but not with
+     * each other (reading R1) */
+    if (k1 == K_READ && k2 == K_READ) return 0;
+    if (k1 == K_ATOMIC && k2 == K_ATOMIC) return 0;
+    return 1;
+}
+
+static int same_thread(const acc_t *a, const acc_t *b)
+{
+    return a->tblock == b->tblock && a->twarp == b->twarp && a->tlane == b->tlane;
+}
+
+static int unordered(const acc_t *a, const acc_t *b)
+{
+    if (a->tblock != b->tblock) return 1;      /* no inter-block barrier */
+    if (a->bc != b->bc) return 0;              /* a __syncthreads separates them */
+    if (a->twarp != b->twarp) return 1;        /* same block epoch, different warps */
+    return a->wc == b->wc;                     /* same warp: ordered iff a __syncwarp separates */
+}
+
+static int cmp_addr(const void *x, const void *y)
+{
+    const acc_t *a = (const acc_t *)x, *b = (const acc_t *)y;
+#define C(f) if (a->f != b->f) return a->f < b->f ? -1 : 1;
+    C(kernel) C(space) C(ablock) C(word)
+    C(tblock) C(bc) C(twarp) C(wc) C(tlane)
+#undef C
+    return 0;
+}
+
+static int same_addr(const acc_t *a, const acc_t *b)
+{
+    return a->kernel == b->kernel && a->space == b->space && a->ablock == b->ablock && a->word == b->word;
+}
+
+/* pairwise: returns 0 (race-free), 1 (BLOCK), 2 (GRID) for one address group */
+static int group_pairwise(const acc_t *g, uint64_t n)
+{
+    int scope = 0;
+    for (uint64_t i = 0; i < n; i++)
+        for (uint64_t j = i + 1; j < n; j++) {
+            const acc_t *a = &g[i], *b = &g[j];
+            if (same_thread(a, b)) continue;
+            if (!conflict(a->kind, b->kind)) continue;
+            if (!unordered(a, b)) continue;
+            if (a->tblock != b->tblock) return 2;
+            scope = 1;
+        }
+    return scope;
+}
+
+/* Kind-set test "∃ two distinct sub-groups i != j with conflicting kinds",
+ * from per-sub-group kind masks (bit k = kind k present).  Pairs are
+ * conflicting iff one is a write, or one is a read and the other atomic. */
+typedef struct { uint64_t n, nW, nR, nA, nRA; } kcount;
+
+static void kc_add(kcount *c, unsigned m)
+{
+    c->n++;
+    if (m & (1u << K_WRITE)) c->nW++;
+    if (m & (1u << K_READ)) c->nR++;
+    if (m & (1u << K_ATOMIC)) c->nA++;
+    if ((m & (1u << K_READ)) && (m & (1u << K_ATOMIC))) c->nRA++;
+}
+
+static int kc_conflict(const kcount *c)
+{
+    if (c->nW >= 1 && c->n >= 2) return 1;       /* a write vs any other sub-group */
+    return c->nR * c->nA - c->nRA > 0;           /* a read vs an atomic of another sub-group */
+}
+
+/* bucketed: same predicate; g is sorted by (tblock, bc, twarp, wc, tlane) */
+static int group_bucketed(const acc_t *g, uint64_t n)
+{
+    /* cross-block pairs are always unordered */
+    kcount blocks = {0};
+    int block_scope = 0;
+    uint64_t i = 0;
+    while (i < n) {
+        uint64_t jb = i;
+        unsigned mb = 0;
+        while (jb < n && g[jb].tblock == g[i].tblock) { mb |= 1u << g[jb].kind; jb++; }
+        kc_add(&blocks, mb);
+        /* inside block: pairs with equal bc, different warps are unordered */
+        uint64_t e = i;
+        while (e < jb && !block_scope) {
+            uint64_t je = e;
+            while (je < jb && g[je].bc == g[e].bc) je++;
+            kcount warps = {0};
+            uint64_t w = e;
+            while (w < je) {
+                uint64_t jw = w;
+                unsigned mw = 0;
+                while (jw < je && g[jw].twarp == g[w].twarp) { mw |= 1u << g[jw].kind; jw++; }
+                kc_add(&warps, mw);
+                /* inside warp: equal wc, different lanes are unordered */
+                uint64_t c = w;
+                while (c < jw) {
+                    uint64_t jc = c;
+                    while (jc < jw && g[jc].wc == g[c].wc) jc++;
+                    kcount lanes = {0};
+                    uint64_t t = c;
+                    while (t < jc) {
+                        uint64_t jt = t;
+                        unsigned mt = 0;
+                        while (jt < jc && g[jt].tlane == g[t].tlane) { mt |= 1u << g[jt].kind; jt++; }
+                        kc_add(&lanes, mt);
+                        t = jt;
+                    }
+                    if (kc_conflict(&lanes)) block_scope = 1;
+                    c = jc;
+                }
+                w = jw;
+            }
+            if (kc_conflict(&warps)) block_scope = 1;
+            e = je;
+        }
+        i = jb;
+    }
+    if (kc_conflict(&blocks)) return 2;
+    return block_scope ? 1 : 0;
+}
+
+/* Entry point.  Returns 0 on success, -1 bad trace, -2 out of memory,
+ * -3 output capacity too small (n_out then holds the needed count). */
+int hro_check(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_kernels,
+              const uint64_t *warp_off, int mode, uint32_t bc_max, uint32_t wc_max,
+              hro_race *out, uint64_t cap, uint64_t *n_out, uint32_t *flags_out,
+              uint64_t *n_accesses_out)
+{
+    acc_t *a = NULL;
+    uint64_t n = 0;
+    uint32_t flags = 0;
+    int rc = materialize(rec, kdesc, n_kernels, warp_off, bc_max, wc_max, &a, &n, &flags);
+    if (rc) return rc;
+    if (n_accesses_out) *n_accesses_out = n;
+    qsort(a, n, sizeof(acc_t), cmp_addr);   /* library sort: groups each address */
+    uint64_t nr = 0;
+    uint64_t i = 0;
+    while (i < n) {
+        uint64_t j = i + 1;
+        while (j < n && same_addr(&a[i], &a[j])) j++;
+        int s = mode == HRO_PAIRWISE ? group_pairwise(a + i, j - i) : group_bucketed(a + i, j - i);
+        if (s) {
+            if (nr < cap) {
+                hro_race *r = &out[nr];
+                memset(r, 0, sizeof *r);
+                r->word = a[i].word;
+                r->kernel = a[i].kernel;
+                r->block = a[i].ablock;
+                r->space = a[i].space;
+                r->scope = (uint8_t)s;
+            }
+            nr++;
+        }
+        i = j;
+    }
+    free(a);
+    *n_out = nr;
+    *flags_out = flags;
+    return nr > cap ? -3 : 0;
+}
+
+uint64_t hro_sizeof_race(void) { return sizeof(hro_race); }

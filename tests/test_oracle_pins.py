@@ -1,0 +1,230 @@
+"""Pins for the CPU oracle (oracle/) against what the paper and the
+mathematics fix — never against the oracle itself.
+
+* paper listing verdicts (tests/golden/listings.txt, each line cited);
+* the C1 tree-reduction closed form (derived below from the race definition);
+* classical vector clocks over EVERY barrier-respecting interleaving
+  (SPEC.md:416-424, 612): the static set must equal the dynamic one on each;
+* pairwise == bucketed modes on random programs;
+* the two-thread property;
+* schedule counts; clock overflow;
+* the scope lemma (racy + >=2 blocks <=> a cross-block racing pair).
+"""
+import os
+import random
+
+import pytest
+
+import oracle
+from oracle import vclock
+from tracegen import format as tf
+from tracegen import programs as tp
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "listings.txt")
+
+
+def _golden():
+    rows = []
+    for line in open(GOLDEN):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        head, words, scope, cite = [x.strip() for x in line.split("|")]
+        name, b, w, l, p = head.split()
+        exp = [] if words == "-" else [int(x) for x in words.split(",")]
+        rows.append((name, int(b), int(w), int(l), int(p), exp, scope, cite))
+    return rows
+
+
+def _make(name, b, w, l, p):
+    if name == "listing1":
+        return tp.listing1(b, w, l)
+    if name == "listing2":
+        return tp.listing2(b, w, l)
+    return tp.listing4(b, w, l, p)
+
+
+@pytest.mark.parametrize("row", _golden(), ids=lambda r: f"{r[0]}-{r[1]}x{r[2]}x{r[3]}")
+@pytest.mark.parametrize("mode", [oracle.PAIRWISE, oracle.BUCKETED])
+def test_paper_listings(row, mode):
+    name, b, w, l, p, exp, scope, cite = row
+    res = oracle.check(_make(name, b, w, l, p), mode=mode)
+    assert [r.word for r in res.races] == exp, cite
+    if exp:
+        want = oracle.SCOPE_GRID if scope == "GRID" else oracle.SCOPE_BLOCK
+        assert all(r.scope == want for r in res.races), cite
+    assert res.flags == 0
+
+
+def test_listing2_all_block_counts():
+    # ">= 2 blocks" racy on data[0..T-2]; 1 block race-free
+    for blocks in (1, 2, 3):
+        for (w, l) in ((1, 2), (2, 2), (1, 5), (3, 3)):
+            t = w * l
+            res = oracle.check(tp.listing2(blocks, w, l))
+            exp = [] if blocks == 1 else list(range(t - 1))
+            assert [r.word for r in res.races] == exp
+
+
+def test_c1_closed_form():
+    """C1: barrier after reduction step s removed merges step s
+    (writes s[i], i<s, lane i%32) with step s/2 (reads s[i], s[i+s/2],
+    i<s/2, lane i%32).  s[j], j in [s/2, s), is written by lane j%32 and read
+    by lane (j-s/2)%32 with no barrier between: distinct lanes (a race) iff
+    s/2 is not a multiple of 32, i.e. s <= 32.  Hence racy = [s/2, s) for
+    s in {32,16,8,4,2}, empty otherwise.  All in one block -> BLOCK scope."""
+    for removed in (None, "load", 128, 64, 32, 16, 8, 4, 2, 1):
+        tr = tp.c1_tree_reduction(removed=removed)
+        res = oracle.check(tr, mode=oracle.BUCKETED)
+        if removed in (32, 16, 8, 4, 2):
+            exp = list(range(removed // 2, removed))
+        else:
+            exp = []
+        assert [r.word for r in res.races] == exp, removed
+        assert all(r.space == tf.SPACE_SHARED and r.block == 0 and r.scope == oracle.SCOPE_BLOCK
+                   for r in res.races)
+        # 10,232 checked accesses per launch (8 x (512 + 765 + 2))
+        assert res.n_accesses == 10232
+
+
+def test_c1_pairwise_equals_bucketed():
+    tr = tp.c1_tree_reduction(removed=16, rounds=2)
+    assert oracle.check(tr, mode=oracle.PAIRWISE) == oracle.check(tr, mode=oracle.BUCKETED)
+
+
+def _static_as_dict(res):
+    return {(r.space, r.block, r.word): r.scope for r in res.races}
+
+
+def test_vclock_every_interleaving_equals_static():
+    """on every interleaving the vector-clock verdict equals
+    the static happens-before set (all events execute in each complete run)."""
+    rng = random.Random(1234)
+    n_sched = 0
+    for _ in range(150):
+        tr = tp.random_program(rng, max_blocks=2, max_warps=2, max_lanes=2, max_slots=3,
+                               n_words=2, spaces=(0, 1))
+        th = vclock.thread_events(tr)[0]
+        static = _static_as_dict(oracle.check(tr, mode=oracle.PAIRWISE))
+        for sched in vclock.enumerate_schedules(th, cap=300):
+            assert vclock.vclock_races(th, sched) == static
+            n_sched += 1
+    assert n_sched > 5000
+
+
+def test_pairwise_equals_bucketed_random():
+    rng = random.Random(99)
+    for i in range(400):
+        tr = tp.random_program(rng, max_blocks=3, max_warps=3, max_lanes=4, max_slots=6,
+                               n_words=3, spaces=(0, 1), n_kernels=rng.randint(1, 2))
+        a = oracle.check(tr, mode=oracle.PAIRWISE)
+        b = oracle.check(tr, mode=oracle.BUCKETED)
+        assert a == b, i
+
+
+def test_two_thread_property():
+    """under barrier-only, data-independent control a race is
+    discoverable within two threads."""
+    rng = random.Random(7)
+    checked = 0
+    for _ in range(300):
+        tr = tp.random_program(rng, max_blocks=2, max_warps=2, max_lanes=2, max_slots=3, n_words=2)
+        th = vclock.thread_events(tr)[0]
+        static = _static_as_dict(oracle.check(tr))
+        if not static:
+            continue
+        found = {}
+        for pair in vclock.thread_pairs(th):
+            sub = vclock.project(th, set(pair))
+            sched = next(vclock.enumerate_schedules(sub))
+            for a, s in vclock.vclock_races(sub, sched).items():
+                found[a] = max(found.get(a, 0), s)
+        assert found == static
+        checked += 1
+    assert checked > 50
+
+
+def test_schedule_counts():
+    # 2 threads x 1 event -> 2 schedules; 2 x 2 events -> C(4,2) = 6
+    tr = tp.from_thread_events(1, 1, 2, {(0, 0, 0): [tf.R(0)], (0, 0, 1): [tf.R(1)]})
+    assert len(list(vclock.enumerate_schedules(vclock.thread_events(tr)[0]))) == 2
+    tr = tp.from_thread_events(1, 1, 2, {(0, 0, 0): [tf.R(0), tf.R(1)], (0, 0, 1): [tf.R(2), tf.R(3)]})
+    assert len(list(vclock.enumerate_schedules(vclock.thread_events(tr)[0]))) == 6
+    # Listing 2 on 1x1x2: both reads precede every post-barrier event
+    th = vclock.thread_events(tp.listing2(1, 1, 2))[0]
+    n = 0
+    for sched in vclock.enumerate_schedules(th):
+        run = vclock._Run(th)
+        kinds = [run.exec(t)[0] for t in sched]
+        accs = [e for e in kinds if e[0] == "acc"]
+        assert [e[3] for e in accs] == [tf.OP_READ, tf.OP_READ, tf.OP_WRITE]
+        n += 1
+    assert n > 1
+
+
+def test_clock_overflow():
+    """detection discontinued with a warning after reporting any
+    previously identified races.  SPEC.md:617: bc_bits = 2 and 4 barriers."""
+    ev = {(0, 0, 0): [tf.W(0), tf.SYNCTHREADS, tf.SYNCTHREADS, tf.SYNCTHREADS, tf.SYNCTHREADS, tf.W(1)],
+          (0, 0, 1): [tf.W(0), tf.SYNCTHREADS, tf.SYNCTHREADS, tf.SYNCTHREADS, tf.SYNCTHREADS, tf.W(1)]}
+    tr = tp.from_thread_events(1, 1, 2, ev)
+    full = oracle.check(tr)
+    assert [r.word for r in full.races] == [0, 1] and full.flags == 0
+    over = oracle.check(tr, bc_bits=2)
+    assert [r.word for r in over.races] == [0]            # race before the overflow kept
+    assert over.flags & oracle.F_CLOCK_OVERFLOW
+    three = tp.from_thread_events(1, 1, 2, {k: v[:4] + v[5:] for k, v in ev.items()})
+    assert oracle.check(three, bc_bits=2).flags == 0      # 3 barriers fit in 2 bits
+
+
+def test_kernel_boundary_orders():
+    k1 = tf.build_kernel(1, 1, 2, lambda b, w, l: [tf.W(0)] if l == 0 else [])
+    k2 = tf.build_kernel(1, 1, 2, lambda b, w, l: [tf.R(0)] if l == 1 else [])
+    assert oracle.check(tf.make_trace([k1, k2])).races == []
+    k3 = tf.build_kernel(1, 1, 2, lambda b, w, l: [tf.W(0)])
+    res = oracle.check(tf.make_trace([k1, k3]))
+    assert [(r.kernel, r.word) for r in res.races] == [(1, 0)]
+
+
+def test_atomics_reading():
+    """Reading R1: A-A never races; A-R and A-W do."""
+    def two(k1, k2):
+        return tp.from_thread_events(1, 1, 2, {(0, 0, 0): [k1(0)], (0, 0, 1): [k2(0)]})
+    assert oracle.check(two(tf.A, tf.A)).races == []
+    assert len(oracle.check(two(tf.A, tf.R)).races) == 1
+    assert len(oracle.check(two(tf.W, tf.A)).races) == 1
+    assert oracle.check(two(tf.R, tf.R)).races == []
+
+
+def test_shared_instances_are_per_block():
+    tr = tp.from_thread_events(2, 1, 1, {(0, 0, 0): [tf.W(5, tf.SPACE_SHARED)],
+                                         (1, 0, 0): [tf.W(5, tf.SPACE_SHARED)]}, smem_words=8)
+    assert oracle.check(tr).races == []
+    tr = tp.from_thread_events(2, 1, 1, {(0, 0, 0): [tf.W(5)], (1, 0, 0): [tf.W(5)]})
+    assert [(r.word, r.scope) for r in oracle.check(tr).races] == [(5, oracle.SCOPE_GRID)]
+
+
+def test_scope_lemma():
+    """For a racy address: a cross-block racing pair exists iff >= 2 blocks
+    accessed it (SURVEY §8(c) Output 2) — brute force on random programs."""
+    from tests.helpers import accesses_by_address
+    rng = random.Random(5)
+    for _ in range(300):
+        tr = tp.random_program(rng, max_blocks=3, max_warps=2, max_lanes=2, max_slots=5, n_words=2)
+        res = oracle.check(tr, mode=oracle.PAIRWISE)
+        acc = accesses_by_address(tr)
+        for r in res.races:
+            blocks = {a[0][0] for a in acc[(r.kernel, r.space, r.block, r.word)]}
+            assert (r.scope == oracle.SCOPE_GRID) == (len(blocks) >= 2)
+
+
+def test_barrier_divergence_flag():
+    # lane 0 syncs, lane 1 does not: built by hand (the builder refuses it)
+    import numpy as np
+    rows = np.full((1, 2, 32), tf.NOP, dtype=np.uint64)
+    rows[0, 0, 0] = tf.SYNCTHREADS
+    rows[0, 1, 1] = tf.W(0)
+    tr = tf.make_trace([tf.kernel_from_rows(1, 1, 2, rows)])
+    assert oracle.check(tr).flags & oracle.F_BARRIER_DIVERGENCE
+    with pytest.raises(tf.BarrierDivergence):
+        tp.from_thread_events(1, 1, 2, {(0, 0, 0): [tf.SYNCTHREADS], (0, 0, 1): [tf.W(0)]})
