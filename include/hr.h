@@ -1,0 +1,180 @@
+/*
+ * hr.h — C ABI of the B200-native HiRace per-access race check
+ * (arXiv 2401.04701, "HiRace: Accurate and Fast Source-Level Race Checking
+ * of GPU Programs").  Citations: PAPER.md:n = /root/reference/PAPER.md line n
+ * (section given alongside).
+ *
+ * The method: every monitored word data[k] has a shadow word shadow[k]
+ * holding <State, TID, BC, WC> (Fig. ssm_shadow); every
+ * read / write / atomic runs Algorithm 1 "UpdateShadow":
+ * atomic read, label = (access, checkSync, compareTids), flat-array FSM
+ * lookup, pack, atomicCAS until it succeeds.  A word
+ * whose FSM enters RACE is reported once per unique address.
+ *
+ * This header is the host side.  The device side (hr_check_read/_write/
+ * _atomic, hr_syncthreads/_syncwarp) is the header-only hr_device.cuh.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", C99 types only; no exceptions or aborts cross the ABI.
+ *   - every host call returns hr_status (0 = HR_OK, < 0 = error); CUDA
+ *     errors map to HR_E_CUDA with the text in hr_last_error(ctx).
+ *   - "device" pointers are CUDA device pointers of ctx->device; "host"
+ *     pointers are ordinary (ideally pinned) host memory.
+ *   - stream arguments are cudaStream_t passed as void* (NULL = legacy stream).
+ *   - one ctx per (device, stream); host calls on one ctx are not re-entrant.
+ *   - nothing is allocated on the check path: all device memory is owned by
+ *     the ctx and allocated in hr_init / hr_shadow_alloc.
+ */
+#ifndef HR_H_
+#define HR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HR_OK = 0,
+    HR_E_ARG = -1,     /* invalid argument (NULL, widths, sizes, grid too large) */
+    HR_E_NOMEM = -2,   /* device or host allocation failed */
+    HR_E_CUDA = -3,    /* CUDA runtime error; see hr_last_error */
+    HR_E_STATE = -4    /* call out of order (e.g. replay before hr_shadow_alloc) */
+} hr_status;
+
+typedef enum { HR_GLOBAL = 0, HR_SHARED = 1 } hr_space;          /* PAPER.md:257 memory spaces */
+typedef enum { HR_READ = 0, HR_WRITE = 1, HR_ATOMIC = 2 } hr_kind; /* PAPER.md:565 "third class" */
+typedef enum { HR_SCOPE_BLOCK = 1, HR_SCOPE_GRID = 2 } hr_scope;  /* DESIGN.md reading R4 */
+
+/* Sticky device-side conditions, surfaced by hr_report (never fatal). */
+enum {
+    HR_F_CLOCK_OVERFLOW = 1u,      /* a BC/WC clock overflowed: later checks of that thread
+                                      skipped, earlier races kept (PAPER.md:540 footnote) */
+    HR_F_RING_OVERFLOW = 2u,       /* report ring full: hr_report falls back to a shadow scan */
+    HR_F_MODEL_VIOLATION = 4u,     /* unknown control record / sub-warp sync */
+    HR_F_BARRIER_DIVERGENCE = 8u,  /* barrier record not uniform across a warp's lanes */
+    HR_F_UNMONITORED = 16u         /* global access outside the registered shadow region */
+};
+
+/* Shadow word layout ("5 bits ... 8 bytes of memory per address"):
+ *   [63:59] state  [58:32] tid = block:17 | warp:5 | lane:5  [31:wc_bits] bc  [wc_bits-1:0] wc
+ * state_bits must be 5 and tid_bits 27; bc_bits + wc_bits must be 32.
+ * Defaults (hr_init with cfg == NULL): 5/27/16/16, ring 1<<20 records, device 0. */
+typedef struct {
+    uint8_t state_bits, tid_bits, bc_bits, wc_bits;
+    uint32_t ring_capacity;   /* race records the device ring holds (>= 1) */
+    int device;               /* CUDA device ordinal */
+    uint32_t options;         /* HR_OPT_* bits */
+} hr_config;
+
+enum {
+    HR_OPT_NO_COALESCE = 1u,   /* disable same-address lane coalescing (a3), for ablations */
+    HR_OPT_NO_FASTEXIT = 2u    /* disable label-insensitive fast exits (a7), for ablations */
+};
+
+/* One unique racy address.  24 bytes.
+ *   word       global: word index; shared: word index inside the block's __shared__ instance
+ *   block      shared: simulated block of the instance; global: 0xFFFFFFFF
+ *   kernel     kernel index (trace kernel index + hr_trace.kernel_base)
+ *   first_tid  packed tid of the access that moved the word into RACE (diagnostic only)
+ *   space      hr_space;  scope: hr_scope
+ *   first_kind hr_kind of that access; prev_state: FSM state before it (diagnostic only) */
+typedef struct {
+    uint64_t word;
+    uint32_t block;
+    uint32_t kernel;
+    uint32_t first_tid;
+    uint8_t space, scope, first_kind, prev_state;
+} hr_race;
+
+/* A batch of synthetic access streams (tracegen/format.py documents the layout).
+ *   rec       DEVICE, n_rows*32 uint64 records; row r, lane l at rec[r*32+l]:
+ *             [63:62] op (0 R, 1 W, 2 A, 3 control) [61] space [60:0] word;
+ *             control words: 0 NOP, 1 __syncthreads, 2 __syncwarp
+ *   kdesc     HOST, n_kernels x 8 uint64: blocks, warps, lanes(<=32), smem_words,
+ *             warp_off_index, 0, 0, 0
+ *   warp_off  DEVICE, uint64 absolute row offsets; warp w of kernel k owns rows
+ *             [warp_off[woi+w], warp_off[woi+w+1]) with woi = kdesc[k][4]
+ *   The ctx never takes ownership.  For hr_replay_trace_host, rec and warp_off are
+ *   HOST pointers instead (copied to ctx-owned device staging buffers). */
+typedef struct {
+    const uint64_t *rec;
+    uint64_t n_rows;
+    const uint64_t *kdesc;
+    uint32_t n_kernels;
+    uint32_t kernel_base;
+    const uint64_t *warp_off;
+    uint64_t n_warp_off;
+} hr_trace;
+
+typedef struct hr_ctx hr_ctx;   /* opaque */
+
+/* Create a context on cfg->device: uploads the FSM table, allocates the report
+ * ring and the flags word.  cfg == NULL selects the defaults above. */
+hr_status hr_init(const hr_config *cfg, hr_ctx **out);
+
+/* Address sharding for multi-GPU replay: this ctx checks only
+ * global words whose 4 KiB shadow granule ((word - base) >> 9) satisfies
+ * granule % count == rank, and shared instances of simulated blocks with
+ * block % count == rank.  count must be a power of two <= 64.  Call before
+ * hr_shadow_alloc.  Default: rank 0 of 1. */
+hr_status hr_set_shard(hr_ctx *ctx, uint32_t rank, uint32_t count);
+
+/* Register a shadow region ("For each shared memory variable, a
+ * shadow value data structure is allocated").
+ *   HR_GLOBAL: words [base_word, base_word + n_words) get a 1:1 8-byte shadow in
+ *     HBM (only this shard's granules are materialised); *dev_region (if not
+ *     NULL) receives the device pointer.  Replaces any previous global region.
+ *   HR_SHARED: per-block __shared__ shadow of n_words words (staged in SMEM by the
+ *     replay kernel, zero = INIT at block start); base_word must be 0;
+ *     *dev_region (if not NULL) receives NULL.  n_words * 8 must fit SMEM with the
+ *     FSM table (<= 227 KB). */
+hr_status hr_shadow_alloc(hr_ctx *ctx, hr_space space, uint64_t base_word, uint64_t n_words,
+                          void **dev_region);
+
+/* New kernel epoch: a kernel boundary orders everything, so the global shadow
+ * is reset to INIT (all-zero words) on `stream`. */
+hr_status hr_kernel_begin(hr_ctx *ctx, void *stream);
+
+/* Replay every kernel of `t` on `stream`: for each kernel, hr_kernel_begin then
+ * one launch whose grid mirrors the traced grid; each CUDA thread walks its
+ * simulated thread's records and runs the per-access check; __syncthreads /
+ * __syncwarp records execute real barriers and advance BC / WC.  Asynchronous;
+ * races accumulate in the ring until hr_report / hr_reset_report. */
+hr_status hr_replay_trace(hr_ctx *ctx, const hr_trace *t, void *stream);
+
+/* Same with t->rec and t->warp_off in HOST memory: the records are copied to
+ * ctx-owned device staging buffers on `stream`, then replayed. */
+hr_status hr_replay_trace_host(hr_ctx *ctx, const hr_trace *t, void *stream);
+
+/* Synchronise the ctx's last stream and return the unique racy addresses,
+ * sorted by (kernel, space, block, word), one record per address with the
+ * widest scope observed.  n_out receives the number of races (may exceed cap:
+ * then only cap are written and HR_E_ARG is returned).  flags_out (may be NULL)
+ * receives the sticky HR_F_* word.  If the ring overflowed, the current global
+ * shadow is scanned for RACE words of the last replayed kernel instead. */
+hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out);
+
+/* Clear the ring, its counter and the flags word (asynchronous on the last stream). */
+hr_status hr_reset_report(hr_ctx *ctx);
+
+/* Device-side counters of the last replay: [0] checked accesses, [1] CAS
+ * retries, [2] fast exits (only maintained when built with HR_COUNTERS). */
+hr_status hr_counters(hr_ctx *ctx, uint64_t out[4]);
+
+/* Copy of the compiled-in FSM table (2048 bytes, index state<<6|kind<<4|sync<<2|rel)
+ * and per-state flags (32 bytes).  Either pointer may be NULL. */
+hr_status hr_fsm_table(uint8_t *table2048, uint8_t *flags32);
+
+/* The device pointer of the packed device context (struct hr_dev in
+ * hr_device.cuh) for user kernels instrumented online; valid until hr_destroy. */
+hr_status hr_device_view(hr_ctx *ctx, void *hr_dev_out, size_t size);
+
+const char *hr_last_error(hr_ctx *ctx);
+void hr_destroy(hr_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HR_H_ */

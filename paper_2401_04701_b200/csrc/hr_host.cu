@@ -1,0 +1,358 @@
+/*
+ * hr_host.cu — implementation of the C ABI in include/hr.h.
+ *
+ * Owns the device state of one checker context: the FSM table (generated,
+ * fsm_table.inc), the global shadow slice, the report ring + tail counter, the
+ * sticky flags word and the replay staging buffers.  All allocation happens
+ * in hr_init / hr_shadow_alloc / the first hr_replay_trace_host; the check
+ * path allocates nothing.
+ */
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "hr.h"
+#include "hr_device.cuh"
+#include "hr_replay.cuh"
+#include "fsm_table.inc"
+
+struct hr_ctx {
+    int device = 0;
+    hr_config cfg{};
+    uint32_t shard_rank = 0, shard_count = 1, shard_log2 = 0;
+    unsigned long long *gshadow = nullptr;
+    uint64_t gbase = 0, gwords = 0, glocal = 0;
+    uint32_t smem_words_max = 0;
+    hr_race *ring = nullptr;
+    unsigned int *tail = nullptr;     /* [0] ring tail, [1] flags, [2] scan count */
+    unsigned long long *counters = nullptr;
+    unsigned char *fsm = nullptr;
+    uint32_t last_kernel = 0;
+    bool have_kernel = false;
+    cudaStream_t stream = nullptr;
+    uint64_t *stage_rec = nullptr;
+    size_t stage_rec_cap = 0;
+    uint64_t *stage_woff = nullptr;
+    size_t stage_woff_cap = 0;
+    char err[512] = {0};
+};
+
+static hr_status fail(hr_ctx *c, hr_status s, const char *fmt, ...)
+{
+    if (c) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(c->err, sizeof c->err, fmt, ap);
+        va_end(ap);
+    }
+    return s;
+}
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(c, HR_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                            \
+    } while (0)
+
+static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
+{
+    hr_dev d;
+    memset(&d, 0, sizeof d);
+    d.gshadow = c->gshadow;
+    d.gbase = c->gbase;
+    d.gwords = c->gwords;
+    d.ring = c->ring;
+    d.ring_tail = c->tail;
+    d.flags = c->tail + 1;
+    d.counters = c->counters;
+    d.fsm = c->fsm;
+    d.ring_cap = c->cfg.ring_capacity;
+    d.kernel_id = kernel_id;
+    d.shard_rank = c->shard_rank;
+    d.shard_log2 = c->shard_log2;
+    d.wc_bits = c->cfg.wc_bits;
+    d.bc_max = (1u << c->cfg.bc_bits) - 1u;
+    d.wc_max = (1u << c->cfg.wc_bits) - 1u;
+    d.options = c->cfg.options;
+    return d;
+}
+
+extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
+{
+    if (!out) return HR_E_ARG;
+    *out = nullptr;
+    hr_config def;
+    def.state_bits = 5;
+    def.tid_bits = 27;
+    def.bc_bits = 16;
+    def.wc_bits = 16;
+    def.ring_capacity = 1u << 20;
+    def.device = 0;
+    def.options = 0;
+    const hr_config &k = cfg ? *cfg : def;
+    if (k.state_bits != 5 || k.tid_bits != 27 || k.bc_bits < 1 || k.wc_bits < 1 ||
+        k.bc_bits + k.wc_bits != 32 || k.ring_capacity < 1)
+        return HR_E_ARG;
+    hr_ctx *c = new (std::nothrow) hr_ctx;
+    if (!c) return HR_E_NOMEM;
+    c->cfg = k;
+    c->device = k.device;
+    hr_status st = HR_OK;
+    do {
+        cudaError_t e = cudaSetDevice(c->device);
+        if (e != cudaSuccess) { st = fail(c, HR_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e)); break; }
+        if (cudaMalloc(&c->fsm, HR_FSM_SMEM_BYTES) != cudaSuccess ||
+            cudaMalloc(&c->ring, sizeof(hr_race) * (size_t)k.ring_capacity) != cudaSuccess ||
+            cudaMalloc(&c->tail, 4 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMalloc(&c->counters, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+            st = fail(c, HR_E_NOMEM, "device allocation failed in hr_init");
+            break;
+        }
+        unsigned char host[HR_FSM_SMEM_BYTES];
+        memcpy(host, hr_fsm_table_init, HR_FSM_BYTES);
+        memcpy(host + HR_FSM_BYTES, hr_fsm_flags_init, 32);
+        if (cudaMemcpy(c->fsm, host, HR_FSM_SMEM_BYTES, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemset(c->tail, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMemset(c->counters, 0, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+            st = fail(c, HR_E_CUDA, "hr_init upload failed");
+            break;
+        }
+    } while (0);
+    if (st != HR_OK) {
+        hr_destroy(c);
+        return st;
+    }
+    *out = c;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_set_shard(hr_ctx *c, uint32_t rank, uint32_t count)
+{
+    if (!c || count == 0 || count > 64 || (count & (count - 1)) || rank >= count)
+        return fail(c, HR_E_ARG, "hr_set_shard: bad rank/count");
+    if (c->gshadow) return fail(c, HR_E_STATE, "hr_set_shard after hr_shadow_alloc");
+    c->shard_rank = rank;
+    c->shard_count = count;
+    c->shard_log2 = 0;
+    while ((1u << c->shard_log2) < count) c->shard_log2++;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_word, uint64_t n_words,
+                                     void **dev_region)
+{
+    if (!c) return HR_E_ARG;
+    CU(cudaSetDevice(c->device));
+    if (space == HR_SHARED) {
+        if (base_word != 0 || n_words * 8 + HR_FSM_SMEM_BYTES > 227 * 1024)
+            return fail(c, HR_E_ARG, "shared shadow too large: %llu words", (unsigned long long)n_words);
+        c->smem_words_max = (uint32_t)n_words;
+        if (dev_region) *dev_region = nullptr;
+        return HR_OK;
+    }
+    if (space != HR_GLOBAL || n_words == 0 || base_word + n_words > (1ull << 61))
+        return fail(c, HR_E_ARG, "bad global region");
+    if (c->gshadow) {
+        cudaFree(c->gshadow);
+        c->gshadow = nullptr;
+    }
+    /* local slice: this shard's 512-word granules, packed */
+    uint64_t gran = (n_words + 511) >> 9;
+    uint64_t local_gran = (gran + c->shard_count - 1) >> c->shard_log2;
+    uint64_t local = local_gran << 9;
+    if (cudaMalloc(&c->gshadow, local * 8) != cudaSuccess)
+        return fail(c, HR_E_NOMEM, "cudaMalloc(%llu B) for the global shadow failed",
+                    (unsigned long long)(local * 8));
+    CU(cudaMemset(c->gshadow, 0, local * 8));
+    c->gbase = base_word;
+    c->gwords = n_words;
+    c->glocal = local;
+    if (dev_region) *dev_region = c->gshadow;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
+{
+    if (!c) return HR_E_ARG;
+    CU(cudaSetDevice(c->device));
+    c->stream = (cudaStream_t)stream;
+    if (c->gshadow) CU(cudaMemsetAsync(c->gshadow, 0, c->glocal * 8, c->stream));
+    return HR_OK;
+}
+
+static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const uint64_t *woff,
+                        cudaStream_t s)
+{
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
+        if (blocks == 0) continue;
+        if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32)
+            return fail(c, HR_E_ARG, "kernel %u: grid %llux%llux%llu outside the 17/5/5-bit tid",
+                        k, (unsigned long long)blocks, (unsigned long long)warps, (unsigned long long)lanes);
+        if (smem_words > c->smem_words_max)
+            return fail(c, HR_E_STATE, "kernel %u needs %llu shared shadow words (registered %u)", k,
+                        (unsigned long long)smem_words, c->smem_words_max);
+        if (woi + blocks * warps + 1 > t->n_warp_off)
+            return fail(c, HR_E_ARG, "kernel %u: warp_off out of range", k);
+        hr_status st = hr_kernel_begin(c, s);
+        if (st) return st;
+        uint32_t kid = t->kernel_base + k;
+        hr_dev d = make_dev(c, kid);
+        size_t smem = HR_FSM_SMEM_BYTES + smem_words * 8;
+        if (smem > 48 * 1024)
+            CU(cudaFuncSetAttribute(hr_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        hr_replay_kernel<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(
+            d, rec, woff + woi, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
+        CU(cudaGetLastError());
+        c->last_kernel = kid;
+        c->have_kernel = true;
+    }
+    return HR_OK;
+}
+
+extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
+{
+    if (!c || !t || (t->n_kernels && (!t->kdesc || !t->rec || !t->warp_off))) return fail(c, HR_E_ARG, "null trace");
+    CU(cudaSetDevice(c->device));
+    c->stream = (cudaStream_t)stream;
+    return replay(c, t, t->rec, t->warp_off, c->stream);
+}
+
+extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *stream)
+{
+    if (!c || !t || (t->n_kernels && (!t->kdesc || !t->rec || !t->warp_off))) return fail(c, HR_E_ARG, "null trace");
+    CU(cudaSetDevice(c->device));
+    c->stream = (cudaStream_t)stream;
+    size_t need_rec = (size_t)t->n_rows * 32, need_woff = (size_t)t->n_warp_off;
+    if (need_rec > c->stage_rec_cap) {
+        if (c->stage_rec) cudaFree(c->stage_rec);
+        c->stage_rec = nullptr;
+        if (cudaMalloc(&c->stage_rec, need_rec * 8) != cudaSuccess)
+            return fail(c, HR_E_NOMEM, "staging %zu records failed", need_rec);
+        c->stage_rec_cap = need_rec;
+    }
+    if (need_woff > c->stage_woff_cap) {
+        if (c->stage_woff) cudaFree(c->stage_woff);
+        c->stage_woff = nullptr;
+        if (cudaMalloc(&c->stage_woff, need_woff * 8) != cudaSuccess)
+            return fail(c, HR_E_NOMEM, "staging warp offsets failed");
+        c->stage_woff_cap = need_woff;
+    }
+    CU(cudaMemcpyAsync(c->stage_woff, t->warp_off, need_woff * 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->stage_rec, t->rec, need_rec * 8, cudaMemcpyHostToDevice, c->stream));
+    return replay(c, t, c->stage_rec, c->stage_woff, c->stream);
+}
+
+static bool race_less(const hr_race &a, const hr_race &b)
+{
+    if (a.kernel != b.kernel) return a.kernel < b.kernel;
+    if (a.space != b.space) return a.space < b.space;
+    if (a.block != b.block) return a.block < b.block;
+    return a.word < b.word;
+}
+
+extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out)
+{
+    if (!c || !n_out || (cap && !out)) return fail(c, HR_E_ARG, "hr_report: bad arguments");
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamSynchronize(c->stream));
+    unsigned int hdr[4];
+    CU(cudaMemcpy(hdr, c->tail, sizeof hdr, cudaMemcpyDeviceToHost));
+    uint32_t n = std::min<uint32_t>(hdr[0], c->cfg.ring_capacity);
+    std::vector<hr_race> v(n);
+    if (n) CU(cudaMemcpy(v.data(), c->ring, n * sizeof(hr_race), cudaMemcpyDeviceToHost));
+    uint32_t flags = hdr[1];
+    if ((flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow) {
+        /* fallback: scan the last kernel's global shadow (shared instances are gone) */
+        uint32_t scap = 1u << 22;
+        hr_race *tmp = nullptr;
+        CU(cudaMalloc(&tmp, sizeof(hr_race) * (size_t)scap));
+        CU(cudaMemset(c->tail + 2, 0, sizeof(unsigned int)));
+        hr_scan_kernel<<<148 * 8, 256>>>(c->gshadow, c->glocal, c->gbase, c->shard_rank, c->shard_log2,
+                                         c->last_kernel, tmp, c->tail + 2, scap);
+        CU(cudaGetLastError());
+        unsigned int cnt = 0;
+        CU(cudaMemcpy(&cnt, c->tail + 2, sizeof cnt, cudaMemcpyDeviceToHost));
+        cnt = std::min(cnt, scap);
+        size_t off = v.size();
+        v.resize(off + cnt);
+        if (cnt) CU(cudaMemcpy(v.data() + off, tmp, cnt * sizeof(hr_race), cudaMemcpyDeviceToHost));
+        cudaFree(tmp);
+    }
+    std::sort(v.begin(), v.end(), race_less);
+    size_t m = 0;
+    for (size_t i = 0; i < v.size(); i++) {
+        if (m && !race_less(v[m - 1], v[i]) && !race_less(v[i], v[m - 1])) {
+            if (v[i].scope > v[m - 1].scope) {
+                uint8_t sc = v[i].scope;
+                if (v[m - 1].first_kind == 0xff) v[m - 1] = v[i];
+                v[m - 1].scope = sc;
+            }
+            continue;
+        }
+        v[m++] = v[i];
+    }
+    *n_out = m;
+    if (flags_out) *flags_out = flags;
+    size_t w = std::min(m, cap);
+    if (w) memcpy(out, v.data(), w * sizeof(hr_race));
+    return m > cap ? fail(c, HR_E_ARG, "hr_report: %zu races, capacity %zu", m, cap) : HR_OK;
+}
+
+extern "C" hr_status hr_reset_report(hr_ctx *c)
+{
+    if (!c) return HR_E_ARG;
+    CU(cudaSetDevice(c->device));
+    CU(cudaMemsetAsync(c->tail, 0, 4 * sizeof(unsigned int), c->stream));
+    CU(cudaMemsetAsync(c->counters, 0, 4 * sizeof(unsigned long long), c->stream));
+    c->have_kernel = false;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_counters(hr_ctx *c, uint64_t out[4])
+{
+    if (!c || !out) return HR_E_ARG;
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpy(out, c->counters, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return HR_OK;
+}
+
+extern "C" hr_status hr_fsm_table(uint8_t *table2048, uint8_t *flags32)
+{
+    if (table2048) memcpy(table2048, hr_fsm_table_init, HR_FSM_BYTES);
+    if (flags32) memcpy(flags32, hr_fsm_flags_init, 32);
+    return HR_OK;
+}
+
+extern "C" hr_status hr_device_view(hr_ctx *c, void *out, size_t size)
+{
+    if (!c || !out || size < sizeof(hr_dev)) return fail(c, HR_E_ARG, "hr_device_view: need %zu bytes", sizeof(hr_dev));
+    hr_dev d = make_dev(c, c->last_kernel);
+    memcpy(out, &d, sizeof d);
+    return HR_OK;
+}
+
+extern "C" const char *hr_last_error(hr_ctx *c) { return c ? c->err : "null context"; }
+
+extern "C" void hr_destroy(hr_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->gshadow) cudaFree(c->gshadow);
+    if (c->ring) cudaFree(c->ring);
+    if (c->tail) cudaFree(c->tail);
+    if (c->counters) cudaFree(c->counters);
+    if (c->fsm) cudaFree(c->fsm);
+    if (c->stage_rec) cudaFree(c->stage_rec);
+    if (c->stage_woff) cudaFree(c->stage_woff);
+    delete c;
+}

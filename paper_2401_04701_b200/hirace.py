@@ -1,0 +1,284 @@
+"""Thin Python binding of the C ABI in include/hr.h (argument marshalling only).
+
+Every step of the check runs in libhirace.so (sm_100a).  PyTorch provides
+device memory, streams and (in ``multigpu``) process groups.  There is no CPU
+fallback: if the library cannot be loaded this module raises on import.
+
+Function names mirror the C ABI: ``hr_init``, ``hr_set_shard``,
+``hr_shadow_alloc``, ``hr_kernel_begin``, ``hr_replay_trace``,
+``hr_replay_trace_host``, ``hr_report``, ``hr_reset_report``, ``hr_counters``,
+``hr_fsm_table``, ``hr_last_error``, ``hr_destroy``.  ``Checker`` bundles them
+for tests and bench.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, NamedTuple, Optional, Tuple
+
+import numpy as np
+
+from . import build as _build
+
+HR_OK, HR_E_ARG, HR_E_NOMEM, HR_E_CUDA, HR_E_STATE = 0, -1, -2, -3, -4
+HR_GLOBAL, HR_SHARED = 0, 1
+HR_F_CLOCK_OVERFLOW, HR_F_RING_OVERFLOW, HR_F_MODEL_VIOLATION = 1, 2, 4
+HR_F_BARRIER_DIVERGENCE, HR_F_UNMONITORED = 8, 16
+HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT = 1, 2
+EXPORTS = ("hr_init", "hr_set_shard", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
+           "hr_replay_trace_host", "hr_report", "hr_reset_report", "hr_counters", "hr_fsm_table",
+           "hr_device_view", "hr_last_error", "hr_destroy")
+
+
+class HrConfig(ctypes.Structure):
+    _fields_ = [("state_bits", ctypes.c_uint8), ("tid_bits", ctypes.c_uint8), ("bc_bits", ctypes.c_uint8),
+                ("wc_bits", ctypes.c_uint8), ("ring_capacity", ctypes.c_uint32), ("device", ctypes.c_int),
+                ("options", ctypes.c_uint32)]
+
+
+class HrRace(ctypes.Structure):
+    _fields_ = [("word", ctypes.c_uint64), ("block", ctypes.c_uint32), ("kernel", ctypes.c_uint32),
+                ("first_tid", ctypes.c_uint32), ("space", ctypes.c_uint8), ("scope", ctypes.c_uint8),
+                ("first_kind", ctypes.c_uint8), ("prev_state", ctypes.c_uint8)]
+
+
+class HrTrace(ctypes.Structure):
+    _fields_ = [("rec", ctypes.c_void_p), ("n_rows", ctypes.c_uint64), ("kdesc", ctypes.c_void_p),
+                ("n_kernels", ctypes.c_uint32), ("kernel_base", ctypes.c_uint32),
+                ("warp_off", ctypes.c_void_p), ("n_warp_off", ctypes.c_uint64)]
+
+
+assert ctypes.sizeof(HrRace) == 24
+
+_lib = None
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load libhirace.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise ImportError(f"{path} missing: run __graft_entry__.build()")
+        _build.build()
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    sig = {
+        "hr_init": ([P(HrConfig), P(vp)], ctypes.c_int),
+        "hr_set_shard": ([vp, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
+        "hr_shadow_alloc": ([vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, P(vp)], ctypes.c_int),
+        "hr_kernel_begin": ([vp, vp], ctypes.c_int),
+        "hr_replay_trace": ([vp, P(HrTrace), vp], ctypes.c_int),
+        "hr_replay_trace_host": ([vp, P(HrTrace), vp], ctypes.c_int),
+        "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
+        "hr_reset_report": ([vp], ctypes.c_int),
+        "hr_counters": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
+        "hr_fsm_table": ([P(ctypes.c_uint8), P(ctypes.c_uint8)], ctypes.c_int),
+        "hr_device_view": ([vp, vp, ctypes.c_size_t], ctypes.c_int),
+        "hr_last_error": ([vp], ctypes.c_char_p),
+        "hr_destroy": ([vp], None),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+class HiraceError(RuntimeError):
+    pass
+
+
+def _check(rc: int, ctx=None, what: str = ""):
+    if rc != HR_OK:
+        msg = load().hr_last_error(ctx).decode() if ctx else ""
+        raise HiraceError(f"{what} failed with status {rc}: {msg}")
+
+
+# ---- C-ABI mirrors -------------------------------------------------------------
+
+def hr_init(bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, device: int = 0,
+            options: int = 0):
+    cfg = HrConfig(5, 27, bc_bits, wc_bits, ring_capacity, device, options)
+    ctx = ctypes.c_void_p()
+    _check(load().hr_init(ctypes.byref(cfg), ctypes.byref(ctx)), None, "hr_init")
+    return ctx
+
+
+def hr_set_shard(ctx, rank: int, count: int):
+    _check(load().hr_set_shard(ctx, rank, count), ctx, "hr_set_shard")
+
+
+def hr_shadow_alloc(ctx, space: int, base_word: int, n_words: int) -> int:
+    region = ctypes.c_void_p()
+    _check(load().hr_shadow_alloc(ctx, space, base_word, n_words, ctypes.byref(region)), ctx,
+           "hr_shadow_alloc")
+    return region.value or 0
+
+
+def hr_kernel_begin(ctx, stream: int = 0):
+    _check(load().hr_kernel_begin(ctx, ctypes.c_void_p(stream)), ctx, "hr_kernel_begin")
+
+
+def hr_replay_trace(ctx, t: HrTrace, stream: int = 0):
+    _check(load().hr_replay_trace(ctx, ctypes.byref(t), ctypes.c_void_p(stream)), ctx, "hr_replay_trace")
+
+
+def hr_replay_trace_host(ctx, t: HrTrace, stream: int = 0):
+    _check(load().hr_replay_trace_host(ctx, ctypes.byref(t), ctypes.c_void_p(stream)), ctx,
+           "hr_replay_trace_host")
+
+
+class Race(NamedTuple):
+    kernel: int
+    space: int
+    block: int
+    word: int
+    scope: int
+
+
+def hr_report(ctx, cap: int = 1 << 16) -> Tuple[List[Race], int, np.ndarray]:
+    """(sorted unique races as (kernel, space, block, word, scope), flags, raw records)."""
+    lib = load()
+    while True:
+        buf = (HrRace * cap)()
+        n = ctypes.c_size_t(0)
+        fl = ctypes.c_uint32(0)
+        rc = lib.hr_report(ctx, buf, cap, ctypes.byref(n), ctypes.byref(fl))
+        if rc == HR_E_ARG and n.value > cap:
+            cap = int(n.value)
+            continue
+        _check(rc, ctx, "hr_report")
+        raw = np.frombuffer(bytes(buf)[: 24 * n.value], dtype=np.dtype([
+            ("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("first_tid", "<u4"), ("space", "u1"),
+            ("scope", "u1"), ("first_kind", "u1"), ("prev_state", "u1")]))
+        races = [Race(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+                 for r in raw]
+        return races, int(fl.value), raw
+
+
+def hr_reset_report(ctx):
+    _check(load().hr_reset_report(ctx), ctx, "hr_reset_report")
+
+
+def hr_counters(ctx) -> List[int]:
+    out = (ctypes.c_uint64 * 4)()
+    _check(load().hr_counters(ctx, out), ctx, "hr_counters")
+    return list(out)
+
+
+def hr_fsm_table() -> Tuple[bytes, bytes]:
+    t = (ctypes.c_uint8 * 2048)()
+    f = (ctypes.c_uint8 * 32)()
+    _check(load().hr_fsm_table(t, f), None, "hr_fsm_table")
+    return bytes(t), bytes(f)
+
+
+def hr_last_error(ctx) -> str:
+    return load().hr_last_error(ctx).decode()
+
+
+def hr_destroy(ctx):
+    load().hr_destroy(ctx)
+
+
+# ---- convenience wrapper -----------------------------------------------------------
+
+class DeviceTrace:
+    """A trace resident in HBM: torch uint64 tensors for rec / warp_off, host kdesc."""
+
+    def __init__(self, rec, warp_off, kdesc: np.ndarray):
+        import torch
+        self.rec = rec
+        self.warp_off = warp_off
+        self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
+        assert rec.dtype == torch.int64 and warp_off.dtype == torch.int64
+        self.n_rows = rec.numel() // 32
+
+    @staticmethod
+    def from_trace(trace, device="cuda") -> "DeviceTrace":
+        import torch
+        rec = torch.from_numpy(np.ascontiguousarray(trace.rec).view(np.int64)).to(device)
+        wo = torch.from_numpy(np.ascontiguousarray(trace.warp_off).view(np.int64)).to(device)
+        return DeviceTrace(rec, wo, trace.kdesc)
+
+    def c(self, kernel_base: int = 0) -> HrTrace:
+        return HrTrace(self.rec.data_ptr(), self.n_rows, self.kdesc.ctypes.data, self.kdesc.shape[0],
+                       kernel_base, self.warp_off.data_ptr(), self.warp_off.numel())
+
+
+def host_trace_c(trace, kernel_base: int = 0) -> HrTrace:
+    """HrTrace over HOST arrays (for hr_replay_trace_host); keep `trace` alive."""
+    return HrTrace(trace.rec.ctypes.data, trace.rec.shape[0] // 32, trace.kdesc.ctypes.data,
+                   trace.kdesc.shape[0], kernel_base, trace.warp_off.ctypes.data, trace.warp_off.shape[0])
+
+
+def trace_extent(trace) -> Tuple[int, int]:
+    """(max global word + 1, max shared words) over a host trace — for sizing shadows."""
+    rec = np.asarray(trace.rec, dtype=np.uint64)
+    op = rec >> np.uint64(62)
+    acc = op != 3
+    sp = ((rec >> np.uint64(61)) & np.uint64(1)).astype(bool)
+    words = rec & np.uint64((1 << 61) - 1)
+    g = words[acc & ~sp]
+    gmax = int(g.max()) + 1 if g.size else 1
+    smem = int(trace.kdesc[:, 3].max()) if trace.kdesc.shape[0] else 0
+    return gmax, smem
+
+
+class Checker:
+    """One hr_ctx with a global shadow region and a shared-shadow budget."""
+
+    def __init__(self, global_words: int, smem_words: int = 0, base_word: int = 0, device: int = 0,
+                 bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, options: int = 0,
+                 shard: Optional[Tuple[int, int]] = None):
+        self.ctx = hr_init(bc_bits, wc_bits, ring_capacity, device, options)
+        if shard is not None:
+            hr_set_shard(self.ctx, shard[0], shard[1])
+        self.shadow_ptr = hr_shadow_alloc(self.ctx, HR_GLOBAL, base_word, max(1, global_words))
+        hr_shadow_alloc(self.ctx, HR_SHARED, 0, smem_words)
+
+    def replay(self, dtrace: DeviceTrace, stream: Optional[int] = None, kernel_base: int = 0):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        hr_replay_trace(self.ctx, dtrace.c(kernel_base), stream)
+
+    def replay_host(self, trace, stream: Optional[int] = None, kernel_base: int = 0):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        self._host_ref = trace
+        hr_replay_trace_host(self.ctx, host_trace_c(trace, kernel_base), stream)
+
+    def report(self):
+        return hr_report(self.ctx)
+
+    def reset(self):
+        hr_reset_report(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            hr_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def check_trace(trace, device: int = 0, **kw) -> Tuple[List[Race], int]:
+    """Replay a host trace on the GPU and return (sorted racy set, flags)."""
+    gmax, smem = trace_extent(trace)
+    ck = Checker(gmax, smem, device=device, **kw)
+    dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}")
+    ck.replay(dt)
+    races, flags, _ = ck.report()
+    ck.close()
+    return races, flags

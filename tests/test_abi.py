@@ -1,0 +1,64 @@
+"""C-ABI library: builds for sm_100a, loads, exports every symbol include/hr.h
+declares, carries the generated FSM table, and fails loudly without a GPU."""
+import ctypes
+import re
+import os
+
+import pytest
+
+from paper_2401_04701_b200 import build, hirace
+from paper_2401_04701_b200.fsm import generate as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "hr.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hr_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_every_declared_symbol():
+    lib = ctypes.CDLL(build.build())
+    names = declared_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(hirace.EXPORTS)
+
+
+def test_compiled_table_matches_generator():
+    table, flags, _ = G.build_table()
+    t, f = hirace.hr_fsm_table()
+    assert t == table and f == flags
+
+
+def test_sass_uses_native_64bit_atomics():
+    """ATOMG.E.CAS.64 for global, ATOMS.CAS.64 for shared,
+    MATCH.ANY.U64 for coalescing, on sm_100a."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-sass", build.build()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert re.search(r"ATOMG\.E\.CAS\.64", out)
+    assert re.search(r"ATOMS\.CAS\.64", out)
+    assert "MATCH.ANY.U64" in out
+
+
+def test_init_without_gpu_fails_loudly():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    with pytest.raises(hirace.HiraceError):
+        hirace.hr_init()
+
+
+def test_config_validation():
+    lib = hirace.load()
+    ctx = ctypes.c_void_p()
+    bad = hirace.HrConfig(5, 27, 20, 20, 16, 0, 0)      # widths must sum to 64
+    assert lib.hr_init(ctypes.byref(bad), ctypes.byref(ctx)) == hirace.HR_E_ARG
+    bad = hirace.HrConfig(6, 26, 16, 16, 16, 0, 0)
+    assert lib.hr_init(ctypes.byref(bad), ctypes.byref(ctx)) == hirace.HR_E_ARG

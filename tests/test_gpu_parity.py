@@ -1,0 +1,182 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
+element (racy address + scope), bit-exact — integer work (north_star).
+
+Covers: paper listings, C1 all variants, random programs over grids up to
+32 warps x 32 lanes with shared/global/atomics/both barriers and multiple
+kernels, schedule fuzzing (coalescing off, lane and block permutations),
+ring overflow fallback, clock overflow, shard emulation, host-buffer replay.
+"""
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from tracegen import format as tf
+from tracegen import programs as tp
+
+pytestmark = pytest.mark.gpu
+
+
+def hr():
+    from paper_2401_04701_b200 import hirace
+    return hirace
+
+
+def gpu_set(trace, **kw):
+    races, flags = hr().check_trace(trace, **kw)
+    return [tuple(r) for r in races], flags
+
+
+def oracle_set(trace, **kw):
+    res = oracle.check(trace, **kw)
+    return [tuple(r) for r in res.races], res.flags
+
+
+def test_listings():
+    for tr in (tp.listing1(1, 1, 2), tp.listing1(2, 2, 2), tp.listing1(64, 8, 32), tp.listing2(1, 1, 4),
+               tp.listing2(2, 2, 2), tp.listing2(1, 32, 32), tp.listing2(3, 4, 32), tp.listing4(1, 1, 4, 4),
+               tp.listing4(1, 4, 32, 100), tp.listing4(2, 1, 2, 4)):
+        assert gpu_set(tr) == oracle_set(tr)
+
+
+@pytest.mark.parametrize("removed", [None, "load", 128, 64, 32, 16, 8, 4, 2, 1])
+def test_c1_tree_reduction(removed):
+    tr = tp.c1_tree_reduction(removed=removed)
+    g, fl = gpu_set(tr)
+    o, ofl = oracle_set(tr)
+    assert g == o and fl == ofl == 0
+
+
+def _random_batch(seed, n, **kw):
+    rng = random.Random(seed)
+    kernels = []
+    for _ in range(n):
+        t = tp.random_program(rng, **kw)
+        blocks, warps, lanes, smem, _ = (int(x) for x in t.kdesc[0, :5])
+        rows = [t.rec[int(t.warp_off[w]) * 32: int(t.warp_off[w + 1]) * 32].reshape(-1, 32)
+                for w in range(blocks * warps)]
+        k = tf.Kernel(blocks, warps, lanes, smem)
+        k.rows = rows
+        kernels.append(k)
+    return tf.make_trace(kernels)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_small_family(seed):
+    tr = _random_batch(seed, 300, max_blocks=2, max_warps=2, max_lanes=2, max_slots=5, n_words=2,
+                       spaces=(0, 1))
+    assert gpu_set(tr) == oracle_set(tr)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_wide_grids(seed):
+    """Full warps and many warps: exercises MATCH coalescing, multi-lane folds,
+    CAS contention, several tiles of the shadow and ragged warp lengths."""
+    tr = _random_batch(100 + seed, 40, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12,
+                       n_words=40, spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
+    g, fl = gpu_set(tr)
+    o, ofl = oracle_set(tr)
+    assert g == o and fl == ofl
+    assert len(o) > 10
+
+
+def test_hot_words_contention():
+    """Few words, 32 warps x 32 lanes x 16 blocks: heavy CAS retry storms."""
+    tr = _random_batch(7, 10, max_blocks=16, max_warps=32, max_lanes=32, max_slots=8, n_words=3,
+                       spaces=(0, 1), p_skip=0.2)
+    assert gpu_set(tr) == oracle_set(tr)
+    tr = _random_batch(8, 10, max_blocks=16, max_warps=32, max_lanes=32, max_slots=8, n_words=3,
+                       kinds="RA", spaces=(0, 1), p_skip=0.2)
+    assert gpu_set(tr) == oracle_set(tr)
+
+
+@pytest.mark.parametrize("options", [1, 2, 3])
+def test_ablations_same_result(options):
+    """Coalescing off / fast exits off change the commit order and the write
+    traffic, never the result (schedule independence)."""
+    tr = _random_batch(21, 60, max_blocks=4, max_warps=4, max_lanes=32, max_slots=10, n_words=8,
+                       spaces=(0, 1))
+    assert gpu_set(tr, options=options) == oracle_set(tr)
+
+
+def test_lane_and_block_permutation_invariance():
+    rng = random.Random(3)
+    tr = _random_batch(31, 30, max_blocks=4, max_warps=2, max_lanes=32, max_slots=8, n_words=10,
+                       spaces=(0,))
+    base, _ = gpu_set(tr)
+    perm = list(range(32))
+    rng.shuffle(perm)
+    rec = tr.rec.reshape(-1, 32)[:, perm].reshape(-1).copy()
+    # lanes of a row are remapped: only words + scopes are compared (global space)
+    tr2 = tf.Trace(rec, tr.kdesc.copy(), tr.warp_off.copy())
+    for k in range(tr2.kdesc.shape[0]):
+        tr2.kdesc[k, 2] = 32
+    assert gpu_set(tr2) == oracle_set(tr2)
+    assert oracle_set(tr2)[0] == base
+
+
+def test_repeated_runs_identical():
+    tr = _random_batch(41, 20, max_blocks=8, max_warps=8, max_lanes=32, max_slots=10, n_words=4,
+                       spaces=(0, 1))
+    o = oracle_set(tr)
+    for _ in range(5):
+        assert gpu_set(tr) == o
+
+
+def test_ring_overflow_falls_back_to_shadow_scan():
+    # one kernel, many racy global words
+    tr = tp.listing2(4, 8, 32)
+    g, fl = gpu_set(tr, ring_capacity=8)
+    o, _ = oracle_set(tr)
+    assert fl & hr().HR_F_RING_OVERFLOW
+    assert g == o
+
+
+def test_clock_overflow():
+    ev = {(0, 0, 0): [tf.W(0)] + [tf.SYNCTHREADS] * 4 + [tf.W(1)],
+          (0, 0, 1): [tf.W(0)] + [tf.SYNCTHREADS] * 4 + [tf.W(1)]}
+    tr = tp.from_thread_events(1, 1, 2, ev)
+    g, fl = gpu_set(tr, bc_bits=2, wc_bits=30)
+    o, ofl = oracle_set(tr, bc_bits=2, wc_bits=30)
+    assert g == o and fl == ofl == hr().HR_F_CLOCK_OVERFLOW
+    assert [r[3] for r in g] == [0]
+
+
+def test_shard_emulation_union_equals_single():
+    """N address shards on one GPU, concatenated, equal the
+    single-GPU result (words are independent FSMs)."""
+    h = hr()
+    tr = _random_batch(51, 20, max_blocks=4, max_warps=4, max_lanes=32, max_slots=10, n_words=3000,
+                       spaces=(0, 1))
+    gmax, smem = h.trace_extent(tr)
+    full, _ = gpu_set(tr)
+    for n in (2, 4, 8):
+        union = []
+        for r in range(n):
+            ck = h.Checker(gmax, smem, shard=(r, n))
+            ck.replay(h.DeviceTrace.from_trace(tr))
+            races, _, _ = ck.report()
+            ck.close()
+            union += [tuple(x) for x in races]
+        assert sorted(union) == full
+
+
+def test_host_buffer_replay():
+    h = hr()
+    tr = tp.c1_tree_reduction(removed=8)
+    gmax, smem = h.trace_extent(tr)
+    ck = h.Checker(gmax, smem)
+    ck.replay_host(tr)
+    races, fl, _ = ck.report()
+    assert [tuple(r) for r in races] == oracle_set(tr)[0]
+
+
+def test_empty_and_degenerate():
+    h = hr()
+    # a kernel with no accesses at all
+    tr = tf.single_kernel(2, 2, 32, lambda b, w, l: [tf.SYNCTHREADS])
+    assert gpu_set(tr) == ([], 0)
+    # single thread: never races
+    tr = tp.from_thread_events(1, 1, 1, {(0, 0, 0): [tf.W(0), tf.R(0), tf.A(0), tf.W(0)]})
+    assert gpu_set(tr) == ([], 0)
