@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: checked accesses/s of the HiRace per-access race check on B200.
+
+Workload (BASELINE.json configs[4], the multi-GPU config the metric is
+quoted on): C5 — a 2^32-access global trace over a 2^32-word (16 GiB)
+address space, 2^16 blocks x 256 threads x 256 accesses, address-sharded
+across N GPUs (tracegen/c5gen.h).  One STEP = one pass of the whole hot path
+over the trace: report-ring reset, kernel-boundary shadow reset (a11), the
+replay kernel (a1-a10, a12), hr_report (a13: D2H + sort/merge) and, for
+N > 1, the NCCL allgather of the per-shard race sets.
+
+  value  device-resident: trace generated in HBM before timing; K steps timed
+         with CUDA events on the launching stream, max over ranks.
+  e2e    same steps through hr_replay_trace_host: the trace lives in pinned
+         host memory and is copied H2D inside every timed step; the race set is
+         read back D2H.
+  roofline  for the replay kernel: algorithmic bytes / live event-timed
+         duration vs MEASURED_PEAKS.json hbm_gbs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "checked_accesses_per_sec"
+UNIT = "accesses/s"
+BYTES_PER_ACCESS_ALGO = 16          # 8 B shadow read + 8 B shadow write-back (a4 + a8)
+BYTES_PER_ACCESS_LITERAL = 8        # north_star: "8 B of shadow read-modify-write per checked access"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lb", type=int, default=16, help="log2 blocks of C5 (16 = full 2^32 accesses)")
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-lb", type=int, default=10, help="C5 sample for the oracle cpu_baseline")
+    ap.add_argument("--ref-lb", type=int, default=8, help="C5 sample per --impl reference step")
+    ap.add_argument("--options", type=int, default=0, help="extra HR_OPT_* bits (ablations)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.idx)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: int, world: int) -> int:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def cpu_baseline(lb: int, seed: int):
+    """The oracle as it stands, single-threaded, on a bounded C5 sample."""
+    import oracle
+    from tracegen import c5
+    tr = c5.cpu_trace(lb, seed)
+    t0 = time.perf_counter()
+    res = oracle.check(tr, mode=oracle.BUCKETED)
+    dt = time.perf_counter() - t0
+    ok = [(r.word, r.scope) for r in res.races] == c5.planted(lb, seed)
+    return {"value": res.n_accesses / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"C5 shape at 2^{lb} blocks ({res.n_accesses} accesses, 1/{2 ** (16 - lb)} of the "
+                      f"blocks), bucketed mode, {dt:.2f} s; racy set == planted: {ok}"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on C5 samples (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from tracegen import c5
+    seed = args.seed if args.seed is not None else c5.DEFAULT_SEED
+    tr = c5.cpu_trace(args.ref_lb, seed)
+    for _ in range(args.warmup):
+        oracle.check(tr)
+    t0 = time.perf_counter()
+    n = 0
+    for _ in range(args.steps):
+        n += oracle.check(tr).n_accesses
+    dt = time.perf_counter() - t0
+    v = n / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": f"C5 sample: 2^{args.ref_lb} blocks x 256 threads x 256 accesses "
+                               f"(same generator as the GPU arm's 2^{args.lb}-block workload)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"C5 at 2^{args.ref_lb} blocks per step, bucketed single-threaded oracle"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def exchange(races_raw, world):
+    """Race-set allgather over NCCL (the one exchange step)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    n = len(races_raw)
+    cnt = torch.tensor([n], dtype=torch.int64, device="cuda")
+    cnts = torch.empty(world, dtype=torch.int64, device="cuda")
+    dist.all_gather_into_tensor(cnts, cnt)
+    mx = int(cnts.max().item())
+    pad = torch.zeros(max(mx, 1) * 3, dtype=torch.int64, device="cuda")
+    if n:
+        pad[: n * 3] = torch.from_numpy(np.ascontiguousarray(races_raw).view(np.int64).copy()).cuda()
+    out = torch.empty(world * pad.numel(), dtype=torch.int64, device="cuda")
+    dist.all_gather_into_tensor(out, pad)
+    host = out.view(world, -1).cpu().numpy()
+    parts = [host[r, : int(cnts[r]) * 3].view(races_raw.dtype) for r in range(world)]
+    merged = np.concatenate(parts) if parts else races_raw
+    order = np.lexsort((merged["word"], merged["block"], merged["space"], merged["kernel"]))
+    return merged[order]
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    from paper_2401_04701_b200 import hirace as hr
+    from tracegen import c5
+
+    rank, world, local = dist_setup(args)
+    assert world == args.gpus or world == 1, "launch with torchrun for --gpus > 1"
+    seed = args.seed if args.seed is not None else c5.DEFAULT_SEED
+    lb = args.lb
+    stream = torch.cuda.current_stream().cuda_stream
+
+    # --- input: this rank's shard of the trace, generated in HBM (untimed) ---
+    rec, woff, kd = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
+    torch.cuda.synchronize()
+    dt = hr.DeviceTrace(rec, woff, kd)
+    ops = (rec >> 62) & 3
+    n_acc_rank = int((ops != 3).sum().item())
+    del ops
+    n_rows = dt.n_rows
+    ck = hr.Checker(c5.total_words(lb), 0, shard=(rank, world), options=hr.HR_OPT_TIMING | args.options,
+                    ring_capacity=1 << 21)
+
+    def step(replay_fn):
+        ck.reset()
+        replay_fn()
+        raw, flags = ck.report_raw()
+        if world > 1:
+            raw = exchange(raw, world)
+        return raw, flags
+
+    dev_replay = lambda: ck.replay(dt, stream)  # noqa: E731
+
+    # warm-up + correctness of this run against the closed form (planted set)
+    for _ in range(max(args.warmup, 1)):
+        raw, flags = step(dev_replay)
+    got = [(int(r["word"]), int(r["scope"])) for r in raw]
+    parity_ok = got == c5.planted(lb, seed) and flags == 0
+    hr.hr_replay_timing(ck.ctx)                     # drop warm-up launches
+
+    clocks = Clocks(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        raw, flags = step(dev_replay)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    reset_ms, n_resets, kern_ms, n_kern = hr.hr_replay_timing(ck.ctx)
+    parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw] == c5.planted(lb, seed)
+
+    ms_step = max_over_ranks(ms_total / args.steps, world)
+    total_acc = sum_over_ranks(n_acc_rank, world)
+    value = total_acc / (ms_step / 1e3)
+    kern_ms_launch = max_over_ranks(kern_ms / max(n_kern, 1), world)
+    reset_ms_launch = max_over_ranks(reset_ms / max(n_resets, 1), world)
+
+    # roofline of the dominant kernel (the replay), rank 0's launch
+    peak, peak_kind = peaks()
+    algo_bytes = n_rows * 32 * 8 + BYTES_PER_ACCESS_ALGO * n_acc_rank
+    achieved = algo_bytes / (kern_ms / max(n_kern, 1) / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "replay_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if world == 1 and int(pj.get("lb", -1)) == lb:
+                traffic = float(pj["dram_bytes_per_launch"])
+        except Exception:
+            traffic = None
+    literal = BYTES_PER_ACCESS_LITERAL * total_acc / (ms_step / 1e3) / 1e9 / (peak * world)
+
+    # --- e2e through the C ABI with HOST buffers ---
+    e2e = None
+    if not args.no_e2e:
+        host_rec = torch.empty(rec.numel(), dtype=torch.int64, pin_memory=True)
+        host_rec.copy_(rec)
+        host_woff = woff.cpu().numpy().view(np.uint64)
+        host_trace = type("T", (), {})()
+        host_trace.rec = host_rec.numpy().view(np.uint64)
+        host_trace.warp_off = host_woff
+        host_trace.kdesc = kd
+        del rec, dt
+        torch.cuda.empty_cache()
+        host_replay = lambda: ck.replay_host(host_trace, stream)  # noqa: E731
+        for _ in range(args.warmup):
+            step(host_replay)
+        barrier(world)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            raw_e, _ = step(host_replay)
+        f1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world)
+        parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == c5.planted(lb, seed)
+        e2e = {"value": total_acc / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host_trace.rec.nbytes + host_woff.nbytes),
+               "d2h_bytes_per_step": int(16 + 24 * len(raw_e) // max(world, 1)),
+               "ms_per_step": e2e_ms}
+        hr.hr_replay_timing(ck.ctx)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_lb, seed)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"C5: {total_acc} checked accesses (2^{lb} blocks x 256 threads x 256), "
+                                   f"global trace over 2^{lb + 16} words, address-sharded (granule mod {world})",
+                       "parallelism": f"address-shard x{world}", "l2": "inputs larger than L2 "
+                       "(trace + shadow >> 126 MB; no flush needed)", "seed": seed},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "hr_replay_kernel", "kernel_ms": kern_ms / max(n_kern, 1),
+                         "algo_bytes_per_launch": algo_bytes,
+                         "algo_bytes_rule": "records (n_rows*32*8) + 16 B shadow RMW per checked access"},
+            "literal_roofline_frac": literal,
+            "step_breakdown_ms": {"replay_kernel": kern_ms_launch, "shadow_reset": reset_ms_launch,
+                                  "rest(report,ring reset,exchange)": ms_step - kern_ms_launch - reset_ms_launch},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": n_kern,
+            "cpu_baseline": cpu,
+            "parity_vs_closed_form": parity_ok,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

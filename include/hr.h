@@ -70,7 +70,9 @@ typedef struct {
 
 enum {
     HR_OPT_NO_COALESCE = 1u,   /* disable same-address lane coalescing (a3), for ablations */
-    HR_OPT_NO_FASTEXIT = 2u    /* disable label-insensitive fast exits (a7), for ablations */
+    HR_OPT_NO_FASTEXIT = 2u,   /* disable label-insensitive fast exits (a7), for ablations */
+    HR_OPT_TIMING = 4u,        /* record CUDA events around every shadow reset and replay launch */
+    HR_OPT_NO_SPECULATE = 8u   /* first attempt loads the shadow word instead of speculating INIT */
 };
 
 /* One unique racy address.  24 bytes.
@@ -162,6 +164,12 @@ hr_status hr_reset_report(hr_ctx *ctx);
 /* Device-side counters of the last replay: [0] checked accesses, [1] CAS
  * retries, [2] fast exits (only maintained when built with HR_COUNTERS). */
 hr_status hr_counters(hr_ctx *ctx, uint64_t out[4]);
+
+/* With HR_OPT_TIMING: synchronise and return the summed device time (ms) and
+ * count of the shadow resets and replay-kernel launches since the last call
+ * (events recorded on the launching stream), then clear them. */
+hr_status hr_replay_timing(hr_ctx *ctx, double *reset_ms, uint64_t *n_resets, double *kernel_ms,
+                           uint64_t *n_kernels);
 
 /* Copy of the compiled-in FSM table (2048 bytes, index state<<6|kind<<4|sync<<2|rel)
  * and per-state flags (32 bytes).  Either pointer may be NULL. */

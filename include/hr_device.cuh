@@ -149,26 +149,41 @@ __device__ __forceinline__ void hr__set_flag(const hr_dev &d, unsigned int f)
 
 /* ---------------- the check core ---------------- */
 
+/* L1-cacheable probe (weak load): only used to take the insensitive-closure exit,
+ * which is valid for any value observed during this kernel (a7). */
+__device__ __forceinline__ unsigned long long hr__ld_g_l1(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.global.ca.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+/* emit-info word (one register instead of a 24-byte record) */
+#define HR_EI_EMIT 0x80000000u
+
 /*
  * hr_check_lanes: every lane of `mask` calls it (convergent), `valid` says
  * whether this lane has an access.  `space` (0 global / 1 shared), `word` the
  * monitored word (global: absolute word; shared: index in the block's
- * instance), `kind` hr_kind.  Lanes of one call share bc/wc (uniform barriers)
- * — COALESCE_SAFE=false re-checks that with a second MATCH for online use.
- * Returns after every lane's access is committed (program order).
+ * instance), `kind` hr_kind.  Lanes of one call share bc/wc (uniform barriers);
+ * ONLINE=true re-checks that with a second MATCH.  Returns after every lane's
+ * access is committed (the final ballot is the warp's convergence point), so a
+ * lane never runs ahead of an access folded into another lane (program order).
+ *
+ * First attempt (a4): global reads/writes speculate INIT and issue the CAS
+ * directly (one round trip for a first touch; a failed CAS returns the current
+ * word, which is the atomic read of Algorithm 1); atomics probe L1 first (hot
+ * GATOMIC words exit without L2 traffic); shared words are read with ld.shared.
  */
-template <bool COALESCE_SAFE>
+template <bool ONLINE>
 __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t, unsigned mask, bool valid,
                                                uint32_t space, uint64_t word, uint32_t kind)
 {
     const uint32_t lane = hr__laneid();
-    const bool coalesce = !(d.options & HR_OPT_NO_COALESCE);
-    const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
     valid = valid && !t.off;
 
     /* a2: shadow address (local index inside the shard) */
-    bool is_shared = space != 0u;
-    uint64_t key = 0;
+    const bool is_shared = space != 0u;
     uint64_t local = 0;
     if (valid) {
         if (is_shared) {
@@ -176,107 +191,113 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
             if (((t.tid >> 10) & ((1u << d.shard_log2) - 1u)) != d.shard_rank) valid = false;
             local = word;
         } else {
-            uint64_t g = word - d.gbase;
+            const uint64_t g = word - d.gbase;
             if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); valid = false; }
-            uint64_t gran = g >> 9;
+            const uint64_t gran = g >> 9;
             if (((uint32_t)gran & ((1u << d.shard_log2) - 1u)) != d.shard_rank) valid = false;
             local = ((gran >> d.shard_log2) << 9) | (g & 511u);
         }
     }
     /* match key: 0 = no access on this lane (filtered lanes must not alias owned words) */
-    if (valid) key = (local << 2) | (is_shared ? 2u : 0u) | 1u;
+    const uint64_t key = valid ? ((local << 2) | (is_shared ? 2u : 0u) | 1u) : 0ull;
 
-    /* a3: same-address coalescing */
+    /* a3: same-address coalescing (skipped when the warp's words are consecutive) */
     unsigned peers = 1u << lane;
-    if (coalesce) {
-        unsigned long long k0 = __shfl_sync(mask, key, __ffs(mask) - 1);
-        bool seq = !valid || key == k0 + ((unsigned long long)(lane - (__ffs(mask) - 1)) << 2);
+    unsigned kb0 = 0, kb1 = 0;
+    if (!(d.options & HR_OPT_NO_COALESCE)) {
+        const uint32_t first = __ffs(mask) - 1;
+        const unsigned long long k0 = __shfl_sync(mask, key, first);
+        const bool seq = !valid || key == k0 + ((unsigned long long)(lane - first) << 2);
         if (!__all_sync(mask, seq)) {
             peers = __match_any_sync(mask, key);
-            if (COALESCE_SAFE) {
-                unsigned same_epoch = __match_any_sync(mask, (unsigned long long)(uint32_t)t.meta);
+            if (ONLINE) {
+                const unsigned same_epoch = __match_any_sync(mask, (unsigned long long)(uint32_t)t.meta);
                 if (peers & ~same_epoch) peers = 1u << lane;
             }
+            kb0 = __ballot_sync(mask, kind & 1u);
+            kb1 = __ballot_sync(mask, (kind >> 1) & 1u);
         }
     }
-    unsigned kb0 = __ballot_sync(mask, kind & 1u);
-    unsigned kb1 = __ballot_sync(mask, (kind >> 1) & 1u);
 
-    bool emit = false;
-    hr_race rr;
+    uint32_t ei = 0;   /* [31] emit [30:26] racing lane [25:24] its kind [23:19] prev state [0] grid */
     if (valid && (__ffs(peers) - 1) == (int)lane) {
         const uint32_t sh_addr = t.sshadow + (uint32_t)(local << 3);
         unsigned long long *gp = d.gshadow + local;
-        unsigned long long old = is_shared ? hr__ld_s(sh_addr) : hr__ld_g(gp);
-        const unsigned rest = peers & ~(1u << lane);
+        const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
         const uint32_t last_lane = 31u - __clz(peers);
         const unsigned long long nmeta = (t.meta & ~(0x1full << HR_TID_SHIFT)) |
                                          ((unsigned long long)last_lane << HR_TID_SHIFT);
-        uint32_t retries = 0;
+        /* 0: value is a guess (INIT); 1: weak L1 probe; 2: coherent (L2/SMEM or CAS return) */
+        uint32_t fresh;
+        unsigned long long old;
+        if (is_shared) { old = hr__ld_s(sh_addr); fresh = 2; }
+        else if (kind == HR_ATOMIC && fastexit) { old = hr__ld_g_l1(gp); fresh = 1; }
+        else if (d.options & HR_OPT_NO_SPECULATE) { old = hr__ld_g(gp); fresh = 2; }
+        else { old = 0ull; fresh = 0; }
         while (true) {
-            uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
-            uint32_t otid = (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu;
-            uint32_t rel = hr__rel(t.tid, otid);
-            uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
+            const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+            const uint32_t rel = hr__rel(t.tid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+            const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
             uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
-            uint32_t race_lane = lane, race_kind = kind, race_prev = os;
-            bool entered = cur >= HR_RACE_BLOCK && cur != os;
+            uint32_t rinfo = (cur >= HR_RACE_BLOCK && cur != os)
+                                 ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19)) : 0u;
             /* fold the rest of the group: (kind_j, Us, Warp) in lane order */
-            unsigned r = rest;
+            unsigned r = peers & ~(1u << lane);
             while (r) {
-                uint32_t j = __ffs(r) - 1;
+                const uint32_t j = __ffs(r) - 1;
                 r &= r - 1;
-                uint32_t kj = ((kb0 >> j) & 1u) | (((kb1 >> j) & 1u) << 1);
-                uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | (0u << 2) | 1u));
-                if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !entered) {
-                    entered = true; race_lane = j; race_kind = kj; race_prev = cur;
-                }
+                const uint32_t kj = ((kb0 >> j) & 1u) | (((kb1 >> j) & 1u) << 1);
+                const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | 1u));
+                if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
+                    rinfo = HR_EI_EMIT | (j << 26) | (kj << 24) | (cur << 19);
                 cur = nx;
             }
-            unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
-            if (nw == old) break;                                         /* a7 (i) */
-            if (fastexit && cur == os) {
-                uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
-                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u))
+            const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
+            if (fastexit && cur == os && fresh) {
+                const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
+                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == 2))
                     break;                                                /* a7 (ii), (iii) */
             }
-            unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+            if (nw == old && fresh == 2) break;                           /* a7 (i) */
+            if (fresh == 1 && nw == old) { old = hr__ld_g(gp); fresh = 2; continue; }
+            const unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
             if (prev == old) {                                            /* a8 committed */
-                if (entered) {
-                    emit = true;
-                    rr.word = word;
-                    rr.block = is_shared ? (t.tid >> 10) : 0xffffffffu;
-                    rr.kernel = d.kernel_id;
-                    rr.first_tid = (t.tid & ~31u) | race_lane;
-                    rr.space = (uint8_t)space;
-                    rr.scope = (uint8_t)(cur == HR_RACE_GRID ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
-                    rr.first_kind = (uint8_t)race_kind;
-                    rr.prev_state = (uint8_t)race_prev;
-                }
+                if (rinfo) ei = rinfo | (cur == HR_RACE_GRID ? 1u : 0u);
                 break;
             }
             old = prev;
-            retries++;
-        }
+            fresh = 2;
 #ifdef HR_COUNTERS
-        if (retries) atomicAdd(&d.counters[1], (unsigned long long)retries);
+            atomicAdd(&d.counters[1], 1ull);
 #endif
+        }
     }
 
-    /* a9: warp-aggregated ring append */
-    unsigned em = __ballot_sync(mask, emit);
+    /* a9: warp-aggregated ring append; also the warp's convergence point */
+    const unsigned em = __ballot_sync(mask, ei != 0u);
     if (em) {
-        uint32_t leader = __ffs(em) - 1;
+        const uint32_t leader = __ffs(em) - 1;
         uint32_t base = 0;
         if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(em));
         base = __shfl_sync(mask, base, leader);
-        if (emit) {
-            uint32_t slot = base + __popc(em & ((1u << lane) - 1u));
-            if (slot < d.ring_cap) d.ring[slot] = rr;
-            else hr__set_flag(d, HR_F_RING_OVERFLOW);
+        if (ei) {
+            const uint32_t slot = base + __popc(em & ((1u << lane) - 1u));
+            if (slot < d.ring_cap) {
+                hr_race rr;
+                rr.word = word;
+                rr.block = is_shared ? (t.tid >> 10) : 0xffffffffu;
+                rr.kernel = d.kernel_id;
+                rr.first_tid = (t.tid & ~31u) | ((ei >> 26) & 31u);
+                rr.space = (uint8_t)space;
+                rr.scope = (uint8_t)((ei & 1u) ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
+                rr.first_kind = (uint8_t)((ei >> 24) & 3u);
+                rr.prev_state = (uint8_t)((ei >> 19) & 31u);
+                d.ring[slot] = rr;
+            } else {
+                hr__set_flag(d, HR_F_RING_OVERFLOW);
+            }
         }
     }
-    __syncwarp(mask);
 }
 
 /* ---------------- online instrumentation API ---------------- */

@@ -39,8 +39,22 @@ struct hr_ctx {
     size_t stage_rec_cap = 0;
     uint64_t *stage_woff = nullptr;
     size_t stage_woff_cap = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
 };
+
+static cudaEvent_t get_event(hr_ctx *c)
+{
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
 
 static hr_status fail(hr_ctx *c, hr_status s, const char *fmt, ...)
 {
@@ -183,7 +197,13 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
-    if (c->gshadow) CU(cudaMemsetAsync(c->gshadow, 0, c->glocal * 8, c->stream));
+    if (c->gshadow) {
+        bool timing = c->cfg.options & HR_OPT_TIMING;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, c->stream)); }
+        CU(cudaMemsetAsync(c->gshadow, 0, c->glocal * 8, c->stream));
+        if (timing) { CU(cudaEventRecord(e1, c->stream)); c->ev_reset.push_back({e0, e1}); }
+    }
     return HR_OK;
 }
 
@@ -209,9 +229,13 @@ static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const
         size_t smem = HR_FSM_SMEM_BYTES + smem_words * 8;
         if (smem > 48 * 1024)
             CU(cudaFuncSetAttribute(hr_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        bool timing = c->cfg.options & HR_OPT_TIMING;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
         hr_replay_kernel<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(
             d, rec, woff + woi, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
         CU(cudaGetLastError());
+        if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
         c->last_kernel = kid;
         c->have_kernel = true;
     }
@@ -326,6 +350,32 @@ extern "C" hr_status hr_counters(hr_ctx *c, uint64_t out[4])
     return HR_OK;
 }
 
+extern "C" hr_status hr_replay_timing(hr_ctx *c, double *reset_ms, uint64_t *n_resets, double *kernel_ms,
+                                      uint64_t *n_kernels)
+{
+    if (!c) return HR_E_ARG;
+    CU(cudaSetDevice(c->device));
+    double acc[2] = {0, 0};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[2] = {&c->ev_reset, &c->ev_kernel};
+    for (int i = 0; i < 2; i++) {
+        for (auto &pr : *lists[i]) {
+            CU(cudaEventSynchronize(pr.second));
+            float ms = 0;
+            CU(cudaEventElapsedTime(&ms, pr.first, pr.second));
+            acc[i] += ms;
+            c->ev_pool.push_back(pr.first);
+            c->ev_pool.push_back(pr.second);
+        }
+    }
+    if (reset_ms) *reset_ms = acc[0];
+    if (n_resets) *n_resets = c->ev_reset.size();
+    if (kernel_ms) *kernel_ms = acc[1];
+    if (n_kernels) *n_kernels = c->ev_kernel.size();
+    c->ev_reset.clear();
+    c->ev_kernel.clear();
+    return HR_OK;
+}
+
 extern "C" hr_status hr_fsm_table(uint8_t *table2048, uint8_t *flags32)
 {
     if (table2048) memcpy(table2048, hr_fsm_table_init, HR_FSM_BYTES);
@@ -354,5 +404,8 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->fsm) cudaFree(c->fsm);
     if (c->stage_rec) cudaFree(c->stage_rec);
     if (c->stage_woff) cudaFree(c->stage_woff);
+    for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
+    for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
 }

@@ -12,17 +12,13 @@
  * kernel's own loads and stores.
  *
  * Record rows are streamed with ld.global.cs (read once, evict-first) and
- * prefetched HR_PREFETCH rows ahead so the record latency is off the
- * shadow-update critical path.
+ * prefetched two rows ahead so the record latency is off the shadow-update
+ * critical path.
  */
 #ifndef HR_REPLAY_CUH_
 #define HR_REPLAY_CUH_
 
 #include "hr_device.cuh"
-
-#ifndef HR_PREFETCH
-#define HR_PREFETCH 4
-#endif
 
 #define HR_NOP_REC (3ull << 62)
 
@@ -31,9 +27,14 @@ __device__ __forceinline__ uint64_t hr__ld_rec(const uint64_t *p)
     return __ldcs(reinterpret_cast<const unsigned long long *>(p));
 }
 
-__global__ void __launch_bounds__(1024) hr_replay_kernel(hr_dev d, const uint64_t *__restrict__ rec,
-                                                         const uint64_t *__restrict__ woff, uint32_t warps,
-                                                         uint32_t lanes, uint32_t smem_words)
+/* minBlocks = 2 at 1024 threads caps registers at 32: 64 resident warps per SM
+ * whatever the simulated block size (occupancy is the latency-hiding lever). */
+#ifndef HR_MIN_BLOCKS
+#define HR_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(1024, HR_MIN_BLOCKS) hr_replay_kernel(hr_dev d, const uint64_t *__restrict__ rec,
+                                                            const uint64_t *__restrict__ woff, uint32_t warps,
+                                                            uint32_t lanes, uint32_t smem_words)
 {
     extern __shared__ __align__(16) unsigned char hr_smem[];
     unsigned long long *sshadow = reinterpret_cast<unsigned long long *>(hr_smem + HR_FSM_SMEM_BYTES);
@@ -46,34 +47,31 @@ __global__ void __launch_bounds__(1024) hr_replay_kernel(hr_dev d, const uint64_
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const bool active = lane < lanes;
     const uint64_t *p = rec + r0 * 32 + lane;
+    const uint64_t n = r1 - r0;
 
-    uint64_t buf[HR_PREFETCH];
-#pragma unroll
-    for (int i = 0; i < HR_PREFETCH; i++)
-        buf[i] = (active && r0 + i < r1) ? hr__ld_rec(p + 32ull * i) : HR_NOP_REC;
-
-    for (uint64_t r = r0; r < r1; r += HR_PREFETCH) {
-#pragma unroll
-        for (int i = 0; i < HR_PREFETCH; i++) {
-            if (r + i >= r1) break;                                  /* warp-uniform */
-            const uint64_t x = buf[i];
-            const uint64_t nr = r + i + HR_PREFETCH;
-            buf[i] = (active && nr < r1) ? hr__ld_rec(p + 32ull * (nr - r0)) : HR_NOP_REC;
-            const uint32_t op = (uint32_t)(x >> 62);
-            const uint64_t w = x & HR_WORD_MASK;
-            const bool st = op == 3u && w == 1u, sw = op == 3u && w == 2u;
-            const unsigned bst = __ballot_sync(0xffffffffu, st);
-            const unsigned bsw = __ballot_sync(0xffffffffu, sw);
-            if (bst | bsw) {                                          /* warp-uniform */
-                if ((bst && bst != lane_mask) || (bsw && bsw != lane_mask))
-                    if (lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
-                if (bst) hr_syncthreads(d, t);
-                else hr_syncwarp(d, t);
-                continue;
+    /* two-deep record prefetch (shift register, body not unrolled) */
+    uint64_t x1 = (active && n > 0) ? hr__ld_rec(p) : HR_NOP_REC;
+    uint64_t x2 = (active && n > 1) ? hr__ld_rec(p + 32) : HR_NOP_REC;
+    for (uint64_t i = 0; i < n; i++) {
+        const uint64_t x = x1;
+        x1 = x2;
+        x2 = (active && i + 2 < n) ? hr__ld_rec(p + 32 * (i + 2)) : HR_NOP_REC;
+        const uint32_t op = (uint32_t)(x >> 62);
+        const uint64_t w = x & HR_WORD_MASK;
+        const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
+        if (ctrl) {                                               /* warp-uniform */
+            const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
+            if ((bst && bst != lane_mask) || (ctrl != lane_mask))
+                if (lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+            if (bst) hr_syncthreads(d, t);
+            else hr_syncwarp(d, t);
+            if (ctrl & ~bst) {
+                const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
+                if (bsw != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
             }
-            if (op == 3u && w != 0u) hr__set_flag(d, HR_F_MODEL_VIOLATION);
-            hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
+            continue;
         }
+        hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
     }
 }
 

@@ -24,9 +24,10 @@ HR_OK, HR_E_ARG, HR_E_NOMEM, HR_E_CUDA, HR_E_STATE = 0, -1, -2, -3, -4
 HR_GLOBAL, HR_SHARED = 0, 1
 HR_F_CLOCK_OVERFLOW, HR_F_RING_OVERFLOW, HR_F_MODEL_VIOLATION = 1, 2, 4
 HR_F_BARRIER_DIVERGENCE, HR_F_UNMONITORED = 8, 16
-HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT = 1, 2
+HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING = 1, 2, 4
 EXPORTS = ("hr_init", "hr_set_shard", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
-           "hr_replay_trace_host", "hr_report", "hr_reset_report", "hr_counters", "hr_fsm_table",
+           "hr_replay_trace_host", "hr_report", "hr_reset_report", "hr_counters", "hr_replay_timing",
+           "hr_fsm_table",
            "hr_device_view", "hr_last_error", "hr_destroy")
 
 
@@ -58,7 +59,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = os.environ.get("HIRACE_LIB", _build.LIB)   # variant builds for A/B measurements
     if not os.path.exists(path):
         if not build_if_missing:
             raise ImportError(f"{path} missing: run __graft_entry__.build()")
@@ -76,6 +77,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
         "hr_counters": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
+        "hr_replay_timing": ([vp, P(ctypes.c_double), P(ctypes.c_uint64), P(ctypes.c_double),
+                              P(ctypes.c_uint64)], ctypes.c_int),
         "hr_fsm_table": ([P(ctypes.c_uint8), P(ctypes.c_uint8)], ctypes.c_int),
         "hr_device_view": ([vp, vp, ctypes.c_size_t], ctypes.c_int),
         "hr_last_error": ([vp], ctypes.c_char_p),
@@ -141,24 +144,36 @@ class Race(NamedTuple):
     scope: int
 
 
-def hr_report(ctx, cap: int = 1 << 16) -> Tuple[List[Race], int, np.ndarray]:
-    """(sorted unique races as (kernel, space, block, word, scope), flags, raw records)."""
+RACE_DTYPE = np.dtype([("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("first_tid", "<u4"),
+                       ("space", "u1"), ("scope", "u1"), ("first_kind", "u1"), ("prev_state", "u1")])
+assert RACE_DTYPE.itemsize == 24
+
+
+def hr_report_raw(ctx, cap: int = 1 << 17) -> Tuple[np.ndarray, int]:
+    """(sorted unique race records as a structured array of hr_race, flags)."""
     lib = load()
     while True:
-        buf = (HrRace * cap)()
+        buf = np.empty(cap, dtype=RACE_DTYPE)
         n = ctypes.c_size_t(0)
         fl = ctypes.c_uint32(0)
-        rc = lib.hr_report(ctx, buf, cap, ctypes.byref(n), ctypes.byref(fl))
+        rc = lib.hr_report(ctx, buf.ctypes.data_as(ctypes.POINTER(HrRace)), cap, ctypes.byref(n),
+                           ctypes.byref(fl))
         if rc == HR_E_ARG and n.value > cap:
             cap = int(n.value)
             continue
         _check(rc, ctx, "hr_report")
-        raw = np.frombuffer(bytes(buf)[: 24 * n.value], dtype=np.dtype([
-            ("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("first_tid", "<u4"), ("space", "u1"),
-            ("scope", "u1"), ("first_kind", "u1"), ("prev_state", "u1")]))
-        races = [Race(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
-                 for r in raw]
-        return races, int(fl.value), raw
+        return buf[: n.value], int(fl.value)
+
+
+def races_of(raw: np.ndarray) -> List[Race]:
+    return [Race(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+            for r in raw]
+
+
+def hr_report(ctx, cap: int = 1 << 17) -> Tuple[List[Race], int, np.ndarray]:
+    """(sorted unique races as (kernel, space, block, word, scope), flags, raw records)."""
+    raw, flags = hr_report_raw(ctx, cap)
+    return races_of(raw), flags, raw
 
 
 def hr_reset_report(ctx):
@@ -169,6 +184,14 @@ def hr_counters(ctx) -> List[int]:
     out = (ctypes.c_uint64 * 4)()
     _check(load().hr_counters(ctx, out), ctx, "hr_counters")
     return list(out)
+
+
+def hr_replay_timing(ctx) -> Tuple[float, int, float, int]:
+    """(reset ms, resets, kernel ms, kernels) since the last call (HR_OPT_TIMING)."""
+    a, b, c, d = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_double(), ctypes.c_uint64()
+    _check(load().hr_replay_timing(ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
+           ctx, "hr_replay_timing")
+    return a.value, int(b.value), c.value, int(d.value)
 
 
 def hr_fsm_table() -> Tuple[bytes, bytes]:
@@ -257,6 +280,9 @@ class Checker:
 
     def report(self):
         return hr_report(self.ctx)
+
+    def report_raw(self):
+        return hr_report_raw(self.ctx)
 
     def reset(self):
         hr_reset_report(self.ctx)

@@ -1,0 +1,20 @@
+"""Profiling driver: generate C5 at 2^lb blocks in HBM and replay it `reps` times
+(so ncu can capture a warm launch).  Not a bench: numbers printed here under a
+profiler are never reported."""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2401_04701_b200 import hirace as hr
+from tracegen import c5
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--lb", type=int, default=12)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--options", type=int, default=0)
+a = ap.parse_args()
+rec, woff, kd = c5.gpu_trace(a.lb)
+dt = hr.DeviceTrace(rec, woff, kd)
+ck = hr.Checker(c5.total_words(a.lb), 0, options=a.options | hr.HR_OPT_TIMING, ring_capacity=1 << 21)
+for i in range(a.reps):
+    ck.reset(); ck.replay(dt); raw, fl = ck.report_raw()
+print("races", len(raw), "flags", fl, "timing", hr.hr_replay_timing(ck.ctx))

@@ -127,6 +127,37 @@ def test_insensitive_flags():
         assert not FLAGS[CODE[n]] & (G.FLAG_INSENSITIVE | G.FLAG_BLOCK_ONLY)
 
 
+def test_stale_probe_exit_is_safe():
+    """hr_device.cuh takes the insensitive exit on a possibly stale L1 value:
+    valid iff every state reachable from it is also a no-op for that kind."""
+    def reach(c):
+        seen, st = {c}, [c]
+        while st:
+            x = st.pop()
+            for m in range(3):
+                for s in range(3):
+                    for t in range(4):
+                        if G.feasible(s, t):
+                            y = TABLE[(x << 6) | (m << 4) | (s << 2) | t]
+                            if y not in seen:
+                                seen.add(y)
+                                st.append(y)
+        return seen
+    n = 0
+    for c in MC.codes():
+        if not FLAGS[c] & G.FLAG_INSENSITIVE:
+            continue
+        for m in range(3):
+            if TABLE[(c << 6) | (m << 4)] != c:
+                continue
+            for y in reach(c):
+                assert FLAGS[y] & G.FLAG_INSENSITIVE
+                assert all(TABLE[(y << 6) | (m << 4) | (s << 2) | t] == y
+                           for s in range(3) for t in range(4) if G.feasible(s, t))
+            n += 1
+    assert n >= 3
+
+
 def _differential(table, programs, cap=2000):
     """For every address and every HB-consistent commit order: Algorithm 1 over
     ``table`` ends in RACE (with the oracle's scope) iff the oracle says racy.
