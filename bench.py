@@ -197,28 +197,6 @@ def run_reference(args):
     }), flush=True)
 
 
-def exchange(races_raw, world):
-    """Race-set allgather over NCCL (the one exchange step)."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    n = len(races_raw)
-    cnt = torch.tensor([n], dtype=torch.int64, device="cuda")
-    cnts = torch.empty(world, dtype=torch.int64, device="cuda")
-    dist.all_gather_into_tensor(cnts, cnt)
-    mx = int(cnts.max().item())
-    pad = torch.zeros(max(mx, 1) * 3, dtype=torch.int64, device="cuda")
-    if n:
-        pad[: n * 3] = torch.from_numpy(np.ascontiguousarray(races_raw).view(np.int64).copy()).cuda()
-    out = torch.empty(world * pad.numel(), dtype=torch.int64, device="cuda")
-    dist.all_gather_into_tensor(out, pad)
-    host = out.view(world, -1).cpu().numpy()
-    parts = [host[r, : int(cnts[r]) * 3].view(races_raw.dtype) for r in range(world)]
-    merged = np.concatenate(parts) if parts else races_raw
-    order = np.lexsort((merged["word"], merged["block"], merged["space"], merged["kernel"]))
-    return merged[order]
-
-
 def main():
     args = parse()
     if args.impl == "reference":
@@ -227,6 +205,7 @@ def main():
     import numpy as np
     import torch
     from paper_2401_04701_b200 import hirace as hr
+    from paper_2401_04701_b200.multigpu import exchange_races
     from tracegen import c5
 
     rank, world, local = dist_setup(args)
@@ -251,7 +230,7 @@ def main():
         replay_fn()
         raw, flags = ck.report_raw()
         if world > 1:
-            raw = exchange(raw, world)
+            raw, flags = exchange_races(raw, flags)
         return raw, flags
 
     dev_replay = lambda: ck.replay(dt, stream)  # noqa: E731

@@ -1,0 +1,119 @@
+"""Address-sharded multi-GPU replay.
+
+Accesses to different words are independent FSMs (the shadow is per word,
+PAPER.md:395-396; no transition reads another word), so rank r of N owns the
+4 KiB shadow granules with ((word - base) >> 9) % N == r and the shared
+instances of simulated blocks with block % N == r.  Each rank replays every
+simulated thread but only its own records, keeping all barrier records so the
+per-word commit order stays happens-before consistent; its shadow is 1/N.
+The ONE exchange is the race-set allgather (NCCL over NVLink on GPUs, gloo
+in the CPU tests) followed by a concatenate-and-sort merge — shards are
+address-disjoint, so no de-duplication is needed.
+
+torch.distributed provides the process group only; the check runs in
+libhirace.so.
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import numpy as np
+
+RACE_DTYPE = np.dtype([("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("first_tid", "<u4"),
+                       ("space", "u1"), ("scope", "u1"), ("first_kind", "u1"), ("prev_state", "u1")])
+NOP = np.uint64(3 << 62)
+
+
+def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: int = 0) -> np.ndarray:
+    """Which records of one warp's rows (n, 32) belong to shard `rank`."""
+    op = rows >> np.uint64(62)
+    space = (rows >> np.uint64(61)) & np.uint64(1)
+    word = rows & np.uint64((1 << 61) - 1)
+    gran = (word - np.uint64(base_word)) >> np.uint64(9)
+    glob = (op != 3) & (space == 0) & ((gran % np.uint64(nshard)) == np.uint64(rank))
+    shared = (op != 3) & (space == 1) & ((block % nshard) == rank)
+    return glob | shared
+
+
+def shard_trace(trace, rank: int, nshard: int, base_word: int = 0):
+    """Host-side shard of a trace: this rank's records compacted per lane inside
+    each barrier-delimited segment, padded with NOPs, barrier rows kept."""
+    from tracegen.format import Trace   # layout container only
+    if nshard == 1:
+        return trace
+    out_rows, offs, kd = [], [], trace.kdesc.copy()
+    row = 0
+    for k in range(trace.kdesc.shape[0]):
+        blocks, warps = int(trace.kdesc[k, 0]), int(trace.kdesc[k, 1])
+        woi = int(trace.kdesc[k, 4])
+        kd[k, 4] = len(offs)
+        for w in range(blocks * warps):
+            r0, r1 = int(trace.warp_off[woi + w]), int(trace.warp_off[woi + w + 1])
+            rows = trace.rec[r0 * 32: r1 * 32].reshape(-1, 32)
+            keep = owner_mask(rows, w // warps, rank, nshard, base_word)
+            op = rows >> np.uint64(62)
+            word = rows & np.uint64((1 << 61) - 1)
+            is_bar = np.any((op == 3) & (word != 0), axis=1)
+            offs.append(row)
+            seg_start = 0
+            for i in list(np.nonzero(is_bar)[0]) + [rows.shape[0]]:
+                seg = rows[seg_start:i]
+                km = keep[seg_start:i]
+                depth = int(km.sum(axis=0).max()) if seg.shape[0] else 0
+                if depth:
+                    out = np.full((depth, 32), NOP, dtype=np.uint64)
+                    for lane in range(32):
+                        v = seg[km[:, lane], lane]
+                        out[: v.shape[0], lane] = v
+                    out_rows.append(out)
+                    row += depth
+                if i < rows.shape[0]:
+                    out_rows.append(rows[i: i + 1])
+                    row += 1
+                seg_start = i + 1
+        offs.append(row)                 # end of the kernel's last warp (nw + 1 entries)
+    rec = np.concatenate([r.reshape(-1) for r in out_rows]) if out_rows else np.zeros(0, np.uint64)
+    return Trace(np.ascontiguousarray(rec, dtype=np.uint64), kd, np.array(offs, dtype=np.uint64))
+
+
+def exchange_races(raw: np.ndarray, flags: int = 0, group=None, device=None) -> Tuple[np.ndarray, int]:
+    """Allgather the per-rank race sets and merge: (sorted global set, OR of flags).
+    Identical on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = device if device is not None else ("cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    meta = torch.tensor([len(raw), flags], dtype=torch.int64, device=dev)
+    metas = [torch.empty_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta, group=group)
+    counts = [int(m[0].item()) for m in metas]
+    all_flags = 0
+    for m in metas:
+        all_flags |= int(m[1].item())
+    mx = max(max(counts), 1)
+    pad = torch.zeros(mx * 3, dtype=torch.int64, device=dev)
+    if len(raw):
+        pad[: len(raw) * 3] = torch.from_numpy(np.ascontiguousarray(raw).view(np.int64).copy()).to(dev)
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    merged = np.concatenate([p.cpu().numpy()[: c * 3].view(RACE_DTYPE) for p, c in zip(parts, counts)])
+    order = np.lexsort((merged["word"], merged["block"], merged["space"], merged["kernel"]))
+    return merged[order], all_flags
+
+
+def replay_sharded(trace, group=None, device: Optional[int] = None, base_word: int = 0, **checker_kw):
+    """Replay a host trace address-sharded over the ranks of `group` (one GPU per
+    rank) and return the global sorted race set (hr_race records) and flags."""
+    import torch
+    import torch.distributed as dist
+    from . import hirace
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.cuda.current_device() if device is None else device
+    gmax, smem = hirace.trace_extent(trace)
+    local = shard_trace(trace, rank, world, base_word)
+    ck = hirace.Checker(gmax - base_word, smem, base_word=base_word, device=dev, shard=(rank, world),
+                        **checker_kw)
+    ck.replay(hirace.DeviceTrace.from_trace(local, device=f"cuda:{dev}"))
+    raw, flags = ck.report_raw()
+    ck.close()
+    return exchange_races(raw, flags, group)
