@@ -117,3 +117,17 @@ def run_word(table: bytes, commits: List[Tuple]) -> Tuple[int, List[int]]:
 
 def scope_of(state: int) -> int:
     return {RACE_BLOCK: 1, RACE_GRID: 2}.get(state, 0)
+
+
+def filter_trace_words(trace, words, space: int = 0):
+    """Sampled-output check support: a copy of `trace` in which every access
+    record not touching one of `words` (in `space`) becomes a NOP; barrier rows
+    are kept, so the sampled words keep their exact access history."""
+    import numpy as np
+    rec = trace.rec.copy()
+    op = rec >> np.uint64(62)
+    sp = (rec >> np.uint64(61)) & np.uint64(1)
+    w = rec & np.uint64((1 << 61) - 1)
+    keep = (op == 3) | ((sp == space) & np.isin(w, np.asarray(sorted(words), dtype=np.uint64)))
+    rec[~keep] = np.uint64(3 << 62)
+    return type(trace)(rec, trace.kdesc.copy(), trace.warp_off.copy())
