@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--cpu-lb", type=int, default=10, help="C5 sample for the oracle cpu_baseline")
     ap.add_argument("--ref-lb", type=int, default=8, help="C5 sample per --impl reference step")
     ap.add_argument("--options", type=int, default=0, help="extra HR_OPT_* bits (ablations)")
+    ap.add_argument("--no-slowdown", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets N ranks share one GPU to test the N>1 path (timings then meaningless)")
+    ap.add_argument("--c4-lv", type=int, default=20, help="log2 vertices of the C4 graph for the slowdown")
     return ap.parse_args()
 
 
@@ -119,9 +123,13 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
+        dev = local % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -133,12 +141,17 @@ def barrier(world):
         dist.barrier()
 
 
+def _coll_device():
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(x: float, world: int) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -148,7 +161,7 @@ def sum_over_ranks(x: int, world: int) -> int:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.int64, device="cuda")
+    t = torch.tensor([x], dtype=torch.int64, device=_coll_device())
     dist.all_reduce(t)
     return int(t.item())
 
@@ -165,6 +178,44 @@ def cpu_baseline(lb: int, seed: int):
     return {"value": res.n_accesses / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"C5 shape at 2^{lb} blocks ({res.n_accesses} accesses, 1/{2 ** (16 - lb)} of the "
                       f"blocks), bucketed mode, {dt:.2f} s; racy set == planted: {ok}"}
+
+
+def measure_slowdown(dt, kern_ms_launch: float, data_words: int, c4_lv: int):
+    """Instrumented vs uninstrumented (SURVEY §8(d) "Slowdown"; paper context:
+    7.5x average / 1.08x median over Indigo).  Replay: the check
+    kernel vs hrb_raw_replay doing only the raw data accesses of the same
+    records.  Online: the same CUDA kernel template with and without hr_check_*."""
+    import torch
+    from paper_2401_04701_b200 import hirace as hr, online as on
+    from tracegen import c4
+    out = {}
+    data = torch.zeros(data_words, dtype=torch.int32, device="cuda")
+    raw_ms = on.time_ms(lambda: on.raw_replay(dt, data, data_words), reps=3, warmup=1)
+    out["c5_replay"] = {"checked_kernel_ms": kern_ms_launch, "raw_replay_ms": raw_ms,
+                        "slowdown": kern_ms_launch / raw_ms}
+    del data
+    torch.cuda.empty_cache()
+    # C1 (1 block), C3 (1024 blocks), C4 (BFS levels + histogram) online
+    d1 = torch.arange(8 * 256 + 8, dtype=torch.int32, device="cuda")
+    ck1 = hr.Checker(8 * 256 + 8, 256)
+    out["c1_online"] = on.slowdown(lambda: on.c1(None, d1, False), lambda: on.c1(ck1.ctx, d1, True), reps=20)
+    ck1.close()
+    d3 = torch.randint(0, 100, (2 * 512 * 512,), dtype=torch.int32, device="cuda")
+    ck3 = hr.Checker(2 * 512 * 512, 648)
+    out["c3_online"] = on.slowdown(lambda: on.c3(None, d3, False), lambda: on.c3(ck3.ctx, d3, True), reps=10)
+    ck3.close()
+    g = c4.Graph(c4_lv)
+    dev = on.C4Device(g)
+    d4 = torch.zeros(g.n + 1024, dtype=torch.int32, device="cuda")
+    ck4 = hr.Checker(g.n + 1024, 0, ring_capacity=1 << 24)
+    for racy in (False, True):
+        out[f"c4_online_{'racy' if racy else 'atomic'}_2^{c4_lv}"] = on.slowdown(
+            lambda: dev.run(None, d4, False, racy), lambda: dev.run(ck4.ctx, d4, True, racy), reps=5)
+    ck4.close()
+    for v in out.values():
+        for k in list(v):
+            v[k] = round(v[k], 4)
+    return out
 
 
 def run_reference(args):
@@ -242,7 +293,7 @@ def main():
     parity_ok = got == c5.planted(lb, seed) and flags == 0
     hr.hr_replay_timing(ck.ctx)                     # drop warm-up launches
 
-    clocks = Clocks(local)
+    clocks = Clocks(torch.cuda.current_device())
     barrier(world)
     torch.cuda.synchronize()
     clocks.start()
@@ -279,6 +330,10 @@ def main():
         except Exception:
             traffic = None
     literal = BYTES_PER_ACCESS_LITERAL * total_acc / (ms_step / 1e3) / 1e9 / (peak * world)
+
+    slow = None
+    if rank == 0 and world == 1 and not args.no_slowdown:
+        slow = measure_slowdown(dt, kern_ms / max(n_kern, 1), c5.total_words(lb), args.c4_lv)
 
     # --- e2e through the C ABI with HOST buffers ---
     e2e = None
@@ -337,6 +392,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": n_kern,
+            "slowdown": slow,
             "cpu_baseline": cpu,
             "parity_vs_closed_form": parity_ok,
         }

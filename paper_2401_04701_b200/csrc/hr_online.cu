@@ -1,0 +1,299 @@
+/*
+ * hr_online.cu — online-instrumented benchmark kernels (include/hr_bench.h).
+ *
+ * Each kernel is one template compiled twice: INSTR = false is the plain
+ * kernel; INSTR = true calls the device API before every monitored access and
+ * replaces __syncthreads by hr_syncthreads, as the paper's wrapper does for
+ * operator[] and the barrier primitives.  The access order
+ * per thread matches the tracegen generators record for record.
+ */
+#include <cuda_runtime.h>
+
+#include "hr.h"
+#include "hr_bench.h"
+#include "hr_device.cuh"
+
+namespace {
+
+template <bool I>
+__device__ __forceinline__ void chk(const hr_dev &d, hr_thr &t, hr_space sp, uint64_t w, int kind)
+{
+    if (I) {
+        if (kind == HR_READ) hr_check_read(d, t, sp, w);
+        else if (kind == HR_WRITE) hr_check_write(d, t, sp, w);
+        else hr_check_atomic(d, t, sp, w);
+    }
+}
+
+template <bool I>
+__device__ __forceinline__ void bar(const hr_dev &d, hr_thr &t)
+{
+    if (I) hr_syncthreads(d, t);
+    else __syncthreads();
+}
+
+/* ---- C1: tree reduction, 1 block x 32 threads ---- */
+template <bool I>
+__global__ void __launch_bounds__(32) c1_kernel(hr_dev d, int *data, int rounds, int removed)
+{
+    __shared__ int s[256];
+    __shared__ __align__(16) unsigned char fsm[HR_FSM_SMEM_BYTES];
+    __shared__ unsigned long long sh[I ? 256 : 1];
+    hr_thr t;
+    if (I) t = hr_thread_begin(d, fsm, sh, 256);
+    const int lane = threadIdx.x;
+    const int out = rounds * 256;
+    for (int r = 0; r < rounds; r++) {
+        for (int i = lane; i < 256; i += 32) {
+            chk<I>(d, t, HR_GLOBAL, r * 256 + i, HR_READ);
+            int v = data[r * 256 + i];
+            chk<I>(d, t, HR_SHARED, i, HR_WRITE);
+            s[i] = v;
+        }
+        if (removed != 0) bar<I>(d, t);
+        for (int st = 128; st >= 1; st >>= 1) {
+            for (int i = lane; i < st; i += 32) {
+                chk<I>(d, t, HR_SHARED, i, HR_READ);
+                int a = s[i];
+                chk<I>(d, t, HR_SHARED, i + st, HR_READ);
+                int b = s[i + st];
+                chk<I>(d, t, HR_SHARED, i, HR_WRITE);
+                s[i] = a + b;
+            }
+            if (removed != st) bar<I>(d, t);
+        }
+        if (lane == 0) {
+            chk<I>(d, t, HR_SHARED, 0, HR_READ);
+            int v = s[0];
+            chk<I>(d, t, HR_GLOBAL, out + r, HR_WRITE);
+            data[out + r] = v;
+        }
+        bar<I>(d, t);
+    }
+}
+
+/* ---- C3: 2D Jacobi stencil through two SMEM tiles ---- */
+template <bool I>
+__global__ void __launch_bounds__(256) c3_kernel(hr_dev d, int *data, int n, int sweeps, int removed)
+{
+    constexpr int T = 16, H = 18, TILE = H * H;
+    __shared__ int tile[2][TILE];
+    __shared__ __align__(16) unsigned char fsm[HR_FSM_SMEM_BYTES];
+    __shared__ unsigned long long sh[I ? 2 * TILE : 1];
+    hr_thr t;
+    if (I) t = hr_thread_begin(d, fsm, sh, 2 * TILE);
+    const int ltid = threadIdx.x, ty = ltid / T, tx = ltid % T;
+    const int tiles = n / T, bx = blockIdx.x % tiles, by = blockIdx.x / tiles;
+    for (int k = 0; k < 2; k++) {
+        const int cell = ltid + 256 * k;
+        if (cell < TILE) {
+            const int hy = cell / H, hx = cell % H;
+            const int gy = min(max(by * T + hy - 1, 0), n - 1), gx = min(max(bx * T + hx - 1, 0), n - 1);
+            chk<I>(d, t, HR_GLOBAL, (uint64_t)gy * n + gx, HR_READ);
+            int v = data[gy * n + gx];
+            chk<I>(d, t, HR_SHARED, cell, HR_WRITE);
+            tile[0][cell] = v;
+        }
+    }
+    bar<I>(d, t);
+    int src = 0, dst = 1;
+    const int c = (ty + 1) * H + (tx + 1);
+    for (int s = 0; s < sweeps; s++) {
+        const int offs[5] = {0, -H, H, -1, 1};
+        int acc = 0;
+#pragma unroll
+        for (int o = 0; o < 5; o++) {
+            chk<I>(d, t, HR_SHARED, src * TILE + c + offs[o], HR_READ);
+            acc += tile[src][c + offs[o]];
+        }
+        chk<I>(d, t, HR_SHARED, dst * TILE + c, HR_WRITE);
+        tile[dst][c] = acc / 5;
+        if (s != removed) bar<I>(d, t);
+        src ^= 1;
+        dst ^= 1;
+    }
+    const int gy = by * T + ty, gx = bx * T + tx;
+    chk<I>(d, t, HR_SHARED, src * TILE + c, HR_READ);
+    int v = tile[src][c];
+    chk<I>(d, t, HR_GLOBAL, (uint64_t)n * n + (uint64_t)gy * n + gx, HR_WRITE);
+    data[n * n + gy * n + gx] = v;
+}
+
+/* ---- C4: BFS level step and degree histogram, thread per vertex ---- */
+template <bool I>
+__global__ void __launch_bounds__(256) c4_level_kernel(hr_dev d, int *data, uint32_t n, const uint64_t *rp,
+                                                       const uint32_t *col, const int *flevel, int L, int racy)
+{
+    __shared__ __align__(16) unsigned char fsm[HR_FSM_SMEM_BYTES];
+    __shared__ unsigned long long sh[1];
+    hr_thr t;
+    if (I) t = hr_thread_begin(d, fsm, sh, 0);
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    if (racy) {
+        chk<I>(d, t, HR_GLOBAL, v, HR_READ);
+        volatile int lv = data[v];
+        (void)lv;
+    } else {
+        chk<I>(d, t, HR_GLOBAL, v, HR_ATOMIC);
+        atomicOr(&data[v], 0);
+    }
+    if (flevel[v] != L) return;
+    for (uint64_t k = rp[v]; k < rp[v + 1]; k++) {
+        const uint32_t x = col[k];
+        if (racy) {
+            chk<I>(d, t, HR_GLOBAL, x, HR_READ);
+            volatile int lx = data[x];
+            (void)lx;
+            if (flevel[x] == L + 1) {
+                chk<I>(d, t, HR_GLOBAL, x, HR_WRITE);
+                data[x] = L + 1;
+            }
+        } else {
+            chk<I>(d, t, HR_GLOBAL, x, HR_ATOMIC);
+            atomicMin(&data[x], L + 1);
+        }
+    }
+}
+
+template <bool I>
+__global__ void __launch_bounds__(256) c4_hist_kernel(hr_dev d, int *data, uint32_t n, const uint64_t *rp,
+                                                      int racy)
+{
+    __shared__ __align__(16) unsigned char fsm[HR_FSM_SMEM_BYTES];
+    __shared__ unsigned long long sh[1];
+    hr_thr t;
+    if (I) t = hr_thread_begin(d, fsm, sh, 0);
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const uint64_t deg = rp[v + 1] - rp[v];
+    const uint64_t bin = n + (deg < 1023 ? deg : 1023);
+    if (racy) {
+        chk<I>(d, t, HR_GLOBAL, bin, HR_READ);
+        int h = data[bin];
+        chk<I>(d, t, HR_GLOBAL, bin, HR_WRITE);
+        data[bin] = h + 1;
+    } else {
+        chk<I>(d, t, HR_GLOBAL, bin, HR_ATOMIC);
+        atomicAdd(&data[bin], 1);
+    }
+}
+
+/* ---- uninstrumented replay: the same record walk and barriers as
+ * hr_replay_kernel, but each access is the raw data access (4-byte word) ---- */
+__global__ void __launch_bounds__(1024, 2) raw_replay_kernel(const uint64_t *__restrict__ rec,
+                                                             const uint64_t *__restrict__ woff, uint32_t warps,
+                                                             uint32_t lanes, int *data, uint64_t data_words)
+{
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t gw = (uint64_t)blockIdx.x * warps + warp;
+    const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
+    const bool active = lane < lanes;
+    const uint64_t *p = rec + r0 * 32 + lane;
+    const uint64_t n = r1 - r0;
+    uint64_t x1 = (active && n > 0) ? __ldcs((const unsigned long long *)p) : (3ull << 62);
+    uint64_t x2 = (active && n > 1) ? __ldcs((const unsigned long long *)(p + 32)) : (3ull << 62);
+    int acc = 0;
+    for (uint64_t i = 0; i < n; i++) {
+        const uint64_t x = x1;
+        x1 = x2;
+        x2 = (active && i + 2 < n) ? __ldcs((const unsigned long long *)(p + 32 * (i + 2))) : (3ull << 62);
+        const uint32_t op = (uint32_t)(x >> 62);
+        const uint64_t w = x & HR_WORD_MASK;
+        const unsigned st = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
+        const unsigned sw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
+        if (st) { __syncthreads(); continue; }
+        if (sw) { __syncwarp(); continue; }
+        if (op == 3u || ((x >> 61) & 1u) || w >= data_words) continue;   /* shared words: not modelled */
+        if (op == 0u) acc += __ldcg(&data[w]);
+        else if (op == 1u) data[w] = (int)i;
+        else atomicAdd(&data[w], 1);
+    }
+    if (acc == 0x7fffffff) data[0] = acc;
+}
+
+hr_status prepare(hr_ctx *ctx, int instrumented, uint32_t kernel_id, void *stream, hr_dev *d)
+{
+    memset(d, 0, sizeof *d);
+    if (!instrumented) return HR_OK;
+    if (!ctx) return HR_E_ARG;
+    hr_status st = hr_device_view(ctx, d, sizeof *d);
+    if (st) return st;
+    d->kernel_id = kernel_id;
+    return hr_kernel_begin(ctx, stream);          /* kernel boundary: fresh global shadow */
+}
+
+hr_status launched()
+{
+    return cudaGetLastError() == cudaSuccess ? HR_OK : HR_E_CUDA;
+}
+
+}  // namespace
+
+extern "C" hr_status hrb_raw_replay(const hr_trace *t, int *data, uint64_t data_words, void *stream)
+{
+    if (!t) return HR_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        if (kd[0] == 0) continue;
+        raw_replay_kernel<<<(unsigned)kd[0], (unsigned)(kd[1] * 32), 0, s>>>(t->rec, t->warp_off + kd[4],
+                                                                             (uint32_t)kd[1], (uint32_t)kd[2],
+                                                                             data, data_words);
+        if (cudaGetLastError() != cudaSuccess) return HR_E_CUDA;
+    }
+    return HR_OK;
+}
+
+extern "C" hr_status hrb_c1(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int rounds, int removed, int *data,
+                            void *stream)
+{
+    hr_dev d;
+    hr_status st = prepare(ctx, instrumented, kernel_id, stream, &d);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (instrumented) c1_kernel<true><<<1, 32, 0, s>>>(d, data, rounds, removed);
+    else c1_kernel<false><<<1, 32, 0, s>>>(d, data, rounds, removed);
+    return launched();
+}
+
+extern "C" hr_status hrb_c3(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int n, int sweeps, int removed,
+                            int *data, void *stream)
+{
+    if (n % 16) return HR_E_ARG;
+    hr_dev d;
+    hr_status st = prepare(ctx, instrumented, kernel_id, stream, &d);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned blocks = (unsigned)((n / 16) * (n / 16));
+    if (instrumented) c3_kernel<true><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
+    else c3_kernel<false><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
+    return launched();
+}
+
+extern "C" hr_status hrb_c4_level(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int racy, uint32_t n,
+                                  const uint64_t *rp, const uint32_t *col, const int *flevel, int level, int *data,
+                                  void *stream)
+{
+    hr_dev d;
+    hr_status st = prepare(ctx, instrumented, kernel_id, stream, &d);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned blocks = (n + 255) / 256;
+    if (instrumented) c4_level_kernel<true><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
+    else c4_level_kernel<false><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
+    return launched();
+}
+
+extern "C" hr_status hrb_c4_hist(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int racy, uint32_t n,
+                                 const uint64_t *rp, int *data, void *stream)
+{
+    hr_dev d;
+    hr_status st = prepare(ctx, instrumented, kernel_id, stream, &d);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned blocks = (n + 255) / 256;
+    if (instrumented) c4_hist_kernel<true><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
+    else c4_hist_kernel<false><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
+    return launched();
+}

@@ -128,6 +128,10 @@ def filter_trace_words(trace, words, space: int = 0):
     op = rec >> np.uint64(62)
     sp = (rec >> np.uint64(61)) & np.uint64(1)
     w = rec & np.uint64((1 << 61) - 1)
-    keep = (op == 3) | ((sp == space) & np.isin(w, np.asarray(sorted(words), dtype=np.uint64)))
+    ws = np.asarray(sorted(words), dtype=np.int64)
+    table = np.zeros(int(ws.max()) + 2, dtype=bool)        # O(n) lookup, not np.isin's O(n*k)
+    table[ws] = True
+    idx = np.minimum(w, np.uint64(table.shape[0] - 1)).astype(np.int64)
+    keep = (op == 3) | ((sp == space) & table[idx] & (w < np.uint64(table.shape[0] - 1)))
     rec[~keep] = np.uint64(3 << 62)
     return type(trace)(rec, trace.kdesc.copy(), trace.warp_off.copy())

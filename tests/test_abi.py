@@ -13,9 +13,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_functions():
-    src = open(os.path.join(ROOT, "include", "hr.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(hr_[a-z_0-9]+)\s*\(", src)))
+    names = set()
+    for h in ("hr.h", "hr_bench.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(hrb?_[a-z_0-9]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_library_builds_and_exports_every_declared_symbol():
@@ -24,7 +27,8 @@ def test_library_builds_and_exports_every_declared_symbol():
     assert len(names) >= 12
     for n in names:
         assert hasattr(lib, n), n
-    assert set(names) == set(hirace.EXPORTS)
+    from paper_2401_04701_b200 import online
+    assert set(names) == set(hirace.EXPORTS) | set(online.EXPORTS)
 
 
 def test_compiled_table_matches_generator():

@@ -36,6 +36,7 @@ def _load():
         _lib.c4_stats.argtypes = [vp, vp]
         _lib.c4_sizes.argtypes = [vp, ctypes.c_int, ctypes.POINTER(u64), ctypes.POINTER(u32), ctypes.POINTER(u64)]
         _lib.c4_fill.argtypes = [vp, ctypes.c_int, vp, vp, vp]
+        _lib.c4_export.argtypes = [vp, vp, vp, vp]
     return _lib
 
 
@@ -55,6 +56,14 @@ class Graph:
         wo = np.empty(nw.value, dtype=np.uint64)
         self.lib.c4_fill(self.h, int(racy), rec.ctypes.data, kd.ctypes.data, wo.ctypes.data)
         return Trace(rec, kd, wo)
+
+    def csr(self):
+        """(row_ptr uint64[n+1], col uint32[m], final BFS level int32[n], -1 = unreached)."""
+        rp = np.empty(self.n + 1, dtype=np.uint64)
+        col = np.empty(self.m, dtype=np.uint32)
+        lvl = np.empty(self.n, dtype=np.int32)
+        self.lib.c4_export(self.h, rp.ctypes.data, col.ctypes.data, lvl.ctypes.data)
+        return rp, col, lvl
 
     def close(self):
         if self.h:

@@ -200,3 +200,12 @@ void c4_fill(void *h, int racy, uint64_t *rec, uint64_t *kdesc, uint64_t *woff)
         woff[wo++] = row;
     }
 }
+
+/* CSR and final BFS levels, for the online-instrumented kernels */
+void c4_export(void *h, uint64_t *rp, uint32_t *col, int32_t *level)
+{
+    c4_graph *g = (c4_graph *)h;
+    if (rp) memcpy(rp, g->rp, ((size_t)g->n + 1) * 8);
+    if (col) memcpy(col, g->col, g->m * 4);
+    if (level) memcpy(level, g->level, (size_t)g->n * 4);
+}
