@@ -283,6 +283,38 @@ static bool race_less(const hr_race &a, const hr_race &b)
     return a.word < b.word;
 }
 
+/* Sort race records by (kernel, space, block, word): LSD radix sort on a
+ * 128-bit key (hi = kernel | space | block, lo = word), 16-bit digits, digits
+ * that are constant across the input skipped.  O(n) per live digit. */
+static void sort_races(std::vector<hr_race> &v)
+{
+    const size_t n = v.size();
+    if (n < 2) return;
+    struct K { uint64_t hi, lo; uint32_t idx; };
+    std::vector<K> a(n), b(n);
+    for (size_t i = 0; i < n; i++) {
+        a[i].hi = ((uint64_t)v[i].kernel << 33) | ((uint64_t)v[i].space << 32) | (uint64_t)v[i].block;
+        a[i].lo = v[i].word;
+        a[i].idx = (uint32_t)i;
+    }
+    std::vector<size_t> cnt(65536);
+    for (int d = 0; d < 8; d++) {
+        const bool hi = d >= 4;
+        const int sh = 16 * (d & 3);
+        auto dig = [&](const K &k) { return (size_t)(((hi ? k.hi : k.lo) >> sh) & 0xffff); };
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (size_t i = 0; i < n; i++) cnt[dig(a[i])]++;
+        if (cnt[dig(a[0])] == n) continue;             /* constant digit */
+        size_t acc = 0;
+        for (size_t j = 0; j < 65536; j++) { size_t t = cnt[j]; cnt[j] = acc; acc += t; }
+        for (size_t i = 0; i < n; i++) b[cnt[dig(a[i])]++] = a[i];
+        a.swap(b);
+    }
+    std::vector<hr_race> out(n);
+    for (size_t i = 0; i < n; i++) out[i] = v[a[i].idx];
+    v.swap(out);
+}
+
 extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out)
 {
     if (!c || !n_out || (cap && !out)) return fail(c, HR_E_ARG, "hr_report: bad arguments");
@@ -311,7 +343,7 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         if (cnt) CU(cudaMemcpy(v.data() + off, tmp, cnt * sizeof(hr_race), cudaMemcpyDeviceToHost));
         cudaFree(tmp);
     }
-    std::sort(v.begin(), v.end(), race_less);
+    sort_races(v);
     size_t m = 0;
     for (size_t i = 0; i < v.size(); i++) {
         if (m && !race_less(v[m - 1], v[i]) && !race_less(v[i], v[m - 1])) {
