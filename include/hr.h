@@ -72,7 +72,9 @@ enum {
     HR_OPT_NO_COALESCE = 1u,   /* disable same-address lane coalescing (a3), for ablations */
     HR_OPT_NO_FASTEXIT = 2u,   /* disable label-insensitive fast exits (a7), for ablations */
     HR_OPT_TIMING = 4u,        /* record CUDA events around every shadow reset and replay launch */
-    HR_OPT_NO_SPECULATE = 8u   /* first attempt loads the shadow word instead of speculating INIT */
+    HR_OPT_NO_SPECULATE = 8u,  /* first attempt loads the shadow word instead of speculating INIT */
+    HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen by sampled record density) */
+    HR_OPT_POOL = 32u          /* replay with warp pools of valid accesses (sparse traces) */
 };
 
 /* One unique racy address.  24 bytes.

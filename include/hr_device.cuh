@@ -158,8 +158,152 @@ __device__ __forceinline__ unsigned long long hr__ld_g_l1(const unsigned long lo
     return v;
 }
 
-/* emit-info word (one register instead of a 24-byte record) */
+/* emit-info word (one register instead of a 24-byte record):
+ * [31] emit  [30:26] racing lane  [25:24] its kind  [23:19] prev state  [0] grid */
 #define HR_EI_EMIT 0x80000000u
+/* first-attempt provenance of `old`: guess (INIT), weak L1 probe, coherent */
+#define HR_OLD_GUESS 0u
+#define HR_OLD_PROBE 1u
+#define HR_OLD_FRESH 2u
+
+/* a2: shard-local shadow index; false if this ctx does not check the access. */
+__device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uint32_t space, uint64_t word,
+                                           uint64_t &local)
+{
+    if (space != 0u) {
+        if (word >= t.swords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
+        local = word;
+        return ((t.tid >> 10) & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
+    }
+    const uint64_t g = word - d.gbase;
+    if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
+    const uint64_t gran = g >> 9;
+    local = ((gran >> d.shard_log2) << 9) | (g & 511u);
+    return ((uint32_t)gran & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
+}
+
+/* a5 + a6 (+ a3 fold): the state after this lane's access from `old`, then the
+ * accesses of the other lanes of `peers` (kinds in kb0/kb1) in lane order with
+ * label (kind_j, Us, Warp).  rinfo receives the first RACE entry, rel the
+ * relation of the first label. */
+__device__ __forceinline__ uint32_t hr__transition(const hr_dev &d, const hr_thr &t, unsigned long long old,
+                                                   uint32_t kind, uint32_t lane, unsigned peers, unsigned kb0,
+                                                   unsigned kb1, uint32_t &rinfo, uint32_t &rel)
+{
+    const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+    rel = hr__rel(t.tid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+    const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
+    uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
+    rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19)) : 0u;
+    unsigned r = peers & ~(1u << lane);
+    while (r) {
+        const uint32_t j = __ffs(r) - 1;
+        r &= r - 1;
+        const uint32_t kj = ((kb0 >> j) & 1u) | (((kb1 >> j) & 1u) << 1);
+        const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | 1u));
+        if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
+            rinfo = HR_EI_EMIT | (j << 26) | (kj << 24) | (cur << 19);
+        cur = nx;
+    }
+    return cur;
+}
+
+__device__ __forceinline__ unsigned long long hr__nmeta(const hr_thr &t, unsigned peers)
+{
+    const uint32_t last_lane = 31u - __clz(peers);
+    return (t.meta & ~(0x1full << HR_TID_SHIFT)) | ((unsigned long long)last_lane << HR_TID_SHIFT);
+}
+
+/* a7 + a8: Algorithm 1's repeat/until loop from a first value `old` of the
+ * given provenance; returns the emit info of the committed transition (0 if
+ * none or a fast exit). */
+__device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t, bool is_shared, uint32_t sh_addr,
+                                               unsigned long long *gp, unsigned long long old, uint32_t fresh,
+                                               uint32_t kind, uint32_t lane, unsigned peers, unsigned kb0,
+                                               unsigned kb1)
+{
+    const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
+    const unsigned long long nmeta = hr__nmeta(t, peers);
+    while (true) {
+        const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+        uint32_t rinfo, rel;
+        const uint32_t cur = hr__transition(d, t, old, kind, lane, peers, kb0, kb1, rinfo, rel);
+        const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
+        if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
+            const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
+            if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+                return 0u;                                                /* a7 (ii), (iii) */
+        }
+        if (nw == old) {
+            if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
+            if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
+        }
+        const unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+        if (prev == old)                                                  /* a8 committed */
+            return rinfo ? (rinfo | (cur == HR_RACE_GRID ? 1u : 0u)) : 0u;
+        old = prev;
+        fresh = HR_OLD_FRESH;
+#ifdef HR_COUNTERS
+        atomicAdd(&d.counters[1], 1ull);
+#endif
+    }
+}
+
+/* First value of Algorithm 1's loop (a4): SMEM load; L1 probe for global
+ * atomics; INIT guess for global reads/writes (the CAS then doubles as the
+ * atomic read); a coherent load with HR_OPT_NO_SPECULATE. */
+__device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, bool is_shared, uint32_t sh_addr,
+                                                        const unsigned long long *gp, uint32_t kind, uint32_t &fresh)
+{
+    if (is_shared) { fresh = HR_OLD_FRESH; return hr__ld_s(sh_addr); }
+    if (kind == HR_ATOMIC && !(d.options & HR_OPT_NO_FASTEXIT)) { fresh = HR_OLD_PROBE; return hr__ld_g_l1(gp); }
+    if (d.options & HR_OPT_NO_SPECULATE) { fresh = HR_OLD_FRESH; return hr__ld_g(gp); }
+    fresh = HR_OLD_GUESS;
+    return 0ull;
+}
+
+__device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t, uint32_t slot, uint32_t space,
+                                               uint64_t word, uint32_t ei)
+{
+    if (slot < d.ring_cap) {
+        hr_race rr;
+        rr.word = word;
+        rr.block = space ? (t.tid >> 10) : 0xffffffffu;
+        rr.kernel = d.kernel_id;
+        rr.first_tid = (t.tid & ~31u) | ((ei >> 26) & 31u);
+        rr.space = (uint8_t)space;
+        rr.scope = (uint8_t)((ei & 1u) ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
+        rr.first_kind = (uint8_t)((ei >> 24) & 3u);
+        rr.prev_state = (uint8_t)((ei >> 19) & 31u);
+        d.ring[slot] = rr;
+    } else {
+        hr__set_flag(d, HR_F_RING_OVERFLOW);
+    }
+}
+
+/* a3 grouping of one row: peers (lanes with the same key, lowest = leader) and
+ * the kind bits for the fold.  Pre-test: strictly increasing keys over the full
+ * warp means all distinct, and MATCH is skipped. */
+template <bool ONLINE>
+__device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, unsigned mask, uint32_t lane,
+                                              uint64_t key, uint32_t kind, unsigned &kb0, unsigned &kb1)
+{
+    unsigned peers = 1u << lane;
+    kb0 = kb1 = 0;
+    if (d.options & HR_OPT_NO_COALESCE) return peers;
+    if (mask == 0xffffffffu) {
+        const unsigned long long prev = __shfl_up_sync(mask, key, 1);
+        if (__all_sync(mask, lane == 0 || key > prev)) return peers;
+    }
+    peers = __match_any_sync(mask, key);
+    if (ONLINE && __any_sync(mask, peers != (1u << lane))) {
+        const unsigned same_epoch = __match_any_sync(mask, (unsigned long long)(uint32_t)t.meta);
+        if (peers & ~same_epoch) peers = 1u << lane;
+    }
+    kb0 = __ballot_sync(mask, kind & 1u);
+    kb1 = __ballot_sync(mask, (kind >> 1) & 1u);
+    return peers;
+}
 
 /*
  * hr_check_lanes: every lane of `mask` calls it (convergent), `valid` says
@@ -169,108 +313,27 @@ __device__ __forceinline__ unsigned long long hr__ld_g_l1(const unsigned long lo
  * ONLINE=true re-checks that with a second MATCH.  Returns after every lane's
  * access is committed (the final ballot is the warp's convergence point), so a
  * lane never runs ahead of an access folded into another lane (program order).
- *
- * First attempt (a4): global reads/writes speculate INIT and issue the CAS
- * directly (one round trip for a first touch; a failed CAS returns the current
- * word, which is the atomic read of Algorithm 1); atomics probe L1 first (hot
- * GATOMIC words exit without L2 traffic); shared words are read with ld.shared.
  */
 template <bool ONLINE>
 __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t, unsigned mask, bool valid,
                                                uint32_t space, uint64_t word, uint32_t kind)
 {
     const uint32_t lane = hr__laneid();
-    valid = valid && !t.off;
-
-    /* a2: shadow address (local index inside the shard) */
     const bool is_shared = space != 0u;
     uint64_t local = 0;
-    if (valid) {
-        if (is_shared) {
-            if (word >= t.swords) { hr__set_flag(d, HR_F_UNMONITORED); valid = false; }
-            if (((t.tid >> 10) & ((1u << d.shard_log2) - 1u)) != d.shard_rank) valid = false;
-            local = word;
-        } else {
-            const uint64_t g = word - d.gbase;
-            if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); valid = false; }
-            const uint64_t gran = g >> 9;
-            if (((uint32_t)gran & ((1u << d.shard_log2) - 1u)) != d.shard_rank) valid = false;
-            local = ((gran >> d.shard_log2) << 9) | (g & 511u);
-        }
-    }
+    valid = valid && !t.off && hr__locate(d, t, space, word, local);
     /* match key: 0 = no access on this lane (filtered lanes must not alias owned words) */
     const uint64_t key = valid ? ((local << 2) | (is_shared ? 2u : 0u) | 1u) : 0ull;
+    unsigned kb0, kb1;
+    const unsigned peers = hr__group<ONLINE>(d, t, mask, lane, key, kind, kb0, kb1);
 
-    /* a3: same-address coalescing (skipped when the warp's words are consecutive) */
-    unsigned peers = 1u << lane;
-    unsigned kb0 = 0, kb1 = 0;
-    if (!(d.options & HR_OPT_NO_COALESCE)) {
-        const uint32_t first = __ffs(mask) - 1;
-        const unsigned long long k0 = __shfl_sync(mask, key, first);
-        const bool seq = !valid || key == k0 + ((unsigned long long)(lane - first) << 2);
-        if (!__all_sync(mask, seq)) {
-            peers = __match_any_sync(mask, key);
-            if (ONLINE) {
-                const unsigned same_epoch = __match_any_sync(mask, (unsigned long long)(uint32_t)t.meta);
-                if (peers & ~same_epoch) peers = 1u << lane;
-            }
-            kb0 = __ballot_sync(mask, kind & 1u);
-            kb1 = __ballot_sync(mask, (kind >> 1) & 1u);
-        }
-    }
-
-    uint32_t ei = 0;   /* [31] emit [30:26] racing lane [25:24] its kind [23:19] prev state [0] grid */
+    uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
         const uint32_t sh_addr = t.sshadow + (uint32_t)(local << 3);
         unsigned long long *gp = d.gshadow + local;
-        const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
-        const uint32_t last_lane = 31u - __clz(peers);
-        const unsigned long long nmeta = (t.meta & ~(0x1full << HR_TID_SHIFT)) |
-                                         ((unsigned long long)last_lane << HR_TID_SHIFT);
-        /* 0: value is a guess (INIT); 1: weak L1 probe; 2: coherent (L2/SMEM or CAS return) */
         uint32_t fresh;
-        unsigned long long old;
-        if (is_shared) { old = hr__ld_s(sh_addr); fresh = 2; }
-        else if (kind == HR_ATOMIC && fastexit) { old = hr__ld_g_l1(gp); fresh = 1; }
-        else if (d.options & HR_OPT_NO_SPECULATE) { old = hr__ld_g(gp); fresh = 2; }
-        else { old = 0ull; fresh = 0; }
-        while (true) {
-            const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
-            const uint32_t rel = hr__rel(t.tid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
-            const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
-            uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
-            uint32_t rinfo = (cur >= HR_RACE_BLOCK && cur != os)
-                                 ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19)) : 0u;
-            /* fold the rest of the group: (kind_j, Us, Warp) in lane order */
-            unsigned r = peers & ~(1u << lane);
-            while (r) {
-                const uint32_t j = __ffs(r) - 1;
-                r &= r - 1;
-                const uint32_t kj = ((kb0 >> j) & 1u) | (((kb1 >> j) & 1u) << 1);
-                const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | 1u));
-                if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
-                    rinfo = HR_EI_EMIT | (j << 26) | (kj << 24) | (cur << 19);
-                cur = nx;
-            }
-            const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
-            if (fastexit && cur == os && fresh) {
-                const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
-                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == 2))
-                    break;                                                /* a7 (ii), (iii) */
-            }
-            if (nw == old && fresh == 2) break;                           /* a7 (i) */
-            if (fresh == 1 && nw == old) { old = hr__ld_g(gp); fresh = 2; continue; }
-            const unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
-            if (prev == old) {                                            /* a8 committed */
-                if (rinfo) ei = rinfo | (cur == HR_RACE_GRID ? 1u : 0u);
-                break;
-            }
-            old = prev;
-            fresh = 2;
-#ifdef HR_COUNTERS
-            atomicAdd(&d.counters[1], 1ull);
-#endif
-        }
+        const unsigned long long old = hr__first(d, is_shared, sh_addr, gp, kind, fresh);
+        ei = hr__commit(d, t, is_shared, sh_addr, gp, old, fresh, kind, lane, peers, kb0, kb1);
     }
 
     /* a9: warp-aggregated ring append; also the warp's convergence point */
@@ -280,23 +343,7 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
         uint32_t base = 0;
         if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(em));
         base = __shfl_sync(mask, base, leader);
-        if (ei) {
-            const uint32_t slot = base + __popc(em & ((1u << lane) - 1u));
-            if (slot < d.ring_cap) {
-                hr_race rr;
-                rr.word = word;
-                rr.block = is_shared ? (t.tid >> 10) : 0xffffffffu;
-                rr.kernel = d.kernel_id;
-                rr.first_tid = (t.tid & ~31u) | ((ei >> 26) & 31u);
-                rr.space = (uint8_t)space;
-                rr.scope = (uint8_t)((ei & 1u) ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
-                rr.first_kind = (uint8_t)((ei >> 24) & 3u);
-                rr.prev_state = (uint8_t)((ei >> 19) & 31u);
-                d.ring[slot] = rr;
-            } else {
-                hr__set_flag(d, HR_F_RING_OVERFLOW);
-            }
-        }
+        if (ei) hr__write_race(d, t, base + __popc(em & ((1u << lane) - 1u)), space, word, ei);
     }
 }
 

@@ -34,6 +34,7 @@ struct hr_ctx {
     unsigned char *fsm = nullptr;
     uint32_t last_kernel = 0;
     bool have_kernel = false;
+    bool last_pooled = false;
     cudaStream_t stream = nullptr;
     uint64_t *stage_rec = nullptr;
     size_t stage_rec_cap = 0;
@@ -165,7 +166,7 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     if (space == HR_SHARED) {
-        if (base_word != 0 || n_words * 8 + HR_FSM_SMEM_BYTES > 227 * 1024)
+        if (base_word != 0 || n_words * 8 + HR_FSM_SMEM_BYTES + 32 * sizeof(hr_pool_smem) > 227 * 1024)
             return fail(c, HR_E_ARG, "shared shadow too large: %llu words", (unsigned long long)n_words);
         c->smem_words_max = (uint32_t)n_words;
         if (dev_region) *dev_region = nullptr;
@@ -207,9 +208,31 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
     return HR_OK;
 }
 
+/* Row or pooled replay: options force one; otherwise probe the density of
+ * access records (pooling pays when rows are mostly NOP, e.g. power-law BFS
+ * frontiers or address-sharded traces). */
+static hr_status choose_pool(hr_ctx *c, const uint64_t *rec, uint64_t n_rows, cudaStream_t s, bool *pool)
+{
+    if (c->cfg.options & HR_OPT_NO_POOL) { *pool = false; return HR_OK; }
+    if (c->cfg.options & HR_OPT_POOL) { *pool = true; return HR_OK; }
+    *pool = false;
+    if (n_rows == 0) return HR_OK;
+    hr_density_kernel<<<1, 1024, 0, s>>>(rec, n_rows, 2048, c->counters + 2);
+    CU(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    CU(cudaMemcpyAsync(h, c->counters + 2, sizeof h, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *pool = h[1] && (double)h[0] < 0.9 * (double)h[1];
+    return HR_OK;
+}
+
 static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const uint64_t *woff,
                         cudaStream_t s)
 {
+    bool pool = false;
+    hr_status pst = choose_pool(c, rec, t->n_rows, s, &pool);
+    if (pst) return pst;
+    c->last_pooled = pool;
     for (uint32_t k = 0; k < t->n_kernels; k++) {
         const uint64_t *kd = t->kdesc + 8ull * k;
         uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
@@ -226,14 +249,16 @@ static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const
         if (st) return st;
         uint32_t kid = t->kernel_base + k;
         hr_dev d = make_dev(c, kid);
-        size_t smem = HR_FSM_SMEM_BYTES + smem_words * 8;
+        size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
+        void (*kern)(hr_dev, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t) =
+            pool ? hr_replay_kernel<true> : hr_replay_kernel<false>;
         if (smem > 48 * 1024)
-            CU(cudaFuncSetAttribute(hr_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
-        hr_replay_kernel<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(
-            d, rec, woff + woi, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
+        kern<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(d, rec, woff + woi, (uint32_t)warps,
+                                                                  (uint32_t)lanes, (uint32_t)smem_words);
         CU(cudaGetLastError());
         if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
         c->last_kernel = kid;

@@ -27,17 +27,140 @@ __device__ __forceinline__ uint64_t hr__ld_rec(const uint64_t *p)
     return __ldcs(reinterpret_cast<const unsigned long long *>(p));
 }
 
-/* minBlocks = 2 at 1024 threads caps registers at 32: 64 resident warps per SM
- * whatever the simulated block size (occupancy is the latency-hiding lever). */
-#ifndef HR_MIN_BLOCKS
-#define HR_MIN_BLOCKS 2
-#endif
-__global__ void __launch_bounds__(1024, HR_MIN_BLOCKS) hr_replay_kernel(hr_dev d, const uint64_t *__restrict__ rec,
-                                                            const uint64_t *__restrict__ woff, uint32_t warps,
-                                                            uint32_t lanes, uint32_t smem_words)
+/*
+ * Pooled replay (default).  A warp compacts the valid accesses of consecutive
+ * non-barrier rows (NOP records skipped) into a 32-slot pool, one access per
+ * lane, each tagged with its simulated lane, and checks the pool with one
+ * collective step.  Record order inside a pool is happens-before consistent:
+ * the rows share one epoch (barrier rows flush the pool), and for each
+ * simulated thread record order is program order.  So each same-word group is
+ * folded in record order — Algorithm 1 applied access by access, labels
+ * computed between consecutive members — and committed with one CAS.  Dense
+ * rows (32 valid accesses) are a pool by themselves; sparse rows (one active
+ * lane walking a hub's adjacency list, shard-filtered rows) are packed 32 per
+ * step instead of one.
+ */
+struct hr_pool_smem {
+    uint64_t rec[32];       /* pooled records */
+    uint8_t src[32];        /* simulated lane of each pooled record */
+};
+
+/* fold + commit of one pooled access group (leader side) */
+__device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const hr_thr &t, unsigned long long old,
+                                                        const hr_pool_smem &ps, uint32_t lane, unsigned peers,
+                                                        uint32_t &rinfo, uint32_t &rel)
+{
+    const uint32_t base = t.tid & ~31u;
+    const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+    const uint32_t src0 = ps.src[lane];
+    const uint32_t kind0 = (uint32_t)(ps.rec[lane] >> 62);
+    rel = hr__rel(base | src0, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+    const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
+    uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind0 << 4) | (sync << 2) | rel));
+    rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (src0 << 26) | (kind0 << 24) | (os << 19)) : 0u;
+    uint32_t prev_src = src0;
+    unsigned r = peers & ~(1u << lane);
+    while (r) {
+        const uint32_t j = __ffs(r) - 1;
+        r &= r - 1;
+        const uint32_t sj = ps.src[j];
+        const uint32_t kj = (uint32_t)(ps.rec[j] >> 62);
+        const uint32_t rj = sj == prev_src ? 0u : 1u;                 /* Self / Warp, same epochs: Us */
+        const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | rj));
+        if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
+            rinfo = HR_EI_EMIT | (sj << 26) | (kj << 24) | (cur << 19);
+        cur = nx;
+        prev_src = sj;
+    }
+    return cur;
+}
+
+/* Check the pool: lanes < n hold one access each (ps.rec[lane], ps.src[lane]). */
+__device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t, const hr_pool_smem &ps, uint32_t n)
+{
+    const uint32_t lane = hr__laneid();
+    const bool valid = lane < n;
+    const uint64_t x = valid ? ps.rec[lane] : HR_NOP_REC;
+    const uint32_t space = (uint32_t)(x >> 61) & 1u;
+    const uint32_t kind = (uint32_t)(x >> 62);
+    const uint64_t word = x & HR_WORD_MASK;
+    uint64_t local = 0;
+    if (valid) hr__locate(d, t, space, word, local);             /* validated when pooled */
+    const uint64_t key = valid ? ((local << 2) | (space << 1) | 1u) : 0ull;
+    unsigned kb0, kb1;
+    const unsigned peers = hr__group<false>(d, t, 0xffffffffu, lane, key, kind, kb0, kb1);
+    uint32_t ei = 0;
+    if (valid && (__ffs(peers) - 1) == (int)lane) {
+        const bool sh = space != 0u;
+        const uint32_t sa = t.sshadow + (uint32_t)(local << 3);
+        unsigned long long *gp = d.gshadow + local;
+        const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
+        const uint32_t last = 31u - __clz(peers);
+        const unsigned long long nmeta = (t.meta & ~(0x1full << HR_TID_SHIFT)) |
+                                         ((unsigned long long)ps.src[last] << HR_TID_SHIFT);
+        uint32_t fresh;
+        unsigned long long old = hr__first(d, sh, sa, gp, kind, fresh);
+        while (true) {
+            const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+            uint32_t rinfo, rel;
+            const uint32_t cur = hr__pool_transition(d, t, old, ps, lane, peers, rinfo, rel);
+            const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
+            if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
+                const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
+                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+                    break;
+            }
+            if (nw == old) {
+                if (fresh == HR_OLD_FRESH) break;
+                if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
+            }
+            const unsigned long long prv = sh ? hr__cas_s(sa, old, nw) : hr__cas_g(gp, old, nw);
+            if (prv == old) {
+                if (rinfo) ei = rinfo | (cur == HR_RACE_GRID ? 1u : 0u);
+                break;
+            }
+            old = prv;
+            fresh = HR_OLD_FRESH;
+        }
+    }
+    const unsigned em = __ballot_sync(0xffffffffu, ei != 0u);
+    if (em) {
+        const uint32_t leader = __ffs(em) - 1;
+        uint32_t b = 0;
+        if (lane == leader) b = atomicAdd(d.ring_tail, (unsigned)__popc(em));
+        b = __shfl_sync(0xffffffffu, b, leader);
+        if (ei) hr__write_race(d, t, b + __popc(em & ((1u << lane) - 1u)), space, word, ei);
+    }
+}
+
+__device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint64_t x, unsigned lane_mask)
+{
+    const uint32_t op = (uint32_t)(x >> 62);
+    const uint64_t w = x & HR_WORD_MASK;
+    const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
+    const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
+    if ((bst && bst != lane_mask) || (ctrl != lane_mask))
+        if ((threadIdx.x & 31u) == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+    if (bst) hr_syncthreads(d, t);
+    else hr_syncwarp(d, t);
+    if (ctrl & ~bst) {
+        const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
+        if (bsw != ctrl && (threadIdx.x & 31u) == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+    }
+}
+
+/* POOL = false: row-by-row (dense traces; 32 registers, 64 warps/SM).
+ * POOL = true: pooled (sparse traces; 64 registers, 32 warps/SM). */
+template <bool POOL>
+__global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d, const uint64_t *__restrict__ rec,
+                                                                       const uint64_t *__restrict__ woff,
+                                                                       uint32_t warps, uint32_t lanes,
+                                                                       uint32_t smem_words)
 {
     extern __shared__ __align__(16) unsigned char hr_smem[];
-    unsigned long long *sshadow = reinterpret_cast<unsigned long long *>(hr_smem + HR_FSM_SMEM_BYTES);
+    hr_pool_smem *pools = reinterpret_cast<hr_pool_smem *>(hr_smem + HR_FSM_SMEM_BYTES);
+    unsigned long long *sshadow = reinterpret_cast<unsigned long long *>(
+        hr_smem + HR_FSM_SMEM_BYTES + (POOL ? warps * sizeof(hr_pool_smem) : 0));
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -49,7 +172,7 @@ __global__ void __launch_bounds__(1024, HR_MIN_BLOCKS) hr_replay_kernel(hr_dev d
     const uint64_t *p = rec + r0 * 32 + lane;
     const uint64_t n = r1 - r0;
 
-    /* two-deep record prefetch (shift register, body not unrolled) */
+    uint32_t cnt = 0;                                                /* warp-uniform pool fill */
     uint64_t x1 = (active && n > 0) ? hr__ld_rec(p) : HR_NOP_REC;
     uint64_t x2 = (active && n > 1) ? hr__ld_rec(p + 32) : HR_NOP_REC;
     for (uint64_t i = 0; i < n; i++) {
@@ -58,21 +181,53 @@ __global__ void __launch_bounds__(1024, HR_MIN_BLOCKS) hr_replay_kernel(hr_dev d
         x2 = (active && i + 2 < n) ? hr__ld_rec(p + 32 * (i + 2)) : HR_NOP_REC;
         const uint32_t op = (uint32_t)(x >> 62);
         const uint64_t w = x & HR_WORD_MASK;
-        const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
-        if (ctrl) {                                               /* warp-uniform */
-            const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
-            if ((bst && bst != lane_mask) || (ctrl != lane_mask))
-                if (lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
-            if (bst) hr_syncthreads(d, t);
-            else hr_syncwarp(d, t);
-            if (ctrl & ~bst) {
-                const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
-                if (bsw != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
-            }
+        if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {          /* barrier row: flush, then sync */
+            if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); cnt = 0; __syncwarp(); }
+            hr__barrier_row(d, t, x, lane_mask);
             continue;
         }
-        hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
+        if (!POOL) {
+            hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
+            continue;
+        }
+        hr_pool_smem &ps = pools[warp];
+        uint64_t local;
+        const bool v = op != 3u && !t.off && hr__locate(d, t, (uint32_t)(x >> 61) & 1u, w, local);
+        const unsigned vm = __ballot_sync(0xffffffffu, v);
+        const uint32_t k = __popc(vm);
+        if (k == 0) continue;
+        if (cnt + k > 32u) { __syncwarp(); hr__check_pool(d, t, ps, cnt); cnt = 0; __syncwarp(); }
+        if (v) {
+            const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
+            ps.rec[slot] = x;
+            ps.src[slot] = (uint8_t)lane;
+        }
+        cnt += k;
+        if (cnt == 32u) { __syncwarp(); hr__check_pool(d, t, ps, 32u); cnt = 0; __syncwarp(); }
     }
+    if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); __syncwarp(); }
+}
+
+/* Density probe for the row/pool choice: counts access records among up to
+ * `samples` rows spread over [0, n_rows) (one block). */
+__global__ void hr_density_kernel(const uint64_t *__restrict__ rec, uint64_t n_rows, uint32_t samples,
+                                  unsigned long long *out)
+{
+    __shared__ unsigned long long acc[2];
+    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long a = 0, tot = 0;
+    for (uint32_t s = threadIdx.x >> 5; s < samples; s += blockDim.x >> 5) {
+        const uint64_t row = (uint64_t)((double)s * (double)n_rows / (double)samples);
+        if (row >= n_rows) break;
+        const uint64_t x = rec[row * 32 + (threadIdx.x & 31u)];
+        a += (x >> 62) != 3u;
+        tot++;
+    }
+    atomicAdd(&acc[0], a);
+    atomicAdd(&acc[1], tot);
+    __syncthreads();
+    if (threadIdx.x < 2) out[threadIdx.x] = acc[threadIdx.x];
 }
 
 /* Overflow fallback / cross-check: every RACE word of the (local) global

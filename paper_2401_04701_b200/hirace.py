@@ -24,7 +24,8 @@ HR_OK, HR_E_ARG, HR_E_NOMEM, HR_E_CUDA, HR_E_STATE = 0, -1, -2, -3, -4
 HR_GLOBAL, HR_SHARED = 0, 1
 HR_F_CLOCK_OVERFLOW, HR_F_RING_OVERFLOW, HR_F_MODEL_VIOLATION = 1, 2, 4
 HR_F_BARRIER_DIVERGENCE, HR_F_UNMONITORED = 8, 16
-HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING = 1, 2, 4
+HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING, HR_OPT_NO_SPECULATE, HR_OPT_NO_POOL, HR_OPT_POOL = \
+    1, 2, 4, 8, 16, 32
 EXPORTS = ("hr_init", "hr_set_shard", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_report", "hr_reset_report", "hr_counters", "hr_replay_timing",
            "hr_fsm_table",

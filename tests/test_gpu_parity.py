@@ -63,38 +63,43 @@ def _random_batch(seed, n, **kw):
 
 
 @pytest.mark.parametrize("seed", range(4))
-def test_random_small_family(seed):
+@pytest.mark.parametrize("options", [16, 32])
+def test_random_small_family(seed, options):
     tr = _random_batch(seed, 300, max_blocks=2, max_warps=2, max_lanes=2, max_slots=5, n_words=2,
                        spaces=(0, 1))
-    assert gpu_set(tr) == oracle_set(tr)
+    assert gpu_set(tr, options=options) == oracle_set(tr)
 
 
 @pytest.mark.parametrize("seed", range(4))
-def test_random_wide_grids(seed):
+@pytest.mark.parametrize("options", [16, 32])
+def test_random_wide_grids(seed, options):
     """Full warps and many warps: exercises MATCH coalescing, multi-lane folds,
-    CAS contention, several tiles of the shadow and ragged warp lengths."""
+    CAS contention, several tiles of the shadow and ragged warp lengths, in
+    both the row and the pooled replay."""
     tr = _random_batch(100 + seed, 40, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12,
                        n_words=40, spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
-    g, fl = gpu_set(tr)
+    g, fl = gpu_set(tr, options=options)
     o, ofl = oracle_set(tr)
     assert g == o and fl == ofl
     assert len(o) > 10
 
 
-def test_hot_words_contention():
+@pytest.mark.parametrize("options", [16, 32])
+def test_hot_words_contention(options):
     """Few words, 32 warps x 32 lanes x 16 blocks: heavy CAS retry storms."""
     tr = _random_batch(7, 10, max_blocks=16, max_warps=32, max_lanes=32, max_slots=8, n_words=3,
                        spaces=(0, 1), p_skip=0.2)
-    assert gpu_set(tr) == oracle_set(tr)
+    assert gpu_set(tr, options=options) == oracle_set(tr)
     tr = _random_batch(8, 10, max_blocks=16, max_warps=32, max_lanes=32, max_slots=8, n_words=3,
                        kinds="RA", spaces=(0, 1), p_skip=0.2)
-    assert gpu_set(tr) == oracle_set(tr)
+    assert gpu_set(tr, options=options) == oracle_set(tr)
 
 
-@pytest.mark.parametrize("options", [1, 2, 3])
+@pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8])
 def test_ablations_same_result(options):
-    """Coalescing off / fast exits off change the commit order and the write
-    traffic, never the result (schedule independence)."""
+    """Coalescing off / fast exits off / no speculation / forced row or pooled
+    replay change the commit order and the traffic, never the result
+    (schedule independence)."""
     tr = _random_batch(21, 60, max_blocks=4, max_warps=4, max_lanes=32, max_slots=10, n_words=8,
                        spaces=(0, 1))
     assert gpu_set(tr, options=options) == oracle_set(tr)
