@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--ref-lb", type=int, default=8, help="C5 sample per --impl reference step")
     ap.add_argument("--options", type=int, default=0, help="extra HR_OPT_* bits (ablations)")
     ap.add_argument("--no-slowdown", action="store_true")
+    ap.add_argument("--format", default="c32", choices=["c32", "u64"],
+                    help="trace record encoding (include/hr.h HR_TRACE_C32 = 140 B/row, U64 = 256 B/row)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU to test the N>1 path (timings then meaningless)")
     ap.add_argument("--c4-lv", type=int, default=20, help="log2 vertices of the C4 graph for the slowdown")
@@ -266,12 +268,17 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
 
     # --- input: this rank's shard of the trace, generated in HBM (untimed) ---
-    rec, woff, kd = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
+    if args.format == "c32":
+        rec32, opsw, spc, woff, kd = c5.gpu_trace_c32(lb, seed, rank=rank, nshard=world)
+        dt = hr.DeviceTrace(None, woff, kd, rec32, opsw, spc)
+        n_acc_rank = 0
+        for lo in range(32):
+            n_acc_rank += int((((opsw >> (2 * lo)) & 3) != 3).sum().item())
+    else:
+        rec, woff, kd = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
+        dt = hr.DeviceTrace(rec, woff, kd)
+        n_acc_rank = int((((rec >> 62) & 3) != 3).sum().item())
     torch.cuda.synchronize()
-    dt = hr.DeviceTrace(rec, woff, kd)
-    ops = (rec >> 62) & 3
-    n_acc_rank = int((ops != 3).sum().item())
-    del ops
     n_rows = dt.n_rows
     ck = hr.Checker(c5.total_words(lb), 0, shard=(rank, world), options=hr.HR_OPT_TIMING | args.options,
                     ring_capacity=1 << 21)
@@ -318,14 +325,14 @@ def main():
 
     # roofline of the dominant kernel (the replay), rank 0's launch
     peak, peak_kind = peaks()
-    algo_bytes = n_rows * 32 * 8 + BYTES_PER_ACCESS_ALGO * n_acc_rank
+    algo_bytes = dt.record_bytes() + BYTES_PER_ACCESS_ALGO * n_acc_rank
     achieved = algo_bytes / (kern_ms / max(n_kern, 1) / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "replay_dram_bytes.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if world == 1 and int(pj.get("lb", -1)) == lb:
+            if world == 1 and int(pj.get("lb", -1)) == lb and pj.get("format", "u64") == args.format:
                 traffic = float(pj["dram_bytes_per_launch"])
         except Exception:
             traffic = None
@@ -338,14 +345,26 @@ def main():
     # --- e2e through the C ABI with HOST buffers ---
     e2e = None
     if not args.no_e2e:
-        host_rec = torch.empty(rec.numel(), dtype=torch.int64, pin_memory=True)
-        host_rec.copy_(rec)
-        host_woff = woff.cpu().numpy().view(np.uint64)
         host_trace = type("T", (), {})()
-        host_trace.rec = host_rec.numpy().view(np.uint64)
-        host_trace.warp_off = host_woff
         host_trace.kdesc = kd
-        del rec, dt
+        host_trace.warp_off = woff.cpu().numpy().view(np.uint64)
+        pinned = []
+        if dt.format == hr.HR_TRACE_C32:
+            for name, tsr in (("rec32", dt.rec32), ("ops", dt.ops), ("spc", dt.spc)):
+                h = torch.empty(tsr.numel(), dtype=tsr.dtype, pin_memory=True)
+                h.copy_(tsr)
+                pinned.append(h)
+                setattr(host_trace, name, h.numpy())
+            host_trace.rec = None
+        else:
+            h = torch.empty(dt.rec.numel(), dtype=torch.int64, pin_memory=True)
+            h.copy_(dt.rec)
+            pinned.append(h)
+            host_trace.rec = h.numpy().view(np.uint64)
+            host_trace.rec32 = None
+        h2d = sum(int(h.numel() * h.element_size()) for h in pinned) + int(host_trace.warp_off.nbytes)
+        dt.rec = dt.rec32 = dt.ops = dt.spc = None          # free the device trace: staging replaces it
+        rec = rec32 = opsw = spc = None  # noqa: F841
         torch.cuda.empty_cache()
         host_replay = lambda: ck.replay_host(host_trace, stream)  # noqa: E731
         for _ in range(args.warmup):
@@ -362,10 +381,9 @@ def main():
         barrier(world)
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world)
         parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == c5.planted(lb, seed)
-        e2e = {"value": total_acc / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(host_trace.rec.nbytes + host_woff.nbytes),
+        e2e = {"value": total_acc / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(16 + 24 * len(raw_e) // max(world, 1)),
-               "ms_per_step": e2e_ms}
+               "ms_per_step": e2e_ms, "format": args.format}
         hr.hr_replay_timing(ck.ctx)
 
     cpu = None
@@ -379,13 +397,15 @@ def main():
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"C5: {total_acc} checked accesses (2^{lb} blocks x 256 threads x 256), "
                                    f"global trace over 2^{lb + 16} words, address-sharded (granule mod {world})",
+                       "trace_format": args.format,
                        "parallelism": f"address-shard x{world}", "l2": "inputs larger than L2 "
                        "(trace + shadow >> 126 MB; no flush needed)", "seed": seed},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "hr_replay_kernel", "kernel_ms": kern_ms / max(n_kern, 1),
                          "algo_bytes_per_launch": algo_bytes,
-                         "algo_bytes_rule": "records (n_rows*32*8) + 16 B shadow RMW per checked access"},
+                         "algo_bytes_rule": f"records ({args.format}: {dt.record_bytes() // max(n_rows, 1)} B/row) "
+                                            "+ 16 B shadow RMW per checked access"},
             "literal_roofline_frac": literal,
             "step_breakdown_ms": {"replay_kernel": kern_ms_launch, "shadow_reset": reset_ms_launch,
                                   "rest(report,ring reset,exchange)": ms_step - kern_ms_launch - reset_ms_launch},

@@ -36,10 +36,8 @@ struct hr_ctx {
     bool have_kernel = false;
     bool last_pooled = false;
     cudaStream_t stream = nullptr;
-    uint64_t *stage_rec = nullptr;
-    size_t stage_rec_cap = 0;
-    uint64_t *stage_woff = nullptr;
-    size_t stage_woff_cap = 0;
+    void *stage[4] = {nullptr, nullptr, nullptr, nullptr};   /* warp_off, rec|rec32, ops, spc */
+    size_t stage_cap[4] = {0, 0, 0, 0};
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
@@ -211,13 +209,14 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
 /* Row or pooled replay: options force one; otherwise probe the density of
  * access records (pooling pays when rows are mostly NOP, e.g. power-law BFS
  * frontiers or address-sharded traces). */
-static hr_status choose_pool(hr_ctx *c, const uint64_t *rec, uint64_t n_rows, cudaStream_t s, bool *pool)
+template <typename SRC>
+static hr_status choose_pool(hr_ctx *c, SRC src, uint64_t n_rows, cudaStream_t s, bool *pool)
 {
     if (c->cfg.options & HR_OPT_NO_POOL) { *pool = false; return HR_OK; }
     if (c->cfg.options & HR_OPT_POOL) { *pool = true; return HR_OK; }
     *pool = false;
     if (n_rows == 0) return HR_OK;
-    hr_density_kernel<<<1, 1024, 0, s>>>(rec, n_rows, 2048, c->counters + 2);
+    hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, n_rows, 2048, c->counters + 2);
     CU(cudaGetLastError());
     unsigned long long h[2] = {0, 0};
     CU(cudaMemcpyAsync(h, c->counters + 2, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -226,11 +225,11 @@ static hr_status choose_pool(hr_ctx *c, const uint64_t *rec, uint64_t n_rows, cu
     return HR_OK;
 }
 
-static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const uint64_t *woff,
-                        cudaStream_t s)
+template <typename SRC>
+static hr_status replay(hr_ctx *c, const hr_trace *t, SRC src, const uint64_t *woff, cudaStream_t s)
 {
     bool pool = false;
-    hr_status pst = choose_pool(c, rec, t->n_rows, s, &pool);
+    hr_status pst = choose_pool(c, src, t->n_rows, s, &pool);
     if (pst) return pst;
     c->last_pooled = pool;
     for (uint32_t k = 0; k < t->n_kernels; k++) {
@@ -250,14 +249,14 @@ static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const
         uint32_t kid = t->kernel_base + k;
         hr_dev d = make_dev(c, kid);
         size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
-        void (*kern)(hr_dev, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t) =
-            pool ? hr_replay_kernel<true> : hr_replay_kernel<false>;
+        void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
+            pool ? hr_replay_kernel<true, SRC> : hr_replay_kernel<false, SRC>;
         if (smem > 48 * 1024)
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
-        kern<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(d, rec, woff + woi, (uint32_t)warps,
+        kern<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(d, src, woff + woi, (uint32_t)warps,
                                                                   (uint32_t)lanes, (uint32_t)smem_words);
         CU(cudaGetLastError());
         if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
@@ -267,37 +266,64 @@ static hr_status replay(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const
     return HR_OK;
 }
 
+static bool trace_ok(const hr_trace *t)
+{
+    if (!t) return false;
+    if (!t->n_kernels) return true;
+    if (!t->kdesc || !t->warp_off) return false;
+    if (t->format == HR_TRACE_U64) return t->rec != nullptr;
+    if (t->format == HR_TRACE_C32) return t->rec32 && t->ops && t->spc;
+    return false;
+}
+
+static hr_status dispatch(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const uint32_t *rec32,
+                          const uint64_t *ops, const uint32_t *spc, const uint64_t *woff)
+{
+    if (t->format == HR_TRACE_C32) {
+        hr_src_c32 src{rec32, ops, spc};
+        return replay(c, t, src, woff, c->stream);
+    }
+    hr_src_u64 src{rec};
+    return replay(c, t, src, woff, c->stream);
+}
+
 extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
 {
-    if (!c || !t || (t->n_kernels && (!t->kdesc || !t->rec || !t->warp_off))) return fail(c, HR_E_ARG, "null trace");
+    if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
-    return replay(c, t, t->rec, t->warp_off, c->stream);
+    return dispatch(c, t, t->rec, t->rec32, t->ops, t->spc, t->warp_off);
+}
+
+static hr_status stage(hr_ctx *c, void **buf, size_t *cap, const void *src, size_t bytes)
+{
+    if (bytes > *cap) {
+        if (*buf) cudaFree(*buf);
+        *buf = nullptr;
+        *cap = 0;
+        if (cudaMalloc(buf, bytes) != cudaSuccess) return fail(c, HR_E_NOMEM, "staging %zu bytes failed", bytes);
+        *cap = bytes;
+    }
+    if (bytes) CU(cudaMemcpyAsync(*buf, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return HR_OK;
 }
 
 extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *stream)
 {
-    if (!c || !t || (t->n_kernels && (!t->kdesc || !t->rec || !t->warp_off))) return fail(c, HR_E_ARG, "null trace");
+    if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
-    size_t need_rec = (size_t)t->n_rows * 32, need_woff = (size_t)t->n_warp_off;
-    if (need_rec > c->stage_rec_cap) {
-        if (c->stage_rec) cudaFree(c->stage_rec);
-        c->stage_rec = nullptr;
-        if (cudaMalloc(&c->stage_rec, need_rec * 8) != cudaSuccess)
-            return fail(c, HR_E_NOMEM, "staging %zu records failed", need_rec);
-        c->stage_rec_cap = need_rec;
+    hr_status st = stage(c, &c->stage[0], &c->stage_cap[0], t->warp_off, (size_t)t->n_warp_off * 8);
+    if (st) return st;
+    if (t->format == HR_TRACE_C32) {
+        if ((st = stage(c, &c->stage[1], &c->stage_cap[1], t->rec32, (size_t)t->n_rows * 128))) return st;
+        if ((st = stage(c, &c->stage[2], &c->stage_cap[2], t->ops, (size_t)t->n_rows * 8))) return st;
+        if ((st = stage(c, &c->stage[3], &c->stage_cap[3], t->spc, (size_t)t->n_rows * 4))) return st;
+    } else {
+        if ((st = stage(c, &c->stage[1], &c->stage_cap[1], t->rec, (size_t)t->n_rows * 256))) return st;
     }
-    if (need_woff > c->stage_woff_cap) {
-        if (c->stage_woff) cudaFree(c->stage_woff);
-        c->stage_woff = nullptr;
-        if (cudaMalloc(&c->stage_woff, need_woff * 8) != cudaSuccess)
-            return fail(c, HR_E_NOMEM, "staging warp offsets failed");
-        c->stage_woff_cap = need_woff;
-    }
-    CU(cudaMemcpyAsync(c->stage_woff, t->warp_off, need_woff * 8, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->stage_rec, t->rec, need_rec * 8, cudaMemcpyHostToDevice, c->stream));
-    return replay(c, t, c->stage_rec, c->stage_woff, c->stream);
+    return dispatch(c, t, (const uint64_t *)c->stage[1], (const uint32_t *)c->stage[1],
+                    (const uint64_t *)c->stage[2], (const uint32_t *)c->stage[3], (const uint64_t *)c->stage[0]);
 }
 
 static bool race_less(const hr_race &a, const hr_race &b)
@@ -459,8 +485,8 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->tail) cudaFree(c->tail);
     if (c->counters) cudaFree(c->counters);
     if (c->fsm) cudaFree(c->fsm);
-    if (c->stage_rec) cudaFree(c->stage_rec);
-    if (c->stage_woff) cudaFree(c->stage_woff);
+    for (int i = 0; i < 4; i++)
+        if (c->stage[i]) cudaFree(c->stage[i]);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

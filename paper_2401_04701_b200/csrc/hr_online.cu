@@ -12,6 +12,7 @@
 #include "hr.h"
 #include "hr_bench.h"
 #include "hr_device.cuh"
+#include "hr_records.cuh"
 
 namespace {
 
@@ -181,23 +182,23 @@ __global__ void __launch_bounds__(256) c4_hist_kernel(hr_dev d, int *data, uint3
 
 /* ---- uninstrumented replay: the same record walk and barriers as
  * hr_replay_kernel, but each access is the raw data access (4-byte word) ---- */
-__global__ void __launch_bounds__(1024, 2) raw_replay_kernel(const uint64_t *__restrict__ rec,
-                                                             const uint64_t *__restrict__ woff, uint32_t warps,
-                                                             uint32_t lanes, int *data, uint64_t data_words)
+template <typename SRC>
+__global__ void __launch_bounds__(1024, 2) raw_replay_kernel(SRC src, const uint64_t *__restrict__ woff,
+                                                             uint32_t warps, uint32_t lanes, int *data,
+                                                             uint64_t data_words)
 {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t gw = (uint64_t)blockIdx.x * warps + warp;
     const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
     const bool active = lane < lanes;
-    const uint64_t *p = rec + r0 * 32 + lane;
     const uint64_t n = r1 - r0;
-    uint64_t x1 = (active && n > 0) ? __ldcs((const unsigned long long *)p) : (3ull << 62);
-    uint64_t x2 = (active && n > 1) ? __ldcs((const unsigned long long *)(p + 32)) : (3ull << 62);
+    uint64_t x1 = (active && n > 0) ? src.row(r0, lane) : HR_NOP_REC;
+    uint64_t x2 = (active && n > 1) ? src.row(r0 + 1, lane) : HR_NOP_REC;
     int acc = 0;
     for (uint64_t i = 0; i < n; i++) {
         const uint64_t x = x1;
         x1 = x2;
-        x2 = (active && i + 2 < n) ? __ldcs((const unsigned long long *)(p + 32 * (i + 2))) : (3ull << 62);
+        x2 = (active && i + 2 < n) ? src.row(r0 + i + 2, lane) : HR_NOP_REC;
         const uint32_t op = (uint32_t)(x >> 62);
         const uint64_t w = x & HR_WORD_MASK;
         const unsigned st = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
@@ -237,9 +238,13 @@ extern "C" hr_status hrb_raw_replay(const hr_trace *t, int *data, uint64_t data_
     for (uint32_t k = 0; k < t->n_kernels; k++) {
         const uint64_t *kd = t->kdesc + 8ull * k;
         if (kd[0] == 0) continue;
-        raw_replay_kernel<<<(unsigned)kd[0], (unsigned)(kd[1] * 32), 0, s>>>(t->rec, t->warp_off + kd[4],
-                                                                             (uint32_t)kd[1], (uint32_t)kd[2],
-                                                                             data, data_words);
+        const dim3 g((unsigned)kd[0]), b((unsigned)(kd[1] * 32));
+        if (t->format == HR_TRACE_C32)
+            raw_replay_kernel<<<g, b, 0, s>>>(hr_src_c32{t->rec32, t->ops, t->spc}, t->warp_off + kd[4],
+                                              (uint32_t)kd[1], (uint32_t)kd[2], data, data_words);
+        else
+            raw_replay_kernel<<<g, b, 0, s>>>(hr_src_u64{t->rec}, t->warp_off + kd[4], (uint32_t)kd[1],
+                                              (uint32_t)kd[2], data, data_words);
         if (cudaGetLastError() != cudaSuccess) return HR_E_CUDA;
     }
     return HR_OK;

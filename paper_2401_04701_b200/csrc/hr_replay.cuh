@@ -19,13 +19,8 @@
 #define HR_REPLAY_CUH_
 
 #include "hr_device.cuh"
+#include "hr_records.cuh"
 
-#define HR_NOP_REC (3ull << 62)
-
-__device__ __forceinline__ uint64_t hr__ld_rec(const uint64_t *p)
-{
-    return __ldcs(reinterpret_cast<const unsigned long long *>(p));
-}
 
 /*
  * Pooled replay (default).  A warp compacts the valid accesses of consecutive
@@ -151,8 +146,8 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
 
 /* POOL = false: row-by-row (dense traces; 32 registers, 64 warps/SM).
  * POOL = true: pooled (sparse traces; 64 registers, 32 warps/SM). */
-template <bool POOL>
-__global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d, const uint64_t *__restrict__ rec,
+template <bool POOL, typename SRC>
+__global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d, SRC src,
                                                                        const uint64_t *__restrict__ woff,
                                                                        uint32_t warps, uint32_t lanes,
                                                                        uint32_t smem_words)
@@ -169,16 +164,15 @@ __global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d,
     const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const bool active = lane < lanes;
-    const uint64_t *p = rec + r0 * 32 + lane;
     const uint64_t n = r1 - r0;
 
     uint32_t cnt = 0;                                                /* warp-uniform pool fill */
-    uint64_t x1 = (active && n > 0) ? hr__ld_rec(p) : HR_NOP_REC;
-    uint64_t x2 = (active && n > 1) ? hr__ld_rec(p + 32) : HR_NOP_REC;
+    uint64_t x1 = (active && n > 0) ? src.row(r0, lane) : HR_NOP_REC;
+    uint64_t x2 = (active && n > 1) ? src.row(r0 + 1, lane) : HR_NOP_REC;
     for (uint64_t i = 0; i < n; i++) {
         const uint64_t x = x1;
         x1 = x2;
-        x2 = (active && i + 2 < n) ? hr__ld_rec(p + 32 * (i + 2)) : HR_NOP_REC;
+        x2 = (active && i + 2 < n) ? src.row(r0 + i + 2, lane) : HR_NOP_REC;
         const uint32_t op = (uint32_t)(x >> 62);
         const uint64_t w = x & HR_WORD_MASK;
         if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {          /* barrier row: flush, then sync */
@@ -210,8 +204,8 @@ __global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d,
 
 /* Density probe for the row/pool choice: counts access records among up to
  * `samples` rows spread over [0, n_rows) (one block). */
-__global__ void hr_density_kernel(const uint64_t *__restrict__ rec, uint64_t n_rows, uint32_t samples,
-                                  unsigned long long *out)
+template <typename SRC>
+__global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, unsigned long long *out)
 {
     __shared__ unsigned long long acc[2];
     if (threadIdx.x < 2) acc[threadIdx.x] = 0;
@@ -220,7 +214,7 @@ __global__ void hr_density_kernel(const uint64_t *__restrict__ rec, uint64_t n_r
     for (uint32_t s = threadIdx.x >> 5; s < samples; s += blockDim.x >> 5) {
         const uint64_t row = (uint64_t)((double)s * (double)n_rows / (double)samples);
         if (row >= n_rows) break;
-        const uint64_t x = rec[row * 32 + (threadIdx.x & 31u)];
+        const uint64_t x = src.row(row, threadIdx.x & 31u);
         a += (x >> 62) != 3u;
         tot++;
     }

@@ -44,10 +44,15 @@ class HrRace(ctypes.Structure):
                 ("first_kind", ctypes.c_uint8), ("prev_state", ctypes.c_uint8)]
 
 
+HR_TRACE_U64, HR_TRACE_C32 = 0, 1
+
+
 class HrTrace(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("n_rows", ctypes.c_uint64), ("kdesc", ctypes.c_void_p),
                 ("n_kernels", ctypes.c_uint32), ("kernel_base", ctypes.c_uint32),
-                ("warp_off", ctypes.c_void_p), ("n_warp_off", ctypes.c_uint64)]
+                ("warp_off", ctypes.c_void_p), ("n_warp_off", ctypes.c_uint64),
+                ("format", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("rec32", ctypes.c_void_p), ("ops", ctypes.c_void_p), ("spc", ctypes.c_void_p)]
 
 
 assert ctypes.sizeof(HrRace) == 24
@@ -213,32 +218,66 @@ def hr_destroy(ctx):
 # ---- convenience wrapper -----------------------------------------------------------
 
 class DeviceTrace:
-    """A trace resident in HBM: torch uint64 tensors for rec / warp_off, host kdesc."""
+    """A trace resident in HBM: torch tensors for the records and warp offsets,
+    host kdesc.  U64 format: ``rec`` int64 (n_rows*32).  C32 format: ``rec32``
+    int32 (n_rows*32), ``ops`` int64 (n_rows), ``spc`` int32 (n_rows)."""
 
-    def __init__(self, rec, warp_off, kdesc: np.ndarray):
-        import torch
-        self.rec = rec
+    def __init__(self, rec, warp_off, kdesc: np.ndarray, rec32=None, ops=None, spc=None):
+        self.rec, self.rec32, self.ops, self.spc = rec, rec32, ops, spc
         self.warp_off = warp_off
         self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
-        assert rec.dtype == torch.int64 and warp_off.dtype == torch.int64
-        self.n_rows = rec.numel() // 32
+        self.format = HR_TRACE_C32 if rec32 is not None else HR_TRACE_U64
+        self.n_rows = (rec32.numel() if rec32 is not None else rec.numel()) // 32
 
     @staticmethod
-    def from_trace(trace, device="cuda") -> "DeviceTrace":
+    def from_trace(trace, device="cuda", compact: bool = False) -> "DeviceTrace":
         import torch
-        rec = torch.from_numpy(np.ascontiguousarray(trace.rec).view(np.int64)).to(device)
         wo = torch.from_numpy(np.ascontiguousarray(trace.warp_off).view(np.int64)).to(device)
+        if compact:
+            from tracegen.format import to_c32
+            r32, ops, spc = to_c32(trace)
+            return DeviceTrace(None, wo, trace.kdesc, torch.from_numpy(r32.view(np.int32)).to(device),
+                               torch.from_numpy(ops.view(np.int64)).to(device),
+                               torch.from_numpy(spc.view(np.int32)).to(device))
+        rec = torch.from_numpy(np.ascontiguousarray(trace.rec).view(np.int64)).to(device)
         return DeviceTrace(rec, wo, trace.kdesc)
 
+    def record_bytes(self) -> int:
+        return self.n_rows * (140 if self.format == HR_TRACE_C32 else 256)
+
     def c(self, kernel_base: int = 0) -> HrTrace:
-        return HrTrace(self.rec.data_ptr(), self.n_rows, self.kdesc.ctypes.data, self.kdesc.shape[0],
-                       kernel_base, self.warp_off.data_ptr(), self.warp_off.numel())
+        t = HrTrace()
+        t.n_rows = self.n_rows
+        t.kdesc = self.kdesc.ctypes.data
+        t.n_kernels = self.kdesc.shape[0]
+        t.kernel_base = kernel_base
+        t.warp_off = self.warp_off.data_ptr()
+        t.n_warp_off = self.warp_off.numel()
+        t.format = self.format
+        if self.format == HR_TRACE_C32:
+            t.rec32, t.ops, t.spc = self.rec32.data_ptr(), self.ops.data_ptr(), self.spc.data_ptr()
+        else:
+            t.rec = self.rec.data_ptr()
+        return t
 
 
 def host_trace_c(trace, kernel_base: int = 0) -> HrTrace:
-    """HrTrace over HOST arrays (for hr_replay_trace_host); keep `trace` alive."""
-    return HrTrace(trace.rec.ctypes.data, trace.rec.shape[0] // 32, trace.kdesc.ctypes.data,
-                   trace.kdesc.shape[0], kernel_base, trace.warp_off.ctypes.data, trace.warp_off.shape[0])
+    """HrTrace over HOST arrays (for hr_replay_trace_host); keep `trace` alive.
+    `trace` has rec (U64) or rec32/ops/spc (C32) numpy arrays, kdesc, warp_off."""
+    t = HrTrace()
+    t.kdesc = trace.kdesc.ctypes.data
+    t.n_kernels = trace.kdesc.shape[0]
+    t.kernel_base = kernel_base
+    t.warp_off = trace.warp_off.ctypes.data
+    t.n_warp_off = trace.warp_off.shape[0]
+    if getattr(trace, "rec32", None) is not None:
+        t.format = HR_TRACE_C32
+        t.n_rows = trace.rec32.shape[0] // 32
+        t.rec32, t.ops, t.spc = trace.rec32.ctypes.data, trace.ops.ctypes.data, trace.spc.ctypes.data
+    else:
+        t.n_rows = trace.rec.shape[0] // 32
+        t.rec = trace.rec.ctypes.data
+    return t
 
 
 def trace_extent(trace) -> Tuple[int, int]:
@@ -273,6 +312,7 @@ class Checker:
         hr_replay_trace(self.ctx, dtrace.c(kernel_base), stream)
 
     def replay_host(self, trace, stream: Optional[int] = None, kernel_base: int = 0):
+        """`trace`: numpy arrays (rec, or rec32/ops/spc) + kdesc + warp_off in host memory."""
         if stream is None:
             import torch
             stream = torch.cuda.current_stream().cuda_stream
@@ -300,11 +340,11 @@ class Checker:
             pass
 
 
-def check_trace(trace, device: int = 0, **kw) -> Tuple[List[Race], int]:
+def check_trace(trace, device: int = 0, compact: bool = False, **kw) -> Tuple[List[Race], int]:
     """Replay a host trace on the GPU and return (sorted racy set, flags)."""
     gmax, smem = trace_extent(trace)
     ck = Checker(gmax, smem, device=device, **kw)
-    dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}")
+    dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}", compact=compact)
     ck.replay(dt)
     races, flags, _ = ck.report()
     ck.close()

@@ -11,9 +11,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--lb", type=int, default=12)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--options", type=int, default=0)
+ap.add_argument("--format", default="c32", choices=["c32", "u64"])
 a = ap.parse_args()
-rec, woff, kd = c5.gpu_trace(a.lb)
-dt = hr.DeviceTrace(rec, woff, kd)
+if a.format == "c32":
+    r32, ops, spc, woff, kd = c5.gpu_trace_c32(a.lb)
+    dt = hr.DeviceTrace(None, woff, kd, r32, ops, spc)
+else:
+    rec, woff, kd = c5.gpu_trace(a.lb)
+    dt = hr.DeviceTrace(rec, woff, kd)
 ck = hr.Checker(c5.total_words(a.lb), 0, options=a.options | hr.HR_OPT_TIMING, ring_capacity=1 << 21)
 for i in range(a.reps):
     ck.reset(); ck.replay(dt); raw, fl = ck.report_raw()

@@ -185,3 +185,29 @@ def test_empty_and_degenerate():
     # single thread: never races
     tr = tp.from_thread_events(1, 1, 1, {(0, 0, 0): [tf.W(0), tf.R(0), tf.A(0), tf.W(0)]})
     assert gpu_set(tr) == ([], 0)
+
+
+@pytest.mark.parametrize("options", [16, 32])
+def test_compact_format_same_result(options):
+    """HR_TRACE_C32 (u32 word + per-row op/space words) decodes to the same
+    records: same racy set as the u64 encoding and the oracle."""
+    tr = _random_batch(61, 40, max_blocks=4, max_warps=8, max_lanes=32, max_slots=12, n_words=500,
+                       spaces=(0, 1), p_skip=0.3)
+    o = oracle_set(tr)
+    assert gpu_set(tr, compact=True, options=options) == o
+    tr = tp.c1_tree_reduction(removed=8)
+    assert gpu_set(tr, compact=True) == oracle_set(tr)
+
+
+def test_compact_host_replay():
+    from tracegen.format import to_c32
+    h = hr()
+    tr = tp.listing2(3, 4, 32)
+    r32, ops, spc = to_c32(tr)
+    host = type("T", (), {"rec32": r32, "ops": ops, "spc": spc, "kdesc": tr.kdesc, "warp_off": tr.warp_off,
+                          "rec": None})()
+    gmax, smem = h.trace_extent(tr)
+    ck = h.Checker(gmax, smem)
+    ck.replay_host(host)
+    races, fl, _ = ck.report()
+    assert [tuple(r) for r in races] == oracle_set(tr)[0]

@@ -67,7 +67,10 @@ def _gpu_lib():
         _gpu = ctypes.CDLL(_GPU_LIB)
         _gpu.c5_gen_gpu.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                    ctypes.c_void_p]
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        _gpu.c5_pack_gpu.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p]
+        _gpu.c5_pack_gpu.restype = ctypes.c_int
         _gpu.c5_gen_gpu.restype = ctypes.c_int
     return _gpu
 
@@ -114,24 +117,49 @@ def planted(lb: int, seed: int = DEFAULT_SEED) -> List[Tuple[int, int]]:
     return sorted(zip((int(x) for x in w), (int(x) for x in s)))
 
 
+def _gpu_offsets(lib, lb, seed, rank, l2, device, stream):
+    import torch
+    nw = (1 << lb) * WARPS
+    if l2 == 0:
+        return torch.arange(nw + 1, dtype=torch.int64, device=device) * ROWS
+    rows = torch.empty(nw, dtype=torch.int64, device=device)
+    rc = lib.c5_gen_gpu(seed, lb, rank, l2, 0, rows.data_ptr(), None, None, None, None, stream)
+    assert rc == 0, rc
+    off = torch.zeros(nw + 1, dtype=torch.int64, device=device)
+    off[1:] = torch.cumsum(rows, 0)
+    return off
+
+
 def gpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda"):
-    """Generate the (shard of the) trace directly in HBM.  Returns
-    (rec int64 tensor, warp_off int64 tensor, kdesc numpy)."""
+    """Generate the (shard of the) trace directly in HBM, u64 records.
+    Returns (rec int64 tensor, warp_off int64 tensor, kdesc numpy)."""
     import torch
     lib = _gpu_lib()
-    nw = (1 << lb) * WARPS
-    l2 = _log2(nshard)
     stream = torch.cuda.current_stream().cuda_stream
-    if l2 == 0:
-        off = torch.arange(nw + 1, dtype=torch.int64, device=device) * ROWS
-    else:
-        rows = torch.empty(nw, dtype=torch.int64, device=device)
-        rc = lib.c5_gen_gpu(seed, lb, rank, l2, 0, rows.data_ptr(), None, None, stream)
-        assert rc == 0, rc
-        off = torch.zeros(nw + 1, dtype=torch.int64, device=device)
-        off[1:] = torch.cumsum(rows, 0)
+    off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), device, stream)
     n_rows = int(off[-1].item())
     rec = torch.empty(n_rows * 32, dtype=torch.int64, device=device)
-    rc = lib.c5_gen_gpu(seed, lb, rank, l2, 1, None, off.data_ptr(), rec.data_ptr(), stream)
+    rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), 1, None, off.data_ptr(), rec.data_ptr(), None, None, stream)
     assert rc == 0, rc
     return rec, off, kdesc(lb)
+
+
+def gpu_trace_c32(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda"):
+    """Same trace in the HR_TRACE_C32 encoding (140 B per row).  Returns
+    (rec32 int32, ops int64, spc int32, warp_off int64) tensors and kdesc."""
+    import torch
+    lib = _gpu_lib()
+    stream = torch.cuda.current_stream().cuda_stream
+    off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), device, stream)
+    n_rows = int(off[-1].item())
+    rec32 = torch.empty(n_rows * 32, dtype=torch.int32, device=device)
+    opb = torch.empty(n_rows * 32, dtype=torch.uint8, device=device)
+    rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), 1, None, off.data_ptr(), None, rec32.data_ptr(),
+                        opb.data_ptr(), stream)
+    assert rc == 0, rc
+    ops = torch.empty(n_rows, dtype=torch.int64, device=device)
+    spc = torch.empty(n_rows, dtype=torch.int32, device=device)
+    rc = lib.c5_pack_gpu(n_rows, opb.data_ptr(), ops.data_ptr(), spc.data_ptr(), stream)
+    assert rc == 0, rc
+    del opb
+    return rec32, ops, spc, off, kdesc(lb)

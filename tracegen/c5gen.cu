@@ -5,9 +5,19 @@
 
 #include "c5gen.h"
 
-/* one CUDA warp per simulated warp; pass 0 counts rows, pass 1 writes them */
+/* one CUDA warp per simulated warp; pass 0 counts rows, pass 1 writes them:
+ * u64 records to `out`, or (compact) the u32 word to out32 and op | space<<2
+ * to the byte array outb (packed per row afterwards by c5_pack_kernel). */
+__device__ __forceinline__ void c5_put(uint64_t *out, uint32_t *out32, uint8_t *outb, uint64_t i, uint64_t x)
+{
+    if (out) { __stcs((unsigned long long *)&out[i], (unsigned long long)x); return; }
+    out32[i] = (uint32_t)(x & 0xffffffffull);
+    outb[i] = (uint8_t)((x >> 62) | (((x >> 61) & 1ull) << 2));
+}
+
 __global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint64_t n_warps, int pass,
-                              uint64_t *rows_out, const uint64_t *row_off, uint64_t *out)
+                              uint64_t *rows_out, const uint64_t *row_off, uint64_t *out, uint32_t *out32,
+                              uint8_t *outb)
 {
     uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t l = threadIdx.x & 31;
@@ -20,22 +30,45 @@ __global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint64
         for (uint32_t i = 0; i < C5_EPOCH; i++) {
             uint64_t x = c5_record(&p, b, w * 32 + l, e * C5_EPOCH + i);
             if (log2n == 0 || c5_owned_by(x, rank, log2n)) {
-                if (pass) __stcs((unsigned long long *)&out[(row + k) * 32 + l], (unsigned long long)x);
+                if (pass) c5_put(out, out32, outb, (row + k) * 32 + l, x);
                 k++;
             }
         }
         uint32_t maxk = __reduce_max_sync(0xffffffffu, k);
         if (pass) {
-            for (uint32_t kk = k; kk < maxk; kk++) out[(row + kk) * 32 + l] = C5_NOP;
-            out[(row + maxk) * 32 + l] = C5_SYNC;
+            for (uint32_t kk = k; kk < maxk; kk++) c5_put(out, out32, outb, (row + kk) * 32 + l, C5_NOP);
+            c5_put(out, out32, outb, (row + maxk) * 32 + l, C5_SYNC);
         }
         row += maxk + 1;
     }
     if (!pass && l == 0) rows_out[gw] = row;
 }
 
+/* per row: ops (2-bit op of lane l at bits 2l+1:2l) and spc (space bit l) */
+__global__ void c5_pack_kernel(uint64_t n_rows, const uint8_t *opb, uint64_t *ops, uint32_t *spc)
+{
+    uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    uint64_t o = 0;
+    uint32_t s = 0;
+    for (uint32_t l = 0; l < 32; l++) {
+        uint8_t b = opb[r * 32 + l];
+        o |= (uint64_t)(b & 3u) << (2 * l);
+        s |= (uint32_t)((b >> 2) & 1u) << l;
+    }
+    ops[r] = o;
+    spc[r] = s;
+}
+
+extern "C" int c5_pack_gpu(uint64_t n_rows, const uint8_t *opb, uint64_t *ops, uint32_t *spc, void *stream)
+{
+    c5_pack_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, opb, ops, spc);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int c5_gen_gpu(uint64_t seed, uint32_t lb, uint32_t rank, uint32_t log2n, int pass,
-                          uint64_t *rows_out, const uint64_t *row_off, uint64_t *out, void *stream)
+                          uint64_t *rows_out, const uint64_t *row_off, uint64_t *out, uint32_t *out32,
+                          uint8_t *outb, void *stream)
 {
     c5_params p;
     p.seed = seed;
@@ -43,6 +76,7 @@ extern "C" int c5_gen_gpu(uint64_t seed, uint32_t lb, uint32_t rank, uint32_t lo
     uint64_t n_warps = (1ull << lb) * C5_WARPS;
     uint64_t threads = n_warps * 32;
     unsigned blocks = (unsigned)((threads + 255) / 256);
-    c5_gen_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, rank, log2n, n_warps, pass, rows_out, row_off, out);
+    c5_gen_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, rank, log2n, n_warps, pass, rows_out, row_off, out,
+                                                              out32, outb);
     return (int)cudaGetLastError();
 }
