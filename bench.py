@@ -53,8 +53,10 @@ def parse():
     ap.add_argument("--ref-lb", type=int, default=8, help="C5 sample per --impl reference step")
     ap.add_argument("--options", type=int, default=0, help="extra HR_OPT_* bits (ablations)")
     ap.add_argument("--no-slowdown", action="store_true")
-    ap.add_argument("--format", default="c32", choices=["c32", "u64"],
-                    help="trace record encoding (include/hr.h HR_TRACE_C32 = 140 B/row, U64 = 256 B/row)")
+    ap.add_argument("--format", default="u64", choices=["c32", "u64"],
+                    help="device-resident trace encoding (include/hr.h HR_TRACE_U64 = 256 B/row, C32 = 160 B/row)")
+    ap.add_argument("--e2e-format", default="c32", choices=["c32", "u64"],
+                    help="host-buffer trace encoding for e2e (C32 moves 37.5%% fewer bytes over PCIe)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU to test the N>1 path (timings then meaningless)")
     ap.add_argument("--c4-lv", type=int, default=20, help="log2 vertices of the C4 graph for the slowdown")
@@ -269,11 +271,9 @@ def main():
 
     # --- input: this rank's shard of the trace, generated in HBM (untimed) ---
     if args.format == "c32":
-        rec32, opsw, spc, woff, kd = c5.gpu_trace_c32(lb, seed, rank=rank, nshard=world)
-        dt = hr.DeviceTrace(None, woff, kd, rec32, opsw, spc)
-        n_acc_rank = 0
-        for lo in range(32):
-            n_acc_rank += int((((opsw >> (2 * lo)) & 3) != 3).sum().item())
+        rec32, recop, woff, kd = c5.gpu_trace_c32(lb, seed, rank=rank, nshard=world)
+        dt = hr.DeviceTrace(None, woff, kd, rec32, recop)
+        n_acc_rank = int(((recop & 3) != 3).sum().item())
     else:
         rec, woff, kd = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
         dt = hr.DeviceTrace(rec, woff, kd)
@@ -348,24 +348,27 @@ def main():
         host_trace = type("T", (), {})()
         host_trace.kdesc = kd
         host_trace.warp_off = woff.cpu().numpy().view(np.uint64)
+        dt.rec = dt.rec32 = dt.recop = None                 # free the device trace: staging replaces it
+        rec = rec32 = recop = None  # noqa: F841
+        torch.cuda.empty_cache()
         pinned = []
-        if dt.format == hr.HR_TRACE_C32:
-            for name, tsr in (("rec32", dt.rec32), ("ops", dt.ops), ("spc", dt.spc)):
-                h = torch.empty(tsr.numel(), dtype=tsr.dtype, pin_memory=True)
-                h.copy_(tsr)
-                pinned.append(h)
-                setattr(host_trace, name, h.numpy())
+        if args.e2e_format == "c32":
+            g32, gop, _, _ = c5.gpu_trace_c32(lb, seed, rank=rank, nshard=world)
+            parts = (("rec32", g32), ("recop", gop))
             host_trace.rec = None
         else:
-            h = torch.empty(dt.rec.numel(), dtype=torch.int64, pin_memory=True)
-            h.copy_(dt.rec)
-            pinned.append(h)
-            host_trace.rec = h.numpy().view(np.uint64)
+            grec, _, _ = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
+            parts = (("rec", grec),)
             host_trace.rec32 = None
-        h2d = sum(int(h.numel() * h.element_size()) for h in pinned) + int(host_trace.warp_off.nbytes)
-        dt.rec = dt.rec32 = dt.ops = dt.spc = None          # free the device trace: staging replaces it
-        rec = rec32 = opsw = spc = None  # noqa: F841
+        for name, tsr in parts:
+            h = torch.empty(tsr.numel(), dtype=tsr.dtype, pin_memory=True)
+            h.copy_(tsr)
+            pinned.append(h)
+            arr = h.numpy()
+            setattr(host_trace, name, arr.view(np.uint64) if name == "rec" else arr)
+        parts = g32 = gop = grec = None  # noqa: F841
         torch.cuda.empty_cache()
+        h2d = sum(int(h.numel() * h.element_size()) for h in pinned) + int(host_trace.warp_off.nbytes)
         host_replay = lambda: ck.replay_host(host_trace, stream)  # noqa: E731
         for _ in range(args.warmup):
             step(host_replay)
@@ -383,7 +386,7 @@ def main():
         parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == c5.planted(lb, seed)
         e2e = {"value": total_acc / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(16 + 24 * len(raw_e) // max(world, 1)),
-               "ms_per_step": e2e_ms, "format": args.format}
+               "ms_per_step": e2e_ms, "format": args.e2e_format}
         hr.hr_replay_timing(ck.ctx)
 
     cpu = None

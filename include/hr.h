@@ -95,7 +95,7 @@ typedef struct {
 /* Record encodings of an hr_trace. */
 enum {
     HR_TRACE_U64 = 0,   /* rec: one u64 record per lane and row (any word < 2^61) */
-    HR_TRACE_C32 = 1    /* rec32 + ops + spc: 140 B per row instead of 256 (words < 2^32) */
+    HR_TRACE_C32 = 1    /* rec32 + recop: 160 B per row instead of 256 (words < 2^32) */
 };
 
 /* A batch of synthetic access streams (tracegen/format.py documents the layout).
@@ -118,14 +118,12 @@ typedef struct {
     uint64_t n_warp_off;
     /* format HR_TRACE_C32 (rec unused): same rows, split into
      *   rec32  n_rows*32 u32: word (control code for control records)
-     *   ops    n_rows u64: 2-bit op of lane l at bits [2l+1:2l]
-     *   spc    n_rows u32: space of lane l at bit l
+     *   recop  n_rows*32 u8: op | space << 2
      * decoded in the kernel to the u64 record above; same ownership rules. */
     uint32_t format;
     uint32_t reserved;
     const uint32_t *rec32;
-    const uint64_t *ops;
-    const uint32_t *spc;
+    const uint8_t *recop;
 } hr_trace;
 
 typedef struct hr_ctx hr_ctx;   /* opaque */

@@ -36,7 +36,7 @@ struct hr_ctx {
     bool have_kernel = false;
     bool last_pooled = false;
     cudaStream_t stream = nullptr;
-    void *stage[4] = {nullptr, nullptr, nullptr, nullptr};   /* warp_off, rec|rec32, ops, spc */
+    void *stage[4] = {nullptr, nullptr, nullptr, nullptr};   /* warp_off, rec|rec32, recop, unused */
     size_t stage_cap[4] = {0, 0, 0, 0};
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
@@ -272,15 +272,15 @@ static bool trace_ok(const hr_trace *t)
     if (!t->n_kernels) return true;
     if (!t->kdesc || !t->warp_off) return false;
     if (t->format == HR_TRACE_U64) return t->rec != nullptr;
-    if (t->format == HR_TRACE_C32) return t->rec32 && t->ops && t->spc;
+    if (t->format == HR_TRACE_C32) return t->rec32 && t->recop;
     return false;
 }
 
 static hr_status dispatch(hr_ctx *c, const hr_trace *t, const uint64_t *rec, const uint32_t *rec32,
-                          const uint64_t *ops, const uint32_t *spc, const uint64_t *woff)
+                          const uint8_t *recop, const uint64_t *woff)
 {
     if (t->format == HR_TRACE_C32) {
-        hr_src_c32 src{rec32, ops, spc};
+        hr_src_c32 src{rec32, recop};
         return replay(c, t, src, woff, c->stream);
     }
     hr_src_u64 src{rec};
@@ -292,7 +292,7 @@ extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
-    return dispatch(c, t, t->rec, t->rec32, t->ops, t->spc, t->warp_off);
+    return dispatch(c, t, t->rec, t->rec32, t->recop, t->warp_off);
 }
 
 static hr_status stage(hr_ctx *c, void **buf, size_t *cap, const void *src, size_t bytes)
@@ -317,13 +317,12 @@ extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *st
     if (st) return st;
     if (t->format == HR_TRACE_C32) {
         if ((st = stage(c, &c->stage[1], &c->stage_cap[1], t->rec32, (size_t)t->n_rows * 128))) return st;
-        if ((st = stage(c, &c->stage[2], &c->stage_cap[2], t->ops, (size_t)t->n_rows * 8))) return st;
-        if ((st = stage(c, &c->stage[3], &c->stage_cap[3], t->spc, (size_t)t->n_rows * 4))) return st;
+        if ((st = stage(c, &c->stage[2], &c->stage_cap[2], t->recop, (size_t)t->n_rows * 32))) return st;
     } else {
         if ((st = stage(c, &c->stage[1], &c->stage_cap[1], t->rec, (size_t)t->n_rows * 256))) return st;
     }
     return dispatch(c, t, (const uint64_t *)c->stage[1], (const uint32_t *)c->stage[1],
-                    (const uint64_t *)c->stage[2], (const uint32_t *)c->stage[3], (const uint64_t *)c->stage[0]);
+                    (const uint8_t *)c->stage[2], (const uint64_t *)c->stage[0]);
 }
 
 static bool race_less(const hr_race &a, const hr_race &b)

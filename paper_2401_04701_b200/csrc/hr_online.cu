@@ -192,13 +192,13 @@ __global__ void __launch_bounds__(1024, 2) raw_replay_kernel(SRC src, const uint
     const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
     const bool active = lane < lanes;
     const uint64_t n = r1 - r0;
-    uint64_t x1 = (active && n > 0) ? src.row(r0, lane) : HR_NOP_REC;
-    uint64_t x2 = (active && n > 1) ? src.row(r0 + 1, lane) : HR_NOP_REC;
+    typename SRC::raw_t x1 = (active && n > 0) ? src.load(r0, lane) : SRC::nop();
+    typename SRC::raw_t x2 = (active && n > 1) ? src.load(r0 + 1, lane) : SRC::nop();
     int acc = 0;
     for (uint64_t i = 0; i < n; i++) {
-        const uint64_t x = x1;
+        const uint64_t x = SRC::decode(x1);
         x1 = x2;
-        x2 = (active && i + 2 < n) ? src.row(r0 + i + 2, lane) : HR_NOP_REC;
+        x2 = (active && i + 2 < n) ? src.load(r0 + i + 2, lane) : SRC::nop();
         const uint32_t op = (uint32_t)(x >> 62);
         const uint64_t w = x & HR_WORD_MASK;
         const unsigned st = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
@@ -240,7 +240,7 @@ extern "C" hr_status hrb_raw_replay(const hr_trace *t, int *data, uint64_t data_
         if (kd[0] == 0) continue;
         const dim3 g((unsigned)kd[0]), b((unsigned)(kd[1] * 32));
         if (t->format == HR_TRACE_C32)
-            raw_replay_kernel<<<g, b, 0, s>>>(hr_src_c32{t->rec32, t->ops, t->spc}, t->warp_off + kd[4],
+            raw_replay_kernel<<<g, b, 0, s>>>(hr_src_c32{t->rec32, t->recop}, t->warp_off + kd[4],
                                               (uint32_t)kd[1], (uint32_t)kd[2], data, data_words);
         else
             raw_replay_kernel<<<g, b, 0, s>>>(hr_src_u64{t->rec}, t->warp_off + kd[4], (uint32_t)kd[1],

@@ -167,12 +167,12 @@ __global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d,
     const uint64_t n = r1 - r0;
 
     uint32_t cnt = 0;                                                /* warp-uniform pool fill */
-    uint64_t x1 = (active && n > 0) ? src.row(r0, lane) : HR_NOP_REC;
-    uint64_t x2 = (active && n > 1) ? src.row(r0 + 1, lane) : HR_NOP_REC;
+    typename SRC::raw_t x1 = (active && n > 0) ? src.load(r0, lane) : SRC::nop();
+    typename SRC::raw_t x2 = (active && n > 1) ? src.load(r0 + 1, lane) : SRC::nop();
     for (uint64_t i = 0; i < n; i++) {
-        const uint64_t x = x1;
+        const uint64_t x = SRC::decode(x1);
         x1 = x2;
-        x2 = (active && i + 2 < n) ? src.row(r0 + i + 2, lane) : HR_NOP_REC;
+        x2 = (active && i + 2 < n) ? src.load(r0 + i + 2, lane) : SRC::nop();
         const uint32_t op = (uint32_t)(x >> 62);
         const uint64_t w = x & HR_WORD_MASK;
         if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {          /* barrier row: flush, then sync */

@@ -52,7 +52,7 @@ class HrTrace(ctypes.Structure):
                 ("n_kernels", ctypes.c_uint32), ("kernel_base", ctypes.c_uint32),
                 ("warp_off", ctypes.c_void_p), ("n_warp_off", ctypes.c_uint64),
                 ("format", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
-                ("rec32", ctypes.c_void_p), ("ops", ctypes.c_void_p), ("spc", ctypes.c_void_p)]
+                ("rec32", ctypes.c_void_p), ("recop", ctypes.c_void_p)]
 
 
 assert ctypes.sizeof(HrRace) == 24
@@ -220,10 +220,10 @@ def hr_destroy(ctx):
 class DeviceTrace:
     """A trace resident in HBM: torch tensors for the records and warp offsets,
     host kdesc.  U64 format: ``rec`` int64 (n_rows*32).  C32 format: ``rec32``
-    int32 (n_rows*32), ``ops`` int64 (n_rows), ``spc`` int32 (n_rows)."""
+    int32 and ``recop`` uint8 (op | space<<2), both n_rows*32."""
 
-    def __init__(self, rec, warp_off, kdesc: np.ndarray, rec32=None, ops=None, spc=None):
-        self.rec, self.rec32, self.ops, self.spc = rec, rec32, ops, spc
+    def __init__(self, rec, warp_off, kdesc: np.ndarray, rec32=None, recop=None):
+        self.rec, self.rec32, self.recop = rec, rec32, recop
         self.warp_off = warp_off
         self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
         self.format = HR_TRACE_C32 if rec32 is not None else HR_TRACE_U64
@@ -235,15 +235,14 @@ class DeviceTrace:
         wo = torch.from_numpy(np.ascontiguousarray(trace.warp_off).view(np.int64)).to(device)
         if compact:
             from tracegen.format import to_c32
-            r32, ops, spc = to_c32(trace)
+            r32, rop = to_c32(trace)
             return DeviceTrace(None, wo, trace.kdesc, torch.from_numpy(r32.view(np.int32)).to(device),
-                               torch.from_numpy(ops.view(np.int64)).to(device),
-                               torch.from_numpy(spc.view(np.int32)).to(device))
+                               torch.from_numpy(rop).to(device))
         rec = torch.from_numpy(np.ascontiguousarray(trace.rec).view(np.int64)).to(device)
         return DeviceTrace(rec, wo, trace.kdesc)
 
     def record_bytes(self) -> int:
-        return self.n_rows * (140 if self.format == HR_TRACE_C32 else 256)
+        return self.n_rows * (160 if self.format == HR_TRACE_C32 else 256)
 
     def c(self, kernel_base: int = 0) -> HrTrace:
         t = HrTrace()
@@ -255,7 +254,7 @@ class DeviceTrace:
         t.n_warp_off = self.warp_off.numel()
         t.format = self.format
         if self.format == HR_TRACE_C32:
-            t.rec32, t.ops, t.spc = self.rec32.data_ptr(), self.ops.data_ptr(), self.spc.data_ptr()
+            t.rec32, t.recop = self.rec32.data_ptr(), self.recop.data_ptr()
         else:
             t.rec = self.rec.data_ptr()
         return t
@@ -263,7 +262,7 @@ class DeviceTrace:
 
 def host_trace_c(trace, kernel_base: int = 0) -> HrTrace:
     """HrTrace over HOST arrays (for hr_replay_trace_host); keep `trace` alive.
-    `trace` has rec (U64) or rec32/ops/spc (C32) numpy arrays, kdesc, warp_off."""
+    `trace` has rec (U64) or rec32/recop (C32) numpy arrays, kdesc, warp_off."""
     t = HrTrace()
     t.kdesc = trace.kdesc.ctypes.data
     t.n_kernels = trace.kdesc.shape[0]
@@ -273,7 +272,7 @@ def host_trace_c(trace, kernel_base: int = 0) -> HrTrace:
     if getattr(trace, "rec32", None) is not None:
         t.format = HR_TRACE_C32
         t.n_rows = trace.rec32.shape[0] // 32
-        t.rec32, t.ops, t.spc = trace.rec32.ctypes.data, trace.ops.ctypes.data, trace.spc.ctypes.data
+        t.rec32, t.recop = trace.rec32.ctypes.data, trace.recop.ctypes.data
     else:
         t.n_rows = trace.rec.shape[0] // 32
         t.rec = trace.rec.ctypes.data
@@ -312,7 +311,7 @@ class Checker:
         hr_replay_trace(self.ctx, dtrace.c(kernel_base), stream)
 
     def replay_host(self, trace, stream: Optional[int] = None, kernel_base: int = 0):
-        """`trace`: numpy arrays (rec, or rec32/ops/spc) + kdesc + warp_off in host memory."""
+        """`trace`: numpy arrays (rec, or rec32/recop) + kdesc + warp_off in host memory."""
         if stream is None:
             import torch
             stream = torch.cuda.current_stream().cuda_stream

@@ -14,8 +14,8 @@ ap.add_argument("--options", type=int, default=0)
 ap.add_argument("--format", default="c32", choices=["c32", "u64"])
 a = ap.parse_args()
 if a.format == "c32":
-    r32, ops, spc, woff, kd = c5.gpu_trace_c32(a.lb)
-    dt = hr.DeviceTrace(None, woff, kd, r32, ops, spc)
+    r32, rop, woff, kd = c5.gpu_trace_c32(a.lb)
+    dt = hr.DeviceTrace(None, woff, kd, r32, rop)
 else:
     rec, woff, kd = c5.gpu_trace(a.lb)
     dt = hr.DeviceTrace(rec, woff, kd)

@@ -86,11 +86,10 @@ def test_c5_gpu_compact_generator_matches_cpu(nshard):
     lb = 3
     for rank in range(nshard):
         cpu = c5.cpu_trace(lb, rank=rank, nshard=nshard)
-        r32, ops, spc = to_c32(cpu)
-        g32, gops, gspc, off, kd = c5.gpu_trace_c32(lb, rank=rank, nshard=nshard)
+        r32, rop = to_c32(cpu)
+        g32, grop, off, kd = c5.gpu_trace_c32(lb, rank=rank, nshard=nshard)
         assert np.array_equal(g32.cpu().numpy().view(np.uint32), r32)
-        assert np.array_equal(gops.cpu().numpy().view(np.uint64), ops)
-        assert np.array_equal(gspc.cpu().numpy().view(np.uint32), spc)
+        assert np.array_equal(grop.cpu().numpy(), rop)
         assert np.array_equal(off.cpu().numpy().view(np.uint64), cpu.warp_off)
 
 
@@ -98,12 +97,12 @@ def test_c5_full_size_compact_closed_form():
     import torch
     h = hr()
     lb = 16
-    r32, ops, spc, off, kd = c5.gpu_trace_c32(lb)
+    r32, rop, off, kd = c5.gpu_trace_c32(lb)
     ck = h.Checker(c5.total_words(lb), 0, ring_capacity=1 << 20)
-    ck.replay(h.DeviceTrace(None, off, kd, r32, ops, spc))
+    ck.replay(h.DeviceTrace(None, off, kd, r32, rop))
     raw, flags = ck.report_raw()
     ck.close()
-    del r32, ops, spc
+    del r32, rop
     torch.cuda.empty_cache()
     assert flags == 0
     assert [(int(r["word"]), int(r["scope"])) for r in raw] == c5.planted(lb)

@@ -189,7 +189,7 @@ def test_empty_and_degenerate():
 
 @pytest.mark.parametrize("options", [16, 32])
 def test_compact_format_same_result(options):
-    """HR_TRACE_C32 (u32 word + per-row op/space words) decodes to the same
+    """HR_TRACE_C32 (u32 word + op/space byte per record) decodes to the same
     records: same racy set as the u64 encoding and the oracle."""
     tr = _random_batch(61, 40, max_blocks=4, max_warps=8, max_lanes=32, max_slots=12, n_words=500,
                        spaces=(0, 1), p_skip=0.3)
@@ -203,8 +203,8 @@ def test_compact_host_replay():
     from tracegen.format import to_c32
     h = hr()
     tr = tp.listing2(3, 4, 32)
-    r32, ops, spc = to_c32(tr)
-    host = type("T", (), {"rec32": r32, "ops": ops, "spc": spc, "kdesc": tr.kdesc, "warp_off": tr.warp_off,
+    r32, rop = to_c32(tr)
+    host = type("T", (), {"rec32": r32, "recop": rop, "kdesc": tr.kdesc, "warp_off": tr.warp_off,
                           "rec": None})()
     gmax, smem = h.trace_extent(tr)
     ck = h.Checker(gmax, smem)

@@ -68,9 +68,6 @@ def _gpu_lib():
         _gpu.c5_gen_gpu.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
-        _gpu.c5_pack_gpu.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                     ctypes.c_void_p]
-        _gpu.c5_pack_gpu.restype = ctypes.c_int
         _gpu.c5_gen_gpu.restype = ctypes.c_int
     return _gpu
 
@@ -145,21 +142,16 @@ def gpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1,
 
 
 def gpu_trace_c32(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda"):
-    """Same trace in the HR_TRACE_C32 encoding (140 B per row).  Returns
-    (rec32 int32, ops int64, spc int32, warp_off int64) tensors and kdesc."""
+    """Same trace in the HR_TRACE_C32 encoding (160 B per row).  Returns
+    (rec32 int32, recop uint8, warp_off int64) tensors and kdesc."""
     import torch
     lib = _gpu_lib()
     stream = torch.cuda.current_stream().cuda_stream
     off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), device, stream)
     n_rows = int(off[-1].item())
     rec32 = torch.empty(n_rows * 32, dtype=torch.int32, device=device)
-    opb = torch.empty(n_rows * 32, dtype=torch.uint8, device=device)
+    recop = torch.empty(n_rows * 32, dtype=torch.uint8, device=device)
     rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), 1, None, off.data_ptr(), None, rec32.data_ptr(),
-                        opb.data_ptr(), stream)
+                        recop.data_ptr(), stream)
     assert rc == 0, rc
-    ops = torch.empty(n_rows, dtype=torch.int64, device=device)
-    spc = torch.empty(n_rows, dtype=torch.int32, device=device)
-    rc = lib.c5_pack_gpu(n_rows, opb.data_ptr(), ops.data_ptr(), spc.data_ptr(), stream)
-    assert rc == 0, rc
-    del opb
-    return rec32, ops, spc, off, kdesc(lb)
+    return rec32, recop, off, kdesc(lb)

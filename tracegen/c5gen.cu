@@ -7,7 +7,7 @@
 
 /* one CUDA warp per simulated warp; pass 0 counts rows, pass 1 writes them:
  * u64 records to `out`, or (compact) the u32 word to out32 and op | space<<2
- * to the byte array outb (packed per row afterwards by c5_pack_kernel). */
+ * to the byte array outb (the HR_TRACE_C32 encoding). */
 __device__ __forceinline__ void c5_put(uint64_t *out, uint32_t *out32, uint8_t *outb, uint64_t i, uint64_t x)
 {
     if (out) { __stcs((unsigned long long *)&out[i], (unsigned long long)x); return; }
@@ -42,28 +42,6 @@ __global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint64
         row += maxk + 1;
     }
     if (!pass && l == 0) rows_out[gw] = row;
-}
-
-/* per row: ops (2-bit op of lane l at bits 2l+1:2l) and spc (space bit l) */
-__global__ void c5_pack_kernel(uint64_t n_rows, const uint8_t *opb, uint64_t *ops, uint32_t *spc)
-{
-    uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_rows) return;
-    uint64_t o = 0;
-    uint32_t s = 0;
-    for (uint32_t l = 0; l < 32; l++) {
-        uint8_t b = opb[r * 32 + l];
-        o |= (uint64_t)(b & 3u) << (2 * l);
-        s |= (uint32_t)((b >> 2) & 1u) << l;
-    }
-    ops[r] = o;
-    spc[r] = s;
-}
-
-extern "C" int c5_pack_gpu(uint64_t n_rows, const uint8_t *opb, uint64_t *ops, uint32_t *spc, void *stream)
-{
-    c5_pack_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, opb, ops, spc);
-    return (int)cudaGetLastError();
 }
 
 extern "C" int c5_gen_gpu(uint64_t seed, uint32_t lb, uint32_t rank, uint32_t log2n, int pass,

@@ -227,19 +227,15 @@ def make_trace(kernels: Sequence[Kernel]) -> Trace:
 
 
 def to_c32(trace: Trace):
-    """The HR_TRACE_C32 encoding of a trace (include/hr.h): per row 32 u32
-    words, one u64 of 2-bit ops (lane l at bits 2l+1:2l) and one u32 space
-    mask.  Requires every word < 2^32."""
-    rows = trace.rec.reshape(-1, LANES_PER_ROW)
-    word = rows & np.uint64(WORD_MASK)
-    if rows.size and int(word.max()) >= (1 << 32):
+    """The HR_TRACE_C32 encoding of a trace (include/hr.h): per record a u32
+    word and a byte op | space << 2 (160 B per row).  Requires words < 2^32."""
+    word = trace.rec & np.uint64(WORD_MASK)
+    if word.size and int(word.max()) >= (1 << 32):
         raise ValueError("C32 encoding needs words < 2^32")
-    op = rows >> np.uint64(62)
-    sp = (rows >> np.uint64(61)) & np.uint64(1)
-    shifts = np.arange(LANES_PER_ROW, dtype=np.uint64)
-    ops = np.bitwise_or.reduce(op << (np.uint64(2) * shifts), axis=1).astype(np.uint64)
-    spc = np.bitwise_or.reduce(sp << shifts, axis=1).astype(np.uint32)
-    return np.ascontiguousarray(word.reshape(-1).astype(np.uint32)), ops, spc
+    op = trace.rec >> np.uint64(62)
+    sp = (trace.rec >> np.uint64(61)) & np.uint64(1)
+    return (np.ascontiguousarray(word.astype(np.uint32)),
+            np.ascontiguousarray((op | (sp << np.uint64(2))).astype(np.uint8)))
 
 
 def single_kernel(blocks, warps, lanes, thread_events, smem_words=0) -> Trace:
