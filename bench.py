@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--ref-lb", type=int, default=8, help="C5 sample per --impl reference step")
     ap.add_argument("--options", type=int, default=0, help="extra HR_OPT_* bits (ablations)")
     ap.add_argument("--no-slowdown", action="store_true")
+    ap.add_argument("--double-shadow", action="store_true",
+                    help="HR_OPT_DOUBLE_SHADOW: reset the previous kernel's shadow on a side stream")
     ap.add_argument("--format", default="u64", choices=["c32", "u64"],
                     help="device-resident trace encoding (include/hr.h HR_TRACE_U64 = 256 B/row, C32 = 160 B/row)")
     ap.add_argument("--e2e-format", default="c32", choices=["c32", "u64"],
@@ -280,8 +282,8 @@ def main():
         n_acc_rank = int((((rec >> 62) & 3) != 3).sum().item())
     torch.cuda.synchronize()
     n_rows = dt.n_rows
-    ck = hr.Checker(c5.total_words(lb), 0, shard=(rank, world), options=hr.HR_OPT_TIMING | args.options,
-                    ring_capacity=1 << 21)
+    opts = hr.HR_OPT_TIMING | args.options | (hr.HR_OPT_DOUBLE_SHADOW if args.double_shadow else 0)
+    ck = hr.Checker(c5.total_words(lb), 0, shard=(rank, world), options=opts, ring_capacity=1 << 21)
 
     def step(replay_fn):
         ck.reset()
@@ -410,8 +412,11 @@ def main():
                          "algo_bytes_rule": f"records ({args.format}: {dt.record_bytes() // max(n_rows, 1)} B/row) "
                                             "+ 16 B shadow RMW per checked access"},
             "literal_roofline_frac": literal,
-            "step_breakdown_ms": {"replay_kernel": kern_ms_launch, "shadow_reset": reset_ms_launch,
-                                  "rest(report,ring reset,exchange)": ms_step - kern_ms_launch - reset_ms_launch},
+            "step_breakdown_ms": {"replay_kernel": kern_ms_launch,
+                                  "shadow_reset" + (" (side stream, overlapped)" if args.double_shadow else ""):
+                                      reset_ms_launch,
+                                  "rest(report,ring reset,exchange)":
+                                      ms_step - kern_ms_launch - (0.0 if args.double_shadow else reset_ms_launch)},
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": n_kern,

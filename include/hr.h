@@ -74,7 +74,9 @@ enum {
     HR_OPT_TIMING = 4u,        /* record CUDA events around every shadow reset and replay launch */
     HR_OPT_NO_SPECULATE = 8u,  /* first attempt loads the shadow word instead of speculating INIT */
     HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen by sampled record density) */
-    HR_OPT_POOL = 32u          /* replay with warp pools of valid accesses (sparse traces) */
+    HR_OPT_POOL = 32u,         /* replay with warp pools of valid accesses (sparse traces) */
+    HR_OPT_DOUBLE_SHADOW = 64u /* two global shadows: the kernel-boundary reset (a11) of one runs on a
+                                  side stream while the next kernel uses the other (2x shadow memory) */
 };
 
 /* One unique racy address.  24 bytes.
@@ -152,7 +154,10 @@ hr_status hr_shadow_alloc(hr_ctx *ctx, hr_space space, uint64_t base_word, uint6
                           void **dev_region);
 
 /* New kernel epoch: a kernel boundary orders everything, so the global shadow
- * is reset to INIT (all-zero words) on `stream`. */
+ * is reset to INIT (all-zero words) on `stream`; skipped if
+ * no kernel used it since the last reset.  With HR_OPT_DOUBLE_SHADOW the other
+ * (already zero) buffer becomes current and the used one is zeroed on a side
+ * stream after its kernel completes. */
 hr_status hr_kernel_begin(hr_ctx *ctx, void *stream);
 
 /* Replay every kernel of `t` on `stream`: for each kernel, hr_kernel_begin then

@@ -64,6 +64,7 @@ struct hr_dev {
     uint32_t wc_bits;             /* bc occupies [31:wc_bits], wc [wc_bits-1:0] */
     uint32_t bc_max, wc_max;
     uint32_t options;             /* HR_OPT_* */
+    uint32_t block_base;          /* simulated block of blockIdx 0 (chunked replay launches) */
 };
 
 /* Per-thread registers. */
@@ -363,7 +364,7 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     for (uint32_t i = ltid; i < smem_words; i += nthr) smem_shadow[i] = 0ull;
     __syncthreads();
     hr_thr t;
-    uint32_t block = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    uint32_t block = d.block_base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     t.tid = (block << 10) | ((ltid >> 5) << 5) | (ltid & 31u);
     t.bc = 0;
     t.wc = 0;

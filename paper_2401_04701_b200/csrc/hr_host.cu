@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -25,7 +26,13 @@ struct hr_ctx {
     int device = 0;
     hr_config cfg{};
     uint32_t shard_rank = 0, shard_count = 1, shard_log2 = 0;
-    unsigned long long *gshadow = nullptr;
+    unsigned long long *gshadow = nullptr;       /* current buffer */
+    unsigned long long *gbuf[2] = {nullptr, nullptr};
+    int gcur = 0;
+    bool double_shadow = false;
+    bool dirty[2] = {false, false};              /* buffer used by a kernel since its last reset */
+    cudaStream_t side = nullptr;                 /* deferred resets (double shadow) */
+    cudaEvent_t used_done[2] = {nullptr, nullptr}, reset_done[2] = {nullptr, nullptr};
     uint64_t gbase = 0, gwords = 0, glocal = 0;
     uint32_t smem_words_max = 0;
     hr_race *ring = nullptr;
@@ -36,6 +43,7 @@ struct hr_ctx {
     bool have_kernel = false;
     bool last_pooled = false;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;                 /* host-trace staging copies */
     void *stage[4] = {nullptr, nullptr, nullptr, nullptr};   /* warp_off, rec|rec32, recop, unused */
     size_t stage_cap[4] = {0, 0, 0, 0};
     std::vector<cudaEvent_t> ev_pool;
@@ -172,22 +180,47 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
     }
     if (space != HR_GLOBAL || n_words == 0 || base_word + n_words > (1ull << 61))
         return fail(c, HR_E_ARG, "bad global region");
-    if (c->gshadow) {
-        cudaFree(c->gshadow);
-        c->gshadow = nullptr;
-    }
+    for (int b = 0; b < 2; b++)
+        if (c->gbuf[b]) { cudaFree(c->gbuf[b]); c->gbuf[b] = nullptr; }
+    c->gshadow = nullptr;
     /* local slice: this shard's 512-word granules, packed */
     uint64_t gran = (n_words + 511) >> 9;
     uint64_t local_gran = (gran + c->shard_count - 1) >> c->shard_log2;
     uint64_t local = local_gran << 9;
-    if (cudaMalloc(&c->gshadow, local * 8) != cudaSuccess)
-        return fail(c, HR_E_NOMEM, "cudaMalloc(%llu B) for the global shadow failed",
-                    (unsigned long long)(local * 8));
-    CU(cudaMemset(c->gshadow, 0, local * 8));
+    c->double_shadow = (c->cfg.options & HR_OPT_DOUBLE_SHADOW) != 0;
+    for (int b = 0; b < (c->double_shadow ? 2 : 1); b++) {
+        if (cudaMalloc(&c->gbuf[b], local * 8) != cudaSuccess)
+            return fail(c, HR_E_NOMEM, "cudaMalloc(%llu B) for the global shadow failed",
+                        (unsigned long long)(local * 8));
+        CU(cudaMemset(c->gbuf[b], 0, local * 8));
+        c->dirty[b] = false;
+    }
+    if (c->double_shadow && !c->side) {
+        CU(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; b++) {
+            CU(cudaEventCreateWithFlags(&c->used_done[b], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->reset_done[b], cudaEventDisableTiming));
+            CU(cudaEventRecord(c->reset_done[b], c->side));
+        }
+    }
+    c->gcur = 0;
+    c->gshadow = c->gbuf[0];
     c->gbase = base_word;
     c->gwords = n_words;
     c->glocal = local;
     if (dev_region) *dev_region = c->gshadow;
+    return HR_OK;
+}
+
+/* Zero one shadow buffer on stream `s`, with HR_OPT_TIMING events. */
+static hr_status reset_buffer(hr_ctx *c, int b, cudaStream_t s)
+{
+    bool timing = c->cfg.options & HR_OPT_TIMING;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+    CU(cudaMemsetAsync(c->gbuf[b], 0, c->glocal * 8, s));
+    if (timing) { CU(cudaEventRecord(e1, s)); c->ev_reset.push_back({e0, e1}); }
+    c->dirty[b] = false;
     return HR_OK;
 }
 
@@ -196,13 +229,26 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
-    if (c->gshadow) {
-        bool timing = c->cfg.options & HR_OPT_TIMING;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, c->stream)); }
-        CU(cudaMemsetAsync(c->gshadow, 0, c->glocal * 8, c->stream));
-        if (timing) { CU(cudaEventRecord(e1, c->stream)); c->ev_reset.push_back({e0, e1}); }
+    if (!c->gshadow) return HR_OK;
+    if (!c->double_shadow) {
+        if (c->dirty[0]) { hr_status st = reset_buffer(c, 0, c->stream); if (st) return st; }
+        c->dirty[0] = true;
+        return HR_OK;
     }
+    /* double shadow: the last kernel's buffer is zeroed on the side stream
+     * (after that kernel, overlapping the next one); the other becomes current */
+    const int prev = c->gcur, next = prev ^ 1;
+    if (c->dirty[prev]) {
+        CU(cudaEventRecord(c->used_done[prev], c->stream));
+        CU(cudaStreamWaitEvent(c->side, c->used_done[prev], 0));
+        hr_status st = reset_buffer(c, prev, c->side);
+        if (st) return st;
+        CU(cudaEventRecord(c->reset_done[prev], c->side));
+    }
+    CU(cudaStreamWaitEvent(c->stream, c->reset_done[next], 0));
+    c->gcur = next;
+    c->gshadow = c->gbuf[next];
+    c->dirty[next] = true;
     return HR_OK;
 }
 
@@ -225,43 +271,62 @@ static hr_status choose_pool(hr_ctx *c, SRC src, uint64_t n_rows, cudaStream_t s
     return HR_OK;
 }
 
+static hr_status check_kernel(hr_ctx *c, const hr_trace *t, uint32_t k)
+{
+    const uint64_t *kd = t->kdesc + 8ull * k;
+    uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
+    if (blocks == 0) return HR_OK;
+    if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32)
+        return fail(c, HR_E_ARG, "kernel %u: grid %llux%llux%llu outside the 17/5/5-bit tid", k,
+                    (unsigned long long)blocks, (unsigned long long)warps, (unsigned long long)lanes);
+    if (smem_words > c->smem_words_max)
+        return fail(c, HR_E_STATE, "kernel %u needs %llu shared shadow words (registered %u)", k,
+                    (unsigned long long)smem_words, c->smem_words_max);
+    if (woi + blocks * warps + 1 > t->n_warp_off) return fail(c, HR_E_ARG, "kernel %u: warp_off out of range", k);
+    return HR_OK;
+}
+
+/* One launch over simulated blocks [b0, b1) of kernel k (the whole kernel in
+ * one launch for device traces; block-range chunks for host traces — blocks
+ * are unordered by happens-before, so chunked launches replay the same kernel). */
+template <typename SRC>
+static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const uint64_t *woff, cudaStream_t s,
+                        bool pool, uint64_t b0, uint64_t b1)
+{
+    const uint64_t *kd = t->kdesc + 8ull * k;
+    uint64_t warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
+    uint32_t kid = t->kernel_base + k;
+    hr_dev d = make_dev(c, kid);
+    d.block_base = (uint32_t)b0;
+    size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
+    void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
+        pool ? hr_replay_kernel<true, SRC> : hr_replay_kernel<false, SRC>;
+    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bool timing = c->cfg.options & HR_OPT_TIMING;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+    kern<<<(unsigned)(b1 - b0), (unsigned)(warps * 32), smem, s>>>(d, src, woff + woi + b0 * warps, (uint32_t)warps,
+                                                                   (uint32_t)lanes, (uint32_t)smem_words);
+    CU(cudaGetLastError());
+    if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
+    c->last_kernel = kid;
+    c->have_kernel = true;
+    return HR_OK;
+}
+
 template <typename SRC>
 static hr_status replay(hr_ctx *c, const hr_trace *t, SRC src, const uint64_t *woff, cudaStream_t s)
 {
     bool pool = false;
-    hr_status pst = choose_pool(c, src, t->n_rows, s, &pool);
-    if (pst) return pst;
+    hr_status st = choose_pool(c, src, t->n_rows, s, &pool);
+    if (st) return st;
     c->last_pooled = pool;
     for (uint32_t k = 0; k < t->n_kernels; k++) {
-        const uint64_t *kd = t->kdesc + 8ull * k;
-        uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
-        if (blocks == 0) continue;
-        if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32)
-            return fail(c, HR_E_ARG, "kernel %u: grid %llux%llux%llu outside the 17/5/5-bit tid",
-                        k, (unsigned long long)blocks, (unsigned long long)warps, (unsigned long long)lanes);
-        if (smem_words > c->smem_words_max)
-            return fail(c, HR_E_STATE, "kernel %u needs %llu shared shadow words (registered %u)", k,
-                        (unsigned long long)smem_words, c->smem_words_max);
-        if (woi + blocks * warps + 1 > t->n_warp_off)
-            return fail(c, HR_E_ARG, "kernel %u: warp_off out of range", k);
-        hr_status st = hr_kernel_begin(c, s);
-        if (st) return st;
-        uint32_t kid = t->kernel_base + k;
-        hr_dev d = make_dev(c, kid);
-        size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
-        void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
-            pool ? hr_replay_kernel<true, SRC> : hr_replay_kernel<false, SRC>;
-        if (smem > 48 * 1024)
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        bool timing = c->cfg.options & HR_OPT_TIMING;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
-        kern<<<(unsigned)blocks, (unsigned)(warps * 32), smem, s>>>(d, src, woff + woi, (uint32_t)warps,
-                                                                  (uint32_t)lanes, (uint32_t)smem_words);
-        CU(cudaGetLastError());
-        if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
-        c->last_kernel = kid;
-        c->have_kernel = true;
+        if ((st = check_kernel(c, t, k))) return st;
+        const uint64_t blocks = t->kdesc[8ull * k];
+        if (!blocks) continue;
+        if ((st = hr_kernel_begin(c, s))) return st;
+        if ((st = launch(c, t, k, src, woff, s, pool, 0, blocks))) return st;
     }
     return HR_OK;
 }
@@ -295,34 +360,99 @@ extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
     return dispatch(c, t, t->rec, t->rec32, t->recop, t->warp_off);
 }
 
-static hr_status stage(hr_ctx *c, void **buf, size_t *cap, const void *src, size_t bytes)
+static hr_status reserve(hr_ctx *c, int i, size_t bytes)
 {
-    if (bytes > *cap) {
-        if (*buf) cudaFree(*buf);
-        *buf = nullptr;
-        *cap = 0;
-        if (cudaMalloc(buf, bytes) != cudaSuccess) return fail(c, HR_E_NOMEM, "staging %zu bytes failed", bytes);
-        *cap = bytes;
+    if (bytes > c->stage_cap[i]) {
+        if (c->stage[i]) cudaFree(c->stage[i]);
+        c->stage[i] = nullptr;
+        c->stage_cap[i] = 0;
+        if (cudaMalloc(&c->stage[i], bytes) != cudaSuccess) return fail(c, HR_E_NOMEM, "staging %zu bytes failed", bytes);
+        c->stage_cap[i] = bytes;
     }
-    if (bytes) CU(cudaMemcpyAsync(*buf, src, bytes, cudaMemcpyHostToDevice, c->stream));
     return HR_OK;
 }
 
+/* Host-side density sample (same rule as the device probe). */
+static bool host_pool_choice(hr_ctx *c, const hr_trace *t)
+{
+    if (c->cfg.options & HR_OPT_NO_POOL) return false;
+    if (c->cfg.options & HR_OPT_POOL) return true;
+    if (!t->n_rows) return false;
+    uint64_t acc = 0, tot = 0;
+    for (uint32_t s = 0; s < 2048; s++) {
+        uint64_t row = (uint64_t)((double)s * (double)t->n_rows / 2048.0);
+        if (row >= t->n_rows) break;
+        for (uint32_t l = 0; l < 32; l++) {
+            uint32_t op = t->format == HR_TRACE_C32 ? (t->recop[row * 32 + l] & 3u) : (uint32_t)(t->rec[row * 32 + l] >> 62);
+            acc += op != 3u;
+            tot++;
+        }
+    }
+    return tot && (double)acc < 0.9 * (double)tot;
+}
+
+/* Host traces: records are copied in block-range chunks on a copy stream and
+ * each chunk is replayed as soon as it lands, so the PCIe transfer of chunk
+ * i+1 overlaps the replay of chunk i. */
 extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *stream)
 {
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
-    hr_status st = stage(c, &c->stage[0], &c->stage_cap[0], t->warp_off, (size_t)t->n_warp_off * 8);
-    if (st) return st;
-    if (t->format == HR_TRACE_C32) {
-        if ((st = stage(c, &c->stage[1], &c->stage_cap[1], t->rec32, (size_t)t->n_rows * 128))) return st;
-        if ((st = stage(c, &c->stage[2], &c->stage_cap[2], t->recop, (size_t)t->n_rows * 32))) return st;
-    } else {
-        if ((st = stage(c, &c->stage[1], &c->stage_cap[1], t->rec, (size_t)t->n_rows * 256))) return st;
+    const bool c32 = t->format == HR_TRACE_C32;
+    hr_status st;
+    if ((st = reserve(c, 0, (size_t)t->n_warp_off * 8))) return st;
+    if ((st = reserve(c, 1, (size_t)t->n_rows * (c32 ? 128 : 256)))) return st;
+    if (c32 && (st = reserve(c, 2, (size_t)t->n_rows * 32))) return st;
+    if (!c->copy) CU(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    /* the copy stream may overwrite staging only after earlier work on `stream` */
+    cudaEvent_t start = get_event(c);
+    CU(cudaEventRecord(start, c->stream));
+    CU(cudaStreamWaitEvent(c->copy, start, 0));
+    c->ev_pool.push_back(start);
+    CU(cudaMemcpyAsync(c->stage[0], t->warp_off, (size_t)t->n_warp_off * 8, cudaMemcpyHostToDevice, c->copy));
+    const bool pool = host_pool_choice(c, t);
+    c->last_pooled = pool;
+    const uint64_t *dwoff = (const uint64_t *)c->stage[0];
+    size_t chunk_bytes = (size_t)1 << 30;                       /* ~1 GiB of records per chunk */
+    if (const char *e = getenv("HR_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)strtoull(e, nullptr, 10);
+    if (chunk_bytes < 256) chunk_bytes = 256;
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        if ((st = check_kernel(c, t, k))) return st;
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        const uint64_t blocks = kd[0], warps = kd[1], woi = kd[4];
+        if (!blocks) continue;
+        if ((st = hr_kernel_begin(c, c->stream))) return st;
+        const uint64_t krows = t->warp_off[woi + blocks * warps] - t->warp_off[woi];
+        const uint64_t row_bytes = c32 ? 160 : 256;
+        uint64_t nchunks = (krows * row_bytes + chunk_bytes - 1) / chunk_bytes;
+        if (nchunks < 1) nchunks = 1;
+        if (nchunks > blocks) nchunks = blocks;
+        for (uint64_t ci = 0; ci < nchunks; ci++) {
+            const uint64_t b0 = blocks * ci / nchunks, b1 = blocks * (ci + 1) / nchunks;
+            const uint64_t r0 = t->warp_off[woi + b0 * warps], r1 = t->warp_off[woi + b1 * warps];
+            if (r1 > r0) {
+                if (c32) {
+                    CU(cudaMemcpyAsync((uint32_t *)c->stage[1] + r0 * 32, t->rec32 + r0 * 32, (r1 - r0) * 128,
+                                       cudaMemcpyHostToDevice, c->copy));
+                    CU(cudaMemcpyAsync((uint8_t *)c->stage[2] + r0 * 32, t->recop + r0 * 32, (r1 - r0) * 32,
+                                       cudaMemcpyHostToDevice, c->copy));
+                } else {
+                    CU(cudaMemcpyAsync((uint64_t *)c->stage[1] + r0 * 32, t->rec + r0 * 32, (r1 - r0) * 256,
+                                       cudaMemcpyHostToDevice, c->copy));
+                }
+            }
+            cudaEvent_t landed = get_event(c);
+            CU(cudaEventRecord(landed, c->copy));
+            CU(cudaStreamWaitEvent(c->stream, landed, 0));
+            c->ev_pool.push_back(landed);
+            if (c32) st = launch(c, t, k, hr_src_c32{(const uint32_t *)c->stage[1], (const uint8_t *)c->stage[2]},
+                                 dwoff, c->stream, pool, b0, b1);
+            else st = launch(c, t, k, hr_src_u64{(const uint64_t *)c->stage[1]}, dwoff, c->stream, pool, b0, b1);
+            if (st) return st;
+        }
     }
-    return dispatch(c, t, (const uint64_t *)c->stage[1], (const uint32_t *)c->stage[1],
-                    (const uint8_t *)c->stage[2], (const uint64_t *)c->stage[0]);
+    return HR_OK;
 }
 
 static bool race_less(const hr_race &a, const hr_race &b)
@@ -479,7 +609,14 @@ extern "C" void hr_destroy(hr_ctx *c)
 {
     if (!c) return;
     cudaSetDevice(c->device);
-    if (c->gshadow) cudaFree(c->gshadow);
+    if (c->side) cudaStreamSynchronize(c->side);
+    for (int b = 0; b < 2; b++) {
+        if (c->gbuf[b]) cudaFree(c->gbuf[b]);
+        if (c->used_done[b]) cudaEventDestroy(c->used_done[b]);
+        if (c->reset_done[b]) cudaEventDestroy(c->reset_done[b]);
+    }
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
     if (c->ring) cudaFree(c->ring);
     if (c->tail) cudaFree(c->tail);
     if (c->counters) cudaFree(c->counters);

@@ -95,7 +95,7 @@ def test_hot_words_contention(options):
     assert gpu_set(tr, options=options) == oracle_set(tr)
 
 
-@pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8])
+@pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8, 64, 64 | 32])
 def test_ablations_same_result(options):
     """Coalescing off / fast exits off / no speculation / forced row or pooled
     replay change the commit order and the traffic, never the result
@@ -129,10 +129,27 @@ def test_repeated_runs_identical():
         assert gpu_set(tr) == o
 
 
-def test_ring_overflow_falls_back_to_shadow_scan():
+@pytest.mark.parametrize("options", [0, 64])
+def test_reused_context_across_replays(options):
+    """One ctx, several replays of multi-kernel traces: every kernel starts from
+    a clean shadow (kernel boundary, a11), with one or two shadow buffers."""
+    h = hr()
+    trs = [_random_batch(70 + i, 12, max_blocks=4, max_warps=4, max_lanes=32, max_slots=10, n_words=64,
+                         spaces=(0, 1)) for i in range(3)]
+    ck = h.Checker(4096, 64, options=options)
+    for tr in trs + trs[::-1]:
+        ck.reset()
+        ck.replay(h.DeviceTrace.from_trace(tr))
+        races, fl, _ = ck.report()
+        assert ([tuple(r) for r in races], fl) == oracle_set(tr)
+    ck.close()
+
+
+@pytest.mark.parametrize("options", [0, 64])
+def test_ring_overflow_falls_back_to_shadow_scan(options):
     # one kernel, many racy global words
     tr = tp.listing2(4, 8, 32)
-    g, fl = gpu_set(tr, ring_capacity=8)
+    g, fl = gpu_set(tr, ring_capacity=8, options=options)
     o, _ = oracle_set(tr)
     assert fl & hr().HR_F_RING_OVERFLOW
     assert g == o
@@ -211,3 +228,30 @@ def test_compact_host_replay():
     ck.replay_host(host)
     races, fl, _ = ck.report()
     assert [tuple(r) for r in races] == oracle_set(tr)[0]
+
+
+@pytest.mark.parametrize("compact", [False, True])
+def test_chunked_host_replay(compact, monkeypatch):
+    """hr_replay_trace_host replays a kernel in block-range chunks as their
+    records land (blocks are unordered by happens-before): force tiny chunks."""
+    from tracegen.format import to_c32
+    monkeypatch.setenv("HR_HOST_CHUNK_BYTES", "4096")
+    h = hr()
+    tr = _random_batch(81, 6, max_blocks=40, max_warps=4, max_lanes=32, max_slots=10, n_words=300,
+                       spaces=(0, 1), grid=(37, 3, 32))
+    tr2 = tp.listing2(33, 2, 32)
+    for t in (tr, tr2):
+        gmax, smem = h.trace_extent(t)
+        ck = h.Checker(gmax, smem)
+        if compact:
+            r32, rop = to_c32(t)
+            host = type("T", (), {"rec32": r32, "recop": rop, "kdesc": t.kdesc, "warp_off": t.warp_off,
+                                  "rec": None})()
+        else:
+            host = t
+        for _ in range(2):
+            ck.reset()
+            ck.replay_host(host)
+            races, fl, _ = ck.report()
+            assert ([tuple(r) for r in races], fl) == oracle_set(t)
+        ck.close()
