@@ -34,6 +34,9 @@ extern "C" {
 hr_status hrb_c1(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int rounds, int removed, int *data,
                  void *stream);
 
+/* C1 written with the transparent wrapper of hr_array.cuh (always instrumented). */
+hr_status hrb_c1_array(hr_ctx *ctx, uint32_t kernel_id, int rounds, int removed, int *data, void *stream);
+
 /* C3: (n/16)^2 blocks x 256 threads, two 18x18 SMEM tiles, `sweeps` Jacobi
  * sweeps; data[0, n*n) input, data[n*n, 2n*n) output; removed = sweep whose
  * trailing barrier is dropped, -1 none (tracegen.stencil.stencil_trace). */

@@ -11,6 +11,7 @@
 
 #include "hr.h"
 #include "hr_bench.h"
+#include "hr_array.cuh"
 #include "hr_device.cuh"
 #include "hr_records.cuh"
 
@@ -70,6 +71,33 @@ __global__ void __launch_bounds__(32) c1_kernel(hr_dev d, int *data, int rounds,
             data[out + r] = v;
         }
         bar<I>(d, t);
+    }
+}
+
+/* ---- C1 again, written against the transparent wrapper (hr_array.cuh):
+ * the kernel body reads like the uninstrumented code ---- */
+__global__ void __launch_bounds__(32) c1_array_kernel(hr_dev d, int *data, int rounds, int removed)
+{
+    __shared__ int s_raw[256];
+    __shared__ __align__(16) unsigned char fsm[HR_FSM_SMEM_BYTES];
+    __shared__ unsigned long long sh[256];
+    hr_ctx_dev ctx(d, fsm, sh, 256);
+    hr_array<int> g(ctx, data, HR_GLOBAL, 0);
+    hr_array<int> s(ctx, s_raw, HR_SHARED, 0);
+    const int lane = threadIdx.x, out = rounds * 256;
+    for (int r = 0; r < rounds; r++) {
+        for (int i = lane; i < 256; i += 32) s[i] = g[r * 256 + i];
+        if (removed != 0) ctx.syncthreads();
+        for (int st = 128; st >= 1; st >>= 1) {
+            for (int i = lane; i < st; i += 32) {
+                int a = s[i];
+                int b = s[i + st];
+                s[i] = a + b;
+            }
+            if (removed != st) ctx.syncthreads();
+        }
+        if (lane == 0) g[out + r] = s[0];
+        ctx.syncthreads();
     }
 }
 
@@ -259,6 +287,16 @@ extern "C" hr_status hrb_c1(hr_ctx *ctx, int instrumented, uint32_t kernel_id, i
     cudaStream_t s = (cudaStream_t)stream;
     if (instrumented) c1_kernel<true><<<1, 32, 0, s>>>(d, data, rounds, removed);
     else c1_kernel<false><<<1, 32, 0, s>>>(d, data, rounds, removed);
+    return launched();
+}
+
+extern "C" hr_status hrb_c1_array(hr_ctx *ctx, uint32_t kernel_id, int rounds, int removed, int *data,
+                                  void *stream)
+{
+    hr_dev d;
+    hr_status st = prepare(ctx, 1, kernel_id, stream, &d);
+    if (st) return st;
+    c1_array_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d, data, rounds, removed);
     return launched();
 }
 

@@ -11,7 +11,7 @@ import numpy as np
 
 from . import hirace
 
-EXPORTS = ("hrb_c1", "hrb_c3", "hrb_c4_level", "hrb_c4_hist", "hrb_raw_replay")
+EXPORTS = ("hrb_c1", "hrb_c1_array", "hrb_c3", "hrb_c4_level", "hrb_c4_hist", "hrb_raw_replay")
 
 
 def _lib():
@@ -19,6 +19,7 @@ def _lib():
     if not getattr(lib, "_hrb_ready", False):
         vp, i, u32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32
         lib.hrb_c1.argtypes = [vp, i, u32, i, i, vp, vp]
+        lib.hrb_c1_array.argtypes = [vp, u32, i, i, vp, vp]
         lib.hrb_c3.argtypes = [vp, i, u32, i, i, i, vp, vp]
         lib.hrb_c4_level.argtypes = [vp, i, u32, i, u32, vp, vp, vp, i, vp, vp]
         lib.hrb_c4_hist.argtypes = [vp, i, u32, i, u32, vp, vp, vp]
@@ -44,6 +45,12 @@ C1_REMOVED = {None: -1, "load": 0}
 def c1(ctx, data, instrumented: bool, removed=32, rounds: int = 8, kernel_id: int = 0):
     r = C1_REMOVED.get(removed, removed)
     _ok(_lib().hrb_c1(ctx, int(instrumented), kernel_id, rounds, r, data.data_ptr(), _stream()), ctx, "hrb_c1")
+
+
+def c1_array(ctx, data, removed=32, rounds: int = 8, kernel_id: int = 0):
+    """C1 through the hr_array<T> wrapper (transparent instrumentation)."""
+    r = C1_REMOVED.get(removed, removed)
+    _ok(_lib().hrb_c1_array(ctx, kernel_id, rounds, r, data.data_ptr(), _stream()), ctx, "hrb_c1_array")
 
 
 def c3(ctx, data, instrumented: bool, n: int = 512, sweeps: int = 42, removed: Optional[int] = 20,

@@ -1,0 +1,20 @@
+"""Profiling driver for one replay config (ncu target).  Not a bench."""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2401_04701_b200 import hirace as hr
+from tracegen import c4, stencil
+
+ap = argparse.ArgumentParser()
+ap.add_argument("config", choices=["c3", "c4"])
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+if a.config == "c3":
+    tr, words, smem = stencil.stencil_trace(removed=20), 2 * 512 * 512, 648
+else:
+    g = c4.Graph(20)
+    tr, words, smem = g.trace(True), c4.total_words(20), 0
+dt = hr.DeviceTrace.from_trace(tr)
+ck = hr.Checker(words, smem, ring_capacity=1 << 22, options=hr.HR_OPT_TIMING)
+for _ in range(a.reps):
+    ck.reset(); ck.replay(dt); raw, fl = ck.report_raw()
+print("races", len(raw), "flags", fl, hr.hr_replay_timing(ck.ctx))

@@ -39,6 +39,23 @@ def test_c1_online_matches_oracle(removed):
         assert d2[2048:].tolist() == exp
 
 
+@pytest.mark.parametrize("removed", [None, 32, 8, "load"])
+def test_c1_transparent_wrapper_matches_oracle(removed):
+    """hr_array<T> (PAPER.md:676-678 wrapper class) instruments plain-looking
+    code; the racy set equals the oracle's on the C1 trace."""
+    import torch
+    hr, on = mods()
+    data = torch.arange(8 * 256 + 8, dtype=torch.int32, device="cuda")
+    ck = hr.Checker(8 * 256 + 8, 256)
+    on.c1_array(ck.ctx, data, removed=removed)
+    raw, flags = ck.report_raw()
+    want = oracle.check(tp.c1_tree_reduction(removed=removed))
+    assert _races(raw) == [tuple(r) for r in want.races] and flags == 0
+    if removed is None:
+        torch.cuda.synchronize()
+        assert data[2048:].tolist() == [sum(range(r * 256, (r + 1) * 256)) for r in range(8)]
+
+
 @pytest.mark.parametrize("n,removed", [(128, 20), (128, None), (512, 20)])
 def test_c3_online_matches_oracle(n, removed):
     import torch
