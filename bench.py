@@ -282,6 +282,21 @@ def main():
         n_acc_rank = int((((rec >> 62) & 3) != 3).sum().item())
     torch.cuda.synchronize()
     n_rows = dt.n_rows
+    # access classes of C5 (tracegen/c5gen.h), for the random-access ceiling (untimed)
+    owned, hot_base = c5.total_words(lb) // 2, c5.total_words(lb) - (1 << (lb + 4))
+    n_gather = n_own = 0
+    n_rec = n_rows * 32
+    for c0 in range(0, n_rec, 1 << 27):                   # chunked: no 34 GB temporaries
+        c1 = min(n_rec, c0 + (1 << 27))
+        if dt.format == hr.HR_TRACE_C32:
+            acc_mask = (dt.recop[c0:c1] & 3) != 3
+            wv = dt.rec32[c0:c1].to(torch.int64) & 0xFFFFFFFF
+        else:
+            acc_mask = ((dt.rec[c0:c1] >> 62) & 3) != 3
+            wv = dt.rec[c0:c1] & ((1 << 61) - 1)
+        n_gather += int((acc_mask & (wv >= owned) & (wv < hot_base)).sum().item())
+        n_own += int((acc_mask & (wv < owned)).sum().item())
+    del acc_mask, wv
     opts = hr.HR_OPT_TIMING | args.options | (hr.HR_OPT_DOUBLE_SHADOW if args.double_shadow else 0)
     ck = hr.Checker(c5.total_words(lb), 0, shard=(rank, world), options=opts, ring_capacity=1 << 21)
 
@@ -339,6 +354,18 @@ def main():
         except Exception:
             traffic = None
     literal = BYTES_PER_ACCESS_LITERAL * total_acc / (ms_step / 1e3) / 1e9 / (peak * world)
+    # the floor that actually binds C5: random 8-byte RMWs on cold HBM words run at
+    # the measured DRAM random-access rate, the rest streams at the copy peak
+    ceiling = None
+    rates_path = os.path.join(ROOT, "profiles", "b200_access_rates.json")
+    if os.path.exists(rates_path):
+        rates = json.load(open(rates_path))
+        floor_ms = 1e3 * (n_gather / rates["random_cas_hbm_per_s"] +
+                          (dt.record_bytes() + BYTES_PER_ACCESS_ALGO * n_own) / (peak * 1e9))
+        ceiling = {"kind": "measured random-DRAM RMW rate + copy peak", "rate_source": rates_path,
+                   "random_gathers": n_gather, "coalesced_own_row": n_own,
+                   "floor_ms_per_launch": floor_ms, "kernel_ms": kern_ms / max(n_kern, 1),
+                   "frac_of_floor": floor_ms / (kern_ms / max(n_kern, 1))}
 
     slow = None
     if rank == 0 and world == 1 and not args.no_slowdown:
@@ -412,6 +439,7 @@ def main():
                          "algo_bytes_rule": f"records ({args.format}: {dt.record_bytes() // max(n_rows, 1)} B/row) "
                                             "+ 16 B shadow RMW per checked access"},
             "literal_roofline_frac": literal,
+            "ceiling": ceiling,
             "step_breakdown_ms": {"replay_kernel": kern_ms_launch,
                                   "shadow_reset" + (" (side stream, overlapped)" if args.double_shadow else ""):
                                       reset_ms_launch,
