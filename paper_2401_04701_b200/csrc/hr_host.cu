@@ -20,6 +20,7 @@
 #include "hr.h"
 #include "hr_device.cuh"
 #include "hr_replay.cuh"
+#include "hr_fh.cuh"
 #include "fsm_table.inc"
 
 struct hr_ctx {
@@ -34,6 +35,7 @@ struct hr_ctx {
     cudaStream_t side = nullptr;                 /* deferred resets (double shadow) */
     cudaEvent_t used_done[2] = {nullptr, nullptr}, reset_done[2] = {nullptr, nullptr};
     uint64_t gbase = 0, gwords = 0, glocal = 0;
+    uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
     hr_race *ring = nullptr;
     unsigned int *tail = nullptr;     /* [0] ring tail, [1] flags, [2] scan count */
@@ -172,7 +174,8 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     if (space == HR_SHARED) {
-        if (base_word != 0 || n_words * 8 + HR_FSM_SMEM_BYTES + 32 * sizeof(hr_pool_smem) > 227 * 1024)
+        const uint64_t per = (c->cfg.options & HR_OPT_FINITE_HISTORY) ? 16 : 8;
+        if (base_word != 0 || n_words * per + HR_FSM_SMEM_BYTES + 32 * sizeof(hr_pool_smem) > 227 * 1024)
             return fail(c, HR_E_ARG, "shared shadow too large: %llu words", (unsigned long long)n_words);
         c->smem_words_max = (uint32_t)n_words;
         if (dev_region) *dev_region = nullptr;
@@ -188,11 +191,12 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
     uint64_t local_gran = (gran + c->shard_count - 1) >> c->shard_log2;
     uint64_t local = local_gran << 9;
     c->double_shadow = (c->cfg.options & HR_OPT_DOUBLE_SHADOW) != 0;
+    c->shadow_bytes = (c->cfg.options & HR_OPT_FINITE_HISTORY) ? 16 : 8;
     for (int b = 0; b < (c->double_shadow ? 2 : 1); b++) {
-        if (cudaMalloc(&c->gbuf[b], local * 8) != cudaSuccess)
+        if (cudaMalloc(&c->gbuf[b], local * c->shadow_bytes) != cudaSuccess)
             return fail(c, HR_E_NOMEM, "cudaMalloc(%llu B) for the global shadow failed",
-                        (unsigned long long)(local * 8));
-        CU(cudaMemset(c->gbuf[b], 0, local * 8));
+                        (unsigned long long)(local * c->shadow_bytes));
+        CU(cudaMemset(c->gbuf[b], 0, local * c->shadow_bytes));
         c->dirty[b] = false;
     }
     if (c->double_shadow && !c->side) {
@@ -218,7 +222,7 @@ static hr_status reset_buffer(hr_ctx *c, int b, cudaStream_t s)
     bool timing = c->cfg.options & HR_OPT_TIMING;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
-    CU(cudaMemsetAsync(c->gbuf[b], 0, c->glocal * 8, s));
+    CU(cudaMemsetAsync(c->gbuf[b], 0, c->glocal * c->shadow_bytes, s));
     if (timing) { CU(cudaEventRecord(e1, s)); c->ev_reset.push_back({e0, e1}); }
     c->dirty[b] = false;
     return HR_OK;
@@ -298,6 +302,21 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     uint32_t kid = t->kernel_base + k;
     hr_dev d = make_dev(c, kid);
     d.block_base = (uint32_t)b0;
+    if (c->shadow_bytes == 16) {                               /* finite-history baseline */
+        size_t smem = HR_FSM_SMEM_BYTES + smem_words * 16;
+        if (smem > 48 * 1024)
+            CU(cudaFuncSetAttribute(hr_fh_replay_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        bool timing = c->cfg.options & HR_OPT_TIMING;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+        hr_fh_replay_kernel<SRC><<<(unsigned)(b1 - b0), (unsigned)(warps * 32), smem, s>>>(
+            d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
+        CU(cudaGetLastError());
+        if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
+        c->last_kernel = kid;
+        c->have_kernel = true;
+        return HR_OK;
+    }
     size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
     void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
         pool ? hr_replay_kernel<true, SRC> : hr_replay_kernel<false, SRC>;
@@ -506,7 +525,7 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
     std::vector<hr_race> v(n);
     if (n) CU(cudaMemcpy(v.data(), c->ring, n * sizeof(hr_race), cudaMemcpyDeviceToHost));
     uint32_t flags = hdr[1];
-    if ((flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow) {
+    if ((flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow && c->shadow_bytes == 8) {
         /* fallback: scan the last kernel's global shadow (shared instances are gone) */
         uint32_t scap = 1u << 22;
         hr_race *tmp = nullptr;

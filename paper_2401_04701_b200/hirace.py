@@ -27,6 +27,7 @@ HR_F_BARRIER_DIVERGENCE, HR_F_UNMONITORED = 8, 16
 HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING, HR_OPT_NO_SPECULATE, HR_OPT_NO_POOL, HR_OPT_POOL = \
     1, 2, 4, 8, 16, 32
 HR_OPT_DOUBLE_SHADOW = 64
+HR_OPT_FINITE_HISTORY = 128
 EXPORTS = ("hr_init", "hr_set_shard", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_report", "hr_reset_report", "hr_counters", "hr_replay_timing",
            "hr_fsm_table",

@@ -276,3 +276,43 @@ def test_soundness_at_scale():
     assert oracle.check(big).races == []
     for options in (16, 32):
         assert gpu_set(big, options=options) == ([], 0)
+
+
+# ---- finite-history BASELINE detector (HR_OPT_FINITE_HISTORY) ----
+
+FH = 128
+
+
+def test_finite_history_misses_listing4_hirace_does_not():
+    """with one reader record, thread 1's read of data[1] is
+    evicted by thread 0's read, so thread 0's write finds no concurrent reader
+    and the race "goes undetected"; HiRace's FSM keeps the summary.
+    Rows run in program order inside a warp, so this eviction schedule is the
+    one the replay executes."""
+    tr = tp.listing4(1, 1, 4, 4)
+    assert [r[3] for r in oracle_set(tr)[0]] == [1]
+    assert [r[3] for r in gpu_set(tr)[0]] == [1]                 # HiRace: found
+    assert gpu_set(tr, options=FH)[0] == []                      # finite history: missed
+    big = tp.listing4(1, 8, 32, 256)                              # every word 1..253 racy
+    assert len(gpu_set(big)[0]) == 253
+    # inside a warp rows run in order, so the evicting read always comes second;
+    # only words read by two warps (thread 32k and 32k-1) can escape eviction
+    fh = {r[3] for r in gpu_set(big, options=FH)[0]}
+    assert fh <= {32 * k for k in range(1, 8)}
+
+
+def test_finite_history_is_sound_but_incomplete_on_c2():
+    """Table II's shape: the finite-history detector never
+    reports a word the oracle calls race-free, and misses some racy ones."""
+    from tracegen import suite
+    missed_traces = found_traces = 0
+    for c in suite.suite():
+        want = {(r.kernel, r.space, r.block, r.word) for r in oracle.check(c.trace).races}
+        got = {tuple(r[:4]) for r in gpu_set(c.trace, options=FH)[0]}
+        assert got <= want, c.name
+        if want:
+            if got:
+                found_traces += 1
+            else:
+                missed_traces += 1
+    assert found_traces > 0 and missed_traces > 0
