@@ -215,6 +215,40 @@ __device__ __forceinline__ unsigned long long hr__nmeta(const hr_thr &t, unsigne
     return (t.meta & ~(0x1full << HR_TID_SHIFT)) | ((unsigned long long)last_lane << HR_TID_SHIFT);
 }
 
+/* Fold-free variant for the common case of a lane alone on its word: one
+ * label, the lane's own meta, no group bookkeeping. */
+__device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_thr &t, bool is_shared,
+                                                      uint32_t sh_addr, unsigned long long *gp,
+                                                      unsigned long long old, uint32_t fresh, uint32_t kind)
+{
+    const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
+    const uint32_t kcol = kind << 4;
+    while (true) {
+        const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+        const uint32_t rel = hr__rel(t.tid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+        const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
+        const uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | kcol | (sync << 2) | rel));
+        const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
+        if (cur == os && fresh != HR_OLD_GUESS && fastexit) {
+            const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
+            if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+                return 0u;                                                /* a7 (ii), (iii) */
+        }
+        if (nw == old) {
+            if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
+            if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
+        }
+        const unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+        if (prev == old) {                                                /* a8 committed */
+            if (cur >= HR_RACE_BLOCK && cur != os)
+                return HR_EI_EMIT | (hr__laneid() << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID);
+            return 0u;
+        }
+        old = prev;
+        fresh = HR_OLD_FRESH;
+    }
+}
+
 /* a7 + a8: Algorithm 1's repeat/until loop from a first value `old` of the
  * given provenance; returns the emit info of the committed transition (0 if
  * none or a fast exit). */
@@ -334,7 +368,8 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
         unsigned long long *gp = d.gshadow + local;
         uint32_t fresh;
         const unsigned long long old = hr__first(d, is_shared, sh_addr, gp, kind, fresh);
-        ei = hr__commit(d, t, is_shared, sh_addr, gp, old, fresh, kind, lane, peers, kb0, kb1);
+        ei = (peers == (1u << lane)) ? hr__commit_single(d, t, is_shared, sh_addr, gp, old, fresh, kind)
+                                     : hr__commit(d, t, is_shared, sh_addr, gp, old, fresh, kind, lane, peers, kb0, kb1);
     }
 
     /* a9: warp-aggregated ring append; also the warp's convergence point */
