@@ -182,6 +182,16 @@ hr_status hr_replay_trace_host(hr_ctx *ctx, const hr_trace *t, void *stream);
  * shadow is scanned for RACE words of the last replayed kernel instead. */
 hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out);
 
+/* Per-pair race classes of already reported racy addresses:
+ * `races` are the n records hr_report returned for this same device trace `t`
+ * (same kernel_base); the trace is replayed again through four class-projected
+ * FSMs (fsm_classes.inc) for those addresses only.  classes_out[i] (host, n
+ * bytes) receives bit0 W-W, bit1 R-W, bit2 A-W, bit3 A-R: the kind pairs among
+ * the race pairs of races[i].  Schedule-independent; synchronises `stream`;
+ * temporary device memory ~ 32 B per race + the hash table. */
+hr_status hr_race_classes(hr_ctx *ctx, const hr_trace *t, const hr_race *races, size_t n, uint8_t *classes_out,
+                          void *stream);
+
 /* Clear the ring, its counter and the flags word (asynchronous on the last stream). */
 hr_status hr_reset_report(hr_ctx *ctx);
 

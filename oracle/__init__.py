@@ -6,7 +6,8 @@ shares no code with the CUDA path (``paper_2401_04701_b200``) and never
 imports it.
 
 * ``check(trace)``       — hr_oracle.c: the plain happens-before race definition
-                           (§II-A), pairwise or bucketed.
+                           (PAPER.md:231 §II-A; SPEC.md:410), pairwise or bucketed;
+                           racy addresses, their scope and their race classes.
 * ``vclock``             — vector-clock detector along explicit interleavings
                            and schedule enumeration,
                            pure Python, tiny traces only.
@@ -44,7 +45,10 @@ class Race(NamedTuple):
 
 class _RaceC(ctypes.Structure):
     _fields_ = [("word", ctypes.c_uint64), ("kernel", ctypes.c_uint32), ("block", ctypes.c_uint32),
-                ("space", ctypes.c_uint8), ("scope", ctypes.c_uint8), ("pad", ctypes.c_uint8 * 6)]
+                ("space", ctypes.c_uint8), ("scope", ctypes.c_uint8), ("classes", ctypes.c_uint8),
+                ("pad", ctypes.c_uint8 * 5)]
+
+CLASS_WW, CLASS_RW, CLASS_AW, CLASS_AR = 1, 2, 4, 8
 
 
 def build(force: bool = False) -> str:
@@ -80,6 +84,7 @@ class Result(NamedTuple):
     races: List[Race]
     flags: int
     n_accesses: int
+    classes: List[int] = []      # per race: bit0 W-W, bit1 R-W, bit2 A-W, bit3 A-R
 
 
 def check(trace, mode: int = BUCKETED, bc_bits: int = 16, wc_bits: int = 16) -> Result:
@@ -105,7 +110,7 @@ def check(trace, mode: int = BUCKETED, bc_bits: int = 16, wc_bits: int = 16) -> 
             raise RuntimeError(f"hro_check failed: {rc}")
         races = [Race(int(r.kernel), int(r.space), int(r.block), int(r.word), int(r.scope))
                  for r in out[: n.value]]
-        return Result(races, int(fl.value), int(na.value))
+        return Result(races, int(fl.value), int(na.value), [int(r.classes) for r in out[: n.value]])
 
 
 def racy_words(result: Result) -> List[int]:

@@ -32,6 +32,8 @@
  * Output 1: the sorted set of racy addresses (kernel, space, block, word).
  * Output 2: scope per racy address — GRID if some race pair has its two
  *   threads in different blocks, BLOCK otherwise (reading R4 in DESIGN.md).
+ * Output 3: race classes per racy address — the set of kind pairs among its
+ *   race pairs: bit0 W–W, bit1 R–W, bit2 A–W, bit3 A–R.
  *
  * Two modes:
  *   HRO_PAIRWISE  — the literal O(n^2) loop over pairs of each address.
@@ -82,8 +84,18 @@ typedef struct {
     uint32_t block;
     uint8_t space;
     uint8_t scope;   /* 1 = BLOCK, 2 = GRID */
-    uint8_t pad[6];
+    uint8_t classes; /* bit0 WW, bit1 RW, bit2 AW, bit3 AR */
+    uint8_t pad[5];
 } hro_race;
+
+static unsigned pair_class(int k1, int k2)
+{
+    if (k1 == K_WRITE && k2 == K_WRITE) return 1u;
+    if ((k1 == K_READ && k2 == K_WRITE) || (k1 == K_WRITE && k2 == K_READ)) return 2u;
+    if ((k1 == K_ATOMIC && k2 == K_WRITE) || (k1 == K_WRITE && k2 == K_ATOMIC)) return 4u;
+    if ((k1 == K_ATOMIC && k2 == K_READ) || (k1 == K_READ && k2 == K_ATOMIC)) return 8u;
+    return 0u;   /* R-R, A-A: not a conflict */
+}
 
 /* ---- step 1: materialise per-access (thread, bc, wc) from the records ---- */
 
@@ -210,92 +222,107 @@ static int same_addr(const acc_t *a, const acc_t *b)
     return a->kernel == b->kernel && a->space == b->space && a->ablock == b->ablock && a->word == b->word;
 }
 
-/* pairwise: returns 0 (race-free), 1 (BLOCK), 2 (GRID) for one address group */
-static int group_pairwise(const acc_t *g, uint64_t n)
+/* pairwise: returns 0 (race-free), 1 (BLOCK), 2 (GRID) for one address group;
+ * *classes receives the kind pairs of all race pairs */
+static int group_pairwise(const acc_t *g, uint64_t n, unsigned *classes)
 {
     int scope = 0;
+    *classes = 0;
     for (uint64_t i = 0; i < n; i++)
         for (uint64_t j = i + 1; j < n; j++) {
             const acc_t *a = &g[i], *b = &g[j];
             if (same_thread(a, b)) continue;
             if (!conflict(a->kind, b->kind)) continue;
             if (!unordered(a, b)) continue;
-            if (a->tblock != b->tblock) return 2;
-            scope = 1;
+            *classes |= pair_class(a->kind, b->kind);
+            scope = (a->tblock != b->tblock) ? 2 : (scope ? scope : 1);
         }
     return scope;
 }
 
-/* Kind-set test "∃ two distinct sub-groups i != j with conflicting kinds",
- * from per-sub-group kind masks (bit k = kind k present).  Pairs are
- * conflicting iff one is a write, or one is a read and the other atomic. */
-typedef struct { uint64_t n, nW, nR, nA, nRA; } kcount;
-
-static void kc_add(kcount *c, unsigned m)
+/* Kind-set test over distinct sub-groups (distinct sub-groups of one level
+ * are pairwise unordered; inside a sub-group the next level decides). For
+ * kinds x != y the number of ordered (x in group i, y in group j, i != j)
+ * choices is n_x * n_y - n_xy; for W-W, at least two groups with a write. */
+static unsigned kc_classes(uint64_t nW, uint64_t nR, uint64_t nA, uint64_t nRW, uint64_t nAW, uint64_t nRA)
 {
+    unsigned m = 0;
+    if (nW >= 2) m |= 1u;
+    if (nR * nW - nRW > 0) m |= 2u;
+    if (nA * nW - nAW > 0) m |= 4u;
+    if (nA * nR - nRA > 0) m |= 8u;
+    return m;
+}
+
+/* per-sub-group kind-mask accumulator for the class test */
+typedef struct { uint64_t n, nW, nR, nA, nRW, nAW, nRA; } kc2;
+
+static void kc2_add(kc2 *c, unsigned m)
+{
+    const int r = (m >> K_READ) & 1, w = (m >> K_WRITE) & 1, a = (m >> K_ATOMIC) & 1;
     c->n++;
-    if (m & (1u << K_WRITE)) c->nW++;
-    if (m & (1u << K_READ)) c->nR++;
-    if (m & (1u << K_ATOMIC)) c->nA++;
-    if ((m & (1u << K_READ)) && (m & (1u << K_ATOMIC))) c->nRA++;
+    c->nW += w; c->nR += r; c->nA += a;
+    c->nRW += r && w; c->nAW += a && w; c->nRA += r && a;
 }
 
-static int kc_conflict(const kcount *c)
+static unsigned kc2_classes(const kc2 *c)
 {
-    if (c->nW >= 1 && c->n >= 2) return 1;       /* a write vs any other sub-group */
-    return c->nR * c->nA - c->nRA > 0;           /* a read vs an atomic of another sub-group */
+    return kc_classes(c->nW, c->nR, c->nA, c->nRW, c->nAW, c->nRA);
 }
 
-/* bucketed: same predicate; g is sorted by (tblock, bc, twarp, wc, tlane) */
-static int group_bucketed(const acc_t *g, uint64_t n)
+/* bucketed: same predicate; g is sorted by (tblock, bc, twarp, wc, tlane).
+ * Returns the scope; *classes receives the classes of all race pairs. */
+static int group_bucketed(const acc_t *g, uint64_t n, unsigned *classes)
 {
     /* cross-block pairs are always unordered */
-    kcount blocks = {0};
-    int block_scope = 0;
+    kc2 blocks = {0};
+    unsigned cls = 0;
     uint64_t i = 0;
     while (i < n) {
         uint64_t jb = i;
         unsigned mb = 0;
         while (jb < n && g[jb].tblock == g[i].tblock) { mb |= 1u << g[jb].kind; jb++; }
-        kc_add(&blocks, mb);
+        kc2_add(&blocks, mb);
         /* inside block: pairs with equal bc, different warps are unordered */
         uint64_t e = i;
-        while (e < jb && !block_scope) {
+        while (e < jb) {
             uint64_t je = e;
             while (je < jb && g[je].bc == g[e].bc) je++;
-            kcount warps = {0};
+            kc2 warps = {0};
             uint64_t w = e;
             while (w < je) {
                 uint64_t jw = w;
                 unsigned mw = 0;
                 while (jw < je && g[jw].twarp == g[w].twarp) { mw |= 1u << g[jw].kind; jw++; }
-                kc_add(&warps, mw);
+                kc2_add(&warps, mw);
                 /* inside warp: equal wc, different lanes are unordered */
                 uint64_t c = w;
                 while (c < jw) {
                     uint64_t jc = c;
                     while (jc < jw && g[jc].wc == g[c].wc) jc++;
-                    kcount lanes = {0};
+                    kc2 lanes = {0};
                     uint64_t t = c;
                     while (t < jc) {
                         uint64_t jt = t;
                         unsigned mt = 0;
                         while (jt < jc && g[jt].tlane == g[t].tlane) { mt |= 1u << g[jt].kind; jt++; }
-                        kc_add(&lanes, mt);
+                        kc2_add(&lanes, mt);
                         t = jt;
                     }
-                    if (kc_conflict(&lanes)) block_scope = 1;
+                    cls |= kc2_classes(&lanes);
                     c = jc;
                 }
                 w = jw;
             }
-            if (kc_conflict(&warps)) block_scope = 1;
+            cls |= kc2_classes(&warps);
             e = je;
         }
         i = jb;
     }
-    if (kc_conflict(&blocks)) return 2;
-    return block_scope ? 1 : 0;
+    const unsigned cross = kc2_classes(&blocks);
+    *classes = cls | cross;
+    if (cross) return 2;
+    return cls ? 1 : 0;
 }
 
 /* Entry point.  Returns 0 on success, -1 bad trace, -2 out of memory,
@@ -317,7 +344,8 @@ int hro_check(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_kernels,
     while (i < n) {
         uint64_t j = i + 1;
         while (j < n && same_addr(&a[i], &a[j])) j++;
-        int s = mode == HRO_PAIRWISE ? group_pairwise(a + i, j - i) : group_bucketed(a + i, j - i);
+        unsigned cls = 0;
+        int s = mode == HRO_PAIRWISE ? group_pairwise(a + i, j - i, &cls) : group_bucketed(a + i, j - i, &cls);
         if (s) {
             if (nr < cap) {
                 hro_race *r = &out[nr];
@@ -327,6 +355,7 @@ int hro_check(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_kernels,
                 r->block = a[i].ablock;
                 r->space = a[i].space;
                 r->scope = (uint8_t)s;
+                r->classes = (uint8_t)cls;
             }
             nr++;
         }

@@ -127,7 +127,26 @@ def _conflict(k1: int, k2: int) -> bool:
     return not ((k1 == 0 and k2 == 0) or (k1 == 2 and k2 == 2))
 
 
-def vclock_races(th: Dict[Thread, List[Event]], schedule: List[Thread]) -> Dict[Tuple, int]:
+def _class(k1: int, k2: int) -> int:
+    """bit0 W-W, bit1 R-W, bit2 A-W, bit3 A-R (kinds: 0 R, 1 W, 2 A)."""
+    s = {k1, k2}
+    if s == {1}:
+        return 1
+    if s == {0, 1}:
+        return 2
+    if s == {1, 2}:
+        return 4
+    if s == {0, 2}:
+        return 8
+    return 0
+
+
+def vclock_race_classes(th: Dict[Thread, List[Event]], schedule: List[Thread]) -> Dict[Tuple, int]:
+    """Like vclock_races, but {address: class mask of all racing pairs seen}."""
+    return vclock_races(th, schedule, classes=True)
+
+
+def vclock_races(th: Dict[Thread, List[Event]], schedule: List[Thread], classes: bool = False) -> Dict[Tuple, int]:
     """Racy addresses along one interleaving: {(space, ablock, word): scope}.
 
     Each thread keeps a vector clock; an access races with any earlier access
@@ -144,8 +163,10 @@ def vclock_races(th: Dict[Thread, List[Event]], schedule: List[Thread]) -> Dict[
             addr = (space, t[0] if space == 1 else 0xFFFFFFFF, word)
             for (u, k2, c2) in hist.get(addr, []):
                 if u != t and _conflict(kind, k2) and not _leq(c2, vc[t]):
-                    scope = 2 if u[0] != t[0] else 1
-                    races[addr] = max(races.get(addr, 0), scope)
+                    if classes:
+                        races[addr] = races.get(addr, 0) | _class(kind, k2)
+                    else:
+                        races[addr] = max(races.get(addr, 0), 2 if u[0] != t[0] else 1)
             hist.setdefault(addr, []).append((t, kind, dict(vc[t])))
             vc[t][t] = vc[t].get(t, 0) + 1
         elif grp is not None:

@@ -21,7 +21,9 @@
 #include "hr_device.cuh"
 #include "hr_replay.cuh"
 #include "hr_fh.cuh"
+#include "hr_classes.cuh"
 #include "fsm_table.inc"
+#include "fsm_classes.inc"
 
 struct hr_ctx {
     int device = 0;
@@ -560,6 +562,77 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
     size_t w = std::min(m, cap);
     if (w) memcpy(out, v.data(), w * sizeof(hr_race));
     return m > cap ? fail(c, HR_E_ARG, "hr_report: %zu races, capacity %zu", m, cap) : HR_OK;
+}
+
+/* Per-pair race classes post-pass (include/hr.h). */
+template <typename SRC>
+static hr_status classes_launch(hr_ctx *c, const hr_trace *t, SRC src, const unsigned char *ctab,
+                                const hr_class_entry *tab, uint64_t mask, unsigned long long *sh, unsigned int *cls,
+                                uint32_t kinds, cudaStream_t s)
+{
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        hr_status st = check_kernel(c, t, k);
+        if (st) return st;
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        if (!kd[0]) continue;
+        hr_dev d = make_dev(c, t->kernel_base + k);
+        size_t smem = HR_FSM_SMEM_BYTES + HR_CLASS_TABLES_BYTES;
+        hr_classes_kernel<SRC><<<(unsigned)kd[0], (unsigned)(kd[1] * 32), smem, s>>>(
+            d, src, t->warp_off + kd[4], (uint32_t)kd[1], (uint32_t)kd[2], ctab, tab, mask, sh, cls, kinds);
+        CU(cudaGetLastError());
+    }
+    return HR_OK;
+}
+
+extern "C" hr_status hr_race_classes(hr_ctx *c, const hr_trace *t, const hr_race *races, size_t n,
+                                     uint8_t *classes_out, void *stream)
+{
+    if (!c || !trace_ok(t) || (n && (!races || !classes_out))) return fail(c, HR_E_ARG, "hr_race_classes: bad arguments");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) return HR_OK;
+    uint64_t cap = 64;
+    while (cap < 2 * n) cap <<= 1;
+    std::vector<hr_class_entry> tab(cap);
+    for (auto &e : tab) { e.word = 0; e.key = ~0ull; e.slot = 0; e.pad = 0; }
+    for (size_t i = 0; i < n; i++) {
+        const uint64_t key = ((uint64_t)races[i].kernel << 33) | ((uint64_t)races[i].space << 32) | races[i].block;
+        uint64_t h = hr__class_hash(races[i].word, key) & (cap - 1);
+        while (tab[h].key != ~0ull) h = (h + 1) & (cap - 1);
+        tab[h].word = races[i].word;
+        tab[h].key = key;
+        tab[h].slot = (uint32_t)i;
+    }
+    unsigned char *ctab = nullptr;
+    hr_class_entry *dtab = nullptr;
+    unsigned long long *sh = nullptr;
+    unsigned int *cls = nullptr;
+    hr_status st = HR_OK;
+    if (cudaMalloc(&ctab, HR_CLASS_TABLES_BYTES) != cudaSuccess || cudaMalloc(&dtab, cap * sizeof(hr_class_entry)) != cudaSuccess ||
+        cudaMalloc(&sh, n * 4 * sizeof(unsigned long long)) != cudaSuccess || cudaMalloc(&cls, n * sizeof(unsigned int)) != cudaSuccess) {
+        st = fail(c, HR_E_NOMEM, "hr_race_classes: device allocation failed");
+    } else {
+        uint32_t kinds = 0;
+        for (int i = 0; i < 4; i++) kinds |= (uint32_t)hr_class_kinds_init[i] << (8 * i);
+        cudaMemcpyAsync(ctab, hr_class_tables_init, HR_CLASS_TABLES_BYTES, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dtab, tab.data(), cap * sizeof(hr_class_entry), cudaMemcpyHostToDevice, s);
+        cudaMemsetAsync(sh, 0, n * 4 * sizeof(unsigned long long), s);
+        cudaMemsetAsync(cls, 0, n * sizeof(unsigned int), s);
+        if (t->format == HR_TRACE_C32)
+            st = classes_launch(c, t, hr_src_c32{t->rec32, t->recop}, ctab, dtab, cap - 1, sh, cls, kinds, s);
+        else
+            st = classes_launch(c, t, hr_src_u64{t->rec}, ctab, dtab, cap - 1, sh, cls, kinds, s);
+        if (!st) {
+            std::vector<unsigned int> h(n);
+            if (cudaMemcpyAsync(h.data(), cls, n * sizeof(unsigned int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                st = fail(c, HR_E_CUDA, "hr_race_classes: %s", cudaGetErrorString(cudaGetLastError()));
+            else
+                for (size_t i = 0; i < n; i++) classes_out[i] = (uint8_t)h[i];
+        }
+    }
+    cudaFree(ctab); cudaFree(dtab); cudaFree(sh); cudaFree(cls);
+    return st;
 }
 
 extern "C" hr_status hr_reset_report(hr_ctx *c)

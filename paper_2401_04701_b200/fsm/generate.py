@@ -123,8 +123,10 @@ def _rebase_mask(mask: int, s: int, t: int) -> int:
     return out | rest                                  # t == Self
 
 
-def step(h: State, m: int, s: int, t: int) -> State:
-    """One FSM transition on the abstract history (module docstring)."""
+def step(h: State, m: int, s: int, t: int, conflict_fn=None) -> State:
+    """One FSM transition on the abstract history (module docstring).
+    `conflict_fn` restricts the conflict relation (class projections)."""
+    cf = conflict_fn or conflict
     if h == "RACE_GRID":
         return "RACE_GRID"
     if h == "RACE_BLOCK":
@@ -135,7 +137,7 @@ def step(h: State, m: int, s: int, t: int) -> State:
         return tuple(hist)
     reb = [_rebase_mask(x, s, t) for x in h]           # type: ignore[union-attr]
     for k in range(3):
-        if conflict(m, k) and (reb[k] & UNORDERED):
+        if cf(m, k) and (reb[k] & UNORDERED):
             any_foreign = any(x & C_F for x in reb)
             return "RACE_GRID" if any_foreign else "RACE_BLOCK"
     reb[m] |= C_S
@@ -164,7 +166,7 @@ NAMED = {
 }
 
 
-def closure(labels: Sequence[Tuple[int, int, int]]):
+def closure(labels: Sequence[Tuple[int, int, int]], conflict_fn=None):
     """Reachable abstract histories from INIT under ``labels`` (BFS order)."""
     order: List[State] = ["INIT"]
     seen = {"INIT": 0}
@@ -172,7 +174,7 @@ def closure(labels: Sequence[Tuple[int, int, int]]):
     while q:
         h = q.popleft()
         for (m, s, t) in labels:
-            n = step(h, m, s, t)
+            n = step(h, m, s, t, conflict_fn)
             if n not in seen:
                 seen[n] = len(order)
                 order.append(n)
@@ -180,11 +182,12 @@ def closure(labels: Sequence[Tuple[int, int, int]]):
     return order
 
 
-def minimize(states: List[State], labels, output) -> Dict[State, int]:
+def minimize(states: List[State], labels, output, conflict_fn=None) -> Dict[State, int]:
     """Moore partition refinement; returns state -> class id (ids in first-seen order)."""
     cls = {h: output(h) for h in states}
     while True:
-        sig = {h: (cls[h],) + tuple(cls[step(h, m, s, t)] for (m, s, t) in labels) for h in states}
+        sig = {h: (cls[h],) + tuple(cls[step(h, m, s, t, conflict_fn)] for (m, s, t) in labels)
+               for h in states}
         ids: Dict[tuple, int] = {}
         new = {}
         for h in states:
@@ -209,10 +212,11 @@ def _output_merged(h: State):
 class Machine:
     """A minimised machine: codes, names, representatives, transition function."""
 
-    def __init__(self, labels=None, split_race: bool = True):
+    def __init__(self, labels=None, split_race: bool = True, conflict_fn=None):
         self.labels = labels if labels is not None else all_labels()
-        states = closure(self.labels)
-        part = minimize(states, self.labels, _output_split if split_race else _output_merged)
+        self.conflict_fn = conflict_fn
+        states = closure(self.labels, conflict_fn)
+        part = minimize(states, self.labels, _output_split if split_race else _output_merged, conflict_fn)
         # representative per class: first in BFS order (shortest history)
         rep: Dict[int, State] = {}
         for h in states:
@@ -232,7 +236,7 @@ class Machine:
             elif h == "RACE_BLOCK":
                 code[c] = RACE_BLOCK_CODE
             elif h == "RACE_GRID":
-                code[c] = RACE_GRID_CODE
+                code[c] = RACE_GRID_CODE if split_race else RACE_BLOCK_CODE
             else:
                 code[c] = nxt
                 nxt += 1
@@ -251,7 +255,7 @@ class Machine:
     def next_code(self, code: int, m: int, s: int, t: int) -> int:
         inv = {v: k for k, v in self.code.items()}
         h = self.rep[inv[code]]
-        return self.code_of(step(h, m, s, t))
+        return self.code_of(step(h, m, s, t, self.conflict_fn))
 
     def codes(self) -> List[int]:
         return sorted(self.code.values())
@@ -338,6 +342,59 @@ def render_inc(table: bytes, flags: bytes, mc: Machine) -> str:
     return "\n".join(lines) + "\n"
 
 
+# ---- per-pair race classes ---------------------------------
+# Class c is a kind pair; its projection sees only the accesses of those kinds
+# and calls a pair a conflict only when it is of class c.  A projection enters
+# RACE iff the word has a race pair of class c (verified against the oracle's
+# classes in tests/test_fsm.py).  Encoding as the main table; RACE = 30.
+CLASSES_PAIRS = (("WW", (K_W,), lambda m, k: m == K_W and k == K_W),
+                 ("RW", (K_R, K_W), lambda m, k: {m, k} == {K_R, K_W}),
+                 ("AW", (K_A, K_W), lambda m, k: {m, k} == {K_A, K_W}),
+                 ("AR", (K_A, K_R), lambda m, k: {m, k} == {K_A, K_R}))
+
+
+def class_machines():
+    out = []
+    for name, kinds, cf in CLASSES_PAIRS:
+        mc = Machine(labels=all_labels(kinds=kinds), split_race=False, conflict_fn=cf)
+        table = bytearray(N_CODES * 64)
+        inv = {v: k for k, v in mc.code.items()}
+        for c in range(N_CODES):
+            for kind in range(4):
+                for sy in range(4):
+                    for t in range(4):
+                        idx = (c << 6) | (kind << 4) | (sy << 2) | t
+                        if c not in inv or kind not in kinds:
+                            table[idx] = c
+                            continue
+                        ss = sy if (sy < 3 and feasible(sy, t)) else S_US
+                        table[idx] = mc.next_code(c, kind, ss, t)
+        out.append((name, kinds, bytes(table), mc))
+    return out
+
+
+def render_classes_inc(machines) -> str:
+    lines = ["/* GENERATED by paper_2401_04701_b200/fsm/generate.py — do not edit.",
+             " * Race-class projections (SURVEY §8(f)-3): table c sees kinds of class c",
+             " * only; RACE (code 30) iff the word has a race pair of that class."]
+    for name, kinds, _, mc in machines:
+        lines.append(f" *   {name}: kinds {'/'.join(KINDS[k] for k in kinds)}, {mc.n_states} states")
+    lines.append(" */")
+    mask = [sum(1 << k for k in kinds) for _, kinds, _, _ in machines]
+    lines.append("static const unsigned char hr_class_kinds_init[4] = {" + ",".join(str(x) for x in mask) + "};")
+    lines.append("static const unsigned char hr_class_tables_init[4][2048] = {")
+    for name, _, table, _ in machines:
+        lines.append("  { /* " + name + " */")
+        for c in range(N_CODES):
+            lines.append("    " + ",".join(str(x) for x in table[c * 64:(c + 1) * 64]) + ",")
+        lines.append("  },")
+    lines.append("};")
+    return "\n".join(lines) + "\n"
+
+
+CLASSES_INC_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "csrc",
+                                "fsm_classes.inc")
+
 INC_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "csrc", "fsm_table.inc")
 
 
@@ -346,6 +403,10 @@ def main() -> None:
     with open(INC_PATH, "w") as f:
         f.write(render_inc(table, flags, mc))
     print(f"wrote {INC_PATH}: {mc.n_states} states")
+    cms = class_machines()
+    with open(CLASSES_INC_PATH, "w") as f:
+        f.write(render_classes_inc(cms))
+    print(f"wrote {CLASSES_INC_PATH}: " + ", ".join(f"{n} {m.n_states} states" for n, _, _, m in cms))
     for c in mc.codes():
         print(f"  {c:2d} {mc.names[c]:32s} flags={flags[c]}")
 

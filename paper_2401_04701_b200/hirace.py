@@ -29,7 +29,8 @@ HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING, HR_OPT_NO_SPECULATE, HR_O
 HR_OPT_DOUBLE_SHADOW = 64
 HR_OPT_FINITE_HISTORY = 128
 EXPORTS = ("hr_init", "hr_set_shard", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
-           "hr_replay_trace_host", "hr_report", "hr_reset_report", "hr_counters", "hr_replay_timing",
+           "hr_replay_trace_host", "hr_report", "hr_race_classes", "hr_reset_report", "hr_counters",
+           "hr_replay_timing",
            "hr_fsm_table",
            "hr_device_view", "hr_last_error", "hr_destroy")
 
@@ -83,6 +84,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_replay_trace": ([vp, P(HrTrace), vp], ctypes.c_int),
         "hr_replay_trace_host": ([vp, P(HrTrace), vp], ctypes.c_int),
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
+        "hr_race_classes": ([vp, P(HrTrace), vp, ctypes.c_size_t, vp, vp], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
         "hr_counters": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
         "hr_replay_timing": ([vp, P(ctypes.c_double), P(ctypes.c_uint64), P(ctypes.c_double),
@@ -182,6 +184,15 @@ def hr_report(ctx, cap: int = 1 << 17) -> Tuple[List[Race], int, np.ndarray]:
     """(sorted unique races as (kernel, space, block, word, scope), flags, raw records)."""
     raw, flags = hr_report_raw(ctx, cap)
     return races_of(raw), flags, raw
+
+
+def hr_race_classes(ctx, t: HrTrace, raw: np.ndarray, stream: int = 0) -> np.ndarray:
+    """Class mask per race record of `raw` (bit0 W-W, bit1 R-W, bit2 A-W, bit3 A-R)."""
+    raw = np.ascontiguousarray(raw)
+    out = np.zeros(len(raw), dtype=np.uint8)
+    _check(load().hr_race_classes(ctx, ctypes.byref(t), raw.ctypes.data, len(raw), out.ctypes.data,
+                                  ctypes.c_void_p(stream)), ctx, "hr_race_classes")
+    return out
 
 
 def hr_reset_report(ctx):
@@ -325,6 +336,13 @@ class Checker:
 
     def report_raw(self):
         return hr_report_raw(self.ctx)
+
+    def classes(self, dtrace: "DeviceTrace", raw: np.ndarray, stream: Optional[int] = None,
+                kernel_base: int = 0) -> np.ndarray:
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        return hr_race_classes(self.ctx, dtrace.c(kernel_base), raw, stream)
 
     def reset(self):
         hr_reset_report(self.ctx)

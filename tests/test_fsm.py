@@ -230,3 +230,46 @@ def test_differential_large():
                     n_words=2, spaces=(0, 1))
     n, bad = _differential(TABLE, progs, cap=5000)
     assert not bad, bad[:1]
+
+
+# ---- race-class projections ----
+
+CLASS_MACHINES = G.class_machines()
+
+
+def test_class_projection_sizes_and_inc():
+    sizes = {name: mc.n_states for name, _, _, mc in CLASS_MACHINES}
+    assert sizes == {"WW": 3, "RW": 21, "AW": 21, "AR": 21}
+    with open(G.CLASSES_INC_PATH) as f:
+        assert f.read() == G.render_classes_inc(CLASS_MACHINES)
+
+
+def _class_differential(programs, cap=500):
+    n, bad = 0, []
+    for tr in programs:
+        res = oracle.check(tr, mode=oracle.PAIRWISE)
+        want = {(r.kernel, r.space, r.block, r.word): c for r, c in zip(res.races, res.classes)}
+        for key, accs in H.accesses_by_address(tr).items():
+            exp = want.get(key, 0)
+            for order in H.linear_extensions(accs, cap=cap):
+                got = 0
+                for bit, (name, kinds, table, _) in enumerate(CLASS_MACHINES):
+                    sub = [a for a in order if a[4] in kinds]
+                    final, _ = H.run_word(table, sub)
+                    if final == G.RACE_BLOCK_CODE:
+                        got |= 1 << bit
+                n += 1
+                if got != exp:
+                    bad.append((key, order, got, exp))
+                    break
+    return n, bad
+
+
+def test_class_projections_match_oracle():
+    """Each projection enters RACE over every HB-consistent order iff the
+    oracle finds a race pair of its class (schedule-independent classes)."""
+    progs = _family(31, 1200, max_blocks=2, max_warps=2, max_lanes=2, max_slots=4, n_words=2,
+                    spaces=(0, 1))
+    n, bad = _class_differential(progs)
+    assert not bad, bad[:1]
+    assert n > 15000

@@ -112,6 +112,39 @@ def test_vclock_every_interleaving_equals_static():
     assert n_sched > 5000
 
 
+def test_race_classes_listings():
+    """Classes follow from the listings' kinds (bit0 W-W, bit1 R-W, bit2 A-W, bit3 A-R):
+    Listing 1: every thread reads then writes data[0] -> R-W and W-W.
+    Listing 2 at 2 blocks: data[0] read by all, written by thread 1 of
+    each block -> R-W and W-W; data[k>0] only written (by thread k+1 of each
+    block) -> W-W.  Listing 4: data[j] read by threads j, j-1 and
+    written by thread j-1 only -> R-W."""
+    assert oracle.check(tp.listing1(1, 1, 4)).classes == [3]
+    r = oracle.check(tp.listing2(2, 1, 4))
+    assert [x.word for x in r.races] == [0, 1, 2] and r.classes == [3, 1, 1]
+    assert set(oracle.check(tp.listing4(1, 1, 8, 8)).classes) == {2}
+    two = lambda k1, k2: tp.from_thread_events(1, 1, 2, {(0, 0, 0): [k1(0)], (0, 0, 1): [k2(0)]})  # noqa: E731
+    assert oracle.check(two(tf.A, tf.W)).classes == [4]
+    assert oracle.check(two(tf.R, tf.A)).classes == [8]
+
+
+def test_vclock_classes_every_interleaving():
+    """The static classes equal the classes of the racing pairs a vector-clock
+    detector sees along every interleaving."""
+    rng = random.Random(4321)
+    n = 0
+    for _ in range(120):
+        tr = tp.random_program(rng, max_blocks=2, max_warps=2, max_lanes=2, max_slots=3, n_words=2,
+                               spaces=(0, 1))
+        th = vclock.thread_events(tr)[0]
+        res = oracle.check(tr, mode=oracle.PAIRWISE)
+        static = {(r.space, r.block, r.word): c for r, c in zip(res.races, res.classes)}
+        for sched in vclock.enumerate_schedules(th, cap=200):
+            assert vclock.vclock_race_classes(th, sched) == static
+            n += 1
+    assert n > 3000
+
+
 def test_pairwise_equals_bucketed_random():
     rng = random.Random(99)
     for i in range(400):
