@@ -57,9 +57,10 @@ hr_status hrb_c4_hist(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int rac
 
 /* Uninstrumented replay of a device trace (hr.h's hr_trace): the same grid,
  * record walk and barriers as hr_replay_trace, but each global record performs
- * only the raw 4-byte data access (read / write / atomicAdd on data[word],
- * words >= data_words and shared records skipped).  The denominator of the
- * replay slowdown (SURVEY §8(d) "Slowdown"). */
+ * only the raw 4-byte data access (read / write / atomicAdd on data[word] for
+ * global records, on the block's __shared__ int[smem_words] for shared ones;
+ * global words >= data_words skipped).  The denominator of the replay slowdown
+ * (SURVEY §8(d) "Slowdown"). */
 hr_status hrb_raw_replay(const hr_trace *t, int *data, uint64_t data_words, void *stream);
 
 #ifdef __cplusplus

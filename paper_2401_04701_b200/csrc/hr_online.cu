@@ -213,8 +213,11 @@ __global__ void __launch_bounds__(256) c4_hist_kernel(hr_dev d, int *data, uint3
 template <typename SRC>
 __global__ void __launch_bounds__(1024, 2) raw_replay_kernel(SRC src, const uint64_t *__restrict__ woff,
                                                              uint32_t warps, uint32_t lanes, int *data,
-                                                             uint64_t data_words)
+                                                             uint64_t data_words, uint32_t smem_words)
 {
+    extern __shared__ int sdata[];                        /* the block's __shared__ data instance */
+    for (uint32_t i = threadIdx.x; i < smem_words; i += blockDim.x) sdata[i] = 0;
+    __syncthreads();
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t gw = (uint64_t)blockIdx.x * warps + warp;
     const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
@@ -233,7 +236,15 @@ __global__ void __launch_bounds__(1024, 2) raw_replay_kernel(SRC src, const uint
         const unsigned sw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
         if (st) { __syncthreads(); continue; }
         if (sw) { __syncwarp(); continue; }
-        if (op == 3u || ((x >> 61) & 1u) || w >= data_words) continue;   /* shared words: not modelled */
+        if (op == 3u) continue;
+        if ((x >> 61) & 1u) {                                /* shared data access */
+            if (w >= smem_words) continue;
+            if (op == 0u) acc += ((volatile int *)sdata)[w];
+            else if (op == 1u) ((volatile int *)sdata)[w] = (int)i;
+            else atomicAdd(&sdata[w], 1);
+            continue;
+        }
+        if (w >= data_words) continue;
         if (op == 0u) acc += __ldcg(&data[w]);
         else if (op == 1u) data[w] = (int)i;
         else atomicAdd(&data[w], 1);
@@ -267,12 +278,13 @@ extern "C" hr_status hrb_raw_replay(const hr_trace *t, int *data, uint64_t data_
         const uint64_t *kd = t->kdesc + 8ull * k;
         if (kd[0] == 0) continue;
         const dim3 g((unsigned)kd[0]), b((unsigned)(kd[1] * 32));
+        const uint32_t sw = (uint32_t)kd[3];
         if (t->format == HR_TRACE_C32)
-            raw_replay_kernel<<<g, b, 0, s>>>(hr_src_c32{t->rec32, t->recop}, t->warp_off + kd[4],
-                                              (uint32_t)kd[1], (uint32_t)kd[2], data, data_words);
+            raw_replay_kernel<<<g, b, sw * 4, s>>>(hr_src_c32{t->rec32, t->recop}, t->warp_off + kd[4],
+                                                   (uint32_t)kd[1], (uint32_t)kd[2], data, data_words, sw);
         else
-            raw_replay_kernel<<<g, b, 0, s>>>(hr_src_u64{t->rec}, t->warp_off + kd[4], (uint32_t)kd[1],
-                                              (uint32_t)kd[2], data, data_words);
+            raw_replay_kernel<<<g, b, sw * 4, s>>>(hr_src_u64{t->rec}, t->warp_off + kd[4], (uint32_t)kd[1],
+                                                   (uint32_t)kd[2], data, data_words, sw);
         if (cudaGetLastError() != cudaSuccess) return HR_E_CUDA;
     }
     return HR_OK;

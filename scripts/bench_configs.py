@@ -12,6 +12,15 @@ from paper_2401_04701_b200 import hirace as hr  # noqa: E402
 from tracegen import c4, c5, programs, stencil, suite  # noqa: E402
 
 
+def raw_ms(dt, words, reps=3):
+    """The uninstrumented replay of the same records (hrb_raw_replay)."""
+    from paper_2401_04701_b200 import online as on
+    data = torch.zeros(words, dtype=torch.int32, device="cuda")
+    t = on.time_ms(lambda: on.raw_replay(dt, data, words), reps=reps, warmup=1)
+    del data
+    return t
+
+
 def run(name, trace=None, dt=None, words=None, smem=0, reps=5, ring=1 << 22, opts=0):
     if dt is None:
         dt = hr.DeviceTrace.from_trace(trace)
@@ -28,7 +37,9 @@ def run(name, trace=None, dt=None, words=None, smem=0, reps=5, ring=1 << 22, opt
     rms, nr, kms, nk = hr.hr_replay_timing(ck.ctx)
     kms /= reps
     ck.close()
+    rms_raw = raw_ms(dt, words) if os.environ.get("RAW") else None
     out = {"config": name, "accesses": n_acc, "kernels": nk // reps, "kernel_ms": round(kms, 4),
+           "raw_replay_ms": rms_raw, "slowdown_vs_raw": (kms / rms_raw) if rms_raw else None,
            "reset_ms": round(rms / reps, 4), "wall_ms": round(wall * 1e3, 3),
            "kernel_acc_per_s": n_acc / (kms / 1e3), "races": len(raw), "flags": fl}
     print(json.dumps(out), flush=True)
