@@ -53,6 +53,11 @@ def parse():
     ap.add_argument("--ref-lb", type=int, default=8, help="C5 sample per --impl reference step")
     ap.add_argument("--options", type=int, default=0, help="extra HR_OPT_* bits (ablations)")
     ap.add_argument("--no-slowdown", action="store_true")
+    ap.add_argument("--emulate-shard", default=None,
+                    help="R/N: replay only address shard R of N on this one GPU (scaling projection; "
+                         "shards share nothing but the final allgather)")
+    ap.add_argument("--granule-log2", type=int, default=9,
+                    help="address-shard granule (2^g words; 9 = 4 KiB of shadow)")
     ap.add_argument("--double-shadow", action="store_true",
                     help="HR_OPT_DOUBLE_SHADOW: reset the previous kernel's shadow on a side stream")
     ap.add_argument("--format", default="u64", choices=["c32", "u64"],
@@ -267,17 +272,24 @@ def main():
 
     rank, world, local = dist_setup(args)
     assert world == args.gpus or world == 1, "launch with torchrun for --gpus > 1"
+    emulated = None
+    if args.emulate_shard:
+        assert world == 1, "--emulate-shard runs one process"
+        er, en = (int(x) for x in args.emulate_shard.split("/"))
+        emulated = (er, en)
     seed = args.seed if args.seed is not None else c5.DEFAULT_SEED
     lb = args.lb
     stream = torch.cuda.current_stream().cuda_stream
 
+    shard_rank, shard_n = emulated if emulated else (rank, world)
     # --- input: this rank's shard of the trace, generated in HBM (untimed) ---
     if args.format == "c32":
-        rec32, recop, woff, kd = c5.gpu_trace_c32(lb, seed, rank=rank, nshard=world)
+        rec32, recop, woff, kd = c5.gpu_trace_c32(lb, seed, rank=shard_rank, nshard=shard_n,
+                                                  granule_log2=args.granule_log2)
         dt = hr.DeviceTrace(None, woff, kd, rec32, recop)
         n_acc_rank = int(((recop & 3) != 3).sum().item())
     else:
-        rec, woff, kd = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
+        rec, woff, kd = c5.gpu_trace(lb, seed, rank=shard_rank, nshard=shard_n, granule_log2=args.granule_log2)
         dt = hr.DeviceTrace(rec, woff, kd)
         n_acc_rank = int((((rec >> 62) & 3) != 3).sum().item())
     torch.cuda.synchronize()
@@ -298,7 +310,8 @@ def main():
         n_own += int((acc_mask & (wv < owned)).sum().item())
     del acc_mask, wv
     opts = hr.HR_OPT_TIMING | args.options | (hr.HR_OPT_DOUBLE_SHADOW if args.double_shadow else 0)
-    ck = hr.Checker(c5.total_words(lb), 0, shard=(rank, world), options=opts, ring_capacity=1 << 21)
+    ck = hr.Checker(c5.total_words(lb), 0, shard=(shard_rank, shard_n), options=opts, ring_capacity=1 << 21,
+                    granule_log2=args.granule_log2)
 
     def step(replay_fn):
         ck.reset()
@@ -313,8 +326,14 @@ def main():
     # warm-up + correctness of this run against the closed form (planted set)
     for _ in range(max(args.warmup, 1)):
         raw, flags = step(dev_replay)
+    def expected():
+        pl = c5.planted(lb, seed)
+        if emulated:
+            return [(w, sc) for w, sc in pl if ((w >> args.granule_log2) % shard_n) == shard_rank]
+        return pl
+
     got = [(int(r["word"]), int(r["scope"])) for r in raw]
-    parity_ok = got == c5.planted(lb, seed) and flags == 0
+    parity_ok = got == expected() and flags == 0
     hr.hr_replay_timing(ck.ctx)                     # drop warm-up launches
 
     clocks = Clocks(torch.cuda.current_device())
@@ -332,7 +351,7 @@ def main():
     clk = clocks.stop()
     ms_total = e0.elapsed_time(e1)
     reset_ms, n_resets, kern_ms, n_kern = hr.hr_replay_timing(ck.ctx)
-    parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw] == c5.planted(lb, seed)
+    parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw] == expected()
 
     ms_step = max_over_ranks(ms_total / args.steps, world)
     total_acc = sum_over_ranks(n_acc_rank, world)
@@ -362,7 +381,7 @@ def main():
         rates = json.load(open(rates_path))
         floor_ms = 1e3 * (n_gather / rates["random_cas_hbm_per_s"] +
                           (dt.record_bytes() + BYTES_PER_ACCESS_ALGO * n_own) / (peak * 1e9))
-        ceiling = {"kind": "measured random-DRAM RMW rate + copy peak", "rate_source": rates_path,
+        ceiling = {"kind": "measured random-DRAM RMW rate + copy peak", "rate_source": os.path.relpath(rates_path, ROOT),
                    "random_gathers": n_gather, "coalesced_own_row": n_own,
                    "floor_ms_per_launch": floor_ms, "kernel_ms": kern_ms / max(n_kern, 1),
                    "frac_of_floor": floor_ms / (kern_ms / max(n_kern, 1))}
@@ -382,11 +401,12 @@ def main():
         torch.cuda.empty_cache()
         pinned = []
         if args.e2e_format == "c32":
-            g32, gop, _, _ = c5.gpu_trace_c32(lb, seed, rank=rank, nshard=world)
+            g32, gop, _, _ = c5.gpu_trace_c32(lb, seed, rank=shard_rank, nshard=shard_n,
+                                              granule_log2=args.granule_log2)
             parts = (("rec32", g32), ("recop", gop))
             host_trace.rec = None
         else:
-            grec, _, _ = c5.gpu_trace(lb, seed, rank=rank, nshard=world)
+            grec, _, _ = c5.gpu_trace(lb, seed, rank=shard_rank, nshard=shard_n, granule_log2=args.granule_log2)
             parts = (("rec", grec),)
             host_trace.rec32 = None
         for name, tsr in parts:
@@ -412,7 +432,7 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world)
-        parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == c5.planted(lb, seed)
+        parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == expected()
         e2e = {"value": total_acc / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(16 + 24 * len(raw_e) // max(world, 1)),
                "ms_per_step": e2e_ms, "format": args.e2e_format}
@@ -452,6 +472,12 @@ def main():
             "cpu_baseline": cpu,
             "parity_vs_closed_form": parity_ok,
         }
+        if emulated:
+            out["emulated_shard"] = {"rank": shard_rank, "of": shard_n, "shard_accesses": total_acc,
+                                     "shard_ms_per_step": ms_step,
+                                     "note": "one shard replayed alone on one GPU: a projection of the N-GPU "
+                                             "step (ranks share nothing but the final allgather), not a "
+                                             "multi-GPU measurement"}
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

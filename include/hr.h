@@ -73,13 +73,15 @@ enum {
     HR_OPT_NO_FASTEXIT = 2u,   /* disable label-insensitive fast exits (a7), for ablations */
     HR_OPT_TIMING = 4u,        /* record CUDA events around every shadow reset and replay launch */
     HR_OPT_NO_SPECULATE = 8u,  /* first attempt loads the shadow word instead of speculating INIT */
-    HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen by sampled record density) */
+    HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen from sampled record density
+                                  and warp-length tail, see hr_host.cu kernel_choice) */
     HR_OPT_POOL = 32u,         /* replay with warp pools of valid accesses (sparse traces) */
     HR_OPT_DOUBLE_SHADOW = 64u, /* two global shadows: the kernel-boundary reset (a11) of one runs on a
                                    side stream while the next kernel uses the other (2x shadow memory) */
-    HR_OPT_FINITE_HISTORY = 128u /* BASELINE, not HiRace: iGUARD-style 16-byte records (one reader, one
+    HR_OPT_FINITE_HISTORY = 128u, /* BASELINE, not HiRace: iGUARD-style 16-byte records (one reader, one
                                    writer) checked with the same replay, for the
                                    paper's comparisons (Listing 4 eviction, memory); shadow scan off */
+    HR_OPT_POOL_WIDE = 256u      /* force the 64-register pooled kernel (few very long warps) */
 };
 
 /* One unique racy address.  24 bytes.
@@ -143,6 +145,11 @@ hr_status hr_init(const hr_config *cfg, hr_ctx **out);
  * block % count == rank.  count must be a power of two <= 64.  Call before
  * hr_shadow_alloc.  Default: rank 0 of 1. */
 hr_status hr_set_shard(hr_ctx *ctx, uint32_t rank, uint32_t count);
+
+/* Same with a shard granule of 2^granule_log2 words (5..24; hr_set_shard uses 9).
+ * Smaller granules spread power-law hot words over more ranks; 5 (32 words)
+ * still keeps a warp's 32 consecutive words on one rank. */
+hr_status hr_set_shard_ex(hr_ctx *ctx, uint32_t rank, uint32_t count, uint32_t granule_log2);
 
 /* Register a shadow region ("For each shared memory variable, a
  * shadow value data structure is allocated").

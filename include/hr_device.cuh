@@ -61,6 +61,7 @@ struct hr_dev {
     uint32_t ring_cap;
     uint32_t kernel_id;
     uint32_t shard_rank, shard_log2; /* owner(granule) = granule & (2^log2 - 1) */
+    uint32_t gran_log2;           /* shard granule = 2^gran_log2 words (default 9: 4 KiB of shadow) */
     uint32_t wc_bits;             /* bc occupies [31:wc_bits], wc [wc_bits-1:0] */
     uint32_t bc_max, wc_max;
     uint32_t options;             /* HR_OPT_* */
@@ -178,8 +179,8 @@ __device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uin
     }
     const uint64_t g = word - d.gbase;
     if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
-    const uint64_t gran = g >> 9;
-    local = ((gran >> d.shard_log2) << 9) | (g & 511u);
+    const uint64_t gran = g >> d.gran_log2;
+    local = ((gran >> d.shard_log2) << d.gran_log2) | (g & ((1ull << d.gran_log2) - 1u));
     return ((uint32_t)gran & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
 }
 

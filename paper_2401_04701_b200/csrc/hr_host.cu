@@ -28,7 +28,7 @@
 struct hr_ctx {
     int device = 0;
     hr_config cfg{};
-    uint32_t shard_rank = 0, shard_count = 1, shard_log2 = 0;
+    uint32_t shard_rank = 0, shard_count = 1, shard_log2 = 0, gran_log2 = 9;
     unsigned long long *gshadow = nullptr;       /* current buffer */
     unsigned long long *gbuf[2] = {nullptr, nullptr};
     int gcur = 0;
@@ -45,7 +45,7 @@ struct hr_ctx {
     unsigned char *fsm = nullptr;
     uint32_t last_kernel = 0;
     bool have_kernel = false;
-    bool last_pooled = false;
+    int last_kind = 0;                           /* HR_K_* of the last replay */
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;                 /* host-trace staging copies */
     void *stage[4] = {nullptr, nullptr, nullptr, nullptr};   /* warp_off, rec|rec32, recop, unused */
@@ -102,6 +102,7 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.kernel_id = kernel_id;
     d.shard_rank = c->shard_rank;
     d.shard_log2 = c->shard_log2;
+    d.gran_log2 = c->gran_log2;
     d.wc_bits = c->cfg.wc_bits;
     d.bc_max = (1u << c->cfg.bc_bits) - 1u;
     d.wc_max = (1u << c->cfg.wc_bits) - 1u;
@@ -136,7 +137,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         if (cudaMalloc(&c->fsm, HR_FSM_SMEM_BYTES) != cudaSuccess ||
             cudaMalloc(&c->ring, sizeof(hr_race) * (size_t)k.ring_capacity) != cudaSuccess ||
             cudaMalloc(&c->tail, 4 * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMalloc(&c->counters, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMalloc(&c->counters, 8 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_NOMEM, "device allocation failed in hr_init");
             break;
         }
@@ -145,7 +146,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         memcpy(host + HR_FSM_BYTES, hr_fsm_flags_init, 32);
         if (cudaMemcpy(c->fsm, host, HR_FSM_SMEM_BYTES, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemset(c->tail, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMemset(c->counters, 0, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMemset(c->counters, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_CUDA, "hr_init upload failed");
             break;
         }
@@ -158,16 +159,23 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
     return HR_OK;
 }
 
-extern "C" hr_status hr_set_shard(hr_ctx *c, uint32_t rank, uint32_t count)
+extern "C" hr_status hr_set_shard_ex(hr_ctx *c, uint32_t rank, uint32_t count, uint32_t granule_log2)
 {
-    if (!c || count == 0 || count > 64 || (count & (count - 1)) || rank >= count)
-        return fail(c, HR_E_ARG, "hr_set_shard: bad rank/count");
+    if (!c || count == 0 || count > 64 || (count & (count - 1)) || rank >= count || granule_log2 < 5 ||
+        granule_log2 > 24)
+        return fail(c, HR_E_ARG, "hr_set_shard: bad rank/count/granule");
     if (c->gshadow) return fail(c, HR_E_STATE, "hr_set_shard after hr_shadow_alloc");
+    c->gran_log2 = granule_log2;
     c->shard_rank = rank;
     c->shard_count = count;
     c->shard_log2 = 0;
     while ((1u << c->shard_log2) < count) c->shard_log2++;
     return HR_OK;
+}
+
+extern "C" hr_status hr_set_shard(hr_ctx *c, uint32_t rank, uint32_t count)
+{
+    return hr_set_shard_ex(c, rank, count, 9);
 }
 
 extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_word, uint64_t n_words,
@@ -189,9 +197,9 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
         if (c->gbuf[b]) { cudaFree(c->gbuf[b]); c->gbuf[b] = nullptr; }
     c->gshadow = nullptr;
     /* local slice: this shard's 512-word granules, packed */
-    uint64_t gran = (n_words + 511) >> 9;
+    uint64_t gran = (n_words + (1ull << c->gran_log2) - 1) >> c->gran_log2;
     uint64_t local_gran = (gran + c->shard_count - 1) >> c->shard_log2;
-    uint64_t local = local_gran << 9;
+    uint64_t local = local_gran << c->gran_log2;
     c->double_shadow = (c->cfg.options & HR_OPT_DOUBLE_SHADOW) != 0;
     c->shadow_bytes = (c->cfg.options & HR_OPT_FINITE_HISTORY) ? 16 : 8;
     for (int b = 0; b < (c->double_shadow ? 2 : 1); b++) {
@@ -258,22 +266,37 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
     return HR_OK;
 }
 
-/* Row or pooled replay: options force one; otherwise probe the density of
- * access records (pooling pays when rows are mostly NOP, e.g. power-law BFS
- * frontiers or address-sharded traces). */
-template <typename SRC>
-static hr_status choose_pool(hr_ctx *c, SRC src, uint64_t n_rows, cudaStream_t s, bool *pool)
+/* Kernel choice from warp-length tail and record density (measured on C4,
+ * C5 shards, C5, C3 — profiles/r01_kernel_choice.md):
+ *   max warp > 16x the mean warp (a few very long warps) -> pooled, 64 registers
+ *   < 90% access records (sparse, even)                   -> pooled, 32 registers
+ *   otherwise (dense)                                     -> row kernel, 32 registers
+ * HR_OPT_NO_POOL forces the row kernel, HR_OPT_POOL a pooled one (tail rule
+ * kept), HR_OPT_POOL_WIDE the 64-register pooled kernel. */
+enum { HR_K_ROW = 0, HR_K_POOL = 1, HR_K_POOL_WIDE = 2 };
+
+static int kernel_choice(hr_ctx *c, double acc, double tot, double maxw, double sumw, double nwarps)
 {
-    if (c->cfg.options & HR_OPT_NO_POOL) { *pool = false; return HR_OK; }
-    if (c->cfg.options & HR_OPT_POOL) { *pool = true; return HR_OK; }
-    *pool = false;
-    if (n_rows == 0) return HR_OK;
-    hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, n_rows, 2048, c->counters + 2);
+    const bool tail = nwarps > 0 && maxw > 16.0 * (sumw / nwarps);
+    if (c->cfg.options & HR_OPT_NO_POOL) return HR_K_ROW;
+    if (c->cfg.options & HR_OPT_POOL_WIDE) return HR_K_POOL_WIDE;
+    if (tail) return HR_K_POOL_WIDE;
+    const bool sparse = (c->cfg.options & HR_OPT_POOL) || (tot > 0 && acc < 0.9 * tot);
+    return sparse ? HR_K_POOL : HR_K_ROW;
+}
+
+template <typename SRC>
+static hr_status choose_kernel(hr_ctx *c, SRC src, const hr_trace *t, const uint64_t *woff, cudaStream_t s, int *kind)
+{
+    *kind = HR_K_ROW;
+    if (t->n_rows == 0 || (c->cfg.options & HR_OPT_NO_POOL)) return HR_OK;
+    hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, t->n_rows, 2048, woff, t->n_warp_off, c->counters + 4);
     CU(cudaGetLastError());
-    unsigned long long h[2] = {0, 0};
-    CU(cudaMemcpyAsync(h, c->counters + 2, sizeof h, cudaMemcpyDeviceToHost, s));
+    unsigned long long h[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync(h, c->counters + 4, sizeof h, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    *pool = h[1] && (double)h[0] < 0.9 * (double)h[1];
+    *kind = kernel_choice(c, (double)h[0], (double)h[1], (double)h[2], (double)h[3],
+                          (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0));
     return HR_OK;
 }
 
@@ -297,7 +320,7 @@ static hr_status check_kernel(hr_ctx *c, const hr_trace *t, uint32_t k)
  * are unordered by happens-before, so chunked launches replay the same kernel). */
 template <typename SRC>
 static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const uint64_t *woff, cudaStream_t s,
-                        bool pool, uint64_t b0, uint64_t b1)
+                        int kind, uint64_t b0, uint64_t b1)
 {
     const uint64_t *kd = t->kdesc + 8ull * k;
     uint64_t warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
@@ -319,9 +342,11 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         c->have_kernel = true;
         return HR_OK;
     }
+    const bool pool = kind != HR_K_ROW;
     size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
     void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
-        pool ? hr_replay_kernel<true, SRC> : hr_replay_kernel<false, SRC>;
+        kind == HR_K_POOL_WIDE ? hr_replay_kernel<true, true, SRC>
+                               : (pool ? hr_replay_kernel<true, false, SRC> : hr_replay_kernel<false, false, SRC>);
     if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool timing = c->cfg.options & HR_OPT_TIMING;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -338,16 +363,16 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
 template <typename SRC>
 static hr_status replay(hr_ctx *c, const hr_trace *t, SRC src, const uint64_t *woff, cudaStream_t s)
 {
-    bool pool = false;
-    hr_status st = choose_pool(c, src, t->n_rows, s, &pool);
+    int kind = HR_K_ROW;
+    hr_status st = choose_kernel(c, src, t, woff, s, &kind);
     if (st) return st;
-    c->last_pooled = pool;
+    c->last_kind = kind;
     for (uint32_t k = 0; k < t->n_kernels; k++) {
         if ((st = check_kernel(c, t, k))) return st;
         const uint64_t blocks = t->kdesc[8ull * k];
         if (!blocks) continue;
         if ((st = hr_kernel_begin(c, s))) return st;
-        if ((st = launch(c, t, k, src, woff, s, pool, 0, blocks))) return st;
+        if ((st = launch(c, t, k, src, woff, s, kind, 0, blocks))) return st;
     }
     return HR_OK;
 }
@@ -393,12 +418,10 @@ static hr_status reserve(hr_ctx *c, int i, size_t bytes)
     return HR_OK;
 }
 
-/* Host-side density sample (same rule as the device probe). */
-static bool host_pool_choice(hr_ctx *c, const hr_trace *t)
+/* Host-side version of the kernel-choice probe. */
+static int host_kernel_choice(hr_ctx *c, const hr_trace *t)
 {
-    if (c->cfg.options & HR_OPT_NO_POOL) return false;
-    if (c->cfg.options & HR_OPT_POOL) return true;
-    if (!t->n_rows) return false;
+    if (!t->n_rows || (c->cfg.options & HR_OPT_NO_POOL)) return HR_K_ROW;
     uint64_t acc = 0, tot = 0;
     for (uint32_t s = 0; s < 2048; s++) {
         uint64_t row = (uint64_t)((double)s * (double)t->n_rows / 2048.0);
@@ -409,7 +432,13 @@ static bool host_pool_choice(hr_ctx *c, const hr_trace *t)
             tot++;
         }
     }
-    return tot && (double)acc < 0.9 * (double)tot;
+    double mx = 0, sm = 0;
+    for (uint64_t i = 0; i + 1 < t->n_warp_off; i++) {
+        const double len = t->warp_off[i + 1] >= t->warp_off[i] ? (double)(t->warp_off[i + 1] - t->warp_off[i]) : 0.0;
+        mx = len > mx ? len : mx;
+        sm += len;
+    }
+    return kernel_choice(c, (double)acc, (double)tot, mx, sm, (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0));
 }
 
 /* Host traces: records are copied in block-range chunks on a copy stream and
@@ -432,8 +461,8 @@ extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *st
     CU(cudaStreamWaitEvent(c->copy, start, 0));
     c->ev_pool.push_back(start);
     CU(cudaMemcpyAsync(c->stage[0], t->warp_off, (size_t)t->n_warp_off * 8, cudaMemcpyHostToDevice, c->copy));
-    const bool pool = host_pool_choice(c, t);
-    c->last_pooled = pool;
+    const int kind = host_kernel_choice(c, t);
+    c->last_kind = kind;
     const uint64_t *dwoff = (const uint64_t *)c->stage[0];
     size_t chunk_bytes = (size_t)1 << 30;                       /* ~1 GiB of records per chunk */
     if (const char *e = getenv("HR_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)strtoull(e, nullptr, 10);
@@ -468,8 +497,8 @@ extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *st
             CU(cudaStreamWaitEvent(c->stream, landed, 0));
             c->ev_pool.push_back(landed);
             if (c32) st = launch(c, t, k, hr_src_c32{(const uint32_t *)c->stage[1], (const uint8_t *)c->stage[2]},
-                                 dwoff, c->stream, pool, b0, b1);
-            else st = launch(c, t, k, hr_src_u64{(const uint64_t *)c->stage[1]}, dwoff, c->stream, pool, b0, b1);
+                                 dwoff, c->stream, kind, b0, b1);
+            else st = launch(c, t, k, hr_src_u64{(const uint64_t *)c->stage[1]}, dwoff, c->stream, kind, b0, b1);
             if (st) return st;
         }
     }
@@ -533,7 +562,7 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         hr_race *tmp = nullptr;
         CU(cudaMalloc(&tmp, sizeof(hr_race) * (size_t)scap));
         CU(cudaMemset(c->tail + 2, 0, sizeof(unsigned int)));
-        hr_scan_kernel<<<148 * 8, 256>>>(c->gshadow, c->glocal, c->gbase, c->shard_rank, c->shard_log2,
+        hr_scan_kernel<<<148 * 8, 256>>>(c->gshadow, c->glocal, c->gbase, c->shard_rank, c->shard_log2, c->gran_log2,
                                          c->last_kernel, tmp, c->tail + 2, scap);
         CU(cudaGetLastError());
         unsigned int cnt = 0;

@@ -145,9 +145,12 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
 }
 
 /* POOL = false: row-by-row (dense traces; 32 registers, 64 warps/SM).
- * POOL = true: pooled (sparse traces; 64 registers, 32 warps/SM). */
-template <bool POOL, typename SRC>
-__global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d, SRC src,
+ * POOL = true, WIDE = false: pooled at 32 registers (sparse, evenly spread
+ *   traces, e.g. address shards: occupancy hides the DRAM latency).
+ * POOL = true, WIDE = true: pooled at up to 64 registers, no spills (a few
+ *   very long warps, e.g. power-law BFS hubs: per-warp latency decides). */
+template <bool POOL, bool WIDE, typename SRC>
+__global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel(hr_dev d, SRC src,
                                                                        const uint64_t *__restrict__ woff,
                                                                        uint32_t warps, uint32_t lanes,
                                                                        uint32_t smem_words)
@@ -202,14 +205,24 @@ __global__ void __launch_bounds__(1024, POOL ? 1 : 2) hr_replay_kernel(hr_dev d,
     if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); __syncwarp(); }
 }
 
-/* Density probe for the row/pool choice: counts access records among up to
- * `samples` rows spread over [0, n_rows) (one block). */
+/* Probe for the kernel choice (one block): out[0..1] = access records / records
+ * among up to `samples` rows spread over [0, n_rows); out[2..3] = max / sum of
+ * the warp lengths (rows) over the warp-offset array. */
 template <typename SRC>
-__global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, unsigned long long *out)
+__global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, const uint64_t *woff, uint64_t n_woff,
+                                  unsigned long long *out)
 {
-    __shared__ unsigned long long acc[2];
-    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
+    __shared__ unsigned long long acc[4];
+    if (threadIdx.x < 4) acc[threadIdx.x] = 0;
     __syncthreads();
+    unsigned long long mx = 0, sm = 0;
+    for (uint64_t i = threadIdx.x; i + 1 < n_woff; i += blockDim.x) {
+        const unsigned long long len = woff[i + 1] >= woff[i] ? woff[i + 1] - woff[i] : 0;
+        mx = len > mx ? len : mx;
+        sm += len;
+    }
+    atomicMax(&acc[2], mx);
+    atomicAdd(&acc[3], sm);
     unsigned long long a = 0, tot = 0;
     for (uint32_t s = threadIdx.x >> 5; s < samples; s += blockDim.x >> 5) {
         const uint64_t row = (uint64_t)((double)s * (double)n_rows / (double)samples);
@@ -221,13 +234,14 @@ __global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, un
     atomicAdd(&acc[0], a);
     atomicAdd(&acc[1], tot);
     __syncthreads();
-    if (threadIdx.x < 2) out[threadIdx.x] = acc[threadIdx.x];
+    if (threadIdx.x < 4) out[threadIdx.x] = acc[threadIdx.x];
 }
 
 /* Overflow fallback / cross-check: every RACE word of the (local) global
  * shadow becomes one record in `out` (a9 "end-of-kernel shadow scan"). */
 __global__ void hr_scan_kernel(const unsigned long long *__restrict__ sh, uint64_t n_local, uint64_t gbase,
-                               uint32_t shard_rank, uint32_t shard_log2, uint32_t kernel_id, hr_race *out,
+                               uint32_t shard_rank, uint32_t shard_log2, uint32_t gran_log2, uint32_t kernel_id,
+                               hr_race *out,
                                unsigned int *count, uint32_t cap)
 {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
@@ -237,8 +251,8 @@ __global__ void hr_scan_kernel(const unsigned long long *__restrict__ sh, uint64
         if (st >= HR_RACE_BLOCK) {
             uint32_t slot = atomicAdd(count, 1u);
             if (slot < cap) {
-                uint64_t gran_local = i >> 9;
-                uint64_t g = (((gran_local << shard_log2) | shard_rank) << 9) | (i & 511u);
+                uint64_t gran_local = i >> gran_log2;
+                uint64_t g = (((gran_local << shard_log2) | shard_rank) << gran_log2) | (i & ((1ull << gran_log2) - 1u));
                 hr_race r;
                 r.word = gbase + g;
                 r.block = 0xffffffffu;

@@ -28,7 +28,8 @@ HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING, HR_OPT_NO_SPECULATE, HR_O
     1, 2, 4, 8, 16, 32
 HR_OPT_DOUBLE_SHADOW = 64
 HR_OPT_FINITE_HISTORY = 128
-EXPORTS = ("hr_init", "hr_set_shard", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
+HR_OPT_POOL_WIDE = 256
+EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_report", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing",
            "hr_fsm_table",
@@ -79,6 +80,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     sig = {
         "hr_init": ([P(HrConfig), P(vp)], ctypes.c_int),
         "hr_set_shard": ([vp, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
+        "hr_set_shard_ex": ([vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
         "hr_shadow_alloc": ([vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, P(vp)], ctypes.c_int),
         "hr_kernel_begin": ([vp, vp], ctypes.c_int),
         "hr_replay_trace": ([vp, P(HrTrace), vp], ctypes.c_int),
@@ -122,8 +124,8 @@ def hr_init(bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, 
     return ctx
 
 
-def hr_set_shard(ctx, rank: int, count: int):
-    _check(load().hr_set_shard(ctx, rank, count), ctx, "hr_set_shard")
+def hr_set_shard(ctx, rank: int, count: int, granule_log2: int = 9):
+    _check(load().hr_set_shard_ex(ctx, rank, count, granule_log2), ctx, "hr_set_shard_ex")
 
 
 def hr_shadow_alloc(ctx, space: int, base_word: int, n_words: int) -> int:
@@ -310,10 +312,10 @@ class Checker:
 
     def __init__(self, global_words: int, smem_words: int = 0, base_word: int = 0, device: int = 0,
                  bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, options: int = 0,
-                 shard: Optional[Tuple[int, int]] = None):
+                 shard: Optional[Tuple[int, int]] = None, granule_log2: int = 9):
         self.ctx = hr_init(bc_bits, wc_bits, ring_capacity, device, options)
         if shard is not None:
-            hr_set_shard(self.ctx, shard[0], shard[1])
+            hr_set_shard(self.ctx, shard[0], shard[1], granule_log2)
         self.shadow_ptr = hr_shadow_alloc(self.ctx, HR_GLOBAL, base_word, max(1, global_words))
         hr_shadow_alloc(self.ctx, HR_SHARED, 0, smem_words)
 

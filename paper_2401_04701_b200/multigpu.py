@@ -24,18 +24,19 @@ RACE_DTYPE = np.dtype([("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("f
 NOP = np.uint64(3 << 62)
 
 
-def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: int = 0) -> np.ndarray:
+def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: int = 0,
+               granule_log2: int = 9) -> np.ndarray:
     """Which records of one warp's rows (n, 32) belong to shard `rank`."""
     op = rows >> np.uint64(62)
     space = (rows >> np.uint64(61)) & np.uint64(1)
     word = rows & np.uint64((1 << 61) - 1)
-    gran = (word - np.uint64(base_word)) >> np.uint64(9)
+    gran = (word - np.uint64(base_word)) >> np.uint64(granule_log2)
     glob = (op != 3) & (space == 0) & ((gran % np.uint64(nshard)) == np.uint64(rank))
     shared = (op != 3) & (space == 1) & ((block % nshard) == rank)
     return glob | shared
 
 
-def shard_trace(trace, rank: int, nshard: int, base_word: int = 0):
+def shard_trace(trace, rank: int, nshard: int, base_word: int = 0, granule_log2: int = 9):
     """Host-side shard of a trace: this rank's records compacted per lane inside
     each barrier-delimited segment, padded with NOPs, barrier rows kept."""
     from tracegen.format import Trace   # layout container only
@@ -50,7 +51,7 @@ def shard_trace(trace, rank: int, nshard: int, base_word: int = 0):
         for w in range(blocks * warps):
             r0, r1 = int(trace.warp_off[woi + w]), int(trace.warp_off[woi + w + 1])
             rows = trace.rec[r0 * 32: r1 * 32].reshape(-1, 32)
-            keep = owner_mask(rows, w // warps, rank, nshard, base_word)
+            keep = owner_mask(rows, w // warps, rank, nshard, base_word, granule_log2)
             op = rows >> np.uint64(62)
             word = rows & np.uint64((1 << 61) - 1)
             is_bar = np.any((op == 3) & (word != 0), axis=1)

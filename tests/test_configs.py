@@ -60,14 +60,14 @@ def test_c5_racy_set_is_planted(lb):
     assert abs(frac[0] - 0.70) < 0.03 and abs(frac[1] - 0.20) < 0.03 and abs(frac[2] - 0.10) < 0.02
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
-def test_c5_shards_partition_the_racy_set(n):
+@pytest.mark.parametrize("n,g", [(2, 9), (4, 9), (8, 9), (8, 5), (4, 12)])
+def test_c5_shards_partition_the_racy_set(n, g):
     lb = 4
     full = [(r.word, r.scope) for r in oracle.check(c5.cpu_trace(lb)).races]
     union = []
     for r in range(n):
-        sh = c5.cpu_trace(lb, rank=r, nshard=n)
+        sh = c5.cpu_trace(lb, rank=r, nshard=n, granule_log2=g)
         got = oracle.check(sh).races
-        assert all(((x.word >> 9) % n) == r for x in got)
+        assert all(((x.word >> g) % n) == r for x in got)
         union += [(x.word, x.scope) for x in got]
     assert sorted(union) == full

@@ -50,9 +50,10 @@ def _cpu_lib():
         build()
         _cpu = ctypes.CDLL(_CPU_LIB)
         P = ctypes.POINTER
-        _cpu.c5_warp_rows.argtypes = [P(Params), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64]
+        _cpu.c5_warp_rows.argtypes = [P(Params), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_uint64]
         _cpu.c5_warp_rows.restype = ctypes.c_uint64
-        _cpu.c5_gen_cpu.argtypes = [P(Params), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
+        _cpu.c5_gen_cpu.argtypes = [P(Params), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                     ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
         _cpu.c5_planted.argtypes = [P(Params), ctypes.c_void_p, ctypes.c_void_p]
         _cpu.c5_record_at.argtypes = [P(Params), ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
@@ -66,7 +67,7 @@ def _gpu_lib():
         build()
         _gpu = ctypes.CDLL(_GPU_LIB)
         _gpu.c5_gen_gpu.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
-                                    ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_uint32, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _gpu.c5_gen_gpu.restype = ctypes.c_int
     return _gpu
@@ -89,17 +90,18 @@ def kdesc(lb: int) -> np.ndarray:
     return np.array([[1 << lb, WARPS, LANES, 0, 0, 0, 0, 0]], dtype=np.uint64)
 
 
-def cpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1) -> Trace:
+def cpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, granule_log2: int = 9) -> Trace:
     """The (shard of the) C5 trace as host arrays."""
     lib = _cpu_lib()
     p = Params(seed, lb)
     nw = (1 << lb) * WARPS
     l2 = _log2(nshard)
-    rows = np.array([lib.c5_warp_rows(ctypes.byref(p), rank, l2, w) for w in range(nw)], dtype=np.uint64)
+    rows = np.array([lib.c5_warp_rows(ctypes.byref(p), rank, l2, granule_log2, w) for w in range(nw)],
+                    dtype=np.uint64)
     off = np.zeros(nw + 1, dtype=np.uint64)
     off[1:] = np.cumsum(rows)
     rec = np.empty(int(off[-1]) * 32, dtype=np.uint64)
-    lib.c5_gen_cpu(ctypes.byref(p), rank, l2, 0, nw, off.ctypes.data, rec.ctypes.data)
+    lib.c5_gen_cpu(ctypes.byref(p), rank, l2, granule_log2, 0, nw, off.ctypes.data, rec.ctypes.data)
     return Trace(rec, kdesc(lb), off)
 
 
@@ -114,44 +116,47 @@ def planted(lb: int, seed: int = DEFAULT_SEED) -> List[Tuple[int, int]]:
     return sorted(zip((int(x) for x in w), (int(x) for x in s)))
 
 
-def _gpu_offsets(lib, lb, seed, rank, l2, device, stream):
+def _gpu_offsets(lib, lb, seed, rank, l2, g2, device, stream):
     import torch
     nw = (1 << lb) * WARPS
     if l2 == 0:
         return torch.arange(nw + 1, dtype=torch.int64, device=device) * ROWS
     rows = torch.empty(nw, dtype=torch.int64, device=device)
-    rc = lib.c5_gen_gpu(seed, lb, rank, l2, 0, rows.data_ptr(), None, None, None, None, stream)
+    rc = lib.c5_gen_gpu(seed, lb, rank, l2, g2, 0, rows.data_ptr(), None, None, None, None, stream)
     assert rc == 0, rc
     off = torch.zeros(nw + 1, dtype=torch.int64, device=device)
     off[1:] = torch.cumsum(rows, 0)
     return off
 
 
-def gpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda"):
+def gpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda",
+              granule_log2: int = 9):
     """Generate the (shard of the) trace directly in HBM, u64 records.
     Returns (rec int64 tensor, warp_off int64 tensor, kdesc numpy)."""
     import torch
     lib = _gpu_lib()
     stream = torch.cuda.current_stream().cuda_stream
-    off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), device, stream)
+    off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), granule_log2, device, stream)
     n_rows = int(off[-1].item())
     rec = torch.empty(n_rows * 32, dtype=torch.int64, device=device)
-    rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), 1, None, off.data_ptr(), rec.data_ptr(), None, None, stream)
+    rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), granule_log2, 1, None, off.data_ptr(), rec.data_ptr(),
+                        None, None, stream)
     assert rc == 0, rc
     return rec, off, kdesc(lb)
 
 
-def gpu_trace_c32(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda"):
+def gpu_trace_c32(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda",
+                  granule_log2: int = 9):
     """Same trace in the HR_TRACE_C32 encoding (160 B per row).  Returns
     (rec32 int32, recop uint8, warp_off int64) tensors and kdesc."""
     import torch
     lib = _gpu_lib()
     stream = torch.cuda.current_stream().cuda_stream
-    off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), device, stream)
+    off = _gpu_offsets(lib, lb, seed, rank, _log2(nshard), granule_log2, device, stream)
     n_rows = int(off[-1].item())
     rec32 = torch.empty(n_rows * 32, dtype=torch.int32, device=device)
     recop = torch.empty(n_rows * 32, dtype=torch.uint8, device=device)
-    rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), 1, None, off.data_ptr(), None, rec32.data_ptr(),
-                        recop.data_ptr(), stream)
+    rc = lib.c5_gen_gpu(seed, lb, rank, _log2(nshard), granule_log2, 1, None, off.data_ptr(), None,
+                        rec32.data_ptr(), recop.data_ptr(), stream)
     assert rc == 0, rc
     return rec32, recop, off, kdesc(lb)

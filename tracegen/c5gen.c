@@ -5,7 +5,7 @@
 #include "c5gen.h"
 
 /* rows warp gw occupies in shard (rank of 2^log2n) */
-uint64_t c5_warp_rows(const c5_params *p, uint32_t rank, uint32_t log2n, uint64_t gw)
+uint64_t c5_warp_rows(const c5_params *p, uint32_t rank, uint32_t log2n, uint32_t glog2, uint64_t gw)
 {
     uint64_t b = gw >> 3;
     uint32_t w = (uint32_t)(gw & 7);
@@ -16,7 +16,7 @@ uint64_t c5_warp_rows(const c5_params *p, uint32_t rank, uint32_t log2n, uint64_
         for (uint32_t l = 0; l < C5_LANES; l++) {
             uint32_t k = 0;
             for (uint32_t i = 0; i < C5_EPOCH; i++)
-                if (c5_owned_by(c5_record(p, b, w * 32 + l, e * C5_EPOCH + i), rank, log2n)) k++;
+                if (c5_owned_by(c5_record(p, b, w * 32 + l, e * C5_EPOCH + i), rank, log2n, glog2)) k++;
             if (k > maxk) maxk = k;
         }
         rows += maxk + 1;
@@ -25,7 +25,7 @@ uint64_t c5_warp_rows(const c5_params *p, uint32_t rank, uint32_t log2n, uint64_
 }
 
 /* write warps [w0, w1) at rows row_off[gw - w0] (relative to out) */
-void c5_gen_cpu(const c5_params *p, uint32_t rank, uint32_t log2n, uint64_t w0, uint64_t w1,
+void c5_gen_cpu(const c5_params *p, uint32_t rank, uint32_t log2n, uint32_t glog2, uint64_t w0, uint64_t w1,
                 const uint64_t *row_off, uint64_t *out)
 {
     for (uint64_t gw = w0; gw < w1; gw++) {
@@ -38,7 +38,7 @@ void c5_gen_cpu(const c5_params *p, uint32_t rank, uint32_t log2n, uint64_t w0, 
                 uint32_t k = 0;
                 for (uint32_t i = 0; i < C5_EPOCH; i++) {
                     uint64_t x = c5_record(p, b, w * 32 + l, e * C5_EPOCH + i);
-                    if (log2n == 0 || c5_owned_by(x, rank, log2n)) {
+                    if (log2n == 0 || c5_owned_by(x, rank, log2n, glog2)) {
                         out[(row + k) * 32 + l] = x;
                         k++;
                     }

@@ -15,7 +15,7 @@ __device__ __forceinline__ void c5_put(uint64_t *out, uint32_t *out32, uint8_t *
     outb[i] = (uint8_t)((x >> 62) | (((x >> 61) & 1ull) << 2));
 }
 
-__global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint64_t n_warps, int pass,
+__global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint32_t glog2, uint64_t n_warps, int pass,
                               uint64_t *rows_out, const uint64_t *row_off, uint64_t *out, uint32_t *out32,
                               uint8_t *outb)
 {
@@ -29,7 +29,7 @@ __global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint64
         uint32_t k = 0;
         for (uint32_t i = 0; i < C5_EPOCH; i++) {
             uint64_t x = c5_record(&p, b, w * 32 + l, e * C5_EPOCH + i);
-            if (log2n == 0 || c5_owned_by(x, rank, log2n)) {
+            if (log2n == 0 || c5_owned_by(x, rank, log2n, glog2)) {
                 if (pass) c5_put(out, out32, outb, (row + k) * 32 + l, x);
                 k++;
             }
@@ -44,7 +44,7 @@ __global__ void c5_gen_kernel(c5_params p, uint32_t rank, uint32_t log2n, uint64
     if (!pass && l == 0) rows_out[gw] = row;
 }
 
-extern "C" int c5_gen_gpu(uint64_t seed, uint32_t lb, uint32_t rank, uint32_t log2n, int pass,
+extern "C" int c5_gen_gpu(uint64_t seed, uint32_t lb, uint32_t rank, uint32_t log2n, uint32_t glog2, int pass,
                           uint64_t *rows_out, const uint64_t *row_off, uint64_t *out, uint32_t *out32,
                           uint8_t *outb, void *stream)
 {
@@ -54,7 +54,7 @@ extern "C" int c5_gen_gpu(uint64_t seed, uint32_t lb, uint32_t rank, uint32_t lo
     uint64_t n_warps = (1ull << lb) * C5_WARPS;
     uint64_t threads = n_warps * 32;
     unsigned blocks = (unsigned)((threads + 255) / 256);
-    c5_gen_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, rank, log2n, n_warps, pass, rows_out, row_off, out,
+    c5_gen_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, rank, log2n, glog2, n_warps, pass, rows_out, row_off, out,
                                                               out32, outb);
     return (int)cudaGetLastError();
 }

@@ -24,7 +24,7 @@
  *
  * Row layout per warp: 8 epochs x (32 access rows, 1 __syncthreads row) = 264
  * rows.  Sharded variant (rank r of N = 2^log2n): a lane keeps only records
- * whose 4 KiB shadow granule (word >> 9) is owned by r (granule mod N), kept
+ * whose shadow granule (word >> glog2; 9 = 4 KiB of shadow) is owned by r (granule mod N), kept
  * records are compacted per lane inside each epoch, epoch segments are padded
  * with NOPs to the warp's longest lane, barrier rows are kept.
  */
@@ -136,10 +136,10 @@ C5_HD uint64_t c5_record(const c5_params *p, uint64_t b, uint32_t t, uint32_t j)
     return (2ull << 62) | (total - (1ull << hl) + rank);   /* atomic */
 }
 
-C5_HD int c5_owned_by(uint64_t rec, uint32_t rank, uint32_t log2n)
+C5_HD int c5_owned_by(uint64_t rec, uint32_t rank, uint32_t log2n, uint32_t glog2)
 {
     uint64_t word = rec & ((1ull << 61) - 1);
-    return (uint32_t)((word >> 9) & ((1ull << log2n) - 1)) == rank;
+    return (uint32_t)((word >> glog2) & ((1ull << log2n) - 1)) == rank;
 }
 
 #endif /* C5GEN_H_ */
