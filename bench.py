@@ -12,8 +12,8 @@ N > 1, the NCCL allgather of the per-shard race sets.
   value  device-resident: trace generated in HBM before timing; K steps timed
          with CUDA events on the launching stream, max over ranks.
   e2e    same steps through hr_replay_trace_host: the trace lives in pinned
-         host memory and is copied H2D inside every timed step; the race set is
-         read back D2H.
+         host memory (HR_TRACE_PACKED by default, decoded on the device) and is
+         copied H2D inside every timed step; the race set is read back D2H.
   roofline  for the replay kernel: algorithmic bytes / live event-timed
          duration vs MEASURED_PEAKS.json hbm_gbs.
 
@@ -62,8 +62,9 @@ def parse():
                     help="HR_OPT_DOUBLE_SHADOW: reset the previous kernel's shadow on a side stream")
     ap.add_argument("--format", default="u64", choices=["c32", "u64"],
                     help="device-resident trace encoding (include/hr.h HR_TRACE_U64 = 256 B/row, C32 = 160 B/row)")
-    ap.add_argument("--e2e-format", default="c32", choices=["c32", "u64"],
-                    help="host-buffer trace encoding for e2e (C32 moves 37.5%% fewer bytes over PCIe)")
+    ap.add_argument("--e2e-format", default="packed", choices=["packed", "c32", "u64"],
+                    help="host-buffer trace encoding for e2e: packed (HR_TRACE_PACKED, decoded on the device), "
+                         "c32 (160 B/row) or u64 (256 B/row)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU to test the N>1 path (timings then meaningless)")
     ap.add_argument("--c4-lv", type=int, default=20, help="log2 vertices of the C4 graph for the slowdown")
@@ -392,7 +393,24 @@ def main():
 
     # --- e2e through the C ABI with HOST buffers ---
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.e2e_format == "packed":
+        # pack the u64 trace on the device (untimed), keep only the pinned host copy
+        src = dt
+        if dt.format != hr.HR_TRACE_U64:
+            dt.rec = dt.rec32 = dt.recop = None
+            rec32 = recop = None  # noqa: F841
+            grec, _, _ = c5.gpu_trace(lb, seed, rank=shard_rank, nshard=shard_n, granule_log2=args.granule_log2)
+            src = hr.DeviceTrace(grec, woff, kd)
+            grec = None  # noqa: F841
+        pk = ck.pack(src, stream)
+        host_trace = pk.to_host()
+        src = pk = None
+        dt.rec = dt.rec32 = dt.recop = None
+        rec = None  # noqa: F841
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        h2d = int(host_trace.packed.nbytes + host_trace.pack_off.nbytes + host_trace.warp_off.nbytes)
+    elif not args.no_e2e:
         host_trace = type("T", (), {})()
         host_trace.kdesc = kd
         host_trace.warp_off = woff.cpu().numpy().view(np.uint64)
@@ -418,6 +436,7 @@ def main():
         parts = g32 = gop = grec = None  # noqa: F841
         torch.cuda.empty_cache()
         h2d = sum(int(h.numel() * h.element_size()) for h in pinned) + int(host_trace.warp_off.nbytes)
+    if not args.no_e2e:
         host_replay = lambda: ck.replay_host(host_trace, stream)  # noqa: E731
         for _ in range(args.warmup):
             step(host_replay)

@@ -102,8 +102,30 @@ typedef struct {
 /* Record encodings of an hr_trace. */
 enum {
     HR_TRACE_U64 = 0,   /* rec: one u64 record per lane and row (any word < 2^61) */
-    HR_TRACE_C32 = 1    /* rec32 + recop: 160 B per row instead of 256 (words < 2^32) */
+    HR_TRACE_C32 = 1,   /* rec32 + recop: 160 B per row instead of 256 (words < 2^32) */
+    HR_TRACE_PACKED = 2 /* packed + pack_off: lossless variable-length rows (below), made by hr_pack_trace */
 };
+
+/* HR_TRACE_PACKED: a lossless, transfer-oriented encoding of the U64 rows
+ * (not in the paper: it shrinks the host->device bytes of hr_replay_trace_host).
+ * Segment i (0 <= i < n_warp_off-1) encodes the rows [warp_off[i], warp_off[i+1])
+ * (warp_off must be non-decreasing) and occupies bytes [pack_off[i], pack_off[i+1])
+ * of `packed`; every pack_off is a multiple of 4.  A segment of n rows is
+ *   n header bytes h_j, zero-padded to a multiple of 4, then n row bodies.
+ * With k = h & 63, affine = h & 64, uniform = h & 128, a row body is
+ *   k == 62 (raw):  the 32 u64 records verbatim (256 B, as lo/hi u32 pairs)
+ *   otherwise:      nibbles: uniform ? one u32 whose low 4 bits apply to every lane
+ *                                    : four u32, lane l at bits 4*(l%8) of u32 l/8
+ *                   if k != 63:  base (u64 as lo, hi u32)
+ *                                if !affine && k > 0: k u32 words holding lane l's
+ *                                k-bit delta at bits [l*k, l*k+k) (little-endian)
+ * A nibble is op | x << 2: for op 0..2 (access) x = space and the word is
+ * base + lane (affine), base + delta_l, or base (k == 0); for op 3 (control)
+ * x = the control word (0..2) and no word bits are used.  k == 63 means the
+ * row has no access lanes (no base).  Rows a nibble cannot express (a control
+ * record with word > 2 or the space bit set) use the raw form.  The decoder
+ * reads up to 8 bytes past a segment's last body; allocate `packed` with 16
+ * bytes of slack (hr_pack_trace's size query includes them). */
 
 /* A batch of synthetic access streams (tracegen/format.py documents the layout).
  *   rec       DEVICE, n_rows*32 uint64 records; row r, lane l at rec[r*32+l]:
@@ -131,6 +153,12 @@ typedef struct {
     uint32_t reserved;
     const uint32_t *rec32;
     const uint8_t *recop;
+    /* format HR_TRACE_PACKED (rec, rec32, recop unused; n_rows and warp_off as
+     * for U64):  packed  the segments described above;
+     *            pack_off  n_warp_off u64 byte offsets into packed.
+     * Same ownership rules; HOST pointers for hr_replay_trace_host. */
+    const uint8_t *packed;
+    const uint64_t *pack_off;
 } hr_trace;
 
 typedef struct hr_ctx hr_ctx;   /* opaque */
@@ -178,8 +206,28 @@ hr_status hr_kernel_begin(hr_ctx *ctx, void *stream);
 hr_status hr_replay_trace(hr_ctx *ctx, const hr_trace *t, void *stream);
 
 /* Same with t->rec and t->warp_off in HOST memory: the records are copied to
- * ctx-owned device staging buffers on `stream`, then replayed. */
+ * ctx-owned device staging buffers on `stream`, then replayed.  Block-range
+ * chunks are copied on a side stream so the copy of chunk i+1 overlaps the
+ * replay of chunk i.  PACKED traces are decoded on the device chunk by chunk
+ * into one u64 staging buffer right before each chunk's replay (on `stream`).
+ * On a device-resident PACKED trace hr_replay_trace does the same decode
+ * (and synchronously reads warp_off/pack_off to the host to plan chunks). */
 hr_status hr_replay_trace_host(hr_ctx *ctx, const hr_trace *t, void *stream);
+
+/* Encode a DEVICE trace `in` (format U64) as HR_TRACE_PACKED on `stream`.
+ *   out == NULL: size query, *bytes receives the packed size (with the 16-byte
+ *                slack), pack_off (DEVICE, in->n_warp_off u64) is filled.
+ *   out != NULL: out (DEVICE, cap bytes) receives the segments; pack_off is
+ *                filled again; HR_E_ARG if cap < the size.
+ * Synchronises `stream`.  HR_E_ARG on a decreasing warp_off.  The trace's
+ * other fields (kdesc, warp_off, n_rows) are shared with the packed trace. */
+hr_status hr_pack_trace(hr_ctx *ctx, const hr_trace *in, uint8_t *out, uint64_t cap, uint64_t *pack_off,
+                        uint64_t *bytes, void *stream);
+
+/* Decode a DEVICE HR_TRACE_PACKED trace `in` into U64 rows: rec_out (DEVICE,
+ * in->n_rows*32 u64) receives row r of every segment at rec_out[r*32..];
+ * rows no segment covers are not written.  Asynchronous on `stream`. */
+hr_status hr_unpack_trace(hr_ctx *ctx, const hr_trace *in, uint64_t *rec_out, void *stream);
 
 /* Synchronise the ctx's last stream and return the unique racy addresses,
  * sorted by (kernel, space, block, word), one record per address with the

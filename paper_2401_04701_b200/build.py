@@ -10,7 +10,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libhirace.so")
 SOURCES = [os.path.join(CSRC, "hr_host.cu"), os.path.join(CSRC, "hr_online.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("hr_replay.cuh", "hr_records.cuh", "hr_fh.cuh", "hr_classes.cuh", "fsm_table.inc",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("hr_replay.cuh", "hr_records.cuh", "hr_fh.cuh", "hr_classes.cuh", "hr_pack.cuh", "fsm_table.inc",
                                             "fsm_classes.inc")] + \
     [os.path.join(INCLUDE, f) for f in ("hr.h", "hr_device.cuh", "hr_bench.h", "hr_array.cuh")]
 

@@ -7,6 +7,7 @@
  * in hr_init / hr_shadow_alloc / the first hr_replay_trace_host; the check
  * path allocates nothing.
  */
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,6 +23,7 @@
 #include "hr_replay.cuh"
 #include "hr_fh.cuh"
 #include "hr_classes.cuh"
+#include "hr_pack.cuh"
 #include "fsm_table.inc"
 #include "fsm_classes.inc"
 
@@ -48,8 +50,10 @@ struct hr_ctx {
     int last_kind = 0;                           /* HR_K_* of the last replay */
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;                 /* host-trace staging copies */
-    void *stage[4] = {nullptr, nullptr, nullptr, nullptr};   /* warp_off, rec|rec32, recop, unused */
-    size_t stage_cap[4] = {0, 0, 0, 0};
+    /* staging: 0 warp_off, 1 rec|rec32|packed, 2 recop|decoded chunk, 3 pack_off,
+     * 4 hr_pack_trace segment sizes + error word, 5 scan temporaries */
+    void *stage[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t stage_cap[6] = {0, 0, 0, 0, 0, 0};
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
@@ -384,6 +388,7 @@ static bool trace_ok(const hr_trace *t)
     if (!t->kdesc || !t->warp_off) return false;
     if (t->format == HR_TRACE_U64) return t->rec != nullptr;
     if (t->format == HR_TRACE_C32) return t->rec32 && t->recop;
+    if (t->format == HR_TRACE_PACKED) return t->packed && t->pack_off;
     return false;
 }
 
@@ -398,11 +403,14 @@ static hr_status dispatch(hr_ctx *c, const hr_trace *t, const uint64_t *rec, con
     return replay(c, t, src, woff, c->stream);
 }
 
+static hr_status replay_packed(hr_ctx *c, const hr_trace *t, bool host);
+
 extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
 {
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
+    if (t->format == HR_TRACE_PACKED) return replay_packed(c, t, false);
     return dispatch(c, t, t->rec, t->rec32, t->recop, t->warp_off);
 }
 
@@ -444,11 +452,183 @@ static int host_kernel_choice(hr_ctx *c, const hr_trace *t)
 /* Host traces: records are copied in block-range chunks on a copy stream and
  * each chunk is replayed as soon as it lands, so the PCIe transfer of chunk
  * i+1 overlaps the replay of chunk i. */
+static size_t host_chunk_bytes()
+{
+    size_t chunk_bytes = (size_t)1 << 30;                       /* ~1 GiB of records per chunk */
+    if (const char *e = getenv("HR_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)strtoull(e, nullptr, 10);
+    return chunk_bytes < 256 ? 256 : chunk_bytes;
+}
+
+/* PACKED traces (host or device resident): per kernel, block-range chunks of
+ * ~chunk_bytes of DECODED rows; each chunk's packed bytes are copied on the
+ * copy stream (host traces), decoded on `stream` into one U64 staging buffer,
+ * then replayed from it.  Decode and replay are ordered on `stream`, so one
+ * decode buffer serves every chunk; only the copies run ahead. */
+static hr_status replay_packed(hr_ctx *c, const hr_trace *t, bool host)
+{
+    hr_status st;
+    const uint64_t nwo = t->n_warp_off;
+    std::vector<uint64_t> hwoff_v, hpoff_v;
+    const uint64_t *hwoff = t->warp_off, *hpoff = t->pack_off;
+    const uint64_t *dwoff = t->warp_off, *dpoff = t->pack_off;
+    const uint8_t *dpacked = t->packed;
+    if (!host) {                                   /* plan chunks from host copies of the offsets */
+        hwoff_v.resize(nwo);
+        hpoff_v.resize(nwo);
+        CU(cudaMemcpyAsync(hwoff_v.data(), t->warp_off, nwo * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(hpoff_v.data(), t->pack_off, nwo * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        hwoff = hwoff_v.data();
+        hpoff = hpoff_v.data();
+    }
+    const size_t chunk_rows = host_chunk_bytes() / 256 ? host_chunk_bytes() / 256 : 1;
+    /* chunk plan and the largest chunk, before any buffer is (re)allocated */
+    struct chunk { uint32_t k; uint64_t b0, b1; };
+    std::vector<chunk> plan;
+    uint64_t max_rows = 0;
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        if ((st = check_kernel(c, t, k))) return st;
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        const uint64_t blocks = kd[0], warps = kd[1], woi = kd[4];
+        if (!blocks) continue;
+        const uint64_t krows = hwoff[woi + blocks * warps] - hwoff[woi];
+        uint64_t nchunks = (krows + chunk_rows - 1) / chunk_rows;
+        if (nchunks < 1) nchunks = 1;
+        if (nchunks > blocks) nchunks = blocks;
+        for (uint64_t ci = 0; ci < nchunks; ci++) {
+            const uint64_t b0 = blocks * ci / nchunks, b1 = blocks * (ci + 1) / nchunks;
+            const uint64_t s0 = woi + b0 * warps, s1 = woi + b1 * warps;
+            if (hwoff[s1] < hwoff[s0] || hpoff[s1] < hpoff[s0])
+                return fail(c, HR_E_ARG, "packed trace: decreasing warp_off or pack_off");
+            plan.push_back({k, b0, b1});
+            max_rows = std::max(max_rows, hwoff[s1] - hwoff[s0]);
+        }
+    }
+    if ((st = reserve(c, 2, (size_t)std::max<uint64_t>(max_rows, 1) * 256))) return st;
+    uint64_t *dec = (uint64_t *)c->stage[2];
+    if (host) {
+        const uint64_t total = hpoff[nwo - 1] + HR_PACK_SLACK;
+        if ((st = reserve(c, 0, (size_t)nwo * 8))) return st;
+        if ((st = reserve(c, 3, (size_t)nwo * 8))) return st;
+        if ((st = reserve(c, 1, (size_t)total))) return st;
+        if (!c->copy) CU(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        cudaEvent_t start = get_event(c);
+        CU(cudaEventRecord(start, c->stream));
+        CU(cudaStreamWaitEvent(c->copy, start, 0));
+        c->ev_pool.push_back(start);
+        CU(cudaMemcpyAsync(c->stage[0], t->warp_off, (size_t)nwo * 8, cudaMemcpyHostToDevice, c->copy));
+        CU(cudaMemcpyAsync(c->stage[3], t->pack_off, (size_t)nwo * 8, cudaMemcpyHostToDevice, c->copy));
+        dwoff = (const uint64_t *)c->stage[0];
+        dpoff = (const uint64_t *)c->stage[3];
+        dpacked = (const uint8_t *)c->stage[1];
+    }
+    int kind = -1;
+    int64_t cur_k = -1;
+    for (const chunk &ch : plan) {
+        const uint64_t *kd = t->kdesc + 8ull * ch.k;
+        const uint64_t warps = kd[1], woi = kd[4];
+        const uint64_t s0 = woi + ch.b0 * warps, s1 = woi + ch.b1 * warps;
+        const uint64_t rbase = hwoff[s0], rows = hwoff[s1] - hwoff[s0];
+        if ((int64_t)ch.k != cur_k) {
+            if ((st = hr_kernel_begin(c, c->stream))) return st;
+            cur_k = ch.k;
+        }
+        if (host) {
+            if (hpoff[s1] > hpoff[s0])
+                CU(cudaMemcpyAsync((uint8_t *)c->stage[1] + hpoff[s0], t->packed + hpoff[s0], hpoff[s1] - hpoff[s0],
+                                   cudaMemcpyHostToDevice, c->copy));
+            cudaEvent_t landed = get_event(c);
+            CU(cudaEventRecord(landed, c->copy));
+            CU(cudaStreamWaitEvent(c->stream, landed, 0));
+            c->ev_pool.push_back(landed);
+        }
+        if (s1 > s0) {
+            const uint64_t threads = (s1 - s0) * 32;
+            hr_unpack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, c->stream>>>(dpacked, dpoff, dwoff, s0, s1,
+                                                                                       rbase, dec);
+            CU(cudaGetLastError());
+        }
+        hr_src_u64 src{dec - rbase * 32};
+        if (kind < 0) {
+            /* kernel choice: density of the first decoded chunk, tail of all warps */
+            if (rows && !(c->cfg.options & HR_OPT_NO_POOL)) {
+                hr_density_kernel<hr_src_u64><<<1, 1024, 0, c->stream>>>(hr_src_u64{dec}, rows, 2048, dwoff, nwo,
+                                                                        c->counters + 4);
+                CU(cudaGetLastError());
+                unsigned long long h[4] = {0, 0, 0, 0};
+                CU(cudaMemcpyAsync(h, c->counters + 4, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+                CU(cudaStreamSynchronize(c->stream));
+                kind = kernel_choice(c, (double)h[0], (double)h[1], (double)h[2], (double)h[3],
+                                     (double)(nwo > 1 ? nwo - 1 : 0));
+            } else {
+                kind = HR_K_ROW;
+            }
+            c->last_kind = kind;
+        }
+        if ((st = launch(c, t, ch.k, src, dwoff, c->stream, kind, ch.b0, ch.b1))) return st;
+    }
+    return HR_OK;
+}
+
+extern "C" hr_status hr_pack_trace(hr_ctx *c, const hr_trace *in, uint8_t *out, uint64_t cap, uint64_t *pack_off,
+                                   uint64_t *bytes, void *stream)
+{
+    if (!c || !in || !pack_off || !bytes || in->format != HR_TRACE_U64 || !in->rec || !in->warp_off ||
+        in->n_warp_off < 1)
+        return fail(c, HR_E_ARG, "hr_pack_trace: bad arguments (U64 device trace required)");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    c->stream = s;
+    hr_status st;
+    const uint64_t n = in->n_warp_off;
+    const size_t sizes_bytes = ((size_t)n * 8 + 15) & ~(size_t)15;
+    if ((st = reserve(c, 4, sizes_bytes + 16))) return st;
+    uint64_t *sizes = (uint64_t *)c->stage[4];
+    unsigned int *err = (unsigned int *)((char *)c->stage[4] + sizes_bytes);
+    CU(cudaMemsetAsync(err, 0, 4, s));
+    const unsigned grid = (unsigned)((n * 32 + 255) / 256);
+    hr_pack_size_kernel<<<grid, 256, 0, s>>>(in->rec, in->warp_off, n, sizes, err);
+    CU(cudaGetLastError());
+    size_t tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, sizes, pack_off, (int64_t)n, s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, sizes, pack_off, (int64_t)n, s));
+    uint64_t total = 0;
+    unsigned int herr = 0;
+    CU(cudaMemcpyAsync(&total, pack_off + (n - 1), 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (herr) return fail(c, HR_E_ARG, "hr_pack_trace: decreasing warp_off");
+    *bytes = total + HR_PACK_SLACK;
+    if (!out) return HR_OK;
+    if (cap < total + HR_PACK_SLACK) return fail(c, HR_E_ARG, "hr_pack_trace: cap %llu < %llu", (unsigned long long)cap,
+                                                 (unsigned long long)(total + HR_PACK_SLACK));
+    hr_pack_write_kernel<<<grid, 256, 0, s>>>(in->rec, in->warp_off, n, pack_off, out);
+    CU(cudaGetLastError());
+    CU(cudaMemsetAsync(out + total, 0, HR_PACK_SLACK, s));
+    CU(cudaStreamSynchronize(s));
+    return HR_OK;
+}
+
+extern "C" hr_status hr_unpack_trace(hr_ctx *c, const hr_trace *in, uint64_t *rec_out, void *stream)
+{
+    if (!c || !in || !rec_out || in->format != HR_TRACE_PACKED || !in->packed || !in->pack_off || !in->warp_off)
+        return fail(c, HR_E_ARG, "hr_unpack_trace: bad arguments (PACKED device trace required)");
+    CU(cudaSetDevice(c->device));
+    if (in->n_warp_off < 2) return HR_OK;
+    const uint64_t nseg = in->n_warp_off - 1;
+    hr_unpack_kernel<<<(unsigned)((nseg * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        in->packed, in->pack_off, in->warp_off, 0, nseg, 0, rec_out);
+    CU(cudaGetLastError());
+    return HR_OK;
+}
+
 extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *stream)
 {
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
+    if (t->format == HR_TRACE_PACKED) return replay_packed(c, t, true);
     const bool c32 = t->format == HR_TRACE_C32;
     hr_status st;
     if ((st = reserve(c, 0, (size_t)t->n_warp_off * 8))) return st;
@@ -464,9 +644,7 @@ extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *st
     const int kind = host_kernel_choice(c, t);
     c->last_kind = kind;
     const uint64_t *dwoff = (const uint64_t *)c->stage[0];
-    size_t chunk_bytes = (size_t)1 << 30;                       /* ~1 GiB of records per chunk */
-    if (const char *e = getenv("HR_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)strtoull(e, nullptr, 10);
-    if (chunk_bytes < 256) chunk_bytes = 256;
+    const size_t chunk_bytes = host_chunk_bytes();
     for (uint32_t k = 0; k < t->n_kernels; k++) {
         if ((st = check_kernel(c, t, k))) return st;
         const uint64_t *kd = t->kdesc + 8ull * k;
@@ -617,6 +795,7 @@ extern "C" hr_status hr_race_classes(hr_ctx *c, const hr_trace *t, const hr_race
                                      uint8_t *classes_out, void *stream)
 {
     if (!c || !trace_ok(t) || (n && (!races || !classes_out))) return fail(c, HR_E_ARG, "hr_race_classes: bad arguments");
+    if (t->format == HR_TRACE_PACKED) return fail(c, HR_E_ARG, "hr_race_classes: U64 or C32 traces only");
     CU(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     if (n == 0) return HR_OK;
@@ -742,7 +921,7 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->tail) cudaFree(c->tail);
     if (c->counters) cudaFree(c->counters);
     if (c->fsm) cudaFree(c->fsm);
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < 6; i++)
         if (c->stage[i]) cudaFree(c->stage[i]);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }

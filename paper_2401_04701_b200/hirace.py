@@ -30,7 +30,7 @@ HR_OPT_DOUBLE_SHADOW = 64
 HR_OPT_FINITE_HISTORY = 128
 HR_OPT_POOL_WIDE = 256
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
-           "hr_replay_trace_host", "hr_report", "hr_race_classes", "hr_reset_report", "hr_counters",
+           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing",
            "hr_fsm_table",
            "hr_device_view", "hr_last_error", "hr_destroy")
@@ -48,7 +48,7 @@ class HrRace(ctypes.Structure):
                 ("first_kind", ctypes.c_uint8), ("prev_state", ctypes.c_uint8)]
 
 
-HR_TRACE_U64, HR_TRACE_C32 = 0, 1
+HR_TRACE_U64, HR_TRACE_C32, HR_TRACE_PACKED = 0, 1, 2
 
 
 class HrTrace(ctypes.Structure):
@@ -56,7 +56,8 @@ class HrTrace(ctypes.Structure):
                 ("n_kernels", ctypes.c_uint32), ("kernel_base", ctypes.c_uint32),
                 ("warp_off", ctypes.c_void_p), ("n_warp_off", ctypes.c_uint64),
                 ("format", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
-                ("rec32", ctypes.c_void_p), ("recop", ctypes.c_void_p)]
+                ("rec32", ctypes.c_void_p), ("recop", ctypes.c_void_p),
+                ("packed", ctypes.c_void_p), ("pack_off", ctypes.c_void_p)]
 
 
 assert ctypes.sizeof(HrRace) == 24
@@ -85,6 +86,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_kernel_begin": ([vp, vp], ctypes.c_int),
         "hr_replay_trace": ([vp, P(HrTrace), vp], ctypes.c_int),
         "hr_replay_trace_host": ([vp, P(HrTrace), vp], ctypes.c_int),
+        "hr_pack_trace": ([vp, P(HrTrace), vp, ctypes.c_uint64, vp, P(ctypes.c_uint64), vp], ctypes.c_int),
+        "hr_unpack_trace": ([vp, P(HrTrace), vp, vp], ctypes.c_int),
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_race_classes": ([vp, P(HrTrace), vp, ctypes.c_size_t, vp, vp], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
@@ -146,6 +149,20 @@ def hr_replay_trace(ctx, t: HrTrace, stream: int = 0):
 def hr_replay_trace_host(ctx, t: HrTrace, stream: int = 0):
     _check(load().hr_replay_trace_host(ctx, ctypes.byref(t), ctypes.c_void_p(stream)), ctx,
            "hr_replay_trace_host")
+
+
+def hr_pack_trace(ctx, t: HrTrace, out: int, cap: int, pack_off: int, stream: int = 0) -> int:
+    """Encode a device U64 trace as HR_TRACE_PACKED; out == 0 is the size query.
+    Returns the packed size in bytes (with the 16-byte slack)."""
+    n = ctypes.c_uint64()
+    _check(load().hr_pack_trace(ctx, ctypes.byref(t), ctypes.c_void_p(out or None), cap, ctypes.c_void_p(pack_off),
+                                ctypes.byref(n), ctypes.c_void_p(stream)), ctx, "hr_pack_trace")
+    return int(n.value)
+
+
+def hr_unpack_trace(ctx, t: HrTrace, rec_out: int, stream: int = 0):
+    _check(load().hr_unpack_trace(ctx, ctypes.byref(t), ctypes.c_void_p(rec_out), ctypes.c_void_p(stream)), ctx,
+           "hr_unpack_trace")
 
 
 class Race(NamedTuple):
@@ -235,14 +252,21 @@ def hr_destroy(ctx):
 class DeviceTrace:
     """A trace resident in HBM: torch tensors for the records and warp offsets,
     host kdesc.  U64 format: ``rec`` int64 (n_rows*32).  C32 format: ``rec32``
-    int32 and ``recop`` uint8 (op | space<<2), both n_rows*32."""
+    int32 and ``recop`` uint8 (op | space<<2), both n_rows*32.  PACKED format:
+    ``packed`` uint8 and ``pack_off`` int64 (made by ``Checker.pack``)."""
 
-    def __init__(self, rec, warp_off, kdesc: np.ndarray, rec32=None, recop=None):
+    def __init__(self, rec, warp_off, kdesc: np.ndarray, rec32=None, recop=None, packed=None, pack_off=None,
+                 n_rows: Optional[int] = None):
         self.rec, self.rec32, self.recop = rec, rec32, recop
+        self.packed, self.pack_off = packed, pack_off
         self.warp_off = warp_off
         self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
-        self.format = HR_TRACE_C32 if rec32 is not None else HR_TRACE_U64
-        self.n_rows = (rec32.numel() if rec32 is not None else rec.numel()) // 32
+        if packed is not None:
+            self.format = HR_TRACE_PACKED
+            self.n_rows = int(n_rows)
+        else:
+            self.format = HR_TRACE_C32 if rec32 is not None else HR_TRACE_U64
+            self.n_rows = (rec32.numel() if rec32 is not None else rec.numel()) // 32
 
     @staticmethod
     def from_trace(trace, device="cuda", compact: bool = False) -> "DeviceTrace":
@@ -257,7 +281,25 @@ class DeviceTrace:
         return DeviceTrace(rec, wo, trace.kdesc)
 
     def record_bytes(self) -> int:
+        if self.format == HR_TRACE_PACKED:
+            return int(self.packed.numel())
         return self.n_rows * (160 if self.format == HR_TRACE_C32 else 256)
+
+    def to_host(self) -> "HostTrace":
+        """Pinned host copy (for hr_replay_trace_host)."""
+        import torch
+
+        def pin(x):
+            h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            h.copy_(x)
+            return h.numpy()
+        wo = pin(self.warp_off).view(np.uint64)
+        if self.format == HR_TRACE_PACKED:
+            return HostTrace(self.kdesc, wo, packed=pin(self.packed), pack_off=pin(self.pack_off).view(np.uint64),
+                             n_rows=self.n_rows)
+        if self.format == HR_TRACE_C32:
+            return HostTrace(self.kdesc, wo, rec32=pin(self.rec32).view(np.uint32), recop=pin(self.recop))
+        return HostTrace(self.kdesc, wo, rec=pin(self.rec).view(np.uint64))
 
     def c(self, kernel_base: int = 0) -> HrTrace:
         t = HrTrace()
@@ -270,21 +312,39 @@ class DeviceTrace:
         t.format = self.format
         if self.format == HR_TRACE_C32:
             t.rec32, t.recop = self.rec32.data_ptr(), self.recop.data_ptr()
+        elif self.format == HR_TRACE_PACKED:
+            t.packed, t.pack_off = self.packed.data_ptr(), self.pack_off.data_ptr()
         else:
             t.rec = self.rec.data_ptr()
         return t
 
 
+class HostTrace:
+    """Host arrays of one trace in any format (fields as in hr_trace)."""
+
+    def __init__(self, kdesc, warp_off, rec=None, rec32=None, recop=None, packed=None, pack_off=None,
+                 n_rows: Optional[int] = None):
+        self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
+        self.warp_off = warp_off
+        self.rec, self.rec32, self.recop, self.packed, self.pack_off = rec, rec32, recop, packed, pack_off
+        self.n_rows = n_rows
+
+
 def host_trace_c(trace, kernel_base: int = 0) -> HrTrace:
     """HrTrace over HOST arrays (for hr_replay_trace_host); keep `trace` alive.
-    `trace` has rec (U64) or rec32/recop (C32) numpy arrays, kdesc, warp_off."""
+    `trace` has rec (U64), rec32/recop (C32) or packed/pack_off/n_rows (PACKED)
+    numpy arrays, kdesc, warp_off."""
     t = HrTrace()
     t.kdesc = trace.kdesc.ctypes.data
     t.n_kernels = trace.kdesc.shape[0]
     t.kernel_base = kernel_base
     t.warp_off = trace.warp_off.ctypes.data
     t.n_warp_off = trace.warp_off.shape[0]
-    if getattr(trace, "rec32", None) is not None:
+    if getattr(trace, "packed", None) is not None:
+        t.format = HR_TRACE_PACKED
+        t.n_rows = int(trace.n_rows)
+        t.packed, t.pack_off = trace.packed.ctypes.data, trace.pack_off.ctypes.data
+    elif getattr(trace, "rec32", None) is not None:
         t.format = HR_TRACE_C32
         t.n_rows = trace.rec32.shape[0] // 32
         t.rec32, t.recop = trace.rec32.ctypes.data, trace.recop.ctypes.data
@@ -333,6 +393,19 @@ class Checker:
         self._host_ref = trace
         hr_replay_trace_host(self.ctx, host_trace_c(trace, kernel_base), stream)
 
+    def pack(self, dtrace: DeviceTrace, stream: Optional[int] = None) -> DeviceTrace:
+        """HR_TRACE_PACKED copy of a device U64 trace (hr_pack_trace)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        dev = dtrace.warp_off.device
+        pack_off = torch.empty(dtrace.warp_off.numel(), dtype=torch.int64, device=dev)
+        t = dtrace.c()
+        n = hr_pack_trace(self.ctx, t, 0, 0, pack_off.data_ptr(), stream)
+        out = torch.empty(n, dtype=torch.uint8, device=dev)
+        hr_pack_trace(self.ctx, t, out.data_ptr(), n, pack_off.data_ptr(), stream)
+        return DeviceTrace(None, dtrace.warp_off, dtrace.kdesc, packed=out, pack_off=pack_off, n_rows=dtrace.n_rows)
+
     def report(self):
         return hr_report(self.ctx)
 
@@ -361,11 +434,14 @@ class Checker:
             pass
 
 
-def check_trace(trace, device: int = 0, compact: bool = False, **kw) -> Tuple[List[Race], int]:
-    """Replay a host trace on the GPU and return (sorted racy set, flags)."""
+def check_trace(trace, device: int = 0, compact: bool = False, packed: bool = False, **kw) -> Tuple[List[Race], int]:
+    """Replay a host trace on the GPU and return (sorted racy set, flags).
+    packed=True replays the hr_pack_trace encoding of it instead."""
     gmax, smem = trace_extent(trace)
     ck = Checker(gmax, smem, device=device, **kw)
-    dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}", compact=compact)
+    dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}", compact=compact and not packed)
+    if packed:
+        dt = ck.pack(dt)
     ck.replay(dt)
     races, flags, _ = ck.report()
     ck.close()
