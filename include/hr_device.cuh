@@ -79,6 +79,26 @@ struct hr_thr {
     uint32_t off;                 /* detection disabled (clock overflow) */
 };
 
+/* ---------------- schedule fuzzing (tests only) ----------------
+ * Built with -DHR_FUZZ (libhirace_fuzz.so, tests/test_gpu_fuzz.py): a
+ * pseudo-random __nanosleep before a quarter of the shadow CASes, same-word
+ * groups folded in descending lane order, and the replay grid's CUDA blocks
+ * mapped to simulated blocks in reverse.  Each changes the commit order of
+ * some words; the racy set must not change (schedule independence). */
+#ifdef HR_FUZZ
+__device__ __forceinline__ void hr__jitter()
+{
+    uint32_t x = (uint32_t)clock64() * 2654435761u ^ (threadIdx.x * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu);
+    x ^= x >> 15;
+    x *= 0x2C1B3C6Du;
+    x ^= x >> 12;
+    if ((x & 3u) == 0u) __nanosleep(x >> 22);
+}
+#define HR_JITTER() hr__jitter()
+#else
+#define HR_JITTER()
+#endif
+
 /* ---------------- memory primitives ---------------- */
 
 __device__ __forceinline__ unsigned long long hr__ld_g(const unsigned long long *p)
@@ -91,6 +111,7 @@ __device__ __forceinline__ unsigned long long hr__ld_g(const unsigned long long 
 __device__ __forceinline__ unsigned long long hr__cas_g(unsigned long long *p, unsigned long long cmp,
                                                         unsigned long long val)
 {
+    HR_JITTER();
     return atomicCAS(p, cmp, val);
 }
 
@@ -105,6 +126,7 @@ __device__ __forceinline__ unsigned long long hr__cas_s(uint32_t a, unsigned lon
                                                         unsigned long long val)
 {
     unsigned long long r;
+    HR_JITTER();
     asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(r) : "r"(a), "l"(cmp), "l"(val) : "memory");
     return r;
 }
@@ -193,14 +215,30 @@ __device__ __forceinline__ uint32_t hr__transition(const hr_dev &d, const hr_thr
                                                    unsigned kb1, uint32_t &rinfo, uint32_t &rel)
 {
     const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
-    rel = hr__rel(t.tid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+#ifdef HR_FUZZ
+    /* descending lane order: the highest peer's access is labelled against `old` */
+    {
+        const uint32_t f = 31u - __clz(peers);
+        kind = ((kb0 >> f) & 1u) | (((kb1 >> f) & 1u) << 1);
+        lane = f;
+    }
+    const uint32_t ftid = (t.tid & ~31u) | lane;
+#else
+    const uint32_t ftid = t.tid;
+#endif
+    rel = hr__rel(ftid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
     const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
     uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
     rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19)) : 0u;
     unsigned r = peers & ~(1u << lane);
     while (r) {
+#ifdef HR_FUZZ
+        const uint32_t j = 31u - __clz(r);
+        r &= ~(1u << j);
+#else
         const uint32_t j = __ffs(r) - 1;
         r &= r - 1;
+#endif
         const uint32_t kj = ((kb0 >> j) & 1u) | (((kb1 >> j) & 1u) << 1);
         const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | 1u));
         if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
@@ -212,7 +250,11 @@ __device__ __forceinline__ uint32_t hr__transition(const hr_dev &d, const hr_thr
 
 __device__ __forceinline__ unsigned long long hr__nmeta(const hr_thr &t, unsigned peers)
 {
+#ifdef HR_FUZZ
+    const uint32_t last_lane = __ffs(peers) - 1;                 /* descending fold ends at the lowest */
+#else
     const uint32_t last_lane = 31u - __clz(peers);
+#endif
     return (t.meta & ~(0x1full << HR_TID_SHIFT)) | ((unsigned long long)last_lane << HR_TID_SHIFT);
 }
 

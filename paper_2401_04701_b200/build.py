@@ -9,6 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libhirace.so")
+LIB_FUZZ = os.path.join(PKG, "libhirace_fuzz.so")   # -DHR_FUZZ schedule-fuzzing variant (tests only)
 SOURCES = [os.path.join(CSRC, "hr_host.cu"), os.path.join(CSRC, "hr_online.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("hr_replay.cuh", "hr_records.cuh", "hr_fh.cuh", "hr_classes.cuh", "hr_pack.cuh", "fsm_table.inc",
                                             "fsm_classes.inc")] + \
@@ -30,15 +31,21 @@ def stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, extra=None, verbose: bool = False) -> str:
-    if force or stale(LIB, DEPS):
-        cmd = [nvcc()] + NVCC_FLAGS + (extra or []) + ["-I", INCLUDE, "-I", CSRC, "-o", LIB] + SOURCES
+def build(force: bool = False, extra=None, verbose: bool = False, lib: str = LIB) -> str:
+    if lib == LIB_FUZZ:
+        extra = ["-DHR_FUZZ"] + (extra or [])
+    if force or stale(lib, DEPS):
+        cmd = [nvcc()] + NVCC_FLAGS + (extra or []) + ["-I", INCLUDE, "-I", CSRC, "-o", lib] + SOURCES
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + out.stdout + out.stderr)
         if verbose:
             print(out.stderr)
-    return LIB
+    return lib
+
+
+def build_fuzz(force: bool = False) -> str:
+    return build(force=force, lib=LIB_FUZZ)
 
 
 if __name__ == "__main__":

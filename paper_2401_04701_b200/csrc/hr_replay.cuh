@@ -160,10 +160,17 @@ __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel
     unsigned long long *sshadow = reinterpret_cast<unsigned long long *>(
         hr_smem + HR_FSM_SMEM_BYTES + (POOL ? warps * sizeof(hr_pool_smem) : 0));
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
+#ifdef HR_FUZZ
+    const uint32_t cta = gridDim.x - 1u - blockIdx.x;               /* reversed block mapping */
+    t.tid = ((d.block_base + cta) << 10) | (t.tid & 1023u);
+    t.meta = (unsigned long long)t.tid << HR_TID_SHIFT;
+#else
+    const uint32_t cta = blockIdx.x;
+#endif
 
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
-    const uint64_t gw = (uint64_t)blockIdx.x * warps + warp;
+    const uint64_t gw = (uint64_t)cta * warps + warp;
     const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const bool active = lane < lanes;
