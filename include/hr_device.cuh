@@ -70,13 +70,15 @@ struct hr_dev {
 
 /* Per-thread registers. */
 struct hr_thr {
-    uint32_t tid;                 /* block:17 | warp:5 | lane:5 */
-    uint32_t bc, wc;              /* thread-private block / warp scalar clocks */
-    unsigned long long meta;      /* tid<<32 | bc<<wc_bits | wc, refreshed at barriers */
+    /* tid<<32 | bc<<wc_bits | wc: the packed tid (block:17 | warp:5 | lane:5) and
+     * the thread-private block / warp scalar clocks, kept in the
+     * shadow word's own layout so a barrier is one add (no separate registers) */
+    unsigned long long meta;
     uint32_t sshadow;             /* shared-space address of this block's shadow instance */
     uint32_t swords;
     uint32_t fsm;                 /* shared-space address of the FSM table copy */
     uint32_t off;                 /* detection disabled (clock overflow) */
+    __device__ __forceinline__ uint32_t tid() const { return (uint32_t)(meta >> HR_TID_SHIFT) & 0x7ffffffu; }
 };
 
 /* ---------------- schedule fuzzing (tests only) ----------------
@@ -197,7 +199,7 @@ __device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uin
     if (space != 0u) {
         if (word >= t.swords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
         local = word;
-        return ((t.tid >> 10) & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
+        return ((t.tid() >> 10) & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
     }
     const uint64_t g = word - d.gbase;
     if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
@@ -222,9 +224,9 @@ __device__ __forceinline__ uint32_t hr__transition(const hr_dev &d, const hr_thr
         kind = ((kb0 >> f) & 1u) | (((kb1 >> f) & 1u) << 1);
         lane = f;
     }
-    const uint32_t ftid = (t.tid & ~31u) | lane;
+    const uint32_t ftid = (t.tid() & ~31u) | lane;
 #else
-    const uint32_t ftid = t.tid;
+    const uint32_t ftid = t.tid();
 #endif
     rel = hr__rel(ftid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
     const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
@@ -268,7 +270,7 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
     const uint32_t kcol = kind << 4;
     while (true) {
         const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
-        const uint32_t rel = hr__rel(t.tid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+        const uint32_t rel = hr__rel(t.tid(), (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
         const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
         const uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | kcol | (sync << 2) | rel));
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
@@ -346,9 +348,9 @@ __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t,
     if (slot < d.ring_cap) {
         hr_race rr;
         rr.word = word;
-        rr.block = space ? (t.tid >> 10) : 0xffffffffu;
+        rr.block = space ? (t.tid() >> 10) : 0xffffffffu;
         rr.kernel = d.kernel_id;
-        rr.first_tid = (t.tid & ~31u) | ((ei >> 26) & 31u);
+        rr.first_tid = (t.tid() & ~31u) | ((ei >> 26) & 31u);
         rr.space = (uint8_t)space;
         rr.scope = (uint8_t)((ei & 1u) ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
         rr.first_kind = (uint8_t)((ei >> 24) & 3u);
@@ -443,10 +445,8 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     __syncthreads();
     hr_thr t;
     uint32_t block = d.block_base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    t.tid = (block << 10) | ((ltid >> 5) << 5) | (ltid & 31u);
-    t.bc = 0;
-    t.wc = 0;
-    t.meta = (unsigned long long)t.tid << HR_TID_SHIFT;
+    const uint32_t tid = (block << 10) | ((ltid >> 5) << 5) | (ltid & 31u);
+    t.meta = (unsigned long long)tid << HR_TID_SHIFT;
     t.sshadow = (uint32_t)__cvta_generic_to_shared(smem_shadow);
     t.swords = smem_words;
     t.fsm = (uint32_t)__cvta_generic_to_shared(smem_fsm);
@@ -454,11 +454,6 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     return t;
 }
 
-__device__ __forceinline__ void hr__refresh_meta(const hr_dev &d, hr_thr &t)
-{
-    t.meta = ((unsigned long long)t.tid << HR_TID_SHIFT) |
-             ((unsigned long long)t.bc << d.wc_bits) | (unsigned long long)t.wc;
-}
 
 __device__ __forceinline__ void hr_check_read(const hr_dev &d, hr_thr &t, hr_space space, uint64_t word)
 {
@@ -480,16 +475,16 @@ __device__ __forceinline__ void hr_check_atomic(const hr_dev &d, hr_thr &t, hr_s
 __device__ __forceinline__ void hr_syncthreads(const hr_dev &d, hr_thr &t)
 {
     __syncthreads();
-    if (t.bc >= d.bc_max) { t.off = 1; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
-    else { t.bc++; hr__refresh_meta(d, t); }
+    if (((uint32_t)t.meta >> d.wc_bits) >= d.bc_max) { t.off = 1; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+    else t.meta += 1ull << d.wc_bits;
 }
 
 /* __syncwarp(); ++wc (full warp only; sub-warp masks are future work). */
 __device__ __forceinline__ void hr_syncwarp(const hr_dev &d, hr_thr &t)
 {
     __syncwarp();
-    if (t.wc >= d.wc_max) { t.off = 1; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
-    else { t.wc++; hr__refresh_meta(d, t); }
+    if (((uint32_t)t.meta & d.wc_max) >= d.wc_max) { t.off = 1; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+    else t.meta += 1ull;
 }
 
 #endif /* HR_DEVICE_CUH_ */

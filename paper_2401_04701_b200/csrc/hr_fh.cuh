@@ -63,18 +63,18 @@ __device__ __forceinline__ hr_u128 hr_fh__cas(hr_u128 *p, hr_u128 cmp, hr_u128 v
 __device__ __forceinline__ uint32_t hr_fh__access(const hr_dev &d, const hr_thr &t, hr_u128 *p, uint32_t kind)
 {
     const uint32_t lo = (uint32_t)t.meta;
-    const uint64_t mine = hr_fh__rec(kind, t.tid, t.meta);
+    const uint64_t mine = hr_fh__rec(kind, t.tid(), t.meta);
     hr_u128 old = *(volatile hr_u128 *)p;
     while (true) {
         const uint64_t wr = (uint64_t)old, rd = (uint64_t)(old >> 64);
         uint32_t scope = 0;
         if (!(rd & HR_FH_REPORTED)) {
             if ((wr & HR_FH_VALID) && hr_fh__conflict(kind, (uint32_t)(wr >> 59) & 3u)) {
-                const uint32_t u = hr_fh__unordered(wr, t.tid, lo, d.wc_bits);
+                const uint32_t u = hr_fh__unordered(wr, t.tid(), lo, d.wc_bits);
                 scope = u > scope ? u : scope;
             }
             if ((rd & HR_FH_VALID) && kind != HR_READ) {
-                const uint32_t u = hr_fh__unordered(rd, t.tid, lo, d.wc_bits);
+                const uint32_t u = hr_fh__unordered(rd, t.tid(), lo, d.wc_bits);
                 scope = u > scope ? u : scope;
             }
         }

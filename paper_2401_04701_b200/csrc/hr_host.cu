@@ -347,7 +347,15 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         return HR_OK;
     }
     const bool pool = kind != HR_K_ROW;
-    size_t smem = HR_FSM_SMEM_BYTES + (pool ? warps * sizeof(hr_pool_smem) : 0) + smem_words * 8;
+    if (!src.aligned_ok()) return fail(c, HR_E_ARG, "trace records must be 16-byte aligned (TMA staging)");
+    const bool wide = kind == HR_K_POOL_WIDE;
+    const uint32_t nb = wide ? hr_stage_cfg<true>::NB : hr_stage_cfg<false>::NB;
+    const uint32_t ch = wide ? hr_stage_cfg<true>::CH : hr_stage_cfg<false>::CH;
+    size_t smem = (size_t)hr_stage_offset(pool, (uint32_t)warps, (uint32_t)smem_words) +
+                  hr_stage_bytes((uint32_t)warps, nb, ch, SRC::ROW_BYTES);
+    if (smem > 227 * 1024)
+        return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (shadow %llu words + staging)", k, smem,
+                    (unsigned long long)smem_words);
     void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
         kind == HR_K_POOL_WIDE ? hr_replay_kernel<true, true, SRC>
                                : (pool ? hr_replay_kernel<true, false, SRC> : hr_replay_kernel<false, false, SRC>);

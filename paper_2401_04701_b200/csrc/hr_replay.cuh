@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
                                                         const hr_pool_smem &ps, uint32_t lane, unsigned peers,
                                                         uint32_t &rinfo, uint32_t &rel)
 {
-    const uint32_t base = t.tid & ~31u;
+    const uint32_t base = t.tid() & ~31u;
     const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
     const uint32_t src0 = ps.src[lane];
     const uint32_t kind0 = (uint32_t)(ps.rec[lane] >> 62);
@@ -144,11 +144,33 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
     }
 }
 
+/* Per-warp TMA staging ring of the replay kernels: NB chunk buffers of CH
+ * rows.  The 32-register kernels run 64 warps/SM, so 2 x 4 rows (2 KiB of u64
+ * rows per warp); the wide pooled kernel runs few long warps: 4 x 4 rows. */
+template <bool WIDE> struct hr_stage_cfg {
+    static constexpr uint32_t NB = WIDE ? 4u : 2u;
+    static constexpr uint32_t CH = 4u;
+};
+
+/* Dynamic shared memory of a replay launch: FSM table, warp pools, the shared
+ * shadow instance, then (16-byte aligned) the staging buffers and mbarriers. */
+__host__ __device__ __forceinline__ uint32_t hr_stage_offset(bool pool, uint32_t warps, uint32_t smem_words)
+{
+    const uint32_t o = HR_FSM_SMEM_BYTES + (pool ? warps * (uint32_t)sizeof(hr_pool_smem) : 0u) + smem_words * 8u;
+    return (o + 15u) & ~15u;
+}
+
+__host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint32_t nb, uint32_t ch, uint32_t row_bytes)
+{
+    return warps * nb * (ch * row_bytes + 8u);
+}
+
 /* POOL = false: row-by-row (dense traces; 32 registers, 64 warps/SM).
  * POOL = true, WIDE = false: pooled at 32 registers (sparse, evenly spread
  *   traces, e.g. address shards: occupancy hides the DRAM latency).
  * POOL = true, WIDE = true: pooled at up to 64 registers, no spills (a few
- *   very long warps, e.g. power-law BFS hubs: per-warp latency decides). */
+ *   very long warps, e.g. power-law BFS hubs: per-warp latency decides).
+ * Rows reach the warp through its TMA staging ring (hr_records.cuh). */
 template <bool POOL, bool WIDE, typename SRC>
 __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel(hr_dev d, SRC src,
                                                                        const uint64_t *__restrict__ woff,
@@ -162,52 +184,78 @@ __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
 #ifdef HR_FUZZ
     const uint32_t cta = gridDim.x - 1u - blockIdx.x;               /* reversed block mapping */
-    t.tid = ((d.block_base + cta) << 10) | (t.tid & 1023u);
-    t.meta = (unsigned long long)t.tid << HR_TID_SHIFT;
+    t.meta = (unsigned long long)(((d.block_base + cta) << 10) | (t.tid() & 1023u)) << HR_TID_SHIFT;
 #else
     const uint32_t cta = blockIdx.x;
 #endif
 
+    constexpr uint32_t NB = hr_stage_cfg<POOL && WIDE>::NB, CH = hr_stage_cfg<POOL && WIDE>::CH;
+    constexpr uint32_t CHB = CH * SRC::ROW_BYTES;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t gw = (uint64_t)cta * warps + warp;
-    const uint64_t r0 = woff[gw], r1 = woff[gw + 1];
+    const uint64_t r0 = woff[gw];
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const bool active = lane < lanes;
-    const uint64_t n = r1 - r0;
+    /* rows per warp < 2^32 (180 GB of HBM holds < 2^30 rows) */
+    const uint32_t n = (uint32_t)(woff[gw + 1] - r0);
+    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(hr_smem) + hr_stage_offset(POOL, warps, smem_words);
+    const uint32_t buf0 = stage + warp * NB * CHB;
+    const uint32_t bar0 = stage + warps * NB * CHB + warp * NB * 8u;
+    if (lane == 0) {
+#pragma unroll
+        for (uint32_t b = 0; b < NB; b++) hr__mbar_init(bar0 + 8u * b, 1u);
+        hr__mbar_init_fence();
+#pragma unroll
+        for (uint32_t b = 0; b < NB; b++)
+            if (b * CH < n) {
+                const uint32_t rows = min(CH, n - b * CH);
+                hr__mbar_expect_tx(bar0 + 8u * b, rows * SRC::ROW_BYTES);
+                src.bulk(buf0 + b * CHB, r0 + b * CH, rows, CH, bar0 + 8u * b);
+            }
+    }
+    __syncwarp();
 
     uint32_t cnt = 0;                                                /* warp-uniform pool fill */
-    typename SRC::raw_t x1 = (active && n > 0) ? src.load(r0, lane) : SRC::nop();
-    typename SRC::raw_t x2 = (active && n > 1) ? src.load(r0 + 1, lane) : SRC::nop();
-    for (uint64_t i = 0; i < n; i++) {
-        const uint64_t x = SRC::decode(x1);
-        x1 = x2;
-        x2 = (active && i + 2 < n) ? src.load(r0 + i + 2, lane) : SRC::nop();
-        const uint32_t op = (uint32_t)(x >> 62);
-        const uint64_t w = x & HR_WORD_MASK;
-        if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {          /* barrier row: flush, then sync */
-            if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); cnt = 0; __syncwarp(); }
-            hr__barrier_row(d, t, x, lane_mask);
-            continue;
+    for (uint32_t c = 0; c * CH < n; c++) {
+        const uint32_t b = c % NB;
+        const uint32_t buf = buf0 + b * CHB;
+        hr__mbar_wait(bar0 + 8u * b, (c / NB) & 1u);
+        const uint32_t rows = min(CH, n - c * CH);
+        for (uint32_t j = 0; j < rows; j++) {
+            const uint64_t x = active ? SRC::sld(buf, j, lane, CH) : HR_NOP_REC;
+            const uint32_t op = (uint32_t)(x >> 62);
+            const uint64_t w = x & HR_WORD_MASK;
+            if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {      /* barrier row: flush, then sync */
+                if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); cnt = 0; __syncwarp(); }
+                hr__barrier_row(d, t, x, lane_mask);
+                continue;
+            }
+            if (!POOL) {
+                hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
+                continue;
+            }
+            hr_pool_smem &ps = pools[warp];
+            uint64_t local;
+            const bool v = op != 3u && !t.off && hr__locate(d, t, (uint32_t)(x >> 61) & 1u, w, local);
+            const unsigned vm = __ballot_sync(0xffffffffu, v);
+            const uint32_t k = __popc(vm);
+            if (k == 0) continue;
+            if (cnt + k > 32u) { __syncwarp(); hr__check_pool(d, t, ps, cnt); cnt = 0; __syncwarp(); }
+            if (v) {
+                const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
+                ps.rec[slot] = x;
+                ps.src[slot] = (uint8_t)lane;
+            }
+            cnt += k;
+            if (cnt == 32u) { __syncwarp(); hr__check_pool(d, t, ps, 32u); cnt = 0; __syncwarp(); }
         }
-        if (!POOL) {
-            hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
-            continue;
+        __syncwarp();                                                /* buffer b fully read: refill it */
+        if (lane == 0 && (c + NB) * CH < n) {
+            const uint32_t rows2 = min(CH, n - (c + NB) * CH);
+            hr__mbar_expect_tx(bar0 + 8u * b, rows2 * SRC::ROW_BYTES);
+            src.bulk(buf, r0 + (c + NB) * CH, rows2, CH, bar0 + 8u * b);
         }
-        hr_pool_smem &ps = pools[warp];
-        uint64_t local;
-        const bool v = op != 3u && !t.off && hr__locate(d, t, (uint32_t)(x >> 61) & 1u, w, local);
-        const unsigned vm = __ballot_sync(0xffffffffu, v);
-        const uint32_t k = __popc(vm);
-        if (k == 0) continue;
-        if (cnt + k > 32u) { __syncwarp(); hr__check_pool(d, t, ps, cnt); cnt = 0; __syncwarp(); }
-        if (v) {
-            const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
-            ps.rec[slot] = x;
-            ps.src[slot] = (uint8_t)lane;
-        }
-        cnt += k;
-        if (cnt == 32u) { __syncwarp(); hr__check_pool(d, t, ps, 32u); cnt = 0; __syncwarp(); }
     }
     if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); __syncwarp(); }
 }
