@@ -73,15 +73,17 @@ enum {
     HR_OPT_NO_FASTEXIT = 2u,   /* disable label-insensitive fast exits (a7), for ablations */
     HR_OPT_TIMING = 4u,        /* record CUDA events around every shadow reset and replay launch */
     HR_OPT_NO_SPECULATE = 8u,  /* first attempt loads the shadow word instead of speculating INIT */
-    HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen from sampled record density
-                                  and warp-length tail, see hr_host.cu kernel_choice) */
+    HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen from sampled record density,
+                                  shared share and warp-length tail, see hr_host.cu kernel_choice) */
     HR_OPT_POOL = 32u,         /* replay with warp pools of valid accesses (sparse traces) */
     HR_OPT_DOUBLE_SHADOW = 64u, /* two global shadows: the kernel-boundary reset (a11) of one runs on a
                                    side stream while the next kernel uses the other (2x shadow memory) */
     HR_OPT_FINITE_HISTORY = 128u, /* BASELINE, not HiRace: iGUARD-style 16-byte records (one reader, one
                                    writer) checked with the same replay, for the
                                    paper's comparisons (Listing 4 eviction, memory); shadow scan off */
-    HR_OPT_POOL_WIDE = 256u      /* force the 64-register pooled kernel (few very long warps) */
+    HR_OPT_POOL_WIDE = 256u,     /* force the 64-register pooled kernel (few very long warps) */
+    HR_OPT_ROW_WIDE = 512u       /* force the 64-register row kernel (chosen by default for
+                                    shared-shadow heavy traces and small grids) */
 };
 
 /* One unique racy address.  24 bytes.

@@ -77,7 +77,8 @@ struct hr_thr {
     uint32_t sshadow;             /* shared-space address of this block's shadow instance */
     uint32_t swords;
     uint32_t fsm;                 /* shared-space address of the FSM table copy */
-    uint32_t off;                 /* detection disabled (clock overflow) */
+    uint32_t off;                 /* bit 0: detection disabled (clock overflow); bit 1: this block's
+                                     shared instance belongs to another shard (set once) */
     __device__ __forceinline__ uint32_t tid() const { return (uint32_t)(meta >> HR_TID_SHIFT) & 0x7ffffffu; }
 };
 
@@ -175,6 +176,15 @@ __device__ __forceinline__ void hr__set_flag(const hr_dev &d, unsigned int f)
 
 /* ---------------- the check core ---------------- */
 
+/* Ablation options (HR_OPT_NO_COALESCE / NO_FASTEXIT / NO_SPECULATE) are read
+ * only when ABL: the default replay kernels are instantiated with ABL = false
+ * and carry no option tests on the per-access path. */
+template <bool ABL>
+__device__ __forceinline__ bool hr__opt(const hr_dev &d, uint32_t bit)
+{
+    return ABL && (d.options & bit);
+}
+
 /* L1-cacheable probe (weak load): only used to take the insensitive-closure exit,
  * which is valid for any value observed during this kernel (a7). */
 __device__ __forceinline__ unsigned long long hr__ld_g_l1(const unsigned long long *p)
@@ -199,7 +209,7 @@ __device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uin
     if (space != 0u) {
         if (word >= t.swords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
         local = word;
-        return ((t.tid() >> 10) & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
+        return !(t.off & 2u);
     }
     const uint64_t g = word - d.gbase;
     if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
@@ -262,11 +272,12 @@ __device__ __forceinline__ unsigned long long hr__nmeta(const hr_thr &t, unsigne
 
 /* Fold-free variant for the common case of a lane alone on its word: one
  * label, the lane's own meta, no group bookkeeping. */
+template <bool ABL>
 __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_thr &t, bool is_shared,
                                                       uint32_t sh_addr, unsigned long long *gp,
                                                       unsigned long long old, uint32_t fresh, uint32_t kind)
 {
-    const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
+    const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
     const uint32_t kcol = kind << 4;
     while (true) {
         const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
@@ -297,12 +308,13 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
 /* a7 + a8: Algorithm 1's repeat/until loop from a first value `old` of the
  * given provenance; returns the emit info of the committed transition (0 if
  * none or a fast exit). */
+template <bool ABL>
 __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t, bool is_shared, uint32_t sh_addr,
                                                unsigned long long *gp, unsigned long long old, uint32_t fresh,
                                                uint32_t kind, uint32_t lane, unsigned peers, unsigned kb0,
                                                unsigned kb1)
 {
-    const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
+    const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
     const unsigned long long nmeta = hr__nmeta(t, peers);
     while (true) {
         const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
@@ -332,12 +344,13 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
 /* First value of Algorithm 1's loop (a4): SMEM load; L1 probe for global
  * atomics; INIT guess for global reads/writes (the CAS then doubles as the
  * atomic read); a coherent load with HR_OPT_NO_SPECULATE. */
+template <bool ABL>
 __device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, bool is_shared, uint32_t sh_addr,
                                                         const unsigned long long *gp, uint32_t kind, uint32_t &fresh)
 {
     if (is_shared) { fresh = HR_OLD_FRESH; return hr__ld_s(sh_addr); }
-    if (kind == HR_ATOMIC && !(d.options & HR_OPT_NO_FASTEXIT)) { fresh = HR_OLD_PROBE; return hr__ld_g_l1(gp); }
-    if (d.options & HR_OPT_NO_SPECULATE) { fresh = HR_OLD_FRESH; return hr__ld_g(gp); }
+    if (kind == HR_ATOMIC && !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT)) { fresh = HR_OLD_PROBE; return hr__ld_g_l1(gp); }
+    if (hr__opt<ABL>(d, HR_OPT_NO_SPECULATE)) { fresh = HR_OLD_FRESH; return hr__ld_g(gp); }
     fresh = HR_OLD_GUESS;
     return 0ull;
 }
@@ -364,13 +377,13 @@ __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t,
 /* a3 grouping of one row: peers (lanes with the same key, lowest = leader) and
  * the kind bits for the fold.  Pre-test: strictly increasing keys over the full
  * warp means all distinct, and MATCH is skipped. */
-template <bool ONLINE>
+template <bool ONLINE, bool ABL>
 __device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, unsigned mask, uint32_t lane,
                                               uint64_t key, uint32_t kind, unsigned &kb0, unsigned &kb1)
 {
     unsigned peers = 1u << lane;
     kb0 = kb1 = 0;
-    if (d.options & HR_OPT_NO_COALESCE) return peers;
+    if (hr__opt<ABL>(d, HR_OPT_NO_COALESCE)) return peers;
     if (mask == 0xffffffffu) {
         const unsigned long long prev = __shfl_up_sync(mask, key, 1);
         if (__all_sync(mask, lane == 0 || key > prev)) return peers;
@@ -394,27 +407,27 @@ __device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, 
  * access is committed (the final ballot is the warp's convergence point), so a
  * lane never runs ahead of an access folded into another lane (program order).
  */
-template <bool ONLINE>
+template <bool ONLINE, bool ABL = true>
 __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t, unsigned mask, bool valid,
                                                uint32_t space, uint64_t word, uint32_t kind)
 {
     const uint32_t lane = hr__laneid();
     const bool is_shared = space != 0u;
     uint64_t local = 0;
-    valid = valid && !t.off && hr__locate(d, t, space, word, local);
+    valid = valid && !(t.off & 1u) && hr__locate(d, t, space, word, local);
     /* match key: 0 = no access on this lane (filtered lanes must not alias owned words) */
     const uint64_t key = valid ? ((local << 2) | (is_shared ? 2u : 0u) | 1u) : 0ull;
     unsigned kb0, kb1;
-    const unsigned peers = hr__group<ONLINE>(d, t, mask, lane, key, kind, kb0, kb1);
+    const unsigned peers = hr__group<ONLINE, ABL>(d, t, mask, lane, key, kind, kb0, kb1);
 
     uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
         const uint32_t sh_addr = t.sshadow + (uint32_t)(local << 3);
         unsigned long long *gp = d.gshadow + local;
         uint32_t fresh;
-        const unsigned long long old = hr__first(d, is_shared, sh_addr, gp, kind, fresh);
-        ei = (peers == (1u << lane)) ? hr__commit_single(d, t, is_shared, sh_addr, gp, old, fresh, kind)
-                                     : hr__commit(d, t, is_shared, sh_addr, gp, old, fresh, kind, lane, peers, kb0, kb1);
+        const unsigned long long old = hr__first<ABL>(d, is_shared, sh_addr, gp, kind, fresh);
+        ei = (peers == (1u << lane)) ? hr__commit_single<ABL>(d, t, is_shared, sh_addr, gp, old, fresh, kind)
+                                     : hr__commit<ABL>(d, t, is_shared, sh_addr, gp, old, fresh, kind, lane, peers, kb0, kb1);
     }
 
     /* a9: warp-aggregated ring append; also the warp's convergence point */
@@ -450,7 +463,7 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     t.sshadow = (uint32_t)__cvta_generic_to_shared(smem_shadow);
     t.swords = smem_words;
     t.fsm = (uint32_t)__cvta_generic_to_shared(smem_fsm);
-    t.off = 0;
+    t.off = ((block & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
     return t;
 }
 
@@ -475,7 +488,7 @@ __device__ __forceinline__ void hr_check_atomic(const hr_dev &d, hr_thr &t, hr_s
 __device__ __forceinline__ void hr_syncthreads(const hr_dev &d, hr_thr &t)
 {
     __syncthreads();
-    if (((uint32_t)t.meta >> d.wc_bits) >= d.bc_max) { t.off = 1; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+    if (((uint32_t)t.meta >> d.wc_bits) >= d.bc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
     else t.meta += 1ull << d.wc_bits;
 }
 
@@ -483,7 +496,7 @@ __device__ __forceinline__ void hr_syncthreads(const hr_dev &d, hr_thr &t)
 __device__ __forceinline__ void hr_syncwarp(const hr_dev &d, hr_thr &t)
 {
     __syncwarp();
-    if (((uint32_t)t.meta & d.wc_max) >= d.wc_max) { t.off = 1; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+    if (((uint32_t)t.meta & d.wc_max) >= d.wc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
     else t.meta += 1ull;
 }
 

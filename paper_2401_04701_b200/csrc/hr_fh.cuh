@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(1024, 1) hr_fh_replay_kernel(hr_dev d, SRC src
         const uint32_t space = (uint32_t)(x >> 61) & 1u;
         uint64_t local = 0;
         uint32_t scope = 0;
-        if (op != 3u && !t.off && hr__locate(d, t, space, w, local))
+        if (op != 3u && !(t.off & 1u) && hr__locate(d, t, space, w, local))
             scope = space ? hr_fh__access(d, t, sshadow + local, op) : hr_fh__access(d, t, gsh + local, op);
         const unsigned em = __ballot_sync(0xffffffffu, scope != 0u);
         if (em) {

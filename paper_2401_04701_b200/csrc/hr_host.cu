@@ -141,7 +141,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         if (cudaMalloc(&c->fsm, HR_FSM_SMEM_BYTES) != cudaSuccess ||
             cudaMalloc(&c->ring, sizeof(hr_race) * (size_t)k.ring_capacity) != cudaSuccess ||
             cudaMalloc(&c->tail, 4 * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMalloc(&c->counters, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMalloc(&c->counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_NOMEM, "device allocation failed in hr_init");
             break;
         }
@@ -150,7 +150,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         memcpy(host + HR_FSM_BYTES, hr_fsm_flags_init, 32);
         if (cudaMemcpy(c->fsm, host, HR_FSM_SMEM_BYTES, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemset(c->tail, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMemset(c->counters, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMemset(c->counters, 0, 16 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_CUDA, "hr_init upload failed");
             break;
         }
@@ -270,37 +270,61 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
     return HR_OK;
 }
 
-/* Kernel choice from warp-length tail and record density (measured on C4,
- * C5 shards, C5, C3 — profiles/r01_kernel_choice.md):
+/* Kernel choice from warp-length tail, record density of the access rows and
+ * the shared-space share (measured on C1, C3, C4, C5 and C5 shards —
+ * profiles/r01_kernel_choice.md):
  *   max warp > 16x the mean warp (a few very long warps) -> pooled, 64 registers
- *   < 90% access records (sparse, even)                   -> pooled, 32 registers
- *   otherwise (dense)                                     -> row kernel, 32 registers
- * HR_OPT_NO_POOL forces the row kernel, HR_OPT_POOL a pooled one (tail rule
- * kept), HR_OPT_POOL_WIDE the 64-register pooled kernel. */
-enum { HR_K_ROW = 0, HR_K_POOL = 1, HR_K_POOL_WIDE = 2 };
+ *   < 90% access records in access rows (sparse), unless a small grid
+ *     (< 2048 warps: latency bound) at >= 50%          -> pooled, 32 registers
+ *   otherwise a row kernel: 64 registers if >= 50% of the accesses are shared
+ *   (SMEM shadow: issue bound) or the grid is small, else 32 registers
+ *   (global shadow: occupancy hides the random DRAM latency).
+ * HR_OPT_NO_POOL forces a row kernel, HR_OPT_POOL a pooled one (tail rule
+ * kept), HR_OPT_POOL_WIDE the 64-register pooled kernel, HR_OPT_ROW_WIDE the
+ * 64-register row kernel. */
+enum { HR_K_ROW = 0, HR_K_POOL = 1, HR_K_POOL_WIDE = 2, HR_K_ROW_WIDE = 3 };
 
-static int kernel_choice(hr_ctx *c, double acc, double tot, double maxw, double sumw, double nwarps)
+static int kernel_choice_rule(hr_ctx *c, double acc, double tot, double maxw, double sumw, double nwarps,
+                              double shared);
+
+static int kernel_choice(hr_ctx *c, double acc, double tot, double maxw, double sumw, double nwarps, double shared)
 {
+    const int k = kernel_choice_rule(c, acc, tot, maxw, sumw, nwarps, shared);
+    if (getenv("HR_DEBUG_CHOICE"))
+        fprintf(stderr, "hr kernel choice %d: acc %.0f tot %.0f shared %.0f maxw %.0f meanw %.1f nwarps %.0f\n", k, acc,
+                tot, shared, maxw, nwarps > 0 ? sumw / nwarps : 0.0, nwarps);
+    return k;
+}
+
+static int kernel_choice_rule(hr_ctx *c, double acc, double tot, double maxw, double sumw, double nwarps,
+                              double shared)
+{
+    const uint32_t o = c->cfg.options;
+    if (o & HR_OPT_ROW_WIDE) return HR_K_ROW_WIDE;
+    const bool small = nwarps < 2048;
+    const int row = (acc > 0 && shared >= 0.5 * acc) || small ? HR_K_ROW_WIDE : HR_K_ROW;
+    if (o & HR_OPT_NO_POOL) return row;
+    if (o & HR_OPT_POOL_WIDE) return HR_K_POOL_WIDE;
     const bool tail = nwarps > 0 && maxw > 16.0 * (sumw / nwarps);
-    if (c->cfg.options & HR_OPT_NO_POOL) return HR_K_ROW;
-    if (c->cfg.options & HR_OPT_POOL_WIDE) return HR_K_POOL_WIDE;
     if (tail) return HR_K_POOL_WIDE;
-    const bool sparse = (c->cfg.options & HR_OPT_POOL) || (tot > 0 && acc < 0.9 * tot);
-    return sparse ? HR_K_POOL : HR_K_ROW;
+    if (o & HR_OPT_POOL) return HR_K_POOL;
+    const double dens = tot > 0 ? acc / tot : 1.0;
+    if (dens < 0.9 && !(small && dens >= 0.5)) return HR_K_POOL;
+    return row;
 }
 
 template <typename SRC>
 static hr_status choose_kernel(hr_ctx *c, SRC src, const hr_trace *t, const uint64_t *woff, cudaStream_t s, int *kind)
 {
     *kind = HR_K_ROW;
-    if (t->n_rows == 0 || (c->cfg.options & HR_OPT_NO_POOL)) return HR_OK;
-    hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, t->n_rows, 2048, woff, t->n_warp_off, c->counters + 4);
+    if (t->n_rows == 0) return HR_OK;
+    hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, t->n_rows, 2048, woff, t->n_warp_off, c->counters + 8);
     CU(cudaGetLastError());
-    unsigned long long h[4] = {0, 0, 0, 0};
-    CU(cudaMemcpyAsync(h, c->counters + 4, sizeof h, cudaMemcpyDeviceToHost, s));
+    unsigned long long h[5] = {0, 0, 0, 0, 0};
+    CU(cudaMemcpyAsync(h, c->counters + 8, sizeof h, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     *kind = kernel_choice(c, (double)h[0], (double)h[1], (double)h[2], (double)h[3],
-                          (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0));
+                          (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0), (double)h[4]);
     return HR_OK;
 }
 
@@ -346,9 +370,9 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         c->have_kernel = true;
         return HR_OK;
     }
-    const bool pool = kind != HR_K_ROW;
+    const bool pool = kind == HR_K_POOL || kind == HR_K_POOL_WIDE;
     if (!src.aligned_ok()) return fail(c, HR_E_ARG, "trace records must be 16-byte aligned (TMA staging)");
-    const bool wide = kind == HR_K_POOL_WIDE;
+    const bool wide = kind == HR_K_POOL_WIDE || kind == HR_K_ROW_WIDE;
     const uint32_t nb = wide ? hr_stage_cfg<true>::NB : hr_stage_cfg<false>::NB;
     const uint32_t ch = wide ? hr_stage_cfg<true>::CH : hr_stage_cfg<false>::CH;
     size_t smem = (size_t)hr_stage_offset(pool, (uint32_t)warps, (uint32_t)smem_words) +
@@ -356,15 +380,21 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     if (smem > 227 * 1024)
         return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (shadow %llu words + staging)", k, smem,
                     (unsigned long long)smem_words);
-    void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t) =
-        kind == HR_K_POOL_WIDE ? hr_replay_kernel<true, true, SRC>
-                               : (pool ? hr_replay_kernel<true, false, SRC> : hr_replay_kernel<false, false, SRC>);
+    const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_NO_SPECULATE);
+    void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t);
+    if (abl)
+        kern = pool ? (wide ? hr_replay_kernel<true, true, true, SRC> : hr_replay_kernel<true, false, true, SRC>)
+                    : (wide ? hr_replay_kernel<false, true, true, SRC> : hr_replay_kernel<false, false, true, SRC>);
+    else
+        kern = pool ? (wide ? hr_replay_kernel<true, true, false, SRC> : hr_replay_kernel<true, false, false, SRC>)
+                    : (wide ? hr_replay_kernel<false, true, false, SRC> : hr_replay_kernel<false, false, false, SRC>);
+    const uint32_t stage_off = hr_stage_offset(pool, (uint32_t)warps, (uint32_t)smem_words);
     if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool timing = c->cfg.options & HR_OPT_TIMING;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
     kern<<<(unsigned)(b1 - b0), (unsigned)(warps * 32), smem, s>>>(d, src, woff + woi + b0 * warps, (uint32_t)warps,
-                                                                   (uint32_t)lanes, (uint32_t)smem_words);
+                                                                   (uint32_t)lanes, (uint32_t)smem_words, stage_off);
     CU(cudaGetLastError());
     if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
     c->last_kernel = kid;
@@ -437,14 +467,30 @@ static hr_status reserve(hr_ctx *c, int i, size_t bytes)
 /* Host-side version of the kernel-choice probe. */
 static int host_kernel_choice(hr_ctx *c, const hr_trace *t)
 {
-    if (!t->n_rows || (c->cfg.options & HR_OPT_NO_POOL)) return HR_K_ROW;
-    uint64_t acc = 0, tot = 0;
-    for (uint32_t s = 0; s < 2048; s++) {
-        uint64_t row = (uint64_t)((double)s * (double)t->n_rows / 2048.0);
+    uint64_t acc = 0, tot = 0, sh = 0;
+    for (uint32_t s = 0; s < 2048 && t->n_rows; s++) {
+        const double u = ((double)s + fmod((double)s * 0.6180339887498949, 1.0)) / 2048.0;   /* as hr_density_kernel */
+        uint64_t row = (uint64_t)(u * (double)t->n_rows);
         if (row >= t->n_rows) break;
+        uint32_t ops[32], spcs[32];
+        bool barrier = false;
         for (uint32_t l = 0; l < 32; l++) {
-            uint32_t op = t->format == HR_TRACE_C32 ? (t->recop[row * 32 + l] & 3u) : (uint32_t)(t->rec[row * 32 + l] >> 62);
-            acc += op != 3u;
+            uint64_t w;
+            if (t->format == HR_TRACE_C32) {
+                ops[l] = t->recop[row * 32 + l] & 3u;
+                spcs[l] = (t->recop[row * 32 + l] >> 2) & 1u;
+                w = t->rec32[row * 32 + l];
+            } else {
+                ops[l] = (uint32_t)(t->rec[row * 32 + l] >> 62);
+                spcs[l] = (uint32_t)(t->rec[row * 32 + l] >> 61) & 1u;
+                w = t->rec[row * 32 + l] & ((1ull << 61) - 1);
+            }
+            barrier |= ops[l] == 3u && w != 0u;
+        }
+        if (barrier) continue;                     /* as hr_density_kernel: access rows only */
+        for (uint32_t l = 0; l < 32; l++) {
+            acc += ops[l] != 3u;
+            sh += ops[l] != 3u && spcs[l];
             tot++;
         }
     }
@@ -454,7 +500,8 @@ static int host_kernel_choice(hr_ctx *c, const hr_trace *t)
         mx = len > mx ? len : mx;
         sm += len;
     }
-    return kernel_choice(c, (double)acc, (double)tot, mx, sm, (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0));
+    return kernel_choice(c, (double)acc, (double)tot, mx, sm, (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0),
+                         (double)sh);
 }
 
 /* Host traces: records are copied in block-range chunks on a copy stream and
@@ -559,15 +606,15 @@ static hr_status replay_packed(hr_ctx *c, const hr_trace *t, bool host)
         hr_src_u64 src{dec - rbase * 32};
         if (kind < 0) {
             /* kernel choice: density of the first decoded chunk, tail of all warps */
-            if (rows && !(c->cfg.options & HR_OPT_NO_POOL)) {
+            if (rows) {
                 hr_density_kernel<hr_src_u64><<<1, 1024, 0, c->stream>>>(hr_src_u64{dec}, rows, 2048, dwoff, nwo,
-                                                                        c->counters + 4);
+                                                                        c->counters + 8);
                 CU(cudaGetLastError());
-                unsigned long long h[4] = {0, 0, 0, 0};
-                CU(cudaMemcpyAsync(h, c->counters + 4, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+                unsigned long long h[5] = {0, 0, 0, 0, 0};
+                CU(cudaMemcpyAsync(h, c->counters + 8, sizeof h, cudaMemcpyDeviceToHost, c->stream));
                 CU(cudaStreamSynchronize(c->stream));
                 kind = kernel_choice(c, (double)h[0], (double)h[1], (double)h[2], (double)h[3],
-                                     (double)(nwo > 1 ? nwo - 1 : 0));
+                                     (double)(nwo > 1 ? nwo - 1 : 0), (double)h[4]);
             } else {
                 kind = HR_K_ROW;
             }

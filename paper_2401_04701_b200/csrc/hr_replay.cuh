@@ -71,6 +71,7 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
 }
 
 /* Check the pool: lanes < n hold one access each (ps.rec[lane], ps.src[lane]). */
+template <bool ABL>
 __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t, const hr_pool_smem &ps, uint32_t n)
 {
     const uint32_t lane = hr__laneid();
@@ -83,18 +84,18 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
     if (valid) hr__locate(d, t, space, word, local);             /* validated when pooled */
     const uint64_t key = valid ? ((local << 2) | (space << 1) | 1u) : 0ull;
     unsigned kb0, kb1;
-    const unsigned peers = hr__group<false>(d, t, 0xffffffffu, lane, key, kind, kb0, kb1);
+    const unsigned peers = hr__group<false, ABL>(d, t, 0xffffffffu, lane, key, kind, kb0, kb1);
     uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
         const bool sh = space != 0u;
         const uint32_t sa = t.sshadow + (uint32_t)(local << 3);
         unsigned long long *gp = d.gshadow + local;
-        const bool fastexit = !(d.options & HR_OPT_NO_FASTEXIT);
+        const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
         const uint32_t last = 31u - __clz(peers);
         const unsigned long long nmeta = (t.meta & ~(0x1full << HR_TID_SHIFT)) |
                                          ((unsigned long long)ps.src[last] << HR_TID_SHIFT);
         uint32_t fresh;
-        unsigned long long old = hr__first(d, sh, sa, gp, kind, fresh);
+        unsigned long long old = hr__first<ABL>(d, sh, sa, gp, kind, fresh);
         while (true) {
             const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
             uint32_t rinfo, rel;
@@ -146,9 +147,12 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
 
 /* Per-warp TMA staging ring of the replay kernels: NB chunk buffers of CH
  * rows.  The 32-register kernels run 64 warps/SM, so 2 x 4 rows (2 KiB of u64
- * rows per warp); the wide pooled kernel runs few long warps: 4 x 4 rows. */
+ * rows per warp); the 64-register kernels run at most 32: 4 x 4 rows. */
+#ifndef HR_STAGE_NB_WIDE
+#define HR_STAGE_NB_WIDE 4u
+#endif
 template <bool WIDE> struct hr_stage_cfg {
-    static constexpr uint32_t NB = WIDE ? 4u : 2u;
+    static constexpr uint32_t NB = WIDE ? HR_STAGE_NB_WIDE : 2u;
     static constexpr uint32_t CH = 4u;
 };
 
@@ -165,17 +169,26 @@ __host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint
     return warps * nb * (ch * row_bytes + 8u);
 }
 
-/* POOL = false: row-by-row (dense traces; 32 registers, 64 warps/SM).
+/* POOL = false, WIDE = false: row-by-row at 32 registers, 64 warps/SM (dense
+ *   global traces: occupancy hides the random-DRAM latency).
+ * POOL = false, WIDE = true: row-by-row at up to 64 registers (shared-shadow
+ *   heavy or small grids: issue and latency bound, spills cost more than warps).
  * POOL = true, WIDE = false: pooled at 32 registers (sparse, evenly spread
- *   traces, e.g. address shards: occupancy hides the DRAM latency).
+ *   traces, e.g. address shards).
  * POOL = true, WIDE = true: pooled at up to 64 registers, no spills (a few
  *   very long warps, e.g. power-law BFS hubs: per-warp latency decides).
  * Rows reach the warp through its TMA staging ring (hr_records.cuh). */
-template <bool POOL, bool WIDE, typename SRC>
-__global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel(hr_dev d, SRC src,
+#ifdef HR_ROW_REGS
+/* register-cap experiments: the 32-register kernels get __maxnreg__ instead */
+#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : HR_ROW_REGS)
+#else
+#define HR_REPLAY_BOUNDS(POOL, WIDE) __launch_bounds__(1024, (WIDE) ? 1 : 2)
+#endif
+template <bool POOL, bool WIDE, bool ABL, typename SRC>
+__global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                                                                        const uint64_t *__restrict__ woff,
                                                                        uint32_t warps, uint32_t lanes,
-                                                                       uint32_t smem_words)
+                                                                       uint32_t smem_words, uint32_t stage_off)
 {
     extern __shared__ __align__(16) unsigned char hr_smem[];
     hr_pool_smem *pools = reinterpret_cast<hr_pool_smem *>(hr_smem + HR_FSM_SMEM_BYTES);
@@ -185,11 +198,12 @@ __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel
 #ifdef HR_FUZZ
     const uint32_t cta = gridDim.x - 1u - blockIdx.x;               /* reversed block mapping */
     t.meta = (unsigned long long)(((d.block_base + cta) << 10) | (t.tid() & 1023u)) << HR_TID_SHIFT;
+    t.off = (((d.block_base + cta) & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
 #else
     const uint32_t cta = blockIdx.x;
 #endif
 
-    constexpr uint32_t NB = hr_stage_cfg<POOL && WIDE>::NB, CH = hr_stage_cfg<POOL && WIDE>::CH;
+    constexpr uint32_t NB = hr_stage_cfg<WIDE>::NB, CH = hr_stage_cfg<WIDE>::CH;
     constexpr uint32_t CHB = CH * SRC::ROW_BYTES;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel
     const bool active = lane < lanes;
     /* rows per warp < 2^32 (180 GB of HBM holds < 2^30 rows) */
     const uint32_t n = (uint32_t)(woff[gw + 1] - r0);
-    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(hr_smem) + hr_stage_offset(POOL, warps, smem_words);
+    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(hr_smem) + stage_off;   /* = hr_stage_offset() */
     const uint32_t buf0 = stage + warp * NB * CHB;
     const uint32_t bar0 = stage + warps * NB * CHB + warp * NB * 8u;
     if (lane == 0) {
@@ -227,28 +241,28 @@ __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel
             const uint32_t op = (uint32_t)(x >> 62);
             const uint64_t w = x & HR_WORD_MASK;
             if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {      /* barrier row: flush, then sync */
-                if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); cnt = 0; __syncwarp(); }
+                if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[warp], cnt); cnt = 0; __syncwarp(); }
                 hr__barrier_row(d, t, x, lane_mask);
                 continue;
             }
             if (!POOL) {
-                hr_check_lanes<false>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
+                hr_check_lanes<false, ABL>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
                 continue;
             }
             hr_pool_smem &ps = pools[warp];
             uint64_t local;
-            const bool v = op != 3u && !t.off && hr__locate(d, t, (uint32_t)(x >> 61) & 1u, w, local);
+            const bool v = op != 3u && !(t.off & 1u) && hr__locate(d, t, (uint32_t)(x >> 61) & 1u, w, local);
             const unsigned vm = __ballot_sync(0xffffffffu, v);
             const uint32_t k = __popc(vm);
             if (k == 0) continue;
-            if (cnt + k > 32u) { __syncwarp(); hr__check_pool(d, t, ps, cnt); cnt = 0; __syncwarp(); }
+            if (cnt + k > 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); cnt = 0; __syncwarp(); }
             if (v) {
                 const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
                 ps.rec[slot] = x;
                 ps.src[slot] = (uint8_t)lane;
             }
             cnt += k;
-            if (cnt == 32u) { __syncwarp(); hr__check_pool(d, t, ps, 32u); cnt = 0; __syncwarp(); }
+            if (cnt == 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, 32u); cnt = 0; __syncwarp(); }
         }
         __syncwarp();                                                /* buffer b fully read: refill it */
         if (lane == 0 && (c + NB) * CH < n) {
@@ -257,18 +271,19 @@ __global__ void __launch_bounds__(1024, (POOL && WIDE) ? 1 : 2) hr_replay_kernel
             src.bulk(buf, r0 + (c + NB) * CH, rows2, CH, bar0 + 8u * b);
         }
     }
-    if (POOL && cnt) { __syncwarp(); hr__check_pool(d, t, pools[warp], cnt); __syncwarp(); }
+    if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[warp], cnt); __syncwarp(); }
 }
 
 /* Probe for the kernel choice (one block): out[0..1] = access records / records
- * among up to `samples` rows spread over [0, n_rows); out[2..3] = max / sum of
- * the warp lengths (rows) over the warp-offset array. */
+ * of the non-barrier rows among up to `samples` rows spread over [0, n_rows); out[2..3] = max / sum of
+ * the warp lengths (rows) over the warp-offset array; out[4] = shared-space
+ * access records among the samples. */
 template <typename SRC>
 __global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, const uint64_t *woff, uint64_t n_woff,
                                   unsigned long long *out)
 {
-    __shared__ unsigned long long acc[4];
-    if (threadIdx.x < 4) acc[threadIdx.x] = 0;
+    __shared__ unsigned long long acc[5];
+    if (threadIdx.x < 5) acc[threadIdx.x] = 0;
     __syncthreads();
     unsigned long long mx = 0, sm = 0;
     for (uint64_t i = threadIdx.x; i + 1 < n_woff; i += blockDim.x) {
@@ -278,18 +293,26 @@ __global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, co
     }
     atomicMax(&acc[2], mx);
     atomicAdd(&acc[3], sm);
-    unsigned long long a = 0, tot = 0;
+    unsigned long long a = 0, tot = 0, sh = 0;
     for (uint32_t s = threadIdx.x >> 5; s < samples; s += blockDim.x >> 5) {
-        const uint64_t row = (uint64_t)((double)s * (double)n_rows / (double)samples);
+        /* one sample per stride, jittered by the golden-ratio sequence: a plain
+         * stride aliases with the warp layout (C3: every sample on row 0) */
+        const double u = ((double)s + fmod((double)s * 0.6180339887498949, 1.0)) / (double)samples;
+        const uint64_t row = (uint64_t)(u * (double)n_rows);
         if (row >= n_rows) break;
         const uint64_t x = src.row(row, threadIdx.x & 31u);
+        /* barrier rows are replayed by every kernel alike: density counts the
+         * NOP lanes of access rows only (what pooling can skip) */
+        if (__any_sync(0xffffffffu, (x >> 62) == 3u && (x & HR_WORD_MASK) != 0u)) continue;
         a += (x >> 62) != 3u;
+        sh += (x >> 62) != 3u && ((x >> 61) & 1u);
         tot++;
     }
     atomicAdd(&acc[0], a);
     atomicAdd(&acc[1], tot);
+    atomicAdd(&acc[4], sh);
     __syncthreads();
-    if (threadIdx.x < 4) out[threadIdx.x] = acc[threadIdx.x];
+    if (threadIdx.x < 5) out[threadIdx.x] = acc[threadIdx.x];
 }
 
 /* Overflow fallback / cross-check: every RACE word of the (local) global

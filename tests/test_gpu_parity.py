@@ -63,7 +63,7 @@ def _random_batch(seed, n, **kw):
 
 
 @pytest.mark.parametrize("seed", range(4))
-@pytest.mark.parametrize("options", [16, 32, 256])
+@pytest.mark.parametrize("options", [16, 32, 256, 512])
 def test_random_small_family(seed, options):
     tr = _random_batch(seed, 300, max_blocks=2, max_warps=2, max_lanes=2, max_slots=5, n_words=2,
                        spaces=(0, 1))
@@ -71,7 +71,7 @@ def test_random_small_family(seed, options):
 
 
 @pytest.mark.parametrize("seed", range(4))
-@pytest.mark.parametrize("options", [16, 32, 256])
+@pytest.mark.parametrize("options", [16, 32, 256, 512])
 def test_random_wide_grids(seed, options):
     """Full warps and many warps: exercises MATCH coalescing, multi-lane folds,
     CAS contention, several tiles of the shadow and ragged warp lengths, in
@@ -84,7 +84,7 @@ def test_random_wide_grids(seed, options):
     assert len(o) > 10
 
 
-@pytest.mark.parametrize("options", [16, 32, 256])
+@pytest.mark.parametrize("options", [16, 32, 256, 512])
 def test_hot_words_contention(options):
     """Few words, 32 warps x 32 lanes x 16 blocks: heavy CAS retry storms."""
     tr = _random_batch(7, 10, max_blocks=16, max_warps=32, max_lanes=32, max_slots=8, n_words=3,
@@ -95,7 +95,8 @@ def test_hot_words_contention(options):
     assert gpu_set(tr, options=options) == oracle_set(tr)
 
 
-@pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8, 64, 64 | 32, 256, 256 | 1, 256 | 8])
+@pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8, 64, 64 | 32, 256, 256 | 1, 256 | 8,
+                                     512, 512 | 1, 512 | 2, 512 | 8])
 def test_ablations_same_result(options):
     """Coalescing off / fast exits off / no speculation / forced row or pooled
     replay change the commit order and the traffic, never the result
