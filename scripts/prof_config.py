@@ -7,12 +7,14 @@ from tracegen import c4, stencil
 ap = argparse.ArgumentParser()
 ap.add_argument("config", choices=["c3", "c4"])
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--lv", type=int, default=20, help="C4 graph: 2^lv vertices")
+ap.add_argument("--atomic", action="store_true", help="C4 race-free (atomic) variant")
 a = ap.parse_args()
 if a.config == "c3":
     tr, words, smem = stencil.stencil_trace(removed=20), 2 * 512 * 512, 648
 else:
-    g = c4.Graph(20)
-    tr, words, smem = g.trace(True), c4.total_words(20), 0
+    g = c4.Graph(a.lv)
+    tr, words, smem = g.trace(not a.atomic), c4.total_words(a.lv), 0
 dt = hr.DeviceTrace.from_trace(tr)
 ck = hr.Checker(words, smem, ring_capacity=1 << 22, options=hr.HR_OPT_TIMING)
 for _ in range(a.reps):
