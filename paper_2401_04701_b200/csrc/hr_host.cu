@@ -375,26 +375,37 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     const bool wide = kind == HR_K_POOL_WIDE || kind == HR_K_ROW_WIDE;
     const uint32_t nb = wide ? hr_stage_cfg<true>::NB : hr_stage_cfg<false>::NB;
     const uint32_t ch = wide ? hr_stage_cfg<true>::CH : hr_stage_cfg<false>::CH;
-    size_t smem = (size_t)hr_stage_offset(pool, (uint32_t)warps, (uint32_t)smem_words) +
-                  hr_stage_bytes((uint32_t)warps, nb, ch, SRC::ROW_BYTES);
+    /* long-tailed grids (wide pooled kernel): split each simulated warp over up
+     * to 4 CUDA warps of the block (hr_replay_kernel); HR_SPLIT_LOG2 overrides */
+    uint32_t split = 0;
+    if (kind == HR_K_POOL_WIDE)
+        while (split < 2 && (warps << (split + 1)) <= 32) split++;
+    if (pool)
+        if (const char *e = getenv("HR_SPLIT_LOG2")) {
+            split = (uint32_t)atoi(e);
+            while (split && (warps << split) > 32) split--;
+        }
+    if (!pool) split = 0;
+    const uint32_t nhw = (uint32_t)warps << split;
+    size_t smem = (size_t)hr_stage_offset(pool, nhw, (uint32_t)smem_words) + hr_stage_bytes(nhw, nb, ch, SRC::ROW_BYTES);
     if (smem > 227 * 1024)
         return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (shadow %llu words + staging)", k, smem,
                     (unsigned long long)smem_words);
     const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_NO_SPECULATE);
-    void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t);
+    void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t);
     if (abl)
         kern = pool ? (wide ? hr_replay_kernel<true, true, true, SRC> : hr_replay_kernel<true, false, true, SRC>)
                     : (wide ? hr_replay_kernel<false, true, true, SRC> : hr_replay_kernel<false, false, true, SRC>);
     else
         kern = pool ? (wide ? hr_replay_kernel<true, true, false, SRC> : hr_replay_kernel<true, false, false, SRC>)
                     : (wide ? hr_replay_kernel<false, true, false, SRC> : hr_replay_kernel<false, false, false, SRC>);
-    const uint32_t stage_off = hr_stage_offset(pool, (uint32_t)warps, (uint32_t)smem_words);
+    const uint32_t stage_off = hr_stage_offset(pool, nhw, (uint32_t)smem_words);
     if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool timing = c->cfg.options & HR_OPT_TIMING;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
-    kern<<<(unsigned)(b1 - b0), (unsigned)(warps * 32), smem, s>>>(d, src, woff + woi + b0 * warps, (uint32_t)warps,
-                                                                   (uint32_t)lanes, (uint32_t)smem_words, stage_off);
+    kern<<<(unsigned)(b1 - b0), nhw * 32u, smem, s>>>(d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes,
+                                                       (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
     if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
     c->last_kernel = kid;

@@ -75,13 +75,14 @@ template <bool ABL>
 __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t, const hr_pool_smem &ps, uint32_t n)
 {
     const uint32_t lane = hr__laneid();
-    const bool valid = lane < n;
-    const uint64_t x = valid ? ps.rec[lane] : HR_NOP_REC;
+    const uint64_t x = lane < n ? ps.rec[lane] : HR_NOP_REC;
     const uint32_t space = (uint32_t)(x >> 61) & 1u;
     const uint32_t kind = (uint32_t)(x >> 62);
     const uint64_t word = x & HR_WORD_MASK;
     uint64_t local = 0;
-    if (valid) hr__locate(d, t, space, word, local);             /* validated when pooled */
+    /* pooled entries passed only the cheap owner test (hr__pool_owned): the
+     * region check (HR_F_UNMONITORED) and the shard-local index happen here */
+    const bool valid = lane < n && hr__locate(d, t, space, word, local);
     const uint64_t key = valid ? ((local << 2) | (space << 1) | 1u) : 0ull;
     unsigned kb0, kb1;
     const unsigned peers = hr__group<false, ABL>(d, t, 0xffffffffu, lane, key, kind, kb0, kb1);
@@ -145,15 +146,46 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
     }
 }
 
+/* Helper warp of a word when a simulated warp is split over 2^split_log2 CUDA
+ * warps (multiplicative hash of the trace word: adjacent and strided words
+ * spread evenly; any fixed function of the word keeps each word on one helper). */
+__device__ __forceinline__ uint32_t hr__helper_of(uint64_t word, uint32_t split_log2)
+{
+    return ((uint32_t)(word ^ (word >> 29)) * 0x9E3779B1u) >> (32u - split_log2);
+}
+
+/* Cheap pre-pool test of a record: an access of an enabled thread whose word
+ * belongs to this shard and (split) this helper.  Region bounds and the
+ * shard-local index are left to hr__check_pool's hr__locate, so a record in a
+ * pool may still turn out unmonitored (flagged there, not checked). */
+__device__ __forceinline__ bool hr__pool_owned(const hr_dev &d, const hr_thr &t, uint64_t x, uint32_t split_log2,
+                                               uint32_t helper)
+{
+    const uint32_t op = (uint32_t)(x >> 62);
+    const uint32_t sp = (uint32_t)(x >> 61) & 1u;
+    const uint64_t w = x & HR_WORD_MASK;
+    bool v = op != 3u && !(t.off & 1u);
+    if (sp) v = v && !(t.off & 2u);
+    else if (d.shard_log2) {
+        /* words outside the region go on to hr__locate on every shard, which flags them */
+        const uint64_t g = w - d.gbase;
+        const bool in = w >= d.gbase && g < d.gwords;
+        v = v && (!in || ((uint32_t)(g >> d.gran_log2) & ((1u << d.shard_log2) - 1u)) == d.shard_rank);
+    }
+    if (split_log2) v = v && hr__helper_of(w, split_log2) == helper;
+    return v;
+}
+
 /* Per-warp TMA staging ring of the replay kernels: NB chunk buffers of CH
  * rows.  The 32-register kernels run 64 warps/SM, so 2 x 4 rows (2 KiB of u64
- * rows per warp); the 64-register kernels run at most 32: 4 x 4 rows. */
+ * rows per warp); the 64-register kernels run at most 32: 2 x 8 rows (the
+ * depth measured indifferent on C4; longer chunks halve the per-chunk work). */
 #ifndef HR_STAGE_NB_WIDE
-#define HR_STAGE_NB_WIDE 4u
+#define HR_STAGE_NB_WIDE 2u
 #endif
 template <bool WIDE> struct hr_stage_cfg {
     static constexpr uint32_t NB = WIDE ? HR_STAGE_NB_WIDE : 2u;
-    static constexpr uint32_t CH = 4u;
+    static constexpr uint32_t CH = WIDE ? 8u : 4u;
 };
 
 /* Dynamic shared memory of a replay launch: FSM table, warp pools, the shared
@@ -188,12 +220,20 @@ template <bool POOL, bool WIDE, bool ABL, typename SRC>
 __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                                                                        const uint64_t *__restrict__ woff,
                                                                        uint32_t warps, uint32_t lanes,
-                                                                       uint32_t smem_words, uint32_t stage_off)
+                                                                       uint32_t smem_words, uint32_t stage_off,
+                                                                       uint32_t split_log2)
 {
+    /* split_log2 > 0 (pooled kernels only): each simulated warp is replayed by
+     * 2^split_log2 CUDA warps of the block ("helpers"); helper h checks only the
+     * accesses whose word hashes to h.  Every helper walks every row (barriers
+     * and clocks stay identical), each word is still committed by one warp in
+     * record order, so the per-word commit orders stay happens-before
+     * consistent.  Parallelises the long warps of power-law traces. */
+    const uint32_t nhw = warps << split_log2;                       /* CUDA warps in the block */
     extern __shared__ __align__(16) unsigned char hr_smem[];
     hr_pool_smem *pools = reinterpret_cast<hr_pool_smem *>(hr_smem + HR_FSM_SMEM_BYTES);
     unsigned long long *sshadow = reinterpret_cast<unsigned long long *>(
-        hr_smem + HR_FSM_SMEM_BYTES + (POOL ? warps * sizeof(hr_pool_smem) : 0));
+        hr_smem + HR_FSM_SMEM_BYTES + (POOL ? nhw * sizeof(hr_pool_smem) : 0));
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
 #ifdef HR_FUZZ
     const uint32_t cta = gridDim.x - 1u - blockIdx.x;               /* reversed block mapping */
@@ -206,7 +246,11 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     constexpr uint32_t NB = hr_stage_cfg<WIDE>::NB, CH = hr_stage_cfg<WIDE>::CH;
     constexpr uint32_t CHB = CH * SRC::ROW_BYTES;
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t hw = threadIdx.x >> 5;                            /* CUDA warp */
+    const uint32_t warp = POOL && split_log2 ? hw % warps : hw;      /* simulated warp */
+    const uint32_t helper = POOL && split_log2 ? hw / warps : 0u;
+    if (POOL && split_log2)
+        t.meta = (unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT;
     const uint64_t gw = (uint64_t)cta * warps + warp;
     const uint64_t r0 = woff[gw];
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
@@ -214,8 +258,8 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     /* rows per warp < 2^32 (180 GB of HBM holds < 2^30 rows) */
     const uint32_t n = (uint32_t)(woff[gw + 1] - r0);
     const uint32_t stage = (uint32_t)__cvta_generic_to_shared(hr_smem) + stage_off;   /* = hr_stage_offset() */
-    const uint32_t buf0 = stage + warp * NB * CHB;
-    const uint32_t bar0 = stage + warps * NB * CHB + warp * NB * 8u;
+    const uint32_t buf0 = stage + hw * NB * CHB;
+    const uint32_t bar0 = stage + nhw * NB * CHB + hw * NB * 8u;
     if (lane == 0) {
 #pragma unroll
         for (uint32_t b = 0; b < NB; b++) hr__mbar_init(bar0 + 8u * b, 1u);
@@ -236,12 +280,47 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
         const uint32_t buf = buf0 + b * CHB;
         hr__mbar_wait(bar0 + 8u * b, (c / NB) & 1u);
         const uint32_t rows = min(CH, n - c * CH);
-        for (uint32_t j = 0; j < rows; j++) {
+        uint32_t j0 = 0;
+        if (POOL && WIDE) {
+            /* whole chunk at once (ILP for the few long warps this kernel runs):
+             * CH independent loads, validity tests and ballots, then the pool
+             * insertion; a chunk holding a barrier row goes row by row below */
+            uint64_t xs[CH];
+            bool bar = false;
+#pragma unroll
+            for (uint32_t j = 0; j < CH; j++) {
+                xs[j] = (active && j < rows) ? SRC::sld(buf, j, lane, CH) : HR_NOP_REC;
+                bar |= (xs[j] >> 62) == 3u && (xs[j] & HR_WORD_MASK) != 0u;
+            }
+            if (!__any_sync(0xffffffffu, bar)) {
+                unsigned vms[CH];
+#pragma unroll
+                for (uint32_t j = 0; j < CH; j++)
+                    vms[j] = __ballot_sync(0xffffffffu, hr__pool_owned(d, t, xs[j], split_log2, helper));
+                hr_pool_smem &ps = pools[hw];
+#pragma unroll
+                for (uint32_t j = 0; j < CH; j++) {
+                    const unsigned vm = vms[j];
+                    const uint32_t k = __popc(vm);
+                    if (k == 0) continue;
+                    if (cnt + k > 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); cnt = 0; __syncwarp(); }
+                    if ((vm >> lane) & 1u) {
+                        const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
+                        ps.rec[slot] = xs[j];
+                        ps.src[slot] = (uint8_t)lane;
+                    }
+                    cnt += k;
+                    if (cnt == 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, 32u); cnt = 0; __syncwarp(); }
+                }
+                j0 = rows;
+            }
+        }
+        for (uint32_t j = j0; j < rows; j++) {
             const uint64_t x = active ? SRC::sld(buf, j, lane, CH) : HR_NOP_REC;
             const uint32_t op = (uint32_t)(x >> 62);
             const uint64_t w = x & HR_WORD_MASK;
             if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {      /* barrier row: flush, then sync */
-                if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[warp], cnt); cnt = 0; __syncwarp(); }
+                if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[hw], cnt); cnt = 0; __syncwarp(); }
                 hr__barrier_row(d, t, x, lane_mask);
                 continue;
             }
@@ -249,9 +328,8 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 hr_check_lanes<false, ABL>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
                 continue;
             }
-            hr_pool_smem &ps = pools[warp];
-            uint64_t local;
-            const bool v = op != 3u && !(t.off & 1u) && hr__locate(d, t, (uint32_t)(x >> 61) & 1u, w, local);
+            hr_pool_smem &ps = pools[hw];
+            const bool v = hr__pool_owned(d, t, x, split_log2, helper);
             const unsigned vm = __ballot_sync(0xffffffffu, v);
             const uint32_t k = __popc(vm);
             if (k == 0) continue;
@@ -271,7 +349,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
             src.bulk(buf, r0 + (c + NB) * CH, rows2, CH, bar0 + 8u * b);
         }
     }
-    if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[warp], cnt); __syncwarp(); }
+    if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[hw], cnt); __syncwarp(); }
 }
 
 /* Probe for the kernel choice (one block): out[0..1] = access records / records
