@@ -317,3 +317,40 @@ def test_finite_history_is_sound_but_incomplete_on_c2():
             else:
                 missed_traces += 1
     assert found_traces > 0 and missed_traces > 0
+
+
+@pytest.mark.parametrize("split", ["1", "2", "5"])
+def test_split_helpers_same_result(split, monkeypatch):
+    """Wide pooled replay with each simulated warp split over 2^split CUDA
+    warps (clamped to 32 warps per block): every word is still committed by
+    one helper in record order, so the racy set is unchanged.  Mixed shared and
+    global accesses, barriers, hot words, ragged warps."""
+    monkeypatch.setenv("HR_SPLIT_LOG2", split)
+    for seed, kw in ((121, dict(max_blocks=5, max_warps=4, max_lanes=32, max_slots=12, n_words=60,
+                                spaces=(0, 1), p_barrier=0.25, p_skip=0.4)),
+                     (122, dict(max_blocks=8, max_warps=8, max_lanes=32, max_slots=8, n_words=3,
+                                spaces=(0, 1), p_skip=0.2)),
+                     (123, dict(max_blocks=3, max_warps=32, max_lanes=32, max_slots=6, n_words=50,
+                                spaces=(0, 1), p_barrier=0.3))):
+        tr = _random_batch(seed, 12, **kw)
+        assert gpu_set(tr, options=256) == oracle_set(tr)
+
+
+def test_split_with_shards(monkeypatch):
+    """Address shards (granule 9 and 5) combined with helper splitting: the
+    union over shards equals the single-GPU set."""
+    monkeypatch.setenv("HR_SPLIT_LOG2", "2")
+    h = hr()
+    tr = _random_batch(131, 16, max_blocks=4, max_warps=8, max_lanes=32, max_slots=10, n_words=3000,
+                       spaces=(0, 1), p_barrier=0.2)
+    gmax, smem = h.trace_extent(tr)
+    full = oracle_set(tr)[0]
+    for n, g in ((4, 9), (8, 5)):
+        union = []
+        for r in range(n):
+            ck = h.Checker(gmax, smem, shard=(r, n), granule_log2=g, options=256)
+            ck.replay(h.DeviceTrace.from_trace(tr))
+            races, _, _ = ck.report()
+            ck.close()
+            union += [tuple(x) for x in races]
+        assert sorted(union) == full
