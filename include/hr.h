@@ -82,8 +82,10 @@ enum {
                                    writer) checked with the same replay, for the
                                    paper's comparisons (Listing 4 eviction, memory); shadow scan off */
     HR_OPT_POOL_WIDE = 256u,     /* force the 64-register pooled kernel (few very long warps) */
-    HR_OPT_ROW_WIDE = 512u       /* force the 64-register row kernel (chosen by default for
+    HR_OPT_ROW_WIDE = 512u,      /* force the 64-register row kernel (chosen by default for
                                     shared-shadow heavy traces and small grids) */
+    HR_OPT_NO_COMPACT = 1024u    /* long-tailed grids: replay the rows as they are instead of
+                                    packing each long warp's accesses first (hr_compact.cuh) */
 };
 
 /* One unique racy address.  24 bytes.

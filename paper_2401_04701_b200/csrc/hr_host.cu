@@ -24,6 +24,7 @@
 #include "hr_fh.cuh"
 #include "hr_classes.cuh"
 #include "hr_pack.cuh"
+#include "hr_compact.cuh"
 #include "fsm_table.inc"
 #include "fsm_classes.inc"
 
@@ -51,9 +52,11 @@ struct hr_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;                 /* host-trace staging copies */
     /* staging: 0 warp_off, 1 rec|rec32|packed, 2 recop|decoded chunk, 3 pack_off,
-     * 4 hr_pack_trace segment sizes + error word, 5 scan temporaries */
-    void *stage[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    size_t stage_cap[6] = {0, 0, 0, 0, 0, 0};
+     * 4 hr_pack_trace segment sizes + error word, 5 scan temporaries,
+     * compacted replay: 6 segment counts, 7 segment offsets, 8 row counts,
+     * 9 row offsets, 10 packed records, 11 packed tags */
+    void *stage[12] = {};
+    size_t stage_cap[12] = {};
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
@@ -343,6 +346,77 @@ static hr_status check_kernel(hr_ctx *c, const hr_trace *t, uint32_t k)
     return HR_OK;
 }
 
+static hr_status reserve(hr_ctx *c, int i, size_t bytes);
+
+/* Compacted replay of blocks [b0, b1) of kernel k (hr_compact.cuh): count and
+ * scan the packed rows of every (warp, helper) stream, write them, replay them.
+ * Two small synchronous reads size the buffers. */
+template <typename SRC>
+static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const uint64_t *woff,
+                                cudaStream_t s, uint64_t b0, uint64_t b1, uint32_t split, bool abl)
+{
+    const uint64_t *kd = t->kdesc + 8ull * k;
+    const uint64_t warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
+    const uint32_t kid = t->kernel_base + k;
+    hr_dev d = make_dev(c, kid);
+    d.block_base = (uint32_t)b0;
+    const uint64_t nw = (b1 - b0) * warps;
+    const uint64_t *wk = woff + woi + b0 * warps;
+    hr_status st;
+    if ((st = reserve(c, 6, (nw + 1) * 8)) || (st = reserve(c, 7, (nw + 1) * 8))) return st;
+    uint64_t *nseg = (uint64_t *)c->stage[6], *segoff = (uint64_t *)c->stage[7];
+    hr_cmp_nseg_kernel<<<(unsigned)((nw + 1 + 255) / 256), 256, 0, s>>>(wk, nw, nseg);
+    CU(cudaGetLastError());
+    size_t tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg, segoff, (int64_t)(nw + 1), s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, nseg, segoff, (int64_t)(nw + 1), s));
+    uint64_t nsegs = 0;
+    CU(cudaMemcpyAsync(&nsegs, segoff + nw, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const uint64_t ncnt = nsegs << split;
+    if ((st = reserve(c, 8, (ncnt + 1) * 8)) || (st = reserve(c, 9, (ncnt + 1) * 8))) return st;
+    uint64_t *cnt = (uint64_t *)c->stage[8], *rowoff = (uint64_t *)c->stage[9];
+    CU(cudaMemsetAsync(cnt + ncnt, 0, 8, s));
+    const unsigned wgrid = (unsigned)((nsegs * 32 + 255) / 256);
+    if (nsegs) {
+        hr_cmp_walk_kernel<false, SRC><<<wgrid, 256, 0, s>>>(d, src, wk, segoff, nw, (uint32_t)lanes, split, cnt,
+                                                             nullptr, nullptr);
+        CU(cudaGetLastError());
+    }
+    tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, rowoff, (int64_t)(ncnt + 1), s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, rowoff, (int64_t)(ncnt + 1), s));
+    uint64_t nrows = 0;
+    CU(cudaMemcpyAsync(&nrows, rowoff + ncnt, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if ((st = reserve(c, 10, (size_t)std::max<uint64_t>(nrows, 1) * 256)) ||
+        (st = reserve(c, 11, (size_t)std::max<uint64_t>(nrows, 1) * 32)))
+        return st;
+    uint64_t *orec = (uint64_t *)c->stage[10];
+    uint8_t *otag = (uint8_t *)c->stage[11];
+    if (nsegs) {
+        hr_cmp_walk_kernel<true, SRC><<<wgrid, 256, 0, s>>>(d, src, wk, segoff, nw, (uint32_t)lanes, split, rowoff,
+                                                            orec, otag);
+        CU(cudaGetLastError());
+    }
+    const uint32_t nhw = (uint32_t)warps << split;
+    const uint32_t stage_off = hr_stage_offset(false, nhw, (uint32_t)smem_words);
+    const size_t smem = (size_t)stage_off + hr_stage_bytes(nhw, 2u, 8u, hr_src_cmp::ROW_BYTES);
+    if (smem > 227 * 1024)
+        return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (compacted replay)", k, smem);
+    void (*kern)(hr_dev, hr_src_cmp, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t,
+                 uint32_t) = abl ? hr_replay_compact_kernel<true> : hr_replay_compact_kernel<false>;
+    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)(b1 - b0), nhw * 32u, smem, s>>>(d, hr_src_cmp{orec, otag}, segoff, rowoff, (uint32_t)warps,
+                                                      (uint32_t)lanes, (uint32_t)smem_words, stage_off, split);
+    CU(cudaGetLastError());
+    c->last_kernel = kid;
+    c->have_kernel = true;
+    return HR_OK;
+}
+
 /* One launch over simulated blocks [b0, b1) of kernel k (the whole kernel in
  * one launch for device traces; block-range chunks for host traces — blocks
  * are unordered by happens-before, so chunked launches replay the same kernel). */
@@ -383,15 +457,25 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     if (pool)
         if (const char *e = getenv("HR_SPLIT_LOG2")) {
             split = (uint32_t)atoi(e);
+            if (split > 2) split = 2;                           /* <= 4 helpers (hr_cmp_walk_kernel) */
             while (split && (warps << split) > 32) split--;
         }
     if (!pool) split = 0;
     const uint32_t nhw = (uint32_t)warps << split;
+    const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_NO_SPECULATE);
+    if (kind == HR_K_POOL_WIDE && !(c->cfg.options & HR_OPT_NO_COMPACT)) {
+        bool timing = c->cfg.options & HR_OPT_TIMING;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+        hr_status st = launch_compact(c, t, k, src, woff, s, b0, b1, split, abl);
+        if (st) return st;
+        if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
+        return HR_OK;
+    }
     size_t smem = (size_t)hr_stage_offset(pool, nhw, (uint32_t)smem_words) + hr_stage_bytes(nhw, nb, ch, SRC::ROW_BYTES);
     if (smem > 227 * 1024)
         return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (shadow %llu words + staging)", k, smem,
                     (unsigned long long)smem_words);
-    const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_NO_SPECULATE);
     void (*kern)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t);
     if (abl)
         kern = pool ? (wide ? hr_replay_kernel<true, true, true, SRC> : hr_replay_kernel<true, false, true, SRC>)
@@ -987,7 +1071,7 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->tail) cudaFree(c->tail);
     if (c->counters) cudaFree(c->counters);
     if (c->fsm) cudaFree(c->fsm);
-    for (int i = 0; i < 6; i++)
+    for (int i = 0; i < 12; i++)
         if (c->stage[i]) cudaFree(c->stage[i]);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }

@@ -40,9 +40,18 @@ struct hr_pool_smem {
     uint8_t src[32];        /* simulated lane of each pooled record */
 };
 
+/* A pool as seen by the check: 32 record slots and their simulated lanes, in
+ * shared memory (a hr_pool_smem, or a staged row of a compacted stream). */
+struct hr_entries {
+    const uint64_t *rec;
+    const uint8_t *src;
+    __device__ __forceinline__ hr_entries(const hr_pool_smem &p) : rec(p.rec), src(p.src) {}
+    __device__ __forceinline__ hr_entries(const uint64_t *r, const uint8_t *s) : rec(r), src(s) {}
+};
+
 /* fold + commit of one pooled access group (leader side) */
 __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const hr_thr &t, unsigned long long old,
-                                                        const hr_pool_smem &ps, uint32_t lane, unsigned peers,
+                                                        const hr_entries ps, uint32_t lane, unsigned peers,
                                                         uint32_t &rinfo, uint32_t &rel)
 {
     const uint32_t base = t.tid() & ~31u;
@@ -72,7 +81,7 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
 
 /* Check the pool: lanes < n hold one access each (ps.rec[lane], ps.src[lane]). */
 template <bool ABL>
-__device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t, const hr_pool_smem &ps, uint32_t n)
+__device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t, const hr_entries ps, uint32_t n)
 {
     const uint32_t lane = hr__laneid();
     const uint64_t x = lane < n ? ps.rec[lane] : HR_NOP_REC;

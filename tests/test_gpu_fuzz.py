@@ -45,7 +45,7 @@ def worker() -> None:
     bad, runs, witnesses = [], 0, []
     for name, tr in _cases():
         exp = ([tuple(r) for r in oracle.check(tr).races], oracle.check(tr).flags)
-        for options in (16, 32, 256, 512, 1):
+        for options in (16, 32, 256, 256 | 1024, 512, 1):
             for rep in range(3):
                 races, fl = hirace.check_trace(tr, options=options)
                 runs += 1
@@ -77,7 +77,7 @@ def test_fuzzed_schedules_match_oracle():
                          capture_output=True, text=True, timeout=1200)
     assert out.returncode == 0, out.stderr[-3000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
-    assert res["runs"] == 9 * 5 * 3
+    assert res["runs"] == 9 * 6 * 3
     assert res["bad"] == []
     # the fuzzing is effective: the race witnesses (which access entered RACE
     # first) differ between fuzzed runs or from the production build

@@ -96,7 +96,7 @@ def test_hot_words_contention(options):
 
 
 @pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8, 64, 64 | 32, 256, 256 | 1, 256 | 8,
-                                     512, 512 | 1, 512 | 2, 512 | 8])
+                                     512, 512 | 1, 512 | 2, 512 | 8, 256 | 1024, 256 | 1024 | 8])
 def test_ablations_same_result(options):
     """Coalescing off / fast exits off / no speculation / forced row or pooled
     replay change the commit order and the traffic, never the result
@@ -322,7 +322,7 @@ def test_finite_history_is_sound_but_incomplete_on_c2():
 @pytest.mark.parametrize("split", ["1", "2", "5"])
 def test_split_helpers_same_result(split, monkeypatch):
     """Wide pooled replay with each simulated warp split over 2^split CUDA
-    warps (clamped to 32 warps per block): every word is still committed by
+    warps (clamped to 4 helpers and 32 warps per block): every word is still committed by
     one helper in record order, so the racy set is unchanged.  Mixed shared and
     global accesses, barriers, hot words, ragged warps."""
     monkeypatch.setenv("HR_SPLIT_LOG2", split)
