@@ -158,6 +158,26 @@ def _coll_device():
     return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
+def h2d_copy_gbs(nbytes: int = 2 << 30, reps: int = 3) -> float:
+    """Plain pinned host->device copy bandwidth of this box (context for e2e,
+    which is H2D bound: PCIe rates differ between boxes)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        d.copy_(h, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    gbs = nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del h, d
+    torch.cuda.empty_cache()
+    return gbs
+
+
 def max_over_ranks(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -437,6 +457,7 @@ def main():
         torch.cuda.empty_cache()
         h2d = sum(int(h.numel() * h.element_size()) for h in pinned) + int(host_trace.warp_off.nbytes)
     if not args.no_e2e:
+        h2d_probe = h2d_copy_gbs()                      # this box's plain pinned H2D rate (untimed)
         host_replay = lambda: ck.replay_host(host_trace, stream)  # noqa: E731
         for _ in range(args.warmup):
             step(host_replay)
@@ -453,6 +474,7 @@ def main():
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world)
         parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == expected()
         e2e = {"value": total_acc / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "h2d_achieved_gbs": h2d / (e2e_ms / 1e3) / 1e9, "h2d_copy_probe_gbs": h2d_probe,
                "d2h_bytes_per_step": int(16 + 24 * len(raw_e) // max(world, 1)),
                "ms_per_step": e2e_ms, "format": args.e2e_format}
         hr.hr_replay_timing(ck.ctx)

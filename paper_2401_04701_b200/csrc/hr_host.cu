@@ -7,6 +7,7 @@
  * in hr_init / hr_shadow_alloc / the first hr_replay_trace_host; the check
  * path allocates nothing.
  */
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
@@ -49,6 +50,10 @@ struct hr_ctx {
     uint32_t last_kernel = 0;
     bool have_kernel = false;
     int last_kind = 0;                           /* HR_K_* of the last replay */
+    /* kernel choice of the last probed device trace (a performance hint only:
+     * every kernel gives the same result, so a stale hint is harmless) */
+    struct { const void *rec; uint64_t n_rows; const void *woff; uint64_t n_woff; uint32_t format, options; int kind; }
+        choice_cache = {nullptr, 0, nullptr, 0, 0, 0, -1};
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;                 /* host-trace staging copies */
     /* staging: 0 warp_off, 1 rec|rec32|packed, 2 recop|decoded chunk, 3 pack_off,
@@ -321,6 +326,13 @@ static hr_status choose_kernel(hr_ctx *c, SRC src, const hr_trace *t, const uint
 {
     *kind = HR_K_ROW;
     if (t->n_rows == 0) return HR_OK;
+    const void *rec = t->format == HR_TRACE_C32 ? (const void *)t->rec32 : (const void *)t->rec;
+    auto &cc = c->choice_cache;
+    if (cc.kind >= 0 && cc.rec == rec && cc.n_rows == t->n_rows && cc.woff == woff && cc.n_woff == t->n_warp_off &&
+        cc.format == t->format && cc.options == c->cfg.options) {
+        *kind = cc.kind;                       /* same trace replayed again: no probe, no sync */
+        return HR_OK;
+    }
     hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, t->n_rows, 2048, woff, t->n_warp_off, c->counters + 8);
     CU(cudaGetLastError());
     unsigned long long h[5] = {0, 0, 0, 0, 0};
@@ -328,6 +340,8 @@ static hr_status choose_kernel(hr_ctx *c, SRC src, const hr_trace *t, const uint
     CU(cudaStreamSynchronize(s));
     *kind = kernel_choice(c, (double)h[0], (double)h[1], (double)h[2], (double)h[3],
                           (double)(t->n_warp_off > 1 ? t->n_warp_off - 1 : 0), (double)h[4]);
+    cc.rec = rec; cc.n_rows = t->n_rows; cc.woff = woff; cc.n_woff = t->n_warp_off;
+    cc.format = t->format; cc.options = c->cfg.options; cc.kind = *kind;
     return HR_OK;
 }
 
@@ -873,6 +887,74 @@ static void sort_races(std::vector<hr_race> &v)
     v.swap(out);
 }
 
+/* Race-record sort on the device (large reports): stable LSD radix sort by
+ * word, then by kernel | space | block, then a gather.  Same order as
+ * sort_races. */
+__global__ void hr_race_keys_kernel(const hr_race *__restrict__ r, uint32_t n, uint64_t *__restrict__ lo,
+                                    uint32_t *__restrict__ idx)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    lo[i] = r[i].word;
+    idx[i] = i;
+}
+
+__global__ void hr_race_hikeys_kernel(const hr_race *__restrict__ r, const uint32_t *__restrict__ idx, uint32_t n,
+                                      uint64_t *__restrict__ hi)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const hr_race &x = r[idx[i]];
+    hi[i] = ((uint64_t)x.kernel << 33) | ((uint64_t)x.space << 32) | (uint64_t)x.block;
+}
+
+__global__ void hr_race_gather_kernel(const hr_race *__restrict__ r, const uint32_t *__restrict__ idx, uint32_t n,
+                                      hr_race *__restrict__ out)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = r[idx[i]];
+}
+
+static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &v)
+{
+    cudaStream_t s = c->stream;
+    /* scratch: lo keys (2 buffers), hi keys (2), idx (2), sorted records */
+    const size_t nb = (size_t)n;
+    size_t off[8];
+    size_t tot = 0;
+    const size_t sz[7] = {nb * 8, nb * 8, nb * 8, nb * 8, nb * 4, nb * 4, nb * sizeof(hr_race)};
+    for (int i = 0; i < 7; i++) { off[i] = tot; tot += (sz[i] + 255) & ~(size_t)255; }
+    size_t t1 = 0, t2 = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
+                                       (uint32_t *)nullptr, (int)n, 0, 64, s));
+    t2 = t1;
+    off[7] = tot;
+    tot += std::max(t1, t2);
+    hr_status st = reserve(c, 5, tot);
+    if (st) return st;
+    char *b = (char *)c->stage[5];
+    uint64_t *lo0 = (uint64_t *)(b + off[0]), *lo1 = (uint64_t *)(b + off[1]);
+    uint64_t *hi0 = (uint64_t *)(b + off[2]), *hi1 = (uint64_t *)(b + off[3]);
+    uint32_t *ix0 = (uint32_t *)(b + off[4]), *ix1 = (uint32_t *)(b + off[5]);
+    hr_race *sorted = (hr_race *)(b + off[6]);
+    void *tmp = b + off[7];
+    const unsigned g = (n + 255) / 256;
+    hr_race_keys_kernel<<<g, 256, 0, s>>>(c->ring, n, lo0, ix0);
+    CU(cudaGetLastError());
+    size_t tb = t1;
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)n, 0, 64, s));
+    hr_race_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, ix1, n, hi0);
+    CU(cudaGetLastError());
+    tb = t1;
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)n, 0, 64, s));
+    hr_race_gather_kernel<<<g, 256, 0, s>>>(c->ring, ix0, n, sorted);
+    CU(cudaGetLastError());
+    v.resize(n);
+    CU(cudaMemcpyAsync(v.data(), sorted, nb * sizeof(hr_race), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    return HR_OK;
+}
+
 extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out)
 {
     if (!c || !n_out || (cap && !out)) return fail(c, HR_E_ARG, "hr_report: bad arguments");
@@ -881,10 +963,19 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
     unsigned int hdr[4];
     CU(cudaMemcpy(hdr, c->tail, sizeof hdr, cudaMemcpyDeviceToHost));
     uint32_t n = std::min<uint32_t>(hdr[0], c->cfg.ring_capacity);
-    std::vector<hr_race> v(n);
-    if (n) CU(cudaMemcpy(v.data(), c->ring, n * sizeof(hr_race), cudaMemcpyDeviceToHost));
     uint32_t flags = hdr[1];
-    if ((flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow && c->shadow_bytes == 8) {
+    std::vector<hr_race> v;
+    const bool scan = (flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow && c->shadow_bytes == 8;
+    bool sorted = false;
+    if (n >= 4096 && !scan) {                   /* large report: sort on the device */
+        hr_status st = sort_races_device(c, n, v);
+        if (st) return st;
+        sorted = true;
+    } else {
+        v.resize(n);
+        if (n) CU(cudaMemcpy(v.data(), c->ring, n * sizeof(hr_race), cudaMemcpyDeviceToHost));
+    }
+    if (scan) {
         /* fallback: scan the last kernel's global shadow (shared instances are gone) */
         uint32_t scap = 1u << 22;
         hr_race *tmp = nullptr;
@@ -901,7 +992,7 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         if (cnt) CU(cudaMemcpy(v.data() + off, tmp, cnt * sizeof(hr_race), cudaMemcpyDeviceToHost));
         cudaFree(tmp);
     }
-    sort_races(v);
+    if (!sorted) sort_races(v);
     size_t m = 0;
     for (size_t i = 0; i < v.size(); i++) {
         if (m && !race_less(v[m - 1], v[i]) && !race_less(v[i], v[m - 1])) {

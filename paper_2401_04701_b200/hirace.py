@@ -180,11 +180,19 @@ RACE_DTYPE = np.dtype([("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("f
 assert RACE_DTYPE.itemsize == 24
 
 
+_report_buf: Optional[np.ndarray] = None
+
+
 def hr_report_raw(ctx, cap: int = 1 << 17) -> Tuple[np.ndarray, int]:
-    """(sorted unique race records as a structured array of hr_race, flags)."""
+    """(sorted unique race records as a structured array of hr_race, flags).
+    The staging buffer is reused between calls; the result is a copy."""
+    global _report_buf
     lib = load()
     while True:
-        buf = np.empty(cap, dtype=RACE_DTYPE)
+        if _report_buf is None or _report_buf.shape[0] < cap:
+            _report_buf = np.empty(cap, dtype=RACE_DTYPE)
+        buf = _report_buf
+        cap = buf.shape[0]
         n = ctypes.c_size_t(0)
         fl = ctypes.c_uint32(0)
         rc = lib.hr_report(ctx, buf.ctypes.data_as(ctypes.POINTER(HrRace)), cap, ctypes.byref(n),
@@ -193,7 +201,7 @@ def hr_report_raw(ctx, cap: int = 1 << 17) -> Tuple[np.ndarray, int]:
             cap = int(n.value)
             continue
         _check(rc, ctx, "hr_report")
-        return buf[: n.value], int(fl.value)
+        return buf[: n.value].copy(), int(fl.value)
 
 
 def races_of(raw: np.ndarray) -> List[Race]:
