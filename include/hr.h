@@ -241,6 +241,14 @@ hr_status hr_unpack_trace(hr_ctx *ctx, const hr_trace *in, uint64_t *rec_out, vo
  * shadow is scanned for RACE words of the last replayed kernel instead. */
 hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out);
 
+/* Merge race sets, HOST only (no CUDA call, no
+ * ctx): `in` holds n hr_race records, e.g. the concatenated hr_report results
+ * of N address shards after an allgather; `out` (host, cap records) receives
+ * them sorted by (kernel, space, block, word), one record per address with the
+ * widest scope.  *n_out = the unique count; HR_E_ARG if it exceeds cap (then
+ * cap records are written) or on NULL arguments.  in and out may not overlap. */
+hr_status hr_merge_races(const hr_race *in, size_t n, hr_race *out, size_t cap, size_t *n_out);
+
 /* Per-pair race classes of already reported racy addresses:
  * `races` are the n records hr_report returned for this same device trace `t`
  * (same kernel_base); the trace is replayed again through four class-projected

@@ -62,6 +62,9 @@ struct hr_ctx {
      * 9 row offsets, 10 packed records, 11 packed tags */
     void *stage[12] = {};
     size_t stage_cap[12] = {};
+    hr_race *rep_host = nullptr;                 /* pinned staging of the sorted report (D2H) */
+    size_t rep_cap = 0;
+    std::vector<hr_race> rep;                    /* report scratch, kept across calls */
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
@@ -915,6 +918,26 @@ __global__ void hr_race_gather_kernel(const hr_race *__restrict__ r, const uint3
     if (i < n) out[i] = r[idx[i]];
 }
 
+/* Sorted records -> one per address (kernel, space, block, word), keeping the
+ * widest scope (a RACE_BLOCK entry plus its later RACE_GRID upgrade, or a ring
+ * record plus its shadow-scan duplicate); returns the unique count. */
+static size_t unique_races(std::vector<hr_race> &v)
+{
+    size_t m = 0;
+    for (size_t i = 0; i < v.size(); i++) {
+        if (m && !race_less(v[m - 1], v[i]) && !race_less(v[i], v[m - 1])) {
+            if (v[i].scope > v[m - 1].scope) {
+                uint8_t sc = v[i].scope;
+                if (v[m - 1].first_kind == 0xff) v[m - 1] = v[i];
+                v[m - 1].scope = sc;
+            }
+            continue;
+        }
+        v[m++] = v[i];
+    }
+    return m;
+}
+
 static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &v)
 {
     cudaStream_t s = c->stream;
@@ -949,9 +972,17 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)n, 0, 64, s));
     hr_race_gather_kernel<<<g, 256, 0, s>>>(c->ring, ix0, n, sorted);
     CU(cudaGetLastError());
-    v.resize(n);
-    CU(cudaMemcpyAsync(v.data(), sorted, nb * sizeof(hr_race), cudaMemcpyDeviceToHost, s));
+    if (n > c->rep_cap) {
+        if (c->rep_host) cudaFreeHost(c->rep_host);
+        c->rep_host = nullptr;
+        c->rep_cap = 0;
+        if (cudaHostAlloc((void **)&c->rep_host, nb * sizeof(hr_race), cudaHostAllocDefault) != cudaSuccess)
+            return fail(c, HR_E_NOMEM, "pinned report staging of %zu records failed", nb);
+        c->rep_cap = n;
+    }
+    CU(cudaMemcpyAsync(c->rep_host, sorted, nb * sizeof(hr_race), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    v.assign(c->rep_host, c->rep_host + n);
     return HR_OK;
 }
 
@@ -964,7 +995,8 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
     CU(cudaMemcpy(hdr, c->tail, sizeof hdr, cudaMemcpyDeviceToHost));
     uint32_t n = std::min<uint32_t>(hdr[0], c->cfg.ring_capacity);
     uint32_t flags = hdr[1];
-    std::vector<hr_race> v;
+    std::vector<hr_race> &v = c->rep;
+    v.clear();
     const bool scan = (flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow && c->shadow_bytes == 8;
     bool sorted = false;
     if (n >= 4096 && !scan) {                   /* large report: sort on the device */
@@ -993,23 +1025,47 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         cudaFree(tmp);
     }
     if (!sorted) sort_races(v);
-    size_t m = 0;
-    for (size_t i = 0; i < v.size(); i++) {
-        if (m && !race_less(v[m - 1], v[i]) && !race_less(v[i], v[m - 1])) {
-            if (v[i].scope > v[m - 1].scope) {
-                uint8_t sc = v[i].scope;
-                if (v[m - 1].first_kind == 0xff) v[m - 1] = v[i];
-                v[m - 1].scope = sc;
-            }
-            continue;
-        }
-        v[m++] = v[i];
-    }
+    const size_t m = unique_races(v);
     *n_out = m;
     if (flags_out) *flags_out = flags;
     size_t w = std::min(m, cap);
     if (w) memcpy(out, v.data(), w * sizeof(hr_race));
     return m > cap ? fail(c, HR_E_ARG, "hr_report: %zu races, capacity %zu", m, cap) : HR_OK;
+}
+
+/* Merge of per-shard race sets (include/hr.h): host only, no CUDA call. */
+extern "C" hr_status hr_merge_races(const hr_race *in, size_t n, hr_race *out, size_t cap, size_t *n_out)
+{
+    if (!n_out || (n && !in) || (cap && !out)) return HR_E_ARG;
+    /* scratch kept across calls: fresh multi-MB vectors cost a page fault per 4 KiB */
+    static thread_local std::vector<hr_race> v, tmp;
+    v.assign(in, in + n);
+    /* the input is usually a concatenation of sorted shard reports: merge its
+     * natural runs pairwise (log2(runs) sequential passes); radix-sort otherwise */
+    std::vector<size_t> run{0};
+    for (size_t i = 1; i < n; i++)
+        if (race_less(v[i], v[i - 1])) run.push_back(i);
+    run.push_back(n);
+    if (run.size() - 1 > 64) {
+        sort_races(v);
+    } else if (run.size() > 2) {
+        tmp.resize(n);
+        while (run.size() > 2) {
+            std::vector<size_t> nr{0};
+            for (size_t r = 0; r + 1 < run.size(); r += 2) {
+                const size_t a = run[r], b = run[r + 1], e = r + 2 < run.size() ? run[r + 2] : b;
+                std::merge(v.begin() + a, v.begin() + b, v.begin() + b, v.begin() + e, tmp.begin() + a, race_less);
+                nr.push_back(e);
+            }
+            v.swap(tmp);
+            run.swap(nr);
+        }
+    }
+    const size_t m = unique_races(v);
+    *n_out = m;
+    const size_t w = std::min(m, cap);
+    if (w) memcpy(out, v.data(), w * sizeof(hr_race));
+    return m > cap ? HR_E_ARG : HR_OK;
 }
 
 /* Per-pair race classes post-pass (include/hr.h). */
@@ -1164,6 +1220,7 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->fsm) cudaFree(c->fsm);
     for (int i = 0; i < 12; i++)
         if (c->stage[i]) cudaFree(c->stage[i]);
+    if (c->rep_host) cudaFreeHost(c->rep_host);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

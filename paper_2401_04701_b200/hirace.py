@@ -32,7 +32,7 @@ HR_OPT_POOL_WIDE = 256
 HR_OPT_ROW_WIDE = 512
 HR_OPT_NO_COMPACT = 1024
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
-           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_race_classes", "hr_reset_report", "hr_counters",
+           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing",
            "hr_fsm_table",
            "hr_device_view", "hr_last_error", "hr_destroy")
@@ -91,6 +91,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_pack_trace": ([vp, P(HrTrace), vp, ctypes.c_uint64, vp, P(ctypes.c_uint64), vp], ctypes.c_int),
         "hr_unpack_trace": ([vp, P(HrTrace), vp, vp], ctypes.c_int),
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
+        "hr_merge_races": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, P(ctypes.c_size_t)], ctypes.c_int),
         "hr_race_classes": ([vp, P(HrTrace), vp, ctypes.c_size_t, vp, vp], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
         "hr_counters": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
@@ -202,6 +203,17 @@ def hr_report_raw(ctx, cap: int = 1 << 17) -> Tuple[np.ndarray, int]:
             continue
         _check(rc, ctx, "hr_report")
         return buf[: n.value].copy(), int(fl.value)
+
+
+def hr_merge_races(parts: np.ndarray) -> np.ndarray:
+    """Sorted unique union of race records (hr_race structured array), e.g. the
+    concatenated per-shard reports after an allgather.  Host-only C call."""
+    src = np.ascontiguousarray(parts, dtype=RACE_DTYPE)
+    out = np.empty(max(len(src), 1), dtype=RACE_DTYPE)
+    n = ctypes.c_size_t(0)
+    _check(load().hr_merge_races(src.ctypes.data if len(src) else None, len(src), out.ctypes.data, len(out),
+                                 ctypes.byref(n)), None, "hr_merge_races")
+    return out[: n.value]
 
 
 def races_of(raw: np.ndarray) -> List[Race]:

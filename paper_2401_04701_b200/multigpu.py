@@ -7,8 +7,9 @@ instances of simulated blocks with block % N == r.  Each rank replays every
 simulated thread but only its own records, keeping all barrier records so the
 per-word commit order stays happens-before consistent; its shadow is 1/N.
 The ONE exchange is the race-set allgather (NCCL over NVLink on GPUs, gloo
-in the CPU tests) followed by a concatenate-and-sort merge — shards are
-address-disjoint, so no de-duplication is needed.
+in the CPU tests) followed by a concatenate-and-sort merge in libhirace
+(hr_merge_races, host C) — shards are address-disjoint, so the merge only
+interleaves the per-rank sorted lists.
 
 torch.distributed provides the process group only; the check runs in
 libhirace.so.
@@ -87,19 +88,20 @@ def exchange_races(raw: np.ndarray, flags: int = 0, group=None, device=None) -> 
     meta = torch.tensor([len(raw), flags], dtype=torch.int64, device=dev)
     metas = [torch.empty_like(meta) for _ in range(world)]
     dist.all_gather(metas, meta, group=group)
-    counts = [int(m[0].item()) for m in metas]
+    allm = torch.stack(metas).cpu()                 # one device->host read
+    counts = [int(c) for c in allm[:, 0]]
     all_flags = 0
-    for m in metas:
-        all_flags |= int(m[1].item())
+    for f in allm[:, 1]:
+        all_flags |= int(f)
     mx = max(max(counts), 1)
     pad = torch.zeros(mx * 3, dtype=torch.int64, device=dev)
     if len(raw):
         pad[: len(raw) * 3] = torch.from_numpy(np.ascontiguousarray(raw).view(np.int64).copy()).to(dev)
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
-    merged = np.concatenate([p.cpu().numpy()[: c * 3].view(RACE_DTYPE) for p, c in zip(parts, counts)])
-    order = np.lexsort((merged["word"], merged["block"], merged["space"], merged["kernel"]))
-    return merged[order], all_flags
+    flat = torch.cat([p[: c * 3] for p, c in zip(parts, counts)]).cpu().numpy()
+    from .hirace import hr_merge_races          # sort + unique in libhirace (host C), not numpy
+    return hr_merge_races(flat.view(RACE_DTYPE)), all_flags
 
 
 def replay_sharded(trace, group=None, device: Optional[int] = None, base_word: int = 0, **checker_kw):

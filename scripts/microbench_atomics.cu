@@ -6,6 +6,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb scripts/microbench_atomics.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint64_t mix(uint64_t x)
@@ -35,8 +36,9 @@ __global__ void kern(unsigned long long *a, uint64_t mask, int iters, unsigned l
             if (OP == 0) r[k] = atomicCAS(&a[idx[k]], 0ull, tid + 1);           // CAS (first touch wins)
             else if (OP == 1) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r[k]) : "l"(&a[idx[k]]));
             else if (OP == 2) r[k] = atomicCAS(&a[idx[k]], 0xdeadull, tid + 1);  // always-failing CAS
-            else { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r[k]) : "l"(&a[idx[k]]));
+            else if (OP == 3) { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r[k]) : "l"(&a[idx[k]]));
                    r[k] = atomicCAS(&a[idx[k]], r[k], r[k] + 1); }              // load + dependent CAS
+            else { a[idx[k]] = tid + 1; r[k] = 0; }                              // plain 8-byte store
         }
 #pragma unroll
         for (int k = 0; k < ILP; k++) acc += r[k];
@@ -67,8 +69,16 @@ void run(const char *name, unsigned long long *a, uint64_t words, int blocks, in
            ms * 1e3 / (iters * ILP));
 }
 
-int main()
+int main(int argc, char **argv)
 {
+    /* optional: cudaLimitMaxL2FetchGranularity in bytes (0..128), and "big" to run only 2^32 words */
+    if (argc > 1) {
+        size_t g = (size_t)atoi(argv[1]), got = 0;
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g);
+        cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+        printf("L2 fetch granularity limit set %zu, reads back %zu\n", g, got);
+    }
+    const bool only_big = argc > 2;
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     unsigned long long *a, *sink;
@@ -78,11 +88,13 @@ int main()
     cudaMalloc(&sink, 8);
     int blocks = nsm * 8, thr = 256, it = 64;
     printf("SMs %d, threads %d\n", nsm, blocks * thr);
-    for (int lg = 22; lg <= 32; lg += 1) {
+    for (int lg = only_big ? 32 : 22; lg <= 32; lg += 1) {
         uint64_t w = 1ull << lg;
         run<1, 4, false>("LD random sweep", a, w, blocks, thr, it, sink);
         run<0, 4, false>("CAS random sweep", a, w, blocks, thr, it, sink);
     }
+    run<4, 4, false>("ST random", a, big, blocks, thr, it, sink);
+    run<3, 1, false>("LD+CAS random", a, big, blocks, thr, it, sink);
     cudaError_t e = cudaGetLastError();
     printf("status %s\n", cudaGetErrorString(e));
     return 0;

@@ -4,6 +4,7 @@ import ctypes
 import re
 import os
 
+import numpy as np
 import pytest
 
 from paper_2401_04701_b200 import build, hirace
@@ -66,3 +67,29 @@ def test_config_validation():
     assert lib.hr_init(ctypes.byref(bad), ctypes.byref(ctx)) == hirace.HR_E_ARG
     bad = hirace.HrConfig(6, 26, 16, 16, 16, 0, 0)
     assert lib.hr_init(ctypes.byref(bad), ctypes.byref(ctx)) == hirace.HR_E_ARG
+
+
+def test_merge_races_host_only():
+    """hr_merge_races (host C, no GPU): the sorted (kernel, space, block, word)
+    union of shuffled, duplicated shard reports, one record per address with the
+    widest scope."""
+    rng = np.random.default_rng(7)
+    n = 5000
+    a = np.zeros(n, dtype=hirace.RACE_DTYPE)
+    a["word"] = rng.integers(0, 1 << 40, n)
+    a["kernel"] = rng.integers(0, 3, n)
+    a["space"] = rng.integers(0, 2, n)
+    a["block"] = np.where(a["space"] == 1, rng.integers(0, 4, n), 0xFFFFFFFF)
+    a["scope"] = 1
+    dup = a[rng.choice(n, 700, replace=False)].copy()
+    dup["scope"] = 2                                   # a later RACE_GRID upgrade of the same address
+    parts = np.concatenate([a, dup, a[:300]])
+    rng.shuffle(parts)
+    got = hirace.hr_merge_races(parts)
+    keys = {}
+    for r in parts:
+        k = (int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]))
+        keys[k] = max(keys.get(k, 0), int(r["scope"]))
+    want = sorted(keys.items())
+    assert [((int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"])), int(r["scope"])) for r in got] == want
+    assert len(hirace.hr_merge_races(parts[:0])) == 0
