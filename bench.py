@@ -22,6 +22,7 @@ N > 1, the NCCL allgather of the per-shard race sets.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -356,6 +357,11 @@ def main():
     got = [(int(r["word"]), int(r["scope"])) for r in raw]
     parity_ok = got == expected() and flags == 0
     hr.hr_replay_timing(ck.ctx)                     # drop warm-up launches
+    hr.hr_launch_count(ck.ctx)
+    # setup objects (torch, traces) out of the collector's way: a full gen-2
+    # pass over them inside a host-side report step costs ~10 ms at random
+    gc.collect()
+    gc.freeze()
 
     clocks = Clocks(torch.cuda.current_device())
     barrier(world)
@@ -372,6 +378,7 @@ def main():
     clk = clocks.stop()
     ms_total = e0.elapsed_time(e1)
     reset_ms, n_resets, kern_ms, n_kern = hr.hr_replay_timing(ck.ctx)
+    n_launch = hr.hr_launch_count(ck.ctx)
     parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw] == expected()
 
     ms_step = max_over_ranks(ms_total / args.steps, world)
@@ -508,7 +515,10 @@ def main():
                                       ms_step - kern_ms_launch - (0.0 if args.double_shadow else reset_ms_launch)},
             "clocks": clk,
             "e2e": e2e,
-            "gpu_launches": n_kern,
+            "gpu_launches": n_launch,
+            "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch,
+                                    "rule": "every libhirace kernel launched in the timed region "
+                                            "(replay + report sort/gather; a CUB call counts as one)"},
             "slowdown": slow,
             "cpu_baseline": cpu,
             "parity_vs_closed_form": parity_ok,

@@ -272,6 +272,12 @@ hr_status hr_counters(hr_ctx *ctx, uint64_t out[4]);
 hr_status hr_replay_timing(hr_ctx *ctx, double *reset_ms, uint64_t *n_resets, double *kernel_ms,
                            uint64_t *n_kernels);
 
+/* Number of device kernels this ctx launched since the last call (every
+ * __global__ launch of libhirace; a CUB scan or sort call counts as one),
+ * then clear it.  Host only, no CUDA call; lets a harness state how many
+ * kernels ran inside a timed region. */
+hr_status hr_launch_count(hr_ctx *ctx, uint64_t *n_launches);
+
 /* Copy of the compiled-in FSM table (2048 bytes, index state<<6|kind<<4|sync<<2|rel)
  * and per-state flags (32 bytes).  Either pointer may be NULL. */
 hr_status hr_fsm_table(uint8_t *table2048, uint8_t *flags32);

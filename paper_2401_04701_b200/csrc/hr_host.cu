@@ -41,6 +41,7 @@ struct hr_ctx {
     cudaStream_t side = nullptr;                 /* deferred resets (double shadow) */
     cudaEvent_t used_done[2] = {nullptr, nullptr}, reset_done[2] = {nullptr, nullptr};
     uint64_t gbase = 0, gwords = 0, glocal = 0;
+    uint64_t launches = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
     hr_race *ring = nullptr;
@@ -336,6 +337,7 @@ static hr_status choose_kernel(hr_ctx *c, SRC src, const hr_trace *t, const uint
         *kind = cc.kind;                       /* same trace replayed again: no probe, no sync */
         return HR_OK;
     }
+    c->launches++;
     hr_density_kernel<SRC><<<1, 1024, 0, s>>>(src, t->n_rows, 2048, woff, t->n_warp_off, c->counters + 8);
     CU(cudaGetLastError());
     unsigned long long h[5] = {0, 0, 0, 0, 0};
@@ -382,11 +384,13 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     hr_status st;
     if ((st = reserve(c, 6, (nw + 1) * 8)) || (st = reserve(c, 7, (nw + 1) * 8))) return st;
     uint64_t *nseg = (uint64_t *)c->stage[6], *segoff = (uint64_t *)c->stage[7];
+    c->launches++;
     hr_cmp_nseg_kernel<<<(unsigned)((nw + 1 + 255) / 256), 256, 0, s>>>(wk, nw, nseg);
     CU(cudaGetLastError());
     size_t tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg, segoff, (int64_t)(nw + 1), s));
     if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches++;
     CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, nseg, segoff, (int64_t)(nw + 1), s));
     uint64_t nsegs = 0;
     CU(cudaMemcpyAsync(&nsegs, segoff + nw, 8, cudaMemcpyDeviceToHost, s));
@@ -397,6 +401,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     CU(cudaMemsetAsync(cnt + ncnt, 0, 8, s));
     const unsigned wgrid = (unsigned)((nsegs * 32 + 255) / 256);
     if (nsegs) {
+        c->launches++;
         hr_cmp_walk_kernel<false, SRC><<<wgrid, 256, 0, s>>>(d, src, wk, segoff, nw, (uint32_t)lanes, split, cnt,
                                                              nullptr, nullptr);
         CU(cudaGetLastError());
@@ -404,6 +409,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, rowoff, (int64_t)(ncnt + 1), s));
     if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches++;
     CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, rowoff, (int64_t)(ncnt + 1), s));
     uint64_t nrows = 0;
     CU(cudaMemcpyAsync(&nrows, rowoff + ncnt, 8, cudaMemcpyDeviceToHost, s));
@@ -414,6 +420,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     uint64_t *orec = (uint64_t *)c->stage[10];
     uint8_t *otag = (uint8_t *)c->stage[11];
     if (nsegs) {
+        c->launches++;
         hr_cmp_walk_kernel<true, SRC><<<wgrid, 256, 0, s>>>(d, src, wk, segoff, nw, (uint32_t)lanes, split, rowoff,
                                                             orec, otag);
         CU(cudaGetLastError());
@@ -426,6 +433,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     void (*kern)(hr_dev, hr_src_cmp, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t,
                  uint32_t) = abl ? hr_replay_compact_kernel<true> : hr_replay_compact_kernel<false>;
     if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    c->launches++;
     kern<<<(unsigned)(b1 - b0), nhw * 32u, smem, s>>>(d, hr_src_cmp{orec, otag}, segoff, rowoff, (uint32_t)warps,
                                                       (uint32_t)lanes, (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
@@ -453,6 +461,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+        c->launches++;
         hr_fh_replay_kernel<SRC><<<(unsigned)(b1 - b0), (unsigned)(warps * 32), smem, s>>>(
             d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
         CU(cudaGetLastError());
@@ -505,6 +514,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     bool timing = c->cfg.options & HR_OPT_TIMING;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+    c->launches++;
     kern<<<(unsigned)(b1 - b0), nhw * 32u, smem, s>>>(d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes,
                                                        (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
@@ -711,6 +721,7 @@ static hr_status replay_packed(hr_ctx *c, const hr_trace *t, bool host)
         }
         if (s1 > s0) {
             const uint64_t threads = (s1 - s0) * 32;
+            c->launches++;
             hr_unpack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, c->stream>>>(dpacked, dpoff, dwoff, s0, s1,
                                                                                        rbase, dec);
             CU(cudaGetLastError());
@@ -719,6 +730,7 @@ static hr_status replay_packed(hr_ctx *c, const hr_trace *t, bool host)
         if (kind < 0) {
             /* kernel choice: density of the first decoded chunk, tail of all warps */
             if (rows) {
+                c->launches++;
                 hr_density_kernel<hr_src_u64><<<1, 1024, 0, c->stream>>>(hr_src_u64{dec}, rows, 2048, dwoff, nwo,
                                                                         c->counters + 8);
                 CU(cudaGetLastError());
@@ -754,11 +766,13 @@ extern "C" hr_status hr_pack_trace(hr_ctx *c, const hr_trace *in, uint8_t *out, 
     unsigned int *err = (unsigned int *)((char *)c->stage[4] + sizes_bytes);
     CU(cudaMemsetAsync(err, 0, 4, s));
     const unsigned grid = (unsigned)((n * 32 + 255) / 256);
+    c->launches++;
     hr_pack_size_kernel<<<grid, 256, 0, s>>>(in->rec, in->warp_off, n, sizes, err);
     CU(cudaGetLastError());
     size_t tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, sizes, pack_off, (int64_t)n, s));
     if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches++;
     CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, sizes, pack_off, (int64_t)n, s));
     uint64_t total = 0;
     unsigned int herr = 0;
@@ -770,6 +784,7 @@ extern "C" hr_status hr_pack_trace(hr_ctx *c, const hr_trace *in, uint8_t *out, 
     if (!out) return HR_OK;
     if (cap < total + HR_PACK_SLACK) return fail(c, HR_E_ARG, "hr_pack_trace: cap %llu < %llu", (unsigned long long)cap,
                                                  (unsigned long long)(total + HR_PACK_SLACK));
+    c->launches++;
     hr_pack_write_kernel<<<grid, 256, 0, s>>>(in->rec, in->warp_off, n, pack_off, out);
     CU(cudaGetLastError());
     CU(cudaMemsetAsync(out + total, 0, HR_PACK_SLACK, s));
@@ -784,6 +799,7 @@ extern "C" hr_status hr_unpack_trace(hr_ctx *c, const hr_trace *in, uint64_t *re
     CU(cudaSetDevice(c->device));
     if (in->n_warp_off < 2) return HR_OK;
     const uint64_t nseg = in->n_warp_off - 1;
+    c->launches++;
     hr_unpack_kernel<<<(unsigned)((nseg * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         in->packed, in->pack_off, in->warp_off, 0, nseg, 0, rec_out);
     CU(cudaGetLastError());
@@ -962,14 +978,19 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
     hr_race *sorted = (hr_race *)(b + off[6]);
     void *tmp = b + off[7];
     const unsigned g = (n + 255) / 256;
+    c->launches++;
     hr_race_keys_kernel<<<g, 256, 0, s>>>(c->ring, n, lo0, ix0);
     CU(cudaGetLastError());
     size_t tb = t1;
+    c->launches++;
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)n, 0, 64, s));
+    c->launches++;
     hr_race_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, ix1, n, hi0);
     CU(cudaGetLastError());
     tb = t1;
+    c->launches++;
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)n, 0, 64, s));
+    c->launches++;
     hr_race_gather_kernel<<<g, 256, 0, s>>>(c->ring, ix0, n, sorted);
     CU(cudaGetLastError());
     if (n > c->rep_cap) {
@@ -1013,6 +1034,7 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         hr_race *tmp = nullptr;
         CU(cudaMalloc(&tmp, sizeof(hr_race) * (size_t)scap));
         CU(cudaMemset(c->tail + 2, 0, sizeof(unsigned int)));
+        c->launches++;
         hr_scan_kernel<<<148 * 8, 256>>>(c->gshadow, c->glocal, c->gbase, c->shard_rank, c->shard_log2, c->gran_log2,
                                          c->last_kernel, tmp, c->tail + 2, scap);
         CU(cudaGetLastError());
@@ -1081,6 +1103,7 @@ static hr_status classes_launch(hr_ctx *c, const hr_trace *t, SRC src, const uns
         if (!kd[0]) continue;
         hr_dev d = make_dev(c, t->kernel_base + k);
         size_t smem = HR_FSM_SMEM_BYTES + HR_CLASS_TABLES_BYTES;
+        c->launches++;
         hr_classes_kernel<SRC><<<(unsigned)kd[0], (unsigned)(kd[1] * 32), smem, s>>>(
             d, src, t->warp_off + kd[4], (uint32_t)kd[1], (uint32_t)kd[2], ctab, tab, mask, sh, cls, kinds);
         CU(cudaGetLastError());
@@ -1182,6 +1205,14 @@ extern "C" hr_status hr_replay_timing(hr_ctx *c, double *reset_ms, uint64_t *n_r
     if (n_kernels) *n_kernels = c->ev_kernel.size();
     c->ev_reset.clear();
     c->ev_kernel.clear();
+    return HR_OK;
+}
+
+extern "C" hr_status hr_launch_count(hr_ctx *c, uint64_t *n)
+{
+    if (!c || !n) return HR_E_ARG;
+    *n = c->launches;
+    c->launches = 0;
     return HR_OK;
 }
 

@@ -33,7 +33,7 @@ HR_OPT_ROW_WIDE = 512
 HR_OPT_NO_COMPACT = 1024
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
-           "hr_replay_timing",
+           "hr_replay_timing", "hr_launch_count",
            "hr_fsm_table",
            "hr_device_view", "hr_last_error", "hr_destroy")
 
@@ -95,6 +95,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_race_classes": ([vp, P(HrTrace), vp, ctypes.c_size_t, vp, vp], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
         "hr_counters": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
+        "hr_launch_count": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
         "hr_replay_timing": ([vp, P(ctypes.c_double), P(ctypes.c_uint64), P(ctypes.c_double),
                               P(ctypes.c_uint64)], ctypes.c_int),
         "hr_fsm_table": ([P(ctypes.c_uint8), P(ctypes.c_uint8)], ctypes.c_int),
@@ -252,6 +253,13 @@ def hr_replay_timing(ctx) -> Tuple[float, int, float, int]:
     _check(load().hr_replay_timing(ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
            ctx, "hr_replay_timing")
     return a.value, int(b.value), c.value, int(d.value)
+
+
+def hr_launch_count(ctx) -> int:
+    """Kernels the ctx launched since the last call (a CUB call counts as one)."""
+    n = ctypes.c_uint64()
+    _check(load().hr_launch_count(ctx, ctypes.byref(n)), ctx, "hr_launch_count")
+    return int(n.value)
 
 
 def hr_fsm_table() -> Tuple[bytes, bytes]:
