@@ -289,7 +289,7 @@ def main():
     import numpy as np
     import torch
     from paper_2401_04701_b200 import hirace as hr
-    from paper_2401_04701_b200.multigpu import exchange_races
+    from paper_2401_04701_b200.multigpu import exchange_races, shard_owner
     from tracegen import c5
 
     rank, world, local = dist_setup(args)
@@ -351,7 +351,7 @@ def main():
     def expected():
         pl = c5.planted(lb, seed)
         if emulated:
-            return [(w, sc) for w, sc in pl if ((w >> args.granule_log2) % shard_n) == shard_rank]
+            return [(w, sc) for w, sc in pl if shard_owner(w >> args.granule_log2, shard_n) == shard_rank]
         return pl
 
     got = [(int(r["word"]), int(r["scope"])) for r in raw]
@@ -496,7 +496,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"C5: {total_acc} checked accesses (2^{lb} blocks x 256 threads x 256), "
-                                   f"global trace over 2^{lb + 16} words, address-sharded (granule mod {world})",
+                                   f"global trace over 2^{lb + 16} words, address-sharded (rotated granule stripes, x{world})",
                        "trace_format": args.format,
                        "parallelism": f"address-shard x{world}", "l2": "inputs larger than L2 "
                        "(trace + shadow >> 126 MB; no flush needed)", "seed": seed},

@@ -172,15 +172,20 @@ typedef struct hr_ctx hr_ctx;   /* opaque */
 hr_status hr_init(const hr_config *cfg, hr_ctx **out);
 
 /* Address sharding for multi-GPU replay: this ctx checks only
- * global words whose 4 KiB shadow granule ((word - base) >> 9) satisfies
- * granule % count == rank, and shared instances of simulated blocks with
- * block % count == rank.  count must be a power of two <= 64.  Call before
+ * the global words whose shadow granule g = (word - base) >> granule_log2 has
+ * hr_shard_owner(g, log2(count)) == rank, and the shared instances of
+ * simulated blocks with block % count == rank.  Granules are dealt out in
+ * stripes of `count` consecutive granules, one granule of each stripe per
+ * rank, the assignment rotated per stripe by a hash of the stripe index; a
+ * rank's shadow holds its granules packed in stripe order (local granule
+ * index = g >> log2(count)).  count must be a power of two <= 64.  Call before
  * hr_shadow_alloc.  Default: rank 0 of 1. */
 hr_status hr_set_shard(hr_ctx *ctx, uint32_t rank, uint32_t count);
 
-/* Same with a shard granule of 2^granule_log2 words (5..24; hr_set_shard uses 9).
- * Smaller granules spread power-law hot words over more ranks; 5 (32 words)
- * still keeps a warp's 32 consecutive words on one rank. */
+/* Same with a shard granule of 2^granule_log2 words (0..24; hr_set_shard uses
+ * 9 = 4 KiB of shadow).  Smaller granules spread power-law hot words over
+ * more ranks; the rotation keeps a block's warps from landing on one rank
+ * when a granule is a warp row (granule_log2 5). */
 hr_status hr_set_shard_ex(hr_ctx *ctx, uint32_t rank, uint32_t count, uint32_t granule_log2);
 
 /* Register a shadow region ("For each shared memory variable, a
@@ -292,4 +297,25 @@ void hr_destroy(hr_ctx *ctx);
 #ifdef __cplusplus
 }
 #endif
+
+/* The address-shard owner function (hr_set_shard above), inline so that
+ * trace partitioners and the device check agree on it. */
+#ifdef __CUDACC__
+#define HR_HD __host__ __device__ __forceinline__
+#else
+#define HR_HD static inline
+#endif
+HR_HD uint32_t hr_shard_rot(uint64_t stripe, uint32_t log2n)
+{
+    return log2n ? ((uint32_t)(stripe ^ (stripe >> 32)) * 0x9E3779B1u) >> (32u - log2n) : 0u;
+}
+HR_HD uint32_t hr_shard_owner(uint64_t granule, uint32_t log2n)
+{
+    return ((uint32_t)granule + hr_shard_rot(granule >> log2n, log2n)) & ((1u << log2n) - 1u);
+}
+/* inverse: the granule of `rank` in stripe `stripe` */
+HR_HD uint64_t hr_shard_granule(uint64_t stripe, uint32_t rank, uint32_t log2n)
+{
+    return (stripe << log2n) | ((rank - hr_shard_rot(stripe, log2n)) & ((1u << log2n) - 1u));
+}
 #endif /* HR_H_ */

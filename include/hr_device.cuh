@@ -60,7 +60,7 @@ struct hr_dev {
     const unsigned char *fsm;     /* HR_FSM_SMEM_BYTES in global memory */
     uint32_t ring_cap;
     uint32_t kernel_id;
-    uint32_t shard_rank, shard_log2; /* owner(granule) = granule & (2^log2 - 1) */
+    uint32_t shard_rank, shard_log2; /* owner(granule) = hr_shard_owner(granule, shard_log2) (hr.h) */
     uint32_t gran_log2;           /* shard granule = 2^gran_log2 words (default 9: 4 KiB of shadow) */
     uint32_t wc_bits;             /* bc occupies [31:wc_bits], wc [wc_bits-1:0] */
     uint32_t bc_max, wc_max;
@@ -215,7 +215,7 @@ __device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uin
     if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
     const uint64_t gran = g >> d.gran_log2;
     local = ((gran >> d.shard_log2) << d.gran_log2) | (g & ((1ull << d.gran_log2) - 1u));
-    return ((uint32_t)gran & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
+    return hr_shard_owner(gran, d.shard_log2) == d.shard_rank;
 }
 
 /* a5 + a6 (+ a3 fold): the state after this lane's access from `old`, then the

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) hr_cmp_walk_kernel(hr_dev d, SRC src, con
         if (v && !((x >> 61) & 1u) && d.shard_log2) {
             const uint64_t g = wd - d.gbase;
             const bool in = wd >= d.gbase && g < d.gwords;
-            v = !in || ((uint32_t)(g >> d.gran_log2) & ((1u << d.shard_log2) - 1u)) == d.shard_rank;
+            v = !in || hr_shard_owner(g >> d.gran_log2, d.shard_log2) == d.shard_rank;
         }
         const uint32_t mine = split_log2 ? hr__helper_of(wd, split_log2) : 0u;
 #pragma unroll
@@ -198,11 +198,9 @@ __global__ void __launch_bounds__(1024, 1) hr_replay_compact_kernel(hr_dev d, hr
         const uint32_t buf = buf0 + b * CHB;
         hr__mbar_wait(bar0 + 8u * b, (c / NB) & 1u);
         const uint32_t rows = min(CH, n - c * CH);
-        const unsigned char *gbuf = hr_smem + (buf - smem0);
         for (uint32_t j = 0; j < rows; j++) {
-            const uint64_t *rec = reinterpret_cast<const uint64_t *>(gbuf + j * 256u);
-            const uint8_t *tag = gbuf + CH * 256u + j * 32u;
-            const uint64_t x = rec[lane];
+            const hr_entries row(buf + j * 256u, buf + CH * 256u + j * 32u);
+            const uint64_t x = row.rec_at(lane);
             const uint32_t op = (uint32_t)(x >> 62);
             const uint64_t wd = x & HR_WORD_MASK;
             if (__any_sync(0xffffffffu, op == 3u && wd != 0u)) {
@@ -211,7 +209,7 @@ __global__ void __launch_bounds__(1024, 1) hr_replay_compact_kernel(hr_dev d, hr
             }
             if (t.off & 1u) continue;                              /* clock overflow (warp uniform) */
             const uint32_t k = __popc(__ballot_sync(0xffffffffu, op != 3u));
-            if (k) hr__check_pool<ABL>(d, t, hr_entries(rec, tag), k);
+            if (k) hr__check_pool<ABL>(d, t, row, k);
         }
         __syncwarp();
         if (lane == 0 && (c + NB) * CH < n) {

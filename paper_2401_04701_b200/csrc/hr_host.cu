@@ -177,7 +177,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
 
 extern "C" hr_status hr_set_shard_ex(hr_ctx *c, uint32_t rank, uint32_t count, uint32_t granule_log2)
 {
-    if (!c || count == 0 || count > 64 || (count & (count - 1)) || rank >= count || granule_log2 < 5 ||
+    if (!c || count == 0 || count > 64 || (count & (count - 1)) || rank >= count || 
         granule_log2 > 24)
         return fail(c, HR_E_ARG, "hr_set_shard: bad rank/count/granule");
     if (c->gshadow) return fail(c, HR_E_STATE, "hr_set_shard after hr_shadow_alloc");

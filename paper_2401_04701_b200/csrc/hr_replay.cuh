@@ -40,14 +40,31 @@ struct hr_pool_smem {
     uint8_t src[32];        /* simulated lane of each pooled record */
 };
 
-/* A pool as seen by the check: 32 record slots and their simulated lanes, in
- * shared memory (a hr_pool_smem, or a staged row of a compacted stream). */
+/* A pool as seen by the check: 32 record slots and their simulated lanes, as
+ * shared-space addresses (a hr_pool_smem, or a staged row of a compacted
+ * stream); 32-bit addresses keep the generic->shared conversion out of the loop. */
 struct hr_entries {
-    const uint64_t *rec;
-    const uint8_t *src;
-    __device__ __forceinline__ hr_entries(const hr_pool_smem &p) : rec(p.rec), src(p.src) {}
-    __device__ __forceinline__ hr_entries(const uint64_t *r, const uint8_t *s) : rec(r), src(s) {}
+    uint32_t rec;               /* 32 x u64 */
+    uint32_t src;               /* 32 x u8 */
+    __device__ __forceinline__ hr_entries(uint32_t r, uint32_t s) : rec(r), src(s) {}
+    __device__ __forceinline__ uint64_t rec_at(uint32_t i) const
+    {
+        uint64_t v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(rec + 8u * i) : "memory");
+        return v;
+    }
+    __device__ __forceinline__ uint32_t src_at(uint32_t i) const { return hr__lds_u8(src + i); }
+    __device__ __forceinline__ void put(uint32_t i, uint64_t x, uint32_t lane) const
+    {
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(rec + 8u * i), "l"(x) : "memory");
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(src + i), "r"(lane) : "memory");
+    }
 };
+
+__device__ __forceinline__ hr_entries hr__pool_at(uint32_t pool_sa)
+{
+    return hr_entries(pool_sa, pool_sa + 32u * 8u);
+}
 
 /* fold + commit of one pooled access group (leader side) */
 __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const hr_thr &t, unsigned long long old,
@@ -56,8 +73,8 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
 {
     const uint32_t base = t.tid() & ~31u;
     const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
-    const uint32_t src0 = ps.src[lane];
-    const uint32_t kind0 = (uint32_t)(ps.rec[lane] >> 62);
+    const uint32_t src0 = ps.src_at(lane);
+    const uint32_t kind0 = (uint32_t)(ps.rec_at(lane) >> 62);
     rel = hr__rel(base | src0, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
     const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
     uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind0 << 4) | (sync << 2) | rel));
@@ -67,8 +84,8 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
     while (r) {
         const uint32_t j = __ffs(r) - 1;
         r &= r - 1;
-        const uint32_t sj = ps.src[j];
-        const uint32_t kj = (uint32_t)(ps.rec[j] >> 62);
+        const uint32_t sj = ps.src_at(j);
+        const uint32_t kj = (uint32_t)(ps.rec_at(j) >> 62);
         const uint32_t rj = sj == prev_src ? 0u : 1u;                 /* Self / Warp, same epochs: Us */
         const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | rj));
         if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
@@ -84,7 +101,7 @@ template <bool ABL>
 __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t, const hr_entries ps, uint32_t n)
 {
     const uint32_t lane = hr__laneid();
-    const uint64_t x = lane < n ? ps.rec[lane] : HR_NOP_REC;
+    const uint64_t x = lane < n ? ps.rec_at(lane) : HR_NOP_REC;
     const uint32_t space = (uint32_t)(x >> 61) & 1u;
     const uint32_t kind = (uint32_t)(x >> 62);
     const uint64_t word = x & HR_WORD_MASK;
@@ -103,7 +120,7 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
         const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
         const uint32_t last = 31u - __clz(peers);
         const unsigned long long nmeta = (t.meta & ~(0x1full << HR_TID_SHIFT)) |
-                                         ((unsigned long long)ps.src[last] << HR_TID_SHIFT);
+                                         ((unsigned long long)ps.src_at(last) << HR_TID_SHIFT);
         uint32_t fresh;
         unsigned long long old = hr__first<ABL>(d, sh, sa, gp, kind, fresh);
         while (true) {
@@ -179,7 +196,7 @@ __device__ __forceinline__ bool hr__pool_owned(const hr_dev &d, const hr_thr &t,
         /* words outside the region go on to hr__locate on every shard, which flags them */
         const uint64_t g = w - d.gbase;
         const bool in = w >= d.gbase && g < d.gwords;
-        v = v && (!in || ((uint32_t)(g >> d.gran_log2) & ((1u << d.shard_log2) - 1u)) == d.shard_rank);
+        v = v && (!in || hr_shard_owner(g >> d.gran_log2, d.shard_log2) == d.shard_rank);
     }
     if (split_log2) v = v && hr__helper_of(w, split_log2) == helper;
     return v;
@@ -240,7 +257,6 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
      * consistent.  Parallelises the long warps of power-law traces. */
     const uint32_t nhw = warps << split_log2;                       /* CUDA warps in the block */
     extern __shared__ __align__(16) unsigned char hr_smem[];
-    hr_pool_smem *pools = reinterpret_cast<hr_pool_smem *>(hr_smem + HR_FSM_SMEM_BYTES);
     unsigned long long *sshadow = reinterpret_cast<unsigned long long *>(
         hr_smem + HR_FSM_SMEM_BYTES + (POOL ? nhw * sizeof(hr_pool_smem) : 0));
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
@@ -266,9 +282,12 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     const bool active = lane < lanes;
     /* rows per warp < 2^32 (180 GB of HBM holds < 2^30 rows) */
     const uint32_t n = (uint32_t)(woff[gw + 1] - r0);
-    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(hr_smem) + stage_off;   /* = hr_stage_offset() */
+    const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(hr_smem);
+    const uint32_t stage = smem0 + stage_off;                       /* = hr_stage_offset() */
     const uint32_t buf0 = stage + hw * NB * CHB;
     const uint32_t bar0 = stage + nhw * NB * CHB + hw * NB * 8u;
+    /* this warp's pool (shared-space address) */
+    const hr_entries ps = hr__pool_at(smem0 + HR_FSM_SMEM_BYTES + hw * (uint32_t)sizeof(hr_pool_smem));
     if (lane == 0) {
 #pragma unroll
         for (uint32_t b = 0; b < NB; b++) hr__mbar_init(bar0 + 8u * b, 1u);
@@ -283,7 +302,27 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     }
     __syncwarp();
 
-    uint32_t cnt = 0;                                                /* warp-uniform pool fill */
+    /* Pool fill (warp-uniform cnt).  A row's owned accesses go to the pool in
+     * lane order; when they overflow it, the first 32 - cnt are checked with the
+     * pool and the rest start the next one.  Lanes of one row are unordered
+     * (same warp, same epochs), so splitting a row between two consecutive pools
+     * keeps every pool in record order: pools stay full except at barriers. */
+    uint32_t cnt = 0;
+    auto insert = [&](bool v, uint64_t x) {
+        const unsigned vm = __ballot_sync(0xffffffffu, v);
+        const uint32_t k = __popc(vm);
+        const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
+        if (v && slot < 32u) ps.put(slot, x, lane);
+        if (cnt + k >= 32u) {
+            __syncwarp();
+            hr__check_pool<ABL>(d, t, ps, 32u);
+            __syncwarp();
+            if (v && slot >= 32u) ps.put(slot - 32u, x, lane);
+            cnt = cnt + k - 32u;
+        } else {
+            cnt += k;
+        }
+    };
     for (uint32_t c = 0; c * CH < n; c++) {
         const uint32_t b = c % NB;
         const uint32_t buf = buf0 + b * CHB;
@@ -292,8 +331,8 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
         uint32_t j0 = 0;
         if (POOL && WIDE) {
             /* whole chunk at once (ILP for the few long warps this kernel runs):
-             * CH independent loads, validity tests and ballots, then the pool
-             * insertion; a chunk holding a barrier row goes row by row below */
+             * CH independent loads and validity tests, then the pool insertion;
+             * a chunk holding a barrier row goes row by row below */
             uint64_t xs[CH];
             bool bar = false;
 #pragma unroll
@@ -302,25 +341,11 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 bar |= (xs[j] >> 62) == 3u && (xs[j] & HR_WORD_MASK) != 0u;
             }
             if (!__any_sync(0xffffffffu, bar)) {
-                unsigned vms[CH];
+                bool vs[CH];
 #pragma unroll
-                for (uint32_t j = 0; j < CH; j++)
-                    vms[j] = __ballot_sync(0xffffffffu, hr__pool_owned(d, t, xs[j], split_log2, helper));
-                hr_pool_smem &ps = pools[hw];
+                for (uint32_t j = 0; j < CH; j++) vs[j] = hr__pool_owned(d, t, xs[j], split_log2, helper);
 #pragma unroll
-                for (uint32_t j = 0; j < CH; j++) {
-                    const unsigned vm = vms[j];
-                    const uint32_t k = __popc(vm);
-                    if (k == 0) continue;
-                    if (cnt + k > 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); cnt = 0; __syncwarp(); }
-                    if ((vm >> lane) & 1u) {
-                        const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
-                        ps.rec[slot] = xs[j];
-                        ps.src[slot] = (uint8_t)lane;
-                    }
-                    cnt += k;
-                    if (cnt == 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, 32u); cnt = 0; __syncwarp(); }
-                }
+                for (uint32_t j = 0; j < CH; j++) insert(vs[j], xs[j]);
                 j0 = rows;
             }
         }
@@ -329,7 +354,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
             const uint32_t op = (uint32_t)(x >> 62);
             const uint64_t w = x & HR_WORD_MASK;
             if (__any_sync(0xffffffffu, op == 3u && w != 0u)) {      /* barrier row: flush, then sync */
-                if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[hw], cnt); cnt = 0; __syncwarp(); }
+                if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); cnt = 0; __syncwarp(); }
                 hr__barrier_row(d, t, x, lane_mask);
                 continue;
             }
@@ -337,19 +362,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 hr_check_lanes<false, ABL>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
                 continue;
             }
-            hr_pool_smem &ps = pools[hw];
-            const bool v = hr__pool_owned(d, t, x, split_log2, helper);
-            const unsigned vm = __ballot_sync(0xffffffffu, v);
-            const uint32_t k = __popc(vm);
-            if (k == 0) continue;
-            if (cnt + k > 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); cnt = 0; __syncwarp(); }
-            if (v) {
-                const uint32_t slot = cnt + __popc(vm & ((1u << lane) - 1u));
-                ps.rec[slot] = x;
-                ps.src[slot] = (uint8_t)lane;
-            }
-            cnt += k;
-            if (cnt == 32u) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, 32u); cnt = 0; __syncwarp(); }
+            insert(hr__pool_owned(d, t, x, split_log2, helper), x);
         }
         __syncwarp();                                                /* buffer b fully read: refill it */
         if (lane == 0 && (c + NB) * CH < n) {
@@ -358,7 +371,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
             src.bulk(buf, r0 + (c + NB) * CH, rows2, CH, bar0 + 8u * b);
         }
     }
-    if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, pools[hw], cnt); __syncwarp(); }
+    if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); __syncwarp(); }
 }
 
 /* Probe for the kernel choice (one block): out[0..1] = access records / records
@@ -417,7 +430,8 @@ __global__ void hr_scan_kernel(const unsigned long long *__restrict__ sh, uint64
             uint32_t slot = atomicAdd(count, 1u);
             if (slot < cap) {
                 uint64_t gran_local = i >> gran_log2;
-                uint64_t g = (((gran_local << shard_log2) | shard_rank) << gran_log2) | (i & ((1ull << gran_log2) - 1u));
+                uint64_t g = (hr_shard_granule(gran_local, shard_rank, shard_log2) << gran_log2) |
+                             (i & ((1ull << gran_log2) - 1u));
                 hr_race r;
                 r.word = gbase + g;
                 r.block = 0xffffffffu;

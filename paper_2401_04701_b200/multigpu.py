@@ -2,8 +2,10 @@
 
 Accesses to different words are independent FSMs (the shadow is per word,
 PAPER.md:395-396; no transition reads another word), so rank r of N owns the
-4 KiB shadow granules with ((word - base) >> 9) % N == r and the shared
-instances of simulated blocks with block % N == r.  Each rank replays every
+shadow granules g = (word - base) >> 9 (4 KiB of shadow) with
+shard_owner(g) == r (include/hr.h hr_shard_owner: stripes of N granules, one
+per rank, rotated per stripe) and the shared instances of simulated blocks
+with block % N == r.  Each rank replays every
 simulated thread but only its own records, keeping all barrier records so the
 per-word commit order stays happens-before consistent; its shadow is 1/N.
 The ONE exchange is the race-set allgather (NCCL over NVLink on GPUs, gloo
@@ -25,6 +27,22 @@ RACE_DTYPE = np.dtype([("word", "<u8"), ("block", "<u4"), ("kernel", "<u4"), ("f
 NOP = np.uint64(3 << 62)
 
 
+def shard_owner(granule, nshard: int):
+    """include/hr.h hr_shard_owner on numpy uint64 granule indices (or an int):
+    granule g of stripe s = g >> log2(N) goes to (g + rot(s)) mod N, where
+    rot(s) = ((s ^ s >> 32) mod 2^32 * 0x9E3779B1 mod 2^32) >> (32 - log2(N))."""
+    l2 = nshard.bit_length() - 1
+    assert nshard == 1 << l2, "shard count must be a power of two"
+    if l2 == 0:
+        return np.zeros_like(np.asarray(granule, dtype=np.uint64)) if not np.isscalar(granule) else 0
+    g = np.asarray(granule, dtype=np.uint64)
+    s = g >> np.uint64(l2)
+    m32 = np.uint64(0xFFFFFFFF)
+    rot = ((((s ^ (s >> np.uint64(32))) & m32) * np.uint64(0x9E3779B1)) & m32) >> np.uint64(32 - l2)
+    own = ((g & m32) + rot) & np.uint64(nshard - 1)
+    return int(own) if np.isscalar(granule) else own
+
+
 def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: int = 0,
                granule_log2: int = 9) -> np.ndarray:
     """Which records of one warp's rows (n, 32) belong to shard `rank`."""
@@ -32,7 +50,7 @@ def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: 
     space = (rows >> np.uint64(61)) & np.uint64(1)
     word = rows & np.uint64((1 << 61) - 1)
     gran = (word - np.uint64(base_word)) >> np.uint64(granule_log2)
-    glob = (op != 3) & (space == 0) & ((gran % np.uint64(nshard)) == np.uint64(rank))
+    glob = (op != 3) & (space == 0) & (shard_owner(gran, nshard) == np.uint64(rank))
     shared = (op != 3) & (space == 1) & ((block % nshard) == rank)
     return glob | shared
 

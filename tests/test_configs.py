@@ -5,6 +5,7 @@ import pytest
 
 import oracle
 from tracegen import c5, stencil, suite
+from paper_2401_04701_b200.multigpu import shard_owner
 
 
 @pytest.fixture(scope="module")
@@ -60,7 +61,7 @@ def test_c5_racy_set_is_planted(lb):
     assert abs(frac[0] - 0.70) < 0.03 and abs(frac[1] - 0.20) < 0.03 and abs(frac[2] - 0.10) < 0.02
 
 
-@pytest.mark.parametrize("n,g", [(2, 9), (4, 9), (8, 9), (8, 5), (4, 12)])
+@pytest.mark.parametrize("n,g", [(2, 9), (4, 9), (8, 9), (8, 5), (8, 0), (4, 3), (4, 12)])
 def test_c5_shards_partition_the_racy_set(n, g):
     lb = 4
     full = [(r.word, r.scope) for r in oracle.check(c5.cpu_trace(lb)).races]
@@ -68,6 +69,25 @@ def test_c5_shards_partition_the_racy_set(n, g):
     for r in range(n):
         sh = c5.cpu_trace(lb, rank=r, nshard=n, granule_log2=g)
         got = oracle.check(sh).races
-        assert all(((x.word >> g) % n) == r for x in got)
+        assert all(shard_owner(x.word >> g, n) == r for x in got)
         union += [(x.word, x.scope) for x in got]
     assert sorted(union) == full
+
+
+@pytest.mark.parametrize("n,g", [(8, 9), (8, 5), (4, 0)])
+def test_c5_shard_records_follow_the_owner_function(n, g):
+    """The C generator's partition (tracegen/c5gen.h) is hr_shard_owner: every
+    access record of shard r has its granule owned by r, the shards together
+    hold every access of the full trace, and no rank is starved (the stripe
+    rotation spreads a block's warps over the ranks)."""
+    lb = 3
+    full = c5.cpu_trace(lb)
+    fw = full.rec[(full.rec >> np.uint64(62)) != 3] & np.uint64((1 << 61) - 1)
+    counts = []
+    for r in range(n):
+        sh = c5.cpu_trace(lb, rank=r, nshard=n, granule_log2=g)
+        acc = sh.rec[(sh.rec >> np.uint64(62)) != 3] & np.uint64((1 << 61) - 1)
+        assert np.all(shard_owner(acc >> np.uint64(g), n) == r)
+        counts.append(len(acc))
+    assert sum(counts) == len(fw)
+    assert min(counts) > 0.6 * len(fw) / n

@@ -174,7 +174,7 @@ def test_shard_emulation_union_equals_single():
                        spaces=(0, 1))
     gmax, smem = h.trace_extent(tr)
     full, _ = gpu_set(tr)
-    for n, g in ((2, 9), (4, 9), (8, 9), (8, 5), (4, 6)):
+    for n, g in ((2, 9), (4, 9), (8, 9), (8, 5), (4, 6), (8, 0), (4, 3)):
         union = []
         for r in range(n):
             ck = h.Checker(gmax, smem, shard=(r, n), granule_log2=g)
@@ -182,6 +182,29 @@ def test_shard_emulation_union_equals_single():
             races, _, _ = ck.report()
             ck.close()
             union += [tuple(x) for x in races]
+        assert sorted(union) == full
+
+
+def test_shard_ring_overflow_scan():
+    """A shard whose race ring overflows falls back to the shadow scan of its
+    (single) kernel, which maps local granules back through the owner
+    function's inverse (hr_shard_granule): the union over shards still equals
+    the oracle's set."""
+    h = hr()
+    tr = tp.listing2(8, 8, 32)                       # one kernel, many racy global words
+    gmax, smem = h.trace_extent(tr)
+    full, _ = oracle_set(tr)
+    assert len(full) > 64
+    for n, g in ((4, 9), (8, 0), (2, 5), (4, 3)):
+        union, ov = [], 0
+        for r in range(n):
+            ck = h.Checker(gmax, smem, shard=(r, n), granule_log2=g, ring_capacity=4)
+            ck.replay(h.DeviceTrace.from_trace(tr))
+            races, fl, _ = ck.report()
+            ck.close()
+            ov |= fl & h.HR_F_RING_OVERFLOW
+            union += [tuple(x) for x in races]
+        assert ov
         assert sorted(union) == full
 
 

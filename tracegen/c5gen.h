@@ -24,7 +24,7 @@
  *
  * Row layout per warp: 8 epochs x (32 access rows, 1 __syncthreads row) = 264
  * rows.  Sharded variant (rank r of N = 2^log2n): a lane keeps only records
- * whose shadow granule (word >> glog2; 9 = 4 KiB of shadow) is owned by r (granule mod N), kept
+ * whose shadow granule (word >> glog2; 9 = 4 KiB of shadow) is owned by r (hr_shard_owner), kept
  * records are compacted per lane inside each epoch, epoch segments are padded
  * with NOPs to the warp's longest lane, barrier rows are kept.
  */
@@ -136,10 +136,14 @@ C5_HD uint64_t c5_record(const c5_params *p, uint64_t b, uint32_t t, uint32_t j)
     return (2ull << 62) | (total - (1ull << hl) + rank);   /* atomic */
 }
 
+/* shard owner of a record's granule: include/hr.h hr_shard_owner (stripes of
+ * 2^log2n granules, rotated per stripe by a multiplicative hash) */
 C5_HD int c5_owned_by(uint64_t rec, uint32_t rank, uint32_t log2n, uint32_t glog2)
 {
-    uint64_t word = rec & ((1ull << 61) - 1);
-    return (uint32_t)((word >> glog2) & ((1ull << log2n) - 1)) == rank;
+    const uint64_t gran = (rec & ((1ull << 61) - 1)) >> glog2;
+    const uint64_t stripe = gran >> log2n;
+    const uint32_t rot = log2n ? ((uint32_t)(stripe ^ (stripe >> 32)) * 0x9E3779B1u) >> (32u - log2n) : 0u;
+    return (((uint32_t)gran + rot) & ((1u << log2n) - 1u)) == rank;
 }
 
 #endif /* C5GEN_H_ */
