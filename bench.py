@@ -57,8 +57,8 @@ def parse():
     ap.add_argument("--emulate-shard", default=None,
                     help="R/N: replay only address shard R of N on this one GPU (scaling projection; "
                          "shards share nothing but the final allgather)")
-    ap.add_argument("--granule-log2", type=int, default=9,
-                    help="address-shard granule (2^g words; 9 = 4 KiB of shadow)")
+    ap.add_argument("--granule-log2", type=int, default=3,
+                    help="address-shard granule (2^g words; 3 = 64 B of shadow)")
     ap.add_argument("--double-shadow", action="store_true",
                     help="HR_OPT_DOUBLE_SHADOW: reset the previous kernel's shadow on a side stream")
     ap.add_argument("--format", default="u64", choices=["c32", "u64"],

@@ -183,7 +183,8 @@ hr_status hr_init(const hr_config *cfg, hr_ctx **out);
 hr_status hr_set_shard(hr_ctx *ctx, uint32_t rank, uint32_t count);
 
 /* Same with a shard granule of 2^granule_log2 words (0..24; hr_set_shard uses
- * 9 = 4 KiB of shadow).  Smaller granules spread power-law hot words over
+ * 3 = 8 words, 64 B of shadow: on C5 it balances the Zipf-hot atomic words
+ * best; 9 = 4 KiB leaves the hottest granule's rank 1.2x slower at N = 8).  Smaller granules spread power-law hot words over
  * more ranks; the rotation keeps a block's warps from landing on one rank
  * when a granule is a warp row (granule_log2 5). */
 hr_status hr_set_shard_ex(hr_ctx *ctx, uint32_t rank, uint32_t count, uint32_t granule_log2);

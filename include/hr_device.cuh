@@ -61,7 +61,7 @@ struct hr_dev {
     uint32_t ring_cap;
     uint32_t kernel_id;
     uint32_t shard_rank, shard_log2; /* owner(granule) = hr_shard_owner(granule, shard_log2) (hr.h) */
-    uint32_t gran_log2;           /* shard granule = 2^gran_log2 words (default 9: 4 KiB of shadow) */
+    uint32_t gran_log2;           /* shard granule = 2^gran_log2 words (default 3: 64 B of shadow) */
     uint32_t wc_bits;             /* bc occupies [31:wc_bits], wc [wc_bits-1:0] */
     uint32_t bc_max, wc_max;
     uint32_t options;             /* HR_OPT_* */

@@ -148,8 +148,11 @@ __global__ void __launch_bounds__(256) hr_cmp_walk_kernel(hr_dev d, SRC src, con
  * CUDA warps; CUDA warp hw replays stream (hw % warps, hw / warps).  Each
  * packed row is either a verbatim barrier row or one pool of up to 32 accesses
  * in record order (NOP-padded at the end). */
+#ifndef HR_CMP_MINB
+#define HR_CMP_MINB 1
+#endif
 template <bool ABL>
-__global__ void __launch_bounds__(1024, 1) hr_replay_compact_kernel(hr_dev d, hr_src_cmp src,
+__global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr_dev d, hr_src_cmp src,
                                                                     const uint64_t *__restrict__ segoff,
                                                                     const uint64_t *__restrict__ rowoff,
                                                                     uint32_t warps, uint32_t lanes,

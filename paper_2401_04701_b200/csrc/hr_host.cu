@@ -32,7 +32,7 @@
 struct hr_ctx {
     int device = 0;
     hr_config cfg{};
-    uint32_t shard_rank = 0, shard_count = 1, shard_log2 = 0, gran_log2 = 9;
+    uint32_t shard_rank = 0, shard_count = 1, shard_log2 = 0, gran_log2 = 3;
     unsigned long long *gshadow = nullptr;       /* current buffer */
     unsigned long long *gbuf[2] = {nullptr, nullptr};
     int gcur = 0;
@@ -191,7 +191,7 @@ extern "C" hr_status hr_set_shard_ex(hr_ctx *c, uint32_t rank, uint32_t count, u
 
 extern "C" hr_status hr_set_shard(hr_ctx *c, uint32_t rank, uint32_t count)
 {
-    return hr_set_shard_ex(c, rank, count, 9);
+    return hr_set_shard_ex(c, rank, count, 3);
 }
 
 extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_word, uint64_t n_words,
@@ -212,7 +212,7 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
     for (int b = 0; b < 2; b++)
         if (c->gbuf[b]) { cudaFree(c->gbuf[b]); c->gbuf[b] = nullptr; }
     c->gshadow = nullptr;
-    /* local slice: this shard's 512-word granules, packed */
+    /* local slice: this shard's granules, packed in stripe order */
     uint64_t gran = (n_words + (1ull << c->gran_log2) - 1) >> c->gran_log2;
     uint64_t local_gran = (gran + c->shard_count - 1) >> c->shard_log2;
     uint64_t local = local_gran << c->gran_log2;

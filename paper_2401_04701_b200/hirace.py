@@ -131,7 +131,7 @@ def hr_init(bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, 
     return ctx
 
 
-def hr_set_shard(ctx, rank: int, count: int, granule_log2: int = 9):
+def hr_set_shard(ctx, rank: int, count: int, granule_log2: int = 3):
     _check(load().hr_set_shard_ex(ctx, rank, count, granule_log2), ctx, "hr_set_shard_ex")
 
 
@@ -402,7 +402,7 @@ class Checker:
 
     def __init__(self, global_words: int, smem_words: int = 0, base_word: int = 0, device: int = 0,
                  bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, options: int = 0,
-                 shard: Optional[Tuple[int, int]] = None, granule_log2: int = 9):
+                 shard: Optional[Tuple[int, int]] = None, granule_log2: int = 3):
         self.ctx = hr_init(bc_bits, wc_bits, ring_capacity, device, options)
         if shard is not None:
             hr_set_shard(self.ctx, shard[0], shard[1], granule_log2)

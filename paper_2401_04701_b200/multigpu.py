@@ -2,7 +2,7 @@
 
 Accesses to different words are independent FSMs (the shadow is per word,
 PAPER.md:395-396; no transition reads another word), so rank r of N owns the
-shadow granules g = (word - base) >> 9 (4 KiB of shadow) with
+shadow granules g = (word - base) >> 3 (8 words, 64 B of shadow) with
 shard_owner(g) == r (include/hr.h hr_shard_owner: stripes of N granules, one
 per rank, rotated per stripe) and the shared instances of simulated blocks
 with block % N == r.  Each rank replays every
@@ -44,7 +44,7 @@ def shard_owner(granule, nshard: int):
 
 
 def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: int = 0,
-               granule_log2: int = 9) -> np.ndarray:
+               granule_log2: int = 3) -> np.ndarray:
     """Which records of one warp's rows (n, 32) belong to shard `rank`."""
     op = rows >> np.uint64(62)
     space = (rows >> np.uint64(61)) & np.uint64(1)
@@ -55,7 +55,7 @@ def owner_mask(rows: np.ndarray, block: int, rank: int, nshard: int, base_word: 
     return glob | shared
 
 
-def shard_trace(trace, rank: int, nshard: int, base_word: int = 0, granule_log2: int = 9):
+def shard_trace(trace, rank: int, nshard: int, base_word: int = 0, granule_log2: int = 3):
     """Host-side shard of a trace: this rank's records compacted per lane inside
     each barrier-delimited segment, padded with NOPs, barrier rows kept."""
     from tracegen.format import Trace   # layout container only

@@ -18,6 +18,7 @@ def declared_functions():
     for h in ("hr.h", "hr_bench.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        src = re.sub(r"HR_HD[^{;]*\{.*?\n\}", "", src, flags=re.S)     # header-inline helpers, not exports
         names |= set(re.findall(r"\b(hrb?_[a-z_0-9]+)\s*\(", src))
     return sorted(names)
 
@@ -93,3 +94,37 @@ def test_merge_races_host_only():
     want = sorted(keys.items())
     assert [((int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"])), int(r["scope"])) for r in got] == want
     assert len(hirace.hr_merge_races(parts[:0])) == 0
+
+
+def test_header_shard_owner_matches_python(tmp_path):
+    """include/hr.h's inline hr_shard_owner / hr_shard_granule (compiled by
+    gcc here) == multigpu.shard_owner, and hr_shard_granule inverts it."""
+    import subprocess
+    import numpy as np
+    from paper_2401_04701_b200.multigpu import shard_owner
+    c = tmp_path / "own.c"
+    c.write_text("""#include <stdio.h>
+#include "hr.h"
+int main(void) {
+    for (unsigned l = 0; l <= 3; l++)
+        for (unsigned long long g = 0; g < 4096; g += 7) {
+            unsigned o = hr_shard_owner(g * 977ull + (g << 33), l);
+            unsigned long long back = hr_shard_granule((g * 977ull + (g << 33)) >> l, o, l);
+            printf("%u %llu %u %d\\n", l, g, o, back == g * 977ull + (g << 33));
+        }
+    return 0;
+}
+""")
+    exe = tmp_path / "own"
+    subprocess.run(["gcc", "-O1", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    n = 0
+    for line in out:
+        if not line:
+            continue
+        l, g, o, inv = (int(x) for x in line.split())
+        gran = g * 977 + (g << 33)
+        assert inv == 1
+        assert shard_owner(np.uint64(gran), 1 << l) == o
+        n += 1
+    assert n == 4 * len(range(0, 4096, 7))

@@ -42,7 +42,7 @@ def _worker(rank, world, port, path, out_dir):
     # every local race is owned by this rank
     for r in res.races:
         if r.space == 0:
-            assert multigpu.shard_owner(r.word >> 9, world) == rank
+            assert multigpu.shard_owner(r.word >> 3, world) == rank
         else:
             assert r.block % world == rank
     merged, flags = multigpu.exchange_races(_to_raw(res.races), res.flags)

@@ -90,7 +90,7 @@ def kdesc(lb: int) -> np.ndarray:
     return np.array([[1 << lb, WARPS, LANES, 0, 0, 0, 0, 0]], dtype=np.uint64)
 
 
-def cpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, granule_log2: int = 9) -> Trace:
+def cpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, granule_log2: int = 3) -> Trace:
     """The (shard of the) C5 trace as host arrays."""
     lib = _cpu_lib()
     p = Params(seed, lb)
@@ -130,7 +130,7 @@ def _gpu_offsets(lib, lb, seed, rank, l2, g2, device, stream):
 
 
 def gpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda",
-              granule_log2: int = 9):
+              granule_log2: int = 3):
     """Generate the (shard of the) trace directly in HBM, u64 records.
     Returns (rec int64 tensor, warp_off int64 tensor, kdesc numpy)."""
     import torch
@@ -146,7 +146,7 @@ def gpu_trace(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1,
 
 
 def gpu_trace_c32(lb: int, seed: int = DEFAULT_SEED, rank: int = 0, nshard: int = 1, device: str = "cuda",
-                  granule_log2: int = 9):
+                  granule_log2: int = 3):
     """Same trace in the HR_TRACE_C32 encoding (160 B per row).  Returns
     (rec32 int32, recop uint8, warp_off int64) tensors and kdesc."""
     import torch

@@ -24,7 +24,7 @@
  *
  * Row layout per warp: 8 epochs x (32 access rows, 1 __syncthreads row) = 264
  * rows.  Sharded variant (rank r of N = 2^log2n): a lane keeps only records
- * whose shadow granule (word >> glog2; 9 = 4 KiB of shadow) is owned by r (hr_shard_owner), kept
+ * whose shadow granule (word >> glog2; default 3 = 64 B of shadow) is owned by r (hr_shard_owner), kept
  * records are compacted per lane inside each epoch, epoch segments are padded
  * with NOPs to the warp's longest lane, barrier rows are kept.
  */
