@@ -82,8 +82,11 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line).
+    The sampler is started before the warm-up (its NVML start-up can stall CUDA
+    calls for tens of ms) and only samples stamped inside [mark_start, mark_stop]
+    are kept."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -91,6 +94,7 @@ class Clocks:
         self.idx = gpu_index
         self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
         self.p = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -99,6 +103,12 @@ class Clocks:
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
 
     def stop(self):
         if self.p is None:
@@ -111,18 +121,25 @@ class Clocks:
             self.p.kill()
         self.f.flush()
         self.f.seek(0)
+        import datetime
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().splitlines():
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if ts is not None and self.t0 is not None and not (self.t0 - 0.05 <= ts <= (self.t1 or ts) + 0.05):
+                continue
+            try:
+                sm.append(float(parts[2]))
+                smax.append(float(parts[3]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[5:9]):
+            for n, v in zip(names, parts[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         os.unlink(self.f.name)
@@ -345,6 +362,9 @@ def main():
 
     dev_replay = lambda: ck.replay(dt, stream)  # noqa: E731
 
+    # clock sampler first: its start-up must not land in the timed region
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
     # warm-up + correctness of this run against the closed form (planted set)
     for _ in range(max(args.warmup, 1)):
         raw, flags = step(dev_replay)
@@ -362,11 +382,13 @@ def main():
     # pass over them inside a host-side report step costs ~10 ms at random
     gc.collect()
     gc.freeze()
+    step(dev_replay)                                # one more warm step after the pause
+    hr.hr_replay_timing(ck.ctx)
+    hr.hr_launch_count(ck.ctx)
 
-    clocks = Clocks(torch.cuda.current_device())
     barrier(world)
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark_start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -374,6 +396,7 @@ def main():
         raw, flags = step(dev_replay)
     e1.record()
     torch.cuda.synchronize()
+    clocks.mark_stop()
     barrier(world)
     clk = clocks.stop()
     ms_total = e0.elapsed_time(e1)

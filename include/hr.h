@@ -72,7 +72,8 @@ enum {
     HR_OPT_NO_COALESCE = 1u,   /* disable same-address lane coalescing (a3), for ablations */
     HR_OPT_NO_FASTEXIT = 2u,   /* disable label-insensitive fast exits (a7), for ablations */
     HR_OPT_TIMING = 4u,        /* record CUDA events around every shadow reset and replay launch */
-    HR_OPT_NO_SPECULATE = 8u,  /* first attempt loads the shadow word instead of speculating INIT */
+    HR_OPT_NO_SPECULATE = 8u,  /* accepted, no effect: loading the shadow word first is the default
+                                  (HR_OPT_SPECULATE below is the ablation) */
     HR_OPT_NO_POOL = 16u,      /* replay row by row (default: chosen from sampled record density,
                                   shared share and warp-length tail, see hr_host.cu kernel_choice) */
     HR_OPT_POOL = 32u,         /* replay with warp pools of valid accesses (sparse traces) */
@@ -84,8 +85,18 @@ enum {
     HR_OPT_POOL_WIDE = 256u,     /* force the 64-register pooled kernel (few very long warps) */
     HR_OPT_ROW_WIDE = 512u,      /* force the 64-register row kernel (chosen by default for
                                     shared-shadow heavy traces and small grids) */
-    HR_OPT_NO_COMPACT = 1024u    /* long-tailed grids: replay the rows as they are instead of
+    HR_OPT_NO_COMPACT = 1024u,   /* long-tailed grids: replay the rows as they are instead of
                                     packing each long warp's accesses first (hr_compact.cuh) */
+    HR_OPT_SMEM32 = 4096u,       /* 32-bit shared-shadow words with the block implicit (SURVEY
+                                    §8(f)-4, "configurable and can be reduced"): state 5 |
+                                    warp 5 | lane 5 | bc 9 | wc 8.  Halves the SMEM shadow; caps
+                                    the block / warp clocks at 511 / 255 (past them a thread stops
+                                    checking and HR_F_CLOCK_OVERFLOW is latched).  Not with
+                                    HR_OPT_FINITE_HISTORY. */
+    HR_OPT_SPECULATE = 2048u     /* ablation: global reads/writes skip Algorithm 1's first atomic read
+                                    and CAS against INIT (the CAS return is the read when it fails).
+                                    Measured slower: a failed CAS costs an L2 atomic round trip that
+                                    a load followed by an unchanged-word exit does not */
 };
 
 /* One unique racy address.  24 bytes.

@@ -134,6 +134,26 @@ __device__ __forceinline__ unsigned long long hr__cas_s(uint32_t a, unsigned lon
     return r;
 }
 
+/* HR_OPT_SMEM32 shared-shadow words: state 5 | warp 5 | lane 5 | bc 9 | wc 8;
+ * the block is implicit (one instance per block).  Converted to and from the
+ * 64-bit layout at the SMEM boundary, so Algorithm 1 itself is unchanged;
+ * exact while bc <= 511 and wc <= 255 (make_dev caps the clocks there). */
+#define HR_S32_STATE_SHIFT 27
+__device__ __forceinline__ uint32_t hr__s32_pack(unsigned long long w, uint32_t wc_bits)
+{
+    const uint32_t lo = (uint32_t)w;
+    return ((uint32_t)(w >> HR_STATE_SHIFT) << HR_S32_STATE_SHIFT) | (((uint32_t)(w >> HR_TID_SHIFT) & 1023u) << 17) |
+           ((lo >> wc_bits) << 8) | (lo & ((1u << wc_bits) - 1u));
+}
+
+__device__ __forceinline__ unsigned long long hr__s32_unpack(uint32_t v, uint32_t own_tid, uint32_t wc_bits)
+{
+    if (v == 0u) return 0ull;                                           /* INIT */
+    const uint32_t tid = (own_tid & ~1023u) | ((v >> 17) & 1023u);
+    return ((unsigned long long)(v >> HR_S32_STATE_SHIFT) << HR_STATE_SHIFT) |
+           ((unsigned long long)tid << HR_TID_SHIFT) | ((((v >> 8) & 511u) << wc_bits) | (v & 255u));
+}
+
 __device__ __forceinline__ uint32_t hr__lds_u8(uint32_t a)
 {
     uint32_t v;
@@ -176,7 +196,7 @@ __device__ __forceinline__ void hr__set_flag(const hr_dev &d, unsigned int f)
 
 /* ---------------- the check core ---------------- */
 
-/* Ablation options (HR_OPT_NO_COALESCE / NO_FASTEXIT / NO_SPECULATE) are read
+/* Ablation options (HR_OPT_NO_COALESCE / NO_FASTEXIT / SPECULATE) are read
  * only when ABL: the default replay kernels are instantiated with ABL = false
  * and carry no option tests on the per-access path. */
 template <bool ABL>
@@ -201,6 +221,35 @@ __device__ __forceinline__ unsigned long long hr__ld_g_l1(const unsigned long lo
 #define HR_OLD_GUESS 0u
 #define HR_OLD_PROBE 1u
 #define HR_OLD_FRESH 2u
+
+/* Shared shadow word of this block's instance: load / CAS in the 64-bit layout. */
+__device__ __forceinline__ uint32_t hr__saddr(const hr_dev &d, const hr_thr &t, uint64_t local)
+{
+    return t.sshadow + ((uint32_t)local << ((d.options & HR_OPT_SMEM32) ? 2 : 3));
+}
+
+__device__ __forceinline__ unsigned long long hr__ld_sh(const hr_dev &d, const hr_thr &t, uint32_t a)
+{
+    if (d.options & HR_OPT_SMEM32) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return hr__s32_unpack(v, t.tid(), d.wc_bits);
+    }
+    return hr__ld_s(a);
+}
+
+__device__ __forceinline__ unsigned long long hr__cas_sh(const hr_dev &d, const hr_thr &t, uint32_t a,
+                                                         unsigned long long cmp, unsigned long long val)
+{
+    if (d.options & HR_OPT_SMEM32) {
+        const uint32_t c = hr__s32_pack(cmp, d.wc_bits), v = hr__s32_pack(val, d.wc_bits);
+        uint32_t r;
+        HR_JITTER();
+        asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(r) : "r"(a), "r"(c), "r"(v) : "memory");
+        return r == c ? cmp : hr__s32_unpack(r, t.tid(), d.wc_bits);
+    }
+    return hr__cas_s(a, cmp, val);
+}
 
 /* a2: shard-local shadow index; false if this ctx does not check the access. */
 __device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uint32_t space, uint64_t word,
@@ -294,7 +343,7 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
             if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
             if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
         }
-        const unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+        const unsigned long long prev = is_shared ? hr__cas_sh(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
         if (prev == old) {                                                /* a8 committed */
             if (cur >= HR_RACE_BLOCK && cur != os)
                 return HR_EI_EMIT | (hr__laneid() << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID);
@@ -330,7 +379,7 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
             if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
             if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
         }
-        const unsigned long long prev = is_shared ? hr__cas_s(sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+        const unsigned long long prev = is_shared ? hr__cas_sh(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
         if (prev == old)                                                  /* a8 committed */
             return rinfo ? (rinfo | (cur == HR_RACE_GRID ? 1u : 0u)) : 0u;
         old = prev;
@@ -342,17 +391,18 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
 }
 
 /* First value of Algorithm 1's loop (a4): SMEM load; L1 probe for global
- * atomics; INIT guess for global reads/writes (the CAS then doubles as the
- * atomic read); a coherent load with HR_OPT_NO_SPECULATE. */
+ * atomics; a coherent L2 load (ld.relaxed.gpu) for global reads/writes, or
+ * with HR_OPT_SPECULATE an INIT guess (the CAS then doubles as the atomic read). */
 template <bool ABL>
-__device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, bool is_shared, uint32_t sh_addr,
-                                                        const unsigned long long *gp, uint32_t kind, uint32_t &fresh)
+__device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, const hr_thr &t, bool is_shared,
+                                                        uint32_t sh_addr, const unsigned long long *gp, uint32_t kind,
+                                                        uint32_t &fresh)
 {
-    if (is_shared) { fresh = HR_OLD_FRESH; return hr__ld_s(sh_addr); }
+    if (is_shared) { fresh = HR_OLD_FRESH; return hr__ld_sh(d, t, sh_addr); }
     if (kind == HR_ATOMIC && !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT)) { fresh = HR_OLD_PROBE; return hr__ld_g_l1(gp); }
-    if (hr__opt<ABL>(d, HR_OPT_NO_SPECULATE)) { fresh = HR_OLD_FRESH; return hr__ld_g(gp); }
-    fresh = HR_OLD_GUESS;
-    return 0ull;
+    if (hr__opt<ABL>(d, HR_OPT_SPECULATE)) { fresh = HR_OLD_GUESS; return 0ull; }
+    fresh = HR_OLD_FRESH;
+    return hr__ld_g(gp);
 }
 
 __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t, uint32_t slot, uint32_t space,
@@ -422,10 +472,10 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
 
     uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
-        const uint32_t sh_addr = t.sshadow + (uint32_t)(local << 3);
+        const uint32_t sh_addr = hr__saddr(d, t, local);
         unsigned long long *gp = d.gshadow + local;
         uint32_t fresh;
-        const unsigned long long old = hr__first<ABL>(d, is_shared, sh_addr, gp, kind, fresh);
+        const unsigned long long old = hr__first<ABL>(d, t, is_shared, sh_addr, gp, kind, fresh);
         ei = (peers == (1u << lane)) ? hr__commit_single<ABL>(d, t, is_shared, sh_addr, gp, old, fresh, kind)
                                      : hr__commit<ABL>(d, t, is_shared, sh_addr, gp, old, fresh, kind, lane, peers, kb0, kb1);
     }
@@ -454,7 +504,8 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     const uint4 *src = reinterpret_cast<const uint4 *>(d.fsm);
     uint4 *dst = reinterpret_cast<uint4 *>(smem_fsm);
     for (uint32_t i = ltid; i < HR_FSM_SMEM_BYTES / 16; i += nthr) dst[i] = src[i];
-    for (uint32_t i = ltid; i < smem_words; i += nthr) smem_shadow[i] = 0ull;
+    const uint32_t n64 = (d.options & HR_OPT_SMEM32) ? (smem_words + 1u) / 2u : smem_words;
+    for (uint32_t i = ltid; i < n64; i += nthr) smem_shadow[i] = 0ull;
     __syncthreads();
     hr_thr t;
     uint32_t block = d.block_base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);

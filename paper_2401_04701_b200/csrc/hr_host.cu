@@ -102,6 +102,12 @@ static hr_status fail(hr_ctx *c, hr_status s, const char *fmt, ...)
                         __LINE__);                                                            \
     } while (0)
 
+/* shared-shadow size of a replay block in 8-byte units (hr_stage_offset) */
+static uint32_t smem_u64(const hr_ctx *c, uint64_t smem_words)
+{
+    return (c->cfg.options & HR_OPT_SMEM32) ? (uint32_t)((smem_words + 1) / 2) : (uint32_t)smem_words;
+}
+
 static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
 {
     hr_dev d;
@@ -123,6 +129,10 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.bc_max = (1u << c->cfg.bc_bits) - 1u;
     d.wc_max = (1u << c->cfg.wc_bits) - 1u;
     d.options = c->cfg.options;
+    if (d.options & HR_OPT_SMEM32) {            /* the 32-bit shared word holds bc:9, wc:8 */
+        d.bc_max = std::min(d.bc_max, 511u);
+        d.wc_max = std::min(d.wc_max, 255u);
+    }
     return d;
 }
 
@@ -140,7 +150,8 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
     def.options = 0;
     const hr_config &k = cfg ? *cfg : def;
     if (k.state_bits != 5 || k.tid_bits != 27 || k.bc_bits < 1 || k.wc_bits < 1 ||
-        k.bc_bits + k.wc_bits != 32 || k.ring_capacity < 1)
+        k.bc_bits + k.wc_bits != 32 || k.ring_capacity < 1 ||
+        ((k.options & HR_OPT_SMEM32) && (k.options & HR_OPT_FINITE_HISTORY)))
         return HR_E_ARG;
     hr_ctx *c = new (std::nothrow) hr_ctx;
     if (!c) return HR_E_NOMEM;
@@ -200,7 +211,7 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     if (space == HR_SHARED) {
-        const uint64_t per = (c->cfg.options & HR_OPT_FINITE_HISTORY) ? 16 : 8;
+        const uint64_t per = (c->cfg.options & HR_OPT_FINITE_HISTORY) ? 16 : (c->cfg.options & HR_OPT_SMEM32) ? 4 : 8;
         if (base_word != 0 || n_words * per + HR_FSM_SMEM_BYTES + 32 * sizeof(hr_pool_smem) > 227 * 1024)
             return fail(c, HR_E_ARG, "shared shadow too large: %llu words", (unsigned long long)n_words);
         c->smem_words_max = (uint32_t)n_words;
@@ -426,7 +437,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
         CU(cudaGetLastError());
     }
     const uint32_t nhw = (uint32_t)warps << split;
-    const uint32_t stage_off = hr_stage_offset(false, nhw, (uint32_t)smem_words);
+    const uint32_t stage_off = hr_stage_offset(false, nhw, smem_u64(c, smem_words));
     const size_t smem = (size_t)stage_off + hr_stage_bytes(nhw, 2u, 8u, hr_src_cmp::ROW_BYTES);
     if (smem > 227 * 1024)
         return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (compacted replay)", k, smem);
@@ -488,7 +499,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         }
     if (!pool) split = 0;
     const uint32_t nhw = (uint32_t)warps << split;
-    const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_NO_SPECULATE);
+    const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE);
     if (kind == HR_K_POOL_WIDE && !(c->cfg.options & HR_OPT_NO_COMPACT)) {
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -498,7 +509,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
         return HR_OK;
     }
-    size_t smem = (size_t)hr_stage_offset(pool, nhw, (uint32_t)smem_words) + hr_stage_bytes(nhw, nb, ch, SRC::ROW_BYTES);
+    size_t smem = (size_t)hr_stage_offset(pool, nhw, smem_u64(c, smem_words)) + hr_stage_bytes(nhw, nb, ch, SRC::ROW_BYTES);
     if (smem > 227 * 1024)
         return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (shadow %llu words + staging)", k, smem,
                     (unsigned long long)smem_words);
@@ -509,7 +520,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     else
         kern = pool ? (wide ? hr_replay_kernel<true, true, false, SRC> : hr_replay_kernel<true, false, false, SRC>)
                     : (wide ? hr_replay_kernel<false, true, false, SRC> : hr_replay_kernel<false, false, false, SRC>);
-    const uint32_t stage_off = hr_stage_offset(pool, nhw, (uint32_t)smem_words);
+    const uint32_t stage_off = hr_stage_offset(pool, nhw, smem_u64(c, smem_words));
     if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool timing = c->cfg.options & HR_OPT_TIMING;
     cudaEvent_t e0 = nullptr, e1 = nullptr;

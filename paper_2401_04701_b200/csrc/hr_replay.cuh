@@ -115,14 +115,14 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
     uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
         const bool sh = space != 0u;
-        const uint32_t sa = t.sshadow + (uint32_t)(local << 3);
+        const uint32_t sa = hr__saddr(d, t, local);
         unsigned long long *gp = d.gshadow + local;
         const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
         const uint32_t last = 31u - __clz(peers);
         const unsigned long long nmeta = (t.meta & ~(0x1full << HR_TID_SHIFT)) |
                                          ((unsigned long long)ps.src_at(last) << HR_TID_SHIFT);
         uint32_t fresh;
-        unsigned long long old = hr__first<ABL>(d, sh, sa, gp, kind, fresh);
+        unsigned long long old = hr__first<ABL>(d, t, sh, sa, gp, kind, fresh);
         while (true) {
             const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
             uint32_t rinfo, rel;
@@ -137,7 +137,7 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
                 if (fresh == HR_OLD_FRESH) break;
                 if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
             }
-            const unsigned long long prv = sh ? hr__cas_s(sa, old, nw) : hr__cas_g(gp, old, nw);
+            const unsigned long long prv = sh ? hr__cas_sh(d, t, sa, old, nw) : hr__cas_g(gp, old, nw);
             if (prv == old) {
                 if (rinfo) ei = rinfo | (cur == HR_RACE_GRID ? 1u : 0u);
                 break;

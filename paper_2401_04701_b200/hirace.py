@@ -31,6 +31,8 @@ HR_OPT_FINITE_HISTORY = 128
 HR_OPT_POOL_WIDE = 256
 HR_OPT_ROW_WIDE = 512
 HR_OPT_NO_COMPACT = 1024
+HR_OPT_SPECULATE = 2048
+HR_OPT_SMEM32 = 4096
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing", "hr_launch_count",

@@ -12,7 +12,7 @@ s = torch.cuda.current_stream().cuda_stream
 for _ in range(2):
     ck.reset(); ck.replay(dt, s); ck.report_raw()
 hr.hr_replay_timing(ck.ctx)
-for _ in range(3):
+for _ in range(int(os.environ.get("STEPS", "3"))):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     ck.reset(); torch.cuda.synchronize(); t1 = time.perf_counter()
     ck.replay(dt, s); t2 = time.perf_counter(); torch.cuda.synchronize(); t3 = time.perf_counter()

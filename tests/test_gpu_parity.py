@@ -95,8 +95,9 @@ def test_hot_words_contention(options):
     assert gpu_set(tr, options=options) == oracle_set(tr)
 
 
-@pytest.mark.parametrize("options", [1, 2, 3, 8, 16, 32, 32 | 1, 32 | 8, 64, 64 | 32, 256, 256 | 1, 256 | 8,
-                                     512, 512 | 1, 512 | 2, 512 | 8, 256 | 1024, 256 | 1024 | 8])
+@pytest.mark.parametrize("options", [1, 2, 3, 8, 2048, 16, 32, 32 | 1, 32 | 2048, 64, 64 | 32, 256, 256 | 1,
+                                     256 | 2048, 512, 512 | 1, 512 | 2, 512 | 2048, 256 | 1024,
+                                     256 | 1024 | 2048, 16 | 2048 | 64])
 def test_ablations_same_result(options):
     """Coalescing off / fast exits off / no speculation / forced row or pooled
     replay change the commit order and the traffic, never the result
@@ -377,3 +378,52 @@ def test_split_with_shards(monkeypatch):
             ck.close()
             union += [tuple(x) for x in races]
         assert sorted(union) == full
+
+
+# ---- HR_OPT_SMEM32: 32-bit block-implicit shared-shadow words ----
+S32 = 4096
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("options", [0, 16, 32, 256, 512])
+def test_smem32_random_programs(seed, options):
+    """Same racy set as the oracle with the clocks the 32-bit word can hold
+    (bc 9 bits, wc 8 bits); shared and global words, full warps, barriers."""
+    tr = _random_batch(300 + seed, 40, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12,
+                       n_words=40, spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
+    g, fl = gpu_set(tr, options=S32 | options)
+    o, ofl = oracle_set(tr, bc_bits=9, wc_bits=8)
+    assert g == o and fl == ofl
+    assert any(r[1] == 1 for r in o)
+
+
+def test_smem32_listings_c1_and_suite():
+    from tracegen import suite
+    for tr in (tp.listing1(2, 2, 32), tp.listing2(1, 32, 32), tp.listing4(1, 2, 32, 40),
+               tp.c1_tree_reduction(removed=32), tp.c1_tree_reduction(removed=None)):
+        assert gpu_set(tr, options=S32) == oracle_set(tr, bc_bits=9, wc_bits=8)
+    for c in suite.suite():
+        if c.trace.kdesc[:, 3].max() == 0:
+            continue                                   # no shared memory in this case
+        assert gpu_set(c.trace, options=S32) == oracle_set(c.trace, bc_bits=9, wc_bits=8), c.name
+
+
+def test_smem32_clock_cap():
+    """Past 511 block barriers the 32-bit word cannot tell epochs apart: the
+    thread stops checking and the overflow flag is latched, exactly
+    as the oracle with a 9-bit block clock does; the race before is kept."""
+    ev = {(0, 0, 0): [tf.W(0, tf.SPACE_SHARED)] + [tf.SYNCTHREADS] * 600 + [tf.W(1, tf.SPACE_SHARED)],
+          (0, 0, 1): [tf.W(0, tf.SPACE_SHARED)] + [tf.SYNCTHREADS] * 600 + [tf.W(1, tf.SPACE_SHARED)]}
+    tr = tp.from_thread_events(1, 1, 2, ev, smem_words=2)
+    g, fl = gpu_set(tr, options=S32)
+    o, ofl = oracle_set(tr, bc_bits=9, wc_bits=8)
+    assert g == o and fl == ofl == hr().HR_F_CLOCK_OVERFLOW
+    assert [r[3] for r in g] == [0]
+    # the 64-bit word keeps checking: both words are racy
+    assert [r[3] for r in gpu_set(tr)[0]] == [0, 1]
+
+
+def test_smem32_with_finite_history_rejected():
+    h = hr()
+    with pytest.raises(Exception):
+        h.Checker(64, 64, options=S32 | h.HR_OPT_FINITE_HISTORY)
