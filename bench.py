@@ -541,7 +541,7 @@ def main():
             "gpu_launches": n_launch,
             "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch,
                                     "rule": "every libhirace kernel launched in the timed region "
-                                            "(replay + report sort/gather; a CUB call counts as one)"},
+                                            "(replay; report keys, 2 CUB radix sorts of 10 kernels each, gather)"},
             "slowdown": slow,
             "cpu_baseline": cpu,
             "parity_vs_closed_form": parity_ok,

@@ -93,6 +93,13 @@ enum {
                                     the block / warp clocks at 511 / 255 (past them a thread stops
                                     checking and HR_F_CLOCK_OVERFLOW is latched).  Not with
                                     HR_OPT_FINITE_HISTORY. */
+    HR_OPT_LAZY_RESET = 8192u,   /* a11 without the per-kernel shadow memset: each
+                                    kernel writes a 4-bit epoch tag (1..15) into bits [31:28] of the
+                                    clock word, a global word with another tag reads as INIT, and
+                                    hr_kernel_begin zeroes the shadow only before a tag is reused
+                                    (every 15 kernels).  Caps the block clock at 2^(28 - wc_bits) - 1
+                                    (4095 at the default 16/16).  Not with FINITE_HISTORY or
+                                    DOUBLE_SHADOW; wc_bits <= 24. */
     HR_OPT_SPECULATE = 2048u     /* ablation: global reads/writes skip Algorithm 1's first atomic read
                                     and CAS against INIT (the CAS return is the read when it fails).
                                     Measured slower: a failed CAS costs an L2 atomic round trip that
@@ -290,7 +297,8 @@ hr_status hr_replay_timing(hr_ctx *ctx, double *reset_ms, uint64_t *n_resets, do
                            uint64_t *n_kernels);
 
 /* Number of device kernels this ctx launched since the last call (every
- * __global__ launch of libhirace; a CUB scan or sort call counts as one),
+ * __global__ launch of libhirace, including the kernels of its CUB scans (2)
+ * and 64-bit radix sorts (10: histogram, scan, 8 onesweep passes)),
  * then clear it.  Host only, no CUDA call; lets a harness state how many
  * kernels ran inside a timed region. */
 hr_status hr_launch_count(hr_ctx *ctx, uint64_t *n_launches);

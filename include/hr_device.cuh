@@ -66,6 +66,9 @@ struct hr_dev {
     uint32_t bc_max, wc_max;
     uint32_t options;             /* HR_OPT_* */
     uint32_t block_base;          /* simulated block of blockIdx 0 (chunked replay launches) */
+    uint32_t epoch_tag;           /* HR_OPT_LAZY_RESET: kernel epoch tag 1..15 in bits [31:28] of the
+                                     shadow's clock word; a global word with another tag is INIT.
+                                     0 = off (the shadow is zeroed at every kernel boundary) */
 };
 
 /* Per-thread registers. */
@@ -143,15 +146,18 @@ __device__ __forceinline__ uint32_t hr__s32_pack(unsigned long long w, uint32_t 
 {
     const uint32_t lo = (uint32_t)w;
     return ((uint32_t)(w >> HR_STATE_SHIFT) << HR_S32_STATE_SHIFT) | (((uint32_t)(w >> HR_TID_SHIFT) & 1023u) << 17) |
-           ((lo >> wc_bits) << 8) | (lo & ((1u << wc_bits) - 1u));
+           (((lo >> wc_bits) & 511u) << 8) | (lo & 255u);
 }
 
-__device__ __forceinline__ unsigned long long hr__s32_unpack(uint32_t v, uint32_t own_tid, uint32_t wc_bits)
+/* `tag_hi` = the epoch-tag bits of the current kernel (shared words are always
+ * of this kernel: the instance is zeroed at block start) */
+__device__ __forceinline__ unsigned long long hr__s32_unpack(uint32_t v, uint32_t own_tid, uint32_t wc_bits,
+                                                             uint32_t tag_hi)
 {
     if (v == 0u) return 0ull;                                           /* INIT */
     const uint32_t tid = (own_tid & ~1023u) | ((v >> 17) & 1023u);
     return ((unsigned long long)(v >> HR_S32_STATE_SHIFT) << HR_STATE_SHIFT) |
-           ((unsigned long long)tid << HR_TID_SHIFT) | ((((v >> 8) & 511u) << wc_bits) | (v & 255u));
+           ((unsigned long long)tid << HR_TID_SHIFT) | (tag_hi | (((v >> 8) & 511u) << wc_bits) | (v & 255u));
 }
 
 __device__ __forceinline__ uint32_t hr__lds_u8(uint32_t a)
@@ -222,6 +228,16 @@ __device__ __forceinline__ unsigned long long hr__ld_g_l1(const unsigned long lo
 #define HR_OLD_PROBE 1u
 #define HR_OLD_FRESH 2u
 
+/* a11 with HR_OPT_LAZY_RESET: the value Algorithm 1 sees.  A word written
+ * under another kernel's epoch tag belongs to an earlier kernel, and a kernel
+ * boundary orders everything, so it is INIT (the CAS still compares against
+ * the raw word).  hr_kernel_begin zeroes the shadow for real before a tag is
+ * reused (every 15 kernels). */
+__device__ __forceinline__ unsigned long long hr__live(const hr_dev &d, unsigned long long old)
+{
+    return (d.epoch_tag && old != 0ull && (((uint32_t)old >> 28) & 15u) != d.epoch_tag) ? 0ull : old;
+}
+
 /* Shared shadow word of this block's instance: load / CAS in the 64-bit layout. */
 __device__ __forceinline__ uint32_t hr__saddr(const hr_dev &d, const hr_thr &t, uint64_t local)
 {
@@ -233,7 +249,7 @@ __device__ __forceinline__ unsigned long long hr__ld_sh(const hr_dev &d, const h
     if (d.options & HR_OPT_SMEM32) {
         uint32_t v;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-        return hr__s32_unpack(v, t.tid(), d.wc_bits);
+        return hr__s32_unpack(v, t.tid(), d.wc_bits, d.epoch_tag << 28);
     }
     return hr__ld_s(a);
 }
@@ -246,7 +262,7 @@ __device__ __forceinline__ unsigned long long hr__cas_sh(const hr_dev &d, const 
         uint32_t r;
         HR_JITTER();
         asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(r) : "r"(a), "r"(c), "r"(v) : "memory");
-        return r == c ? cmp : hr__s32_unpack(r, t.tid(), d.wc_bits);
+        return r == c ? cmp : hr__s32_unpack(r, t.tid(), d.wc_bits, d.epoch_tag << 28);
     }
     return hr__cas_s(a, cmp, val);
 }
@@ -329,9 +345,10 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
     const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
     const uint32_t kcol = kind << 4;
     while (true) {
-        const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
-        const uint32_t rel = hr__rel(t.tid(), (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
-        const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
+        const unsigned long long lv = hr__live(d, old);
+        const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
+        const uint32_t rel = hr__rel(t.tid(), (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu);
+        const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)lv, d.wc_bits);
         const uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | kcol | (sync << 2) | rel));
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
         if (cur == os && fresh != HR_OLD_GUESS && fastexit) {
@@ -366,9 +383,10 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
     const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
     const unsigned long long nmeta = hr__nmeta(t, peers);
     while (true) {
-        const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+        const unsigned long long lv = hr__live(d, old);
+        const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
         uint32_t rinfo, rel;
-        const uint32_t cur = hr__transition(d, t, old, kind, lane, peers, kb0, kb1, rinfo, rel);
+        const uint32_t cur = hr__transition(d, t, lv, kind, lane, peers, kb0, kb1, rinfo, rel);
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
         if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
             const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
@@ -510,7 +528,7 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     hr_thr t;
     uint32_t block = d.block_base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const uint32_t tid = (block << 10) | ((ltid >> 5) << 5) | (ltid & 31u);
-    t.meta = (unsigned long long)tid << HR_TID_SHIFT;
+    t.meta = ((unsigned long long)tid << HR_TID_SHIFT) | ((unsigned long long)d.epoch_tag << 28);
     t.sshadow = (uint32_t)__cvta_generic_to_shared(smem_shadow);
     t.swords = smem_words;
     t.fsm = (uint32_t)__cvta_generic_to_shared(smem_fsm);

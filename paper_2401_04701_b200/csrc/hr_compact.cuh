@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr
     const uint32_t hw = threadIdx.x >> 5;
     const uint32_t warp = hw % warps, helper = hw / warps;
     const uint32_t nhw = warps << split_log2;
-    t.meta = (unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT;
+    t.meta = ((unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT) | (uint32_t)t.meta;
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const uint64_t w = (uint64_t)cta * warps + warp;
     const uint64_t nsg = segoff[w + 1] - segoff[w];

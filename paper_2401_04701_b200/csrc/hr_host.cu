@@ -41,7 +41,8 @@ struct hr_ctx {
     cudaStream_t side = nullptr;                 /* deferred resets (double shadow) */
     cudaEvent_t used_done[2] = {nullptr, nullptr}, reset_done[2] = {nullptr, nullptr};
     uint64_t gbase = 0, gwords = 0, glocal = 0;
-    uint64_t launches = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
+    uint64_t launches = 0;
+    uint32_t epoch_tag = 0;                      /* HR_OPT_LAZY_RESET: tag of the current kernel (1..15) */                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
     hr_race *ring = nullptr;
@@ -133,6 +134,10 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
         d.bc_max = std::min(d.bc_max, 511u);
         d.wc_max = std::min(d.wc_max, 255u);
     }
+    if (d.options & HR_OPT_LAZY_RESET) {        /* the epoch tag takes bits [31:28] of the clock word */
+        d.epoch_tag = c->epoch_tag;
+        d.bc_max = std::min(d.bc_max, (1u << (28 - c->cfg.wc_bits)) - 1u);
+    }
     return d;
 }
 
@@ -151,7 +156,9 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
     const hr_config &k = cfg ? *cfg : def;
     if (k.state_bits != 5 || k.tid_bits != 27 || k.bc_bits < 1 || k.wc_bits < 1 ||
         k.bc_bits + k.wc_bits != 32 || k.ring_capacity < 1 ||
-        ((k.options & HR_OPT_SMEM32) && (k.options & HR_OPT_FINITE_HISTORY)))
+        ((k.options & HR_OPT_SMEM32) && (k.options & HR_OPT_FINITE_HISTORY)) ||
+        ((k.options & HR_OPT_LAZY_RESET) &&
+         ((k.options & (HR_OPT_FINITE_HISTORY | HR_OPT_DOUBLE_SHADOW)) || k.wc_bits > 24)))
         return HR_E_ARG;
     hr_ctx *c = new (std::nothrow) hr_ctx;
     if (!c) return HR_E_NOMEM;
@@ -245,6 +252,7 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
         }
     }
     c->gcur = 0;
+    c->epoch_tag = 0;
     c->gshadow = c->gbuf[0];
     c->gbase = base_word;
     c->gwords = n_words;
@@ -271,6 +279,18 @@ extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
     if (!c->gshadow) return HR_OK;
+    if (c->cfg.options & HR_OPT_LAZY_RESET) {
+        /* epoch tags 1..15: words of earlier kernels read as INIT (hr__live);
+         * the shadow is zeroed for real only before a tag would be reused */
+        if (c->dirty[0] && c->epoch_tag == 15) {
+            hr_status st = reset_buffer(c, 0, c->stream);
+            if (st) return st;
+            c->epoch_tag = 0;
+        }
+        c->epoch_tag++;
+        c->dirty[0] = true;
+        return HR_OK;
+    }
     if (!c->double_shadow) {
         if (c->dirty[0]) { hr_status st = reset_buffer(c, 0, c->stream); if (st) return st; }
         c->dirty[0] = true;
@@ -401,7 +421,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     size_t tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg, segoff, (int64_t)(nw + 1), s));
     if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
-    c->launches++;
+    c->launches += 2;                   /* scan-init + scan */
     CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, nseg, segoff, (int64_t)(nw + 1), s));
     uint64_t nsegs = 0;
     CU(cudaMemcpyAsync(&nsegs, segoff + nw, 8, cudaMemcpyDeviceToHost, s));
@@ -420,7 +440,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, rowoff, (int64_t)(ncnt + 1), s));
     if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
-    c->launches++;
+    c->launches += 2;                   /* scan-init + scan */
     CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, rowoff, (int64_t)(ncnt + 1), s));
     uint64_t nrows = 0;
     CU(cudaMemcpyAsync(&nrows, rowoff + ncnt, 8, cudaMemcpyDeviceToHost, s));
@@ -783,7 +803,7 @@ extern "C" hr_status hr_pack_trace(hr_ctx *c, const hr_trace *in, uint8_t *out, 
     size_t tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, sizes, pack_off, (int64_t)n, s));
     if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
-    c->launches++;
+    c->launches += 2;                   /* scan-init + scan */
     CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, sizes, pack_off, (int64_t)n, s));
     uint64_t total = 0;
     unsigned int herr = 0;
@@ -993,13 +1013,13 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
     hr_race_keys_kernel<<<g, 256, 0, s>>>(c->ring, n, lo0, ix0);
     CU(cudaGetLastError());
     size_t tb = t1;
-    c->launches++;
+    c->launches += 10;                  /* onesweep, 64-bit keys: histogram + scan + 8 passes */
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)n, 0, 64, s));
     c->launches++;
     hr_race_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, ix1, n, hi0);
     CU(cudaGetLastError());
     tb = t1;
-    c->launches++;
+    c->launches += 10;                  /* onesweep, 64-bit keys: histogram + scan + 8 passes */
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)n, 0, 64, s));
     c->launches++;
     hr_race_gather_kernel<<<g, 256, 0, s>>>(c->ring, ix0, n, sorted);
@@ -1047,7 +1067,8 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         CU(cudaMemset(c->tail + 2, 0, sizeof(unsigned int)));
         c->launches++;
         hr_scan_kernel<<<148 * 8, 256>>>(c->gshadow, c->glocal, c->gbase, c->shard_rank, c->shard_log2, c->gran_log2,
-                                         c->last_kernel, tmp, c->tail + 2, scap);
+                                         c->last_kernel, (c->cfg.options & HR_OPT_LAZY_RESET) ? c->epoch_tag : 0u,
+                                         tmp, c->tail + 2, scap);
         CU(cudaGetLastError());
         unsigned int cnt = 0;
         CU(cudaMemcpy(&cnt, c->tail + 2, sizeof cnt, cudaMemcpyDeviceToHost));

@@ -124,9 +124,10 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
         uint32_t fresh;
         unsigned long long old = hr__first<ABL>(d, t, sh, sa, gp, kind, fresh);
         while (true) {
-            const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
+            const unsigned long long lv = hr__live(d, old);
+            const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
             uint32_t rinfo, rel;
-            const uint32_t cur = hr__pool_transition(d, t, old, ps, lane, peers, rinfo, rel);
+            const uint32_t cur = hr__pool_transition(d, t, lv, ps, lane, peers, rinfo, rel);
             const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
             if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
                 const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
@@ -262,7 +263,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
 #ifdef HR_FUZZ
     const uint32_t cta = gridDim.x - 1u - blockIdx.x;               /* reversed block mapping */
-    t.meta = (unsigned long long)(((d.block_base + cta) << 10) | (t.tid() & 1023u)) << HR_TID_SHIFT;
+    t.meta = ((unsigned long long)(((d.block_base + cta) << 10) | (t.tid() & 1023u)) << HR_TID_SHIFT) | (uint32_t)t.meta;
     t.off = (((d.block_base + cta) & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
 #else
     const uint32_t cta = blockIdx.x;
@@ -275,7 +276,8 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     const uint32_t warp = POOL && split_log2 ? hw % warps : hw;      /* simulated warp */
     const uint32_t helper = POOL && split_log2 ? hw / warps : 0u;
     if (POOL && split_log2)
-        t.meta = (unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT;
+        t.meta = ((unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT) |
+                 (uint32_t)t.meta;
     const uint64_t gw = (uint64_t)cta * warps + warp;
     const uint64_t r0 = woff[gw];
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
@@ -419,12 +421,13 @@ __global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, co
  * shadow becomes one record in `out` (a9 "end-of-kernel shadow scan"). */
 __global__ void hr_scan_kernel(const unsigned long long *__restrict__ sh, uint64_t n_local, uint64_t gbase,
                                uint32_t shard_rank, uint32_t shard_log2, uint32_t gran_log2, uint32_t kernel_id,
-                               hr_race *out,
+                               uint32_t epoch_tag, hr_race *out,
                                unsigned int *count, uint32_t cap)
 {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
          i += (uint64_t)gridDim.x * blockDim.x) {
         unsigned long long v = sh[i];
+        if (epoch_tag && (((uint32_t)v >> 28) & 15u) != epoch_tag) continue;   /* an earlier kernel's word */
         uint32_t st = (uint32_t)(v >> HR_STATE_SHIFT);
         if (st >= HR_RACE_BLOCK) {
             uint32_t slot = atomicAdd(count, 1u);

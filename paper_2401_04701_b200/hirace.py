@@ -33,6 +33,7 @@ HR_OPT_ROW_WIDE = 512
 HR_OPT_NO_COMPACT = 1024
 HR_OPT_SPECULATE = 2048
 HR_OPT_SMEM32 = 4096
+HR_OPT_LAZY_RESET = 8192
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing", "hr_launch_count",
@@ -258,7 +259,7 @@ def hr_replay_timing(ctx) -> Tuple[float, int, float, int]:
 
 
 def hr_launch_count(ctx) -> int:
-    """Kernels the ctx launched since the last call (a CUB call counts as one)."""
+    """Kernels the ctx launched since the last call (CUB scans and sorts counted by their kernels)."""
     n = ctypes.c_uint64()
     _check(load().hr_launch_count(ctx, ctypes.byref(n)), ctx, "hr_launch_count")
     return int(n.value)

@@ -427,3 +427,60 @@ def test_smem32_with_finite_history_rejected():
     h = hr()
     with pytest.raises(Exception):
         h.Checker(64, 64, options=S32 | h.HR_OPT_FINITE_HISTORY)
+
+
+# ---- HR_OPT_LAZY_RESET: epoch-tagged global shadow, no per-kernel memset (§8(f)-4) ----
+LAZY = 8192
+
+
+def _concat(traces):
+    """One multi-kernel trace from single-kernel traces (kernel boundaries between)."""
+    kernels = []
+    for t in traces:
+        for k in range(t.kdesc.shape[0]):
+            blocks, warps, lanes, smem, woi = (int(x) for x in t.kdesc[k, :5])
+            kk = tf.Kernel(blocks, warps, lanes, smem)
+            kk.rows = [t.rec[int(t.warp_off[woi + w]) * 32: int(t.warp_off[woi + w + 1]) * 32].reshape(-1, 32)
+                       for w in range(blocks * warps)]
+            kernels.append(kk)
+    return tf.make_trace(kernels)
+
+
+@pytest.mark.parametrize("options", [0, 16, 32, 256, 512, 4096])
+def test_lazy_reset_many_kernels(options):
+    """300 and 40 kernels reusing the same words: tags wrap every 15 kernels
+    (real reset), stale words of earlier kernels must read as INIT."""
+    tr = _random_batch(11, 300, max_blocks=2, max_warps=2, max_lanes=2, max_slots=5, n_words=2, spaces=(0, 1))
+    assert gpu_set(tr, options=LAZY | options) == oracle_set(tr)
+    tr = _random_batch(12, 40, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12, n_words=40,
+                       spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
+    assert gpu_set(tr, options=LAZY | options) == oracle_set(tr)
+
+
+def test_lazy_reset_suite_and_c1():
+    from tracegen import suite
+    for c in suite.suite():
+        assert gpu_set(c.trace, options=LAZY) == oracle_set(c.trace), c.name
+    tr = tp.c1_tree_reduction(removed=16)
+    assert gpu_set(tr, options=LAZY) == oracle_set(tr)
+
+
+def test_lazy_reset_overflow_scan_skips_stale_words():
+    """Kernel A leaves RACE words in the global shadow; kernel B (other words)
+    overflows the ring, so the report scans B's shadow: A's words carry A's
+    tag and must not come back as B's races."""
+    a = tp.from_thread_events(1, 1, 2, {(0, 0, 0): [tf.W(1000)], (0, 0, 1): [tf.W(1000)]})   # kernel 0: word 1000
+    b = tp.listing2(4, 8, 32)                         # many racy words in kernel 1
+    tr = _concat([a, b])
+    want, _ = oracle_set(tr)
+    assert [r[3] for r in want if r[0] == 0] == [1000] and any(r[0] == 1 for r in want)
+    assert all(r[3] != 1000 for r in want if r[0] == 1)
+    g, fl = gpu_set(tr, options=LAZY, ring_capacity=8)
+    assert fl & hr().HR_F_RING_OVERFLOW
+    assert g == want
+
+
+def test_lazy_reset_rejected_with_double_shadow():
+    h = hr()
+    with pytest.raises(Exception):
+        h.Checker(64, 0, options=LAZY | h.HR_OPT_DOUBLE_SHADOW)
