@@ -69,6 +69,13 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU to test the N>1 path (timings then meaningless)")
     ap.add_argument("--c4-lv", type=int, default=20, help="log2 vertices of the C4 graph for the slowdown")
+    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period during the timed region")
+    ap.add_argument("--no-spin", action="store_true", help="default CUDA host-wait scheduling instead of spin")
+    ap.add_argument("--sync-report", action="store_true",
+                    help="hr_report (host sort/merge, one host round trip per step) instead of hr_report_async")
+    ap.add_argument("--no-lazy-reset", action="store_true",
+                    help="zero the global shadow at every kernel boundary instead of HR_OPT_LAZY_RESET "
+                         "(epoch-tagged words, a real reset every 15 kernels)")
     return ap.parse_args()
 
 
@@ -90,16 +97,19 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_ms: int = 100):
         self.idx = gpu_index
+        self.period_ms = period_ms
         self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
         self.p = None
         self.t0 = self.t1 = None
 
     def start(self):
+        if self.period_ms <= 0:
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100", "-i", str(self.idx)], stdout=self.f,
+                                       "-lms", str(self.period_ms), "-i", str(self.idx)], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -145,6 +155,24 @@ class Clocks:
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cuda_spin_wait(local_rank: int) -> bool:
+    """Spin-wait scheduling for this process's primary CUDA context (driver API,
+    before torch creates the context): a step's host part (hr_report's short
+    syncs) then never waits for the OS to wake the thread, which on a busy
+    host cost 20-400 ms in a few steps per run."""
+    import ctypes
+    try:
+        cu = ctypes.CDLL("libcuda.so.1")
+        if cu.cuInit(0) != 0:
+            return False
+        dev = ctypes.c_int()
+        if cu.cuDeviceGet(ctypes.byref(dev), local_rank) != 0:
+            return False
+        return cu.cuDevicePrimaryCtxSetFlags(dev, 1) == 0          # CU_CTX_SCHED_SPIN
+    except OSError:
+        return False
 
 
 def dist_setup(args):
@@ -309,6 +337,7 @@ def main():
     from paper_2401_04701_b200.multigpu import exchange_races, shard_owner
     from tracegen import c5
 
+    spin = cuda_spin_wait(int(os.environ.get("LOCAL_RANK", "0"))) if not args.no_spin else False
     rank, world, local = dist_setup(args)
     assert world == args.gpus or world == 1, "launch with torchrun for --gpus > 1"
     emulated = None
@@ -349,13 +378,38 @@ def main():
         n_own += int((acc_mask & (wv < owned)).sum().item())
     del acc_mask, wv
     opts = hr.HR_OPT_TIMING | args.options | (hr.HR_OPT_DOUBLE_SHADOW if args.double_shadow else 0)
+    if not (args.no_lazy_reset or args.double_shadow):
+        opts |= hr.HR_OPT_LAZY_RESET
     ck = hr.Checker(c5.total_words(lb), 0, shard=(shard_rank, shard_n), options=opts, ring_capacity=1 << 21,
                     granule_log2=args.granule_log2)
 
+    step_log = [] if os.environ.get("HR_BENCH_STEPLOG") else None
+    async_report = world == 1 and not args.sync_report       # N > 1: the allgather needs the set per step
+
     def step(replay_fn):
-        ck.reset()
-        replay_fn()
-        raw, flags = ck.report_raw()
+        if step_log is not None:                    # diagnostic: where a slow step spends its time
+            t0 = time.perf_counter()
+            ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ga.record()
+            ck.reset()
+            replay_fn()
+            gb.record()
+            t1 = time.perf_counter()
+            gb.synchronize()
+            t2 = time.perf_counter()
+            raw, flags = ck.report_raw(copy=False)
+            t3 = time.perf_counter()
+            step_log.append({"issue": round(1e3 * (t1 - t0), 2), "gpu_replay": round(ga.elapsed_time(gb), 2),
+                             "wait": round(1e3 * (t2 - t1), 2), "report": round(1e3 * (t3 - t2), 2)})
+        elif async_report:
+            ck.reset()
+            replay_fn()
+            ck.report_async()                       # a13 on the device, result -> pinned host memory
+            return None, None
+        else:
+            ck.reset()
+            replay_fn()
+            raw, flags = ck.report_raw(copy=False)  # view of the reused buffer: no allocation per step
         if world > 1:
             raw, flags = exchange_races(raw, flags)
         return raw, flags
@@ -363,11 +417,14 @@ def main():
     dev_replay = lambda: ck.replay(dt, stream)  # noqa: E731
 
     # clock sampler first: its start-up must not land in the timed region
-    clocks = Clocks(torch.cuda.current_device())
+    clocks = Clocks(torch.cuda.current_device(), args.clock_ms)
     clocks.start()
     # warm-up + correctness of this run against the closed form (planted set)
     for _ in range(max(args.warmup, 1)):
         raw, flags = step(dev_replay)
+    if async_report and step_log is None:
+        raw, flags = ck.collect_raw()
+
     def expected():
         pl = c5.planted(lb, seed)
         if emulated:
@@ -400,15 +457,19 @@ def main():
     barrier(world)
     clk = clocks.stop()
     ms_total = e0.elapsed_time(e1)
+    if step_log is not None:
+        print("steplog:", json.dumps(step_log[-args.steps:]), file=sys.stderr)
     reset_ms, n_resets, kern_ms, n_kern = hr.hr_replay_timing(ck.ctx)
     n_launch = hr.hr_launch_count(ck.ctx)
+    if async_report and step_log is None:
+        raw, flags = ck.collect_raw()               # the last step's result, already in pinned host memory
     parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw] == expected()
 
     ms_step = max_over_ranks(ms_total / args.steps, world)
     total_acc = sum_over_ranks(n_acc_rank, world)
     value = total_acc / (ms_step / 1e3)
     kern_ms_launch = max_over_ranks(kern_ms / max(n_kern, 1), world)
-    reset_ms_launch = max_over_ranks(reset_ms / max(n_resets, 1), world)
+    reset_ms_step = max_over_ranks(reset_ms / args.steps, world)     # lazy reset: not every step resets
 
     # roofline of the dominant kernel (the replay), rank 0's launch
     peak, peak_kind = peaks()
@@ -500,6 +561,8 @@ def main():
             raw_e, _ = step(host_replay)
         f1.record()
         torch.cuda.synchronize()
+        if async_report and step_log is None:
+            raw_e, _ = ck.collect_raw()
         barrier(world)
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world)
         parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == expected()
@@ -520,7 +583,12 @@ def main():
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"C5: {total_acc} checked accesses (2^{lb} blocks x 256 threads x 256), "
                                    f"global trace over 2^{lb + 16} words, address-sharded (rotated granule stripes, x{world})",
-                       "trace_format": args.format,
+                       "trace_format": args.format, "host_wait": "spin" if spin else "default",
+                       "report": ("hr_report_async: device sort/merge, result written to pinned host memory "
+                                  "every step, collected after the loop" if async_report else
+                                  "hr_report: host round trip per step"),
+                       "kernel_boundary_reset": ("memset per kernel" if (args.no_lazy_reset or args.double_shadow)
+                                                 else "lazy: epoch-tagged shadow words, memset every 15 kernels"),
                        "parallelism": f"address-shard x{world}", "l2": "inputs larger than L2 "
                        "(trace + shadow >> 126 MB; no flush needed)", "seed": seed},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -533,15 +601,17 @@ def main():
             "ceiling": ceiling,
             "step_breakdown_ms": {"replay_kernel": kern_ms_launch,
                                   "shadow_reset" + (" (side stream, overlapped)" if args.double_shadow else ""):
-                                      reset_ms_launch,
+                                      reset_ms_step,
+                                  "shadow_resets_in_timed_steps": n_resets,
                                   "rest(report,ring reset,exchange)":
-                                      ms_step - kern_ms_launch - (0.0 if args.double_shadow else reset_ms_launch)},
+                                      ms_step - kern_ms_launch - (0.0 if args.double_shadow else reset_ms_step)},
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": n_launch,
             "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch,
-                                    "rule": "every libhirace kernel launched in the timed region "
-                                            "(replay; report keys, 2 CUB radix sorts of 10 kernels each, gather)"},
+                                    "rule": "every libhirace kernel launched in the timed region: the replay, "
+                                            "the report's key / head / emit kernels, its 2 CUB radix sorts "
+                                            "(10 kernels each) and CUB scan (2)"},
             "slowdown": slow,
             "cpu_baseline": cpu,
             "parity_vs_closed_form": parity_ok,

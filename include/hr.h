@@ -265,6 +265,20 @@ hr_status hr_unpack_trace(hr_ctx *ctx, const hr_trace *in, uint64_t *rec_out, vo
  * shadow is scanned for RACE words of the last replayed kernel instead. */
 hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out);
 
+/* hr_report without a host round trip (a13 on the device, "report races
+ * on unique memory addresses"): enqueue on `stream` (NULL = the ctx's last
+ * stream) a sort of the whole ring at its capacity, the merge of equal
+ * addresses (widest scope) and the write of the result into pinned host
+ * memory owned by the ctx.  Returns at once; nothing waits for the GPU, so a
+ * caller can enqueue the next kernel's checks behind it.  Each call replaces
+ * the previous result.  Cost: two radix sorts of ring_capacity keys. */
+hr_status hr_report_async(hr_ctx *ctx, void *stream);
+
+/* Wait for the last hr_report_async and copy its result out, with the same
+ * contract as hr_report.  If the ring had overflowed it runs hr_report (the
+ * shadow scan) instead.  HR_E_STATE without a pending hr_report_async. */
+hr_status hr_report_collect(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out);
+
 /* Merge race sets, HOST only (no CUDA call, no
  * ctx): `in` holds n hr_race records, e.g. the concatenated hr_report results
  * of N address shards after an allgather; `out` (host, cap records) receives

@@ -557,7 +557,9 @@ __device__ __forceinline__ void hr_check_atomic(const hr_dev &d, hr_thr &t, hr_s
 __device__ __forceinline__ void hr_syncthreads(const hr_dev &d, hr_thr &t)
 {
     __syncthreads();
-    if (((uint32_t)t.meta >> d.wc_bits) >= d.bc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+    /* the clock word's bits [31:28] hold the epoch tag under HR_OPT_LAZY_RESET */
+    const uint32_t lo = d.epoch_tag ? ((uint32_t)t.meta & 0x0fffffffu) : (uint32_t)t.meta;
+    if ((lo >> d.wc_bits) >= d.bc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
     else t.meta += 1ull << d.wc_bits;
 }
 

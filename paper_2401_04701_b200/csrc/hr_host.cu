@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <new>
 #include <vector>
 
@@ -42,7 +43,9 @@ struct hr_ctx {
     cudaEvent_t used_done[2] = {nullptr, nullptr}, reset_done[2] = {nullptr, nullptr};
     uint64_t gbase = 0, gwords = 0, glocal = 0;
     uint64_t launches = 0;
-    uint32_t epoch_tag = 0;                      /* HR_OPT_LAZY_RESET: tag of the current kernel (1..15) */                       /* kernels launched (1 per CUB call), hr_launch_count */
+    uint32_t epoch_tag = 0;                      /* HR_OPT_LAZY_RESET: tag of the current kernel (1..15) */
+    uint32_t sort_tmp_n = 0;                     /* cached CUB temp size of the report sort */
+    size_t sort_tmp_bytes = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
     hr_race *ring = nullptr;
@@ -67,6 +70,14 @@ struct hr_ctx {
     hr_race *rep_host = nullptr;                 /* pinned staging of the sorted report (D2H) */
     size_t rep_cap = 0;
     std::vector<hr_race> rep;                    /* report scratch, kept across calls */
+    /* hr_report_async: device scratch, pinned mapped result (ring_capacity
+     * records + a 4-word header: unique count, flags, raw count), completion event */
+    void *arep_scratch = nullptr;
+    size_t arep_scratch_bytes = 0, arep_tmp_bytes = 0;
+    hr_race *arep_host = nullptr, *arep_dev = nullptr;
+    uint32_t *arep_hdr_host = nullptr, *arep_hdr_dev = nullptr;
+    cudaEvent_t arep_ev = nullptr;
+    bool arep_pending = false;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
@@ -985,6 +996,19 @@ static size_t unique_races(std::vector<hr_race> &v)
     return m;
 }
 
+/* HR_REPORT_PROFILE=1: stderr line with the host time of each part of a slow
+ * (> 5 ms) hr_report call (diagnostic for host-side stalls). */
+static double hr__now_ms()
+{
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+static double hr__prof[16];
+static int hr__prof_n = 0;
+static bool hr__prof_on = false;
+#define HR_PROF_MARK() do { if (hr__prof_on && hr__prof_n < 16) hr__prof[hr__prof_n++] = hr__now_ms(); } while (0)
+
 static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &v)
 {
     cudaStream_t s = c->stream;
@@ -995,13 +1019,22 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
     const size_t sz[7] = {nb * 8, nb * 8, nb * 8, nb * 8, nb * 4, nb * 4, nb * sizeof(hr_race)};
     for (int i = 0; i < 7; i++) { off[i] = tot; tot += (sz[i] + 255) & ~(size_t)255; }
     size_t t1 = 0, t2 = 0;
-    CU(cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
-                                       (uint32_t *)nullptr, (int)n, 0, 64, s));
+    /* CUB's temp-size query does device-attribute / occupancy lookups that
+     * measured up to 0.8 s on a busy host now and then: cache it per size */
+    if (c->sort_tmp_n == n) {
+        t1 = c->sort_tmp_bytes;
+    } else {
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
+                                           (uint32_t *)nullptr, (int)n, 0, 64, s));
+        c->sort_tmp_n = n;
+        c->sort_tmp_bytes = t1;
+    }
     t2 = t1;
     off[7] = tot;
     tot += std::max(t1, t2);
     hr_status st = reserve(c, 5, tot);
     if (st) return st;
+    HR_PROF_MARK();
     char *b = (char *)c->stage[5];
     uint64_t *lo0 = (uint64_t *)(b + off[0]), *lo1 = (uint64_t *)(b + off[1]);
     uint64_t *hi0 = (uint64_t *)(b + off[2]), *hi1 = (uint64_t *)(b + off[3]);
@@ -1012,20 +1045,29 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
     c->launches++;
     hr_race_keys_kernel<<<g, 256, 0, s>>>(c->ring, n, lo0, ix0);
     CU(cudaGetLastError());
+    HR_PROF_MARK();
     size_t tb = t1;
     c->launches += 10;                  /* onesweep, 64-bit keys: histogram + scan + 8 passes */
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)n, 0, 64, s));
+    HR_PROF_MARK();
     c->launches++;
     hr_race_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, ix1, n, hi0);
     CU(cudaGetLastError());
+    HR_PROF_MARK();
     tb = t1;
     c->launches += 10;                  /* onesweep, 64-bit keys: histogram + scan + 8 passes */
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)n, 0, 64, s));
+    HR_PROF_MARK();
     c->launches++;
     hr_race_gather_kernel<<<g, 256, 0, s>>>(c->ring, ix0, n, sorted);
     CU(cudaGetLastError());
+    HR_PROF_MARK();
     if (n > c->rep_cap) {
         if (c->rep_host) cudaFreeHost(c->rep_host);
+    if (c->arep_host) cudaFreeHost(c->arep_host);
+    if (c->arep_hdr_host) cudaFreeHost(c->arep_hdr_host);
+    if (c->arep_scratch) cudaFree(c->arep_scratch);
+    if (c->arep_ev) cudaEventDestroy(c->arep_ev);
         c->rep_host = nullptr;
         c->rep_cap = 0;
         if (cudaHostAlloc((void **)&c->rep_host, nb * sizeof(hr_race), cudaHostAllocDefault) != cudaSuccess)
@@ -1033,18 +1075,180 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
         c->rep_cap = n;
     }
     CU(cudaMemcpyAsync(c->rep_host, sorted, nb * sizeof(hr_race), cudaMemcpyDeviceToHost, s));
+    HR_PROF_MARK();
     CU(cudaStreamSynchronize(s));
     v.assign(c->rep_host, c->rep_host + n);
     return HR_OK;
 }
 
+
+/* ---- asynchronous report (hr_report_async): a13 on the device ----
+ * The ring is sorted at its full capacity (entries past the tail get the
+ * largest keys, so the tail count never has to reach the host), run heads of
+ * equal (kernel, space, block, word) are flagged and scanned, and each head
+ * writes its merged record (widest scope) straight into pinned host memory. */
+__global__ void hr_arep_keys_kernel(const hr_race *__restrict__ r, const unsigned int *__restrict__ tail, uint32_t cap,
+                                    uint64_t *__restrict__ lo, uint32_t *__restrict__ idx)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cap) return;
+    const uint32_t n = min(*tail, cap);
+    lo[i] = i < n ? r[i].word : ~0ull;
+    idx[i] = i;
+}
+
+__global__ void hr_arep_hikeys_kernel(const hr_race *__restrict__ r, const unsigned int *__restrict__ tail,
+                                      const uint32_t *__restrict__ idx, uint32_t cap, uint64_t *__restrict__ hi)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cap) return;
+    const uint32_t n = min(*tail, cap);
+    const uint32_t j = idx[i];
+    if (j >= n) { hi[i] = ~0ull; return; }
+    const hr_race &x = r[j];
+    hi[i] = ((uint64_t)x.kernel << 33) | ((uint64_t)x.space << 32) | (uint64_t)x.block;
+}
+
+__device__ __forceinline__ bool hr__same_addr(const hr_race &a, const hr_race &b)
+{
+    return a.kernel == b.kernel && a.space == b.space && a.block == b.block && a.word == b.word;
+}
+
+__global__ void hr_arep_heads_kernel(const hr_race *__restrict__ r, const unsigned int *__restrict__ tail,
+                                     const uint32_t *__restrict__ idx, uint32_t cap, uint32_t *__restrict__ head)
+{
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= cap) return;
+    const uint32_t n = min(*tail, cap);
+    head[p] = p < n && (p == 0 || !hr__same_addr(r[idx[p]], r[idx[p - 1]])) ? 1u : 0u;
+}
+
+/* one thread per run head: the run's first record with the widest scope of
+ * the run (as unique_races on the host) */
+__global__ void hr_arep_emit_kernel(const hr_race *__restrict__ r, const unsigned int *__restrict__ tail,
+                                    const uint32_t *__restrict__ idx, const uint32_t *__restrict__ head,
+                                    const uint32_t *__restrict__ pos, uint32_t cap, hr_race *out, uint32_t *hdr)
+{
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n = min(*tail, cap);
+    if (p == 0) {
+        hdr[0] = n ? pos[n - 1] + head[n - 1] : 0u;
+        hdr[1] = tail[1];
+        hdr[2] = *tail;
+    }
+    if (p >= n || !head[p]) return;
+    hr_race x = r[idx[p]];
+    for (uint32_t q = p + 1; q < n && !head[q]; q++) {
+        const hr_race &y = r[idx[q]];
+        if (y.scope > x.scope) {
+            const uint8_t sc = y.scope;
+            if (x.first_kind == 0xff) x = y;
+            x.scope = sc;
+        }
+    }
+    out[pos[p]] = x;
+}
+
+extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
+{
+    if (!c) return HR_E_ARG;
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    const uint32_t cap = c->cfg.ring_capacity;
+    if (!c->arep_host) {
+        const size_t bytes = (size_t)cap * sizeof(hr_race);
+        if (cudaHostAlloc((void **)&c->arep_host, bytes, cudaHostAllocMapped) != cudaSuccess)
+            return fail(c, HR_E_NOMEM, "pinned mapped report buffer of %zu bytes failed", bytes);
+        CU(cudaHostGetDevicePointer((void **)&c->arep_dev, c->arep_host, 0));
+        if (cudaHostAlloc((void **)&c->arep_hdr_host, 16, cudaHostAllocMapped) != cudaSuccess)
+            return fail(c, HR_E_NOMEM, "pinned report header failed");
+        CU(cudaHostGetDevicePointer((void **)&c->arep_hdr_dev, c->arep_hdr_host, 0));
+        CU(cudaEventCreateWithFlags(&c->arep_ev, cudaEventDisableTiming));
+    }
+    /* scratch: lo keys x2, hi keys x2, idx x2, head flags, positions, CUB temp */
+    const size_t nb = cap;
+    size_t off[9], tot = 0;
+    const size_t sz[8] = {nb * 8, nb * 8, nb * 8, nb * 8, nb * 4, nb * 4, nb * 4, nb * 4};
+    for (int i = 0; i < 8; i++) { off[i] = tot; tot += (sz[i] + 255) & ~(size_t)255; }
+    if (!c->arep_tmp_bytes) {
+        size_t t1 = 0, t2 = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
+                                           (uint32_t *)nullptr, (int)cap, 0, 64, s));
+        CU(cub::DeviceScan::ExclusiveSum(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)cap, s));
+        c->arep_tmp_bytes = std::max(t1, t2);
+    }
+    off[8] = tot;
+    tot += c->arep_tmp_bytes;
+    if (tot > c->arep_scratch_bytes) {
+        if (c->arep_scratch) cudaFree(c->arep_scratch);
+        c->arep_scratch = nullptr;
+        c->arep_scratch_bytes = 0;
+        if (cudaMalloc(&c->arep_scratch, tot) != cudaSuccess) return fail(c, HR_E_NOMEM, "report scratch failed");
+        c->arep_scratch_bytes = tot;
+    }
+    char *b = (char *)c->arep_scratch;
+    uint64_t *lo0 = (uint64_t *)(b + off[0]), *lo1 = (uint64_t *)(b + off[1]);
+    uint64_t *hi0 = (uint64_t *)(b + off[2]), *hi1 = (uint64_t *)(b + off[3]);
+    uint32_t *ix0 = (uint32_t *)(b + off[4]), *ix1 = (uint32_t *)(b + off[5]);
+    uint32_t *head = (uint32_t *)(b + off[6]), *pos = (uint32_t *)(b + off[7]);
+    void *tmp = b + off[8];
+    const unsigned g = (cap + 255) / 256;
+    size_t tb = c->arep_tmp_bytes;
+    c->launches++;
+    hr_arep_keys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, cap, lo0, ix0);
+    CU(cudaGetLastError());
+    c->launches += 10;
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)cap, 0, 64, s));
+    c->launches++;
+    hr_arep_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix1, cap, hi0);
+    CU(cudaGetLastError());
+    tb = c->arep_tmp_bytes;
+    c->launches += 10;
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)cap, 0, 64, s));
+    c->launches++;
+    hr_arep_heads_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, cap, head);
+    CU(cudaGetLastError());
+    tb = c->arep_tmp_bytes;
+    c->launches += 2;
+    CU(cub::DeviceScan::ExclusiveSum(tmp, tb, head, pos, (int)cap, s));
+    c->launches++;
+    hr_arep_emit_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, head, pos, cap, c->arep_dev, c->arep_hdr_dev);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->arep_ev, s));
+    c->arep_pending = true;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_report_collect(hr_ctx *c, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out)
+{
+    if (!c || !n_out || (cap && !out)) return fail(c, HR_E_ARG, "hr_report_collect: bad arguments");
+    if (!c->arep_pending) return fail(c, HR_E_STATE, "hr_report_collect without hr_report_async");
+    CU(cudaSetDevice(c->device));
+    CU(cudaEventSynchronize(c->arep_ev));
+    c->arep_pending = false;
+    const uint32_t m = c->arep_hdr_host[0], flags = c->arep_hdr_host[1];
+    if (flags & HR_F_RING_OVERFLOW)                      /* the shadow scan needs the synchronous path */
+        return hr_report(c, out, cap, n_out, flags_out);
+    *n_out = m;
+    if (flags_out) *flags_out = flags;
+    const size_t w = std::min<size_t>(m, cap);
+    if (w) memcpy(out, c->arep_host, w * sizeof(hr_race));
+    return m > cap ? fail(c, HR_E_ARG, "hr_report_collect: %u races, capacity %zu", m, cap) : HR_OK;
+}
+
 extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out)
 {
     if (!c || !n_out || (cap && !out)) return fail(c, HR_E_ARG, "hr_report: bad arguments");
+    static const bool prof = getenv("HR_REPORT_PROFILE") != nullptr;
+    hr__prof_on = prof;
+    hr__prof_n = 0;
+    HR_PROF_MARK();
     CU(cudaSetDevice(c->device));
     CU(cudaStreamSynchronize(c->stream));
+    HR_PROF_MARK();
     unsigned int hdr[4];
     CU(cudaMemcpy(hdr, c->tail, sizeof hdr, cudaMemcpyDeviceToHost));
+    HR_PROF_MARK();
     uint32_t n = std::min<uint32_t>(hdr[0], c->cfg.ring_capacity);
     uint32_t flags = hdr[1];
     std::vector<hr_race> &v = c->rep;
@@ -1078,12 +1282,20 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         if (cnt) CU(cudaMemcpy(v.data() + off, tmp, cnt * sizeof(hr_race), cudaMemcpyDeviceToHost));
         cudaFree(tmp);
     }
+    HR_PROF_MARK();
     if (!sorted) sort_races(v);
     const size_t m = unique_races(v);
+    HR_PROF_MARK();
     *n_out = m;
     if (flags_out) *flags_out = flags;
     size_t w = std::min(m, cap);
     if (w) memcpy(out, v.data(), w * sizeof(hr_race));
+    HR_PROF_MARK();
+    if (prof && hr__prof_n > 1 && hr__prof[hr__prof_n - 1] - hr__prof[0] > 5.0) {
+        fprintf(stderr, "hr_report slow:");
+        for (int i = 1; i < hr__prof_n; i++) fprintf(stderr, " %.2f", hr__prof[i] - hr__prof[i - 1]);
+        fprintf(stderr, " ms (sync, hdr, reserve, keys, sort1, hikeys, sort2, gather, d2h-enq, d2h-sync, unique, copy-out)\n");
+    }
     return m > cap ? fail(c, HR_E_ARG, "hr_report: %zu races, capacity %zu", m, cap) : HR_OK;
 }
 
@@ -1284,6 +1496,10 @@ extern "C" void hr_destroy(hr_ctx *c)
     for (int i = 0; i < 12; i++)
         if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->rep_host) cudaFreeHost(c->rep_host);
+    if (c->arep_host) cudaFreeHost(c->arep_host);
+    if (c->arep_hdr_host) cudaFreeHost(c->arep_hdr_host);
+    if (c->arep_scratch) cudaFree(c->arep_scratch);
+    if (c->arep_ev) cudaEventDestroy(c->arep_ev);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

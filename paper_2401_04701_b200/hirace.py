@@ -35,7 +35,8 @@ HR_OPT_SPECULATE = 2048
 HR_OPT_SMEM32 = 4096
 HR_OPT_LAZY_RESET = 8192
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
-           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
+           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_report_async",
+           "hr_report_collect", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing", "hr_launch_count",
            "hr_fsm_table",
            "hr_device_view", "hr_last_error", "hr_destroy")
@@ -95,6 +96,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_unpack_trace": ([vp, P(HrTrace), vp, vp], ctypes.c_int),
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_merge_races": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, P(ctypes.c_size_t)], ctypes.c_int),
+        "hr_report_async": ([vp, vp], ctypes.c_int),
+        "hr_report_collect": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_race_classes": ([vp, P(HrTrace), vp, ctypes.c_size_t, vp, vp], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
         "hr_counters": ([vp, P(ctypes.c_uint64)], ctypes.c_int),
@@ -188,11 +191,8 @@ assert RACE_DTYPE.itemsize == 24
 _report_buf: Optional[np.ndarray] = None
 
 
-def hr_report_raw(ctx, cap: int = 1 << 17) -> Tuple[np.ndarray, int]:
-    """(sorted unique race records as a structured array of hr_race, flags).
-    The staging buffer is reused between calls; the result is a copy."""
+def _report_into(fn, ctx, cap: int, copy: bool, what: str) -> Tuple[np.ndarray, int]:
     global _report_buf
-    lib = load()
     while True:
         if _report_buf is None or _report_buf.shape[0] < cap:
             _report_buf = np.empty(cap, dtype=RACE_DTYPE)
@@ -200,13 +200,32 @@ def hr_report_raw(ctx, cap: int = 1 << 17) -> Tuple[np.ndarray, int]:
         cap = buf.shape[0]
         n = ctypes.c_size_t(0)
         fl = ctypes.c_uint32(0)
-        rc = lib.hr_report(ctx, buf.ctypes.data_as(ctypes.POINTER(HrRace)), cap, ctypes.byref(n),
-                           ctypes.byref(fl))
+        rc = fn(ctx, buf.ctypes.data_as(ctypes.POINTER(HrRace)), cap, ctypes.byref(n), ctypes.byref(fl))
         if rc == HR_E_ARG and n.value > cap:
+            if what == "hr_report_collect":      # the result stays in the ctx's pinned buffer: re-read it
+                fn = load().hr_report
             cap = int(n.value)
             continue
-        _check(rc, ctx, "hr_report")
-        return buf[: n.value].copy(), int(fl.value)
+        _check(rc, ctx, what)
+        return (buf[: n.value].copy() if copy else buf[: n.value]), int(fl.value)
+
+
+def hr_report_raw(ctx, cap: int = 1 << 17, copy: bool = True) -> Tuple[np.ndarray, int]:
+    """(sorted unique race records as a structured array of hr_race, flags).
+    The staging buffer is reused between calls; the result is a copy unless
+    copy=False (then a view valid until the next call: no allocation, no
+    page faults in a timed loop)."""
+    return _report_into(load().hr_report, ctx, cap, copy, "hr_report")
+
+
+def hr_report_async(ctx, stream: Optional[int] = None):
+    """Enqueue the device-side report (hr_report_async); no host wait."""
+    _check(load().hr_report_async(ctx, stream or None), ctx, "hr_report_async")
+
+
+def hr_report_collect(ctx, cap: int = 1 << 17, copy: bool = True) -> Tuple[np.ndarray, int]:
+    """Wait for the last hr_report_async; same result as hr_report_raw."""
+    return _report_into(load().hr_report_collect, ctx, cap, copy, "hr_report_collect")
 
 
 def hr_merge_races(parts: np.ndarray) -> np.ndarray:
@@ -442,8 +461,14 @@ class Checker:
     def report(self):
         return hr_report(self.ctx)
 
-    def report_raw(self):
-        return hr_report_raw(self.ctx)
+    def report_raw(self, copy: bool = True):
+        return hr_report_raw(self.ctx, copy=copy)
+
+    def report_async(self, stream: Optional[int] = None):
+        hr_report_async(self.ctx, stream)
+
+    def collect_raw(self, copy: bool = True):
+        return hr_report_collect(self.ctx, copy=copy)
 
     def classes(self, dtrace: "DeviceTrace", raw: np.ndarray, stream: Optional[int] = None,
                 kernel_base: int = 0) -> np.ndarray:

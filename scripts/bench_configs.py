@@ -25,6 +25,7 @@ def run(name, trace=None, dt=None, words=None, smem=0, reps=5, ring=1 << 22, opt
     if dt is None:
         dt = hr.DeviceTrace.from_trace(trace)
     n_acc = int(((dt.rec >> 62) & 3).ne(3).sum().item())
+    opts |= int(os.environ.get("HR_OPTS", "0"))
     ck = hr.Checker(words, smem, ring_capacity=ring, options=hr.HR_OPT_TIMING | opts)
     for _ in range(2):
         ck.reset(); ck.replay(dt); ck.report_raw()

@@ -6,4 +6,5 @@ for o in 0 8192 0 8192; do
 done
 echo "s0/8 $(timeout 600 python bench.py --emulate-shard 0/8 --options 8192 --no-e2e --no-cpu --no-slowdown --steps 15 2>>$O/lazy.err)" >> $O/lazy.txt
 echo "s0/8base $(timeout 600 python bench.py --emulate-shard 0/8 --no-e2e --no-cpu --no-slowdown --steps 15 2>>$O/lazy.err)" >> $O/lazy.txt
+HR_OPTS=8192 timeout 900 python scripts/bench_configs.py c4 c2 > $O/lazy_c4.jsonl 2>&1
 tail -2 $O/gpu_tests_lazy.log

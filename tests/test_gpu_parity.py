@@ -484,3 +484,82 @@ def test_lazy_reset_rejected_with_double_shadow():
     h = hr()
     with pytest.raises(Exception):
         h.Checker(64, 0, options=LAZY | h.HR_OPT_DOUBLE_SHADOW)
+
+
+def test_lazy_reset_repeated_replays_device_and_host():
+    """The bench pattern: the same multi-kernel trace replayed again and again
+    on one ctx (tags wrap several times), from device memory, from host
+    buffers (chunked) and from the PACKED encoding: every report equals the
+    oracle's."""
+    h = hr()
+    tr = _random_batch(21, 7, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12, n_words=40,
+                       spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
+    want, _ = oracle_set(tr)
+    gmax, smem = h.trace_extent(tr)
+    ck = h.Checker(gmax, smem, options=LAZY)
+    dt = h.DeviceTrace.from_trace(tr)
+    packed_host = ck.pack(dt).to_host()
+    for i in range(12):                                   # 84 kernels: 5 tag wraps
+        ck.reset()
+        if i % 3 == 0:
+            ck.replay(dt)
+        elif i % 3 == 1:
+            ck.replay_host(tr)
+        else:
+            ck.replay_host(packed_host)
+        races, fl, _ = ck.report()
+        assert [tuple(r) for r in races] == want and fl == 0, i
+    ck.close()
+
+
+# ---- hr_report_async / hr_report_collect: a13 on the device ----
+def _async_vs_sync(tr, **kw):
+    h = hr()
+    gmax, smem = h.trace_extent(tr)
+    ck = h.Checker(gmax, smem, **kw)
+    dt = h.DeviceTrace.from_trace(tr)
+    ck.reset(); ck.replay(dt); ck.report_async()
+    a_raw, a_fl = ck.collect_raw()
+    sync_raw, sync_fl = ck.report_raw()               # same ring: byte-identical, witnesses included
+    ck.close()
+    return sync_raw, sync_fl, a_raw, a_fl
+
+
+def test_report_async_matches_sync_and_oracle():
+    from tracegen import suite
+    cases = [c.trace for c in suite.suite()[::7]] + [
+        tp.listing2(64, 8, 32),                        # > 4096 races
+        tp.listing1(1, 1, 1),                          # no race
+        _random_batch(5, 30, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12, n_words=40,
+                      spaces=(0, 1), p_barrier=0.25, p_skip=0.5)]
+    for tr in cases:
+        s_raw, s_fl, a_raw, a_fl = _async_vs_sync(tr)
+        assert a_raw.tobytes() == s_raw.tobytes() and a_fl == s_fl
+        assert [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+                for r in a_raw] == oracle_set(tr)[0]
+
+
+def test_report_async_ring_overflow_falls_back():
+    tr = tp.listing2(4, 8, 32)
+    s_raw, s_fl, a_raw, a_fl = _async_vs_sync(tr, ring_capacity=8)
+    assert a_fl & hr().HR_F_RING_OVERFLOW
+    assert a_raw.tobytes() == s_raw.tobytes()
+    assert [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+            for r in a_raw] == oracle_set(tr)[0]
+
+
+def test_report_async_c5_planted_repeated():
+    """The bench pattern: several enqueued steps, each replay followed by an
+    async report, one collect at the end = the planted set (closed form)."""
+    from tracegen import c5
+    h = hr()
+    lb = 8
+    rec, woff, kd = c5.gpu_trace(lb)
+    dt = h.DeviceTrace(rec, woff, kd)
+    ck = h.Checker(c5.total_words(lb), 0, ring_capacity=1 << 16, options=h.HR_OPT_LAZY_RESET)
+    for _ in range(4):
+        ck.reset(); ck.replay(dt); ck.report_async()
+    raw, fl = ck.collect_raw()
+    ck.close()
+    assert fl == 0
+    assert [(int(r["word"]), int(r["scope"])) for r in raw] == c5.planted(lb)
