@@ -239,14 +239,18 @@ __device__ __forceinline__ unsigned long long hr__live(const hr_dev &d, unsigned
 }
 
 /* Shared shadow word of this block's instance: load / CAS in the 64-bit layout. */
+template <bool ABL>
 __device__ __forceinline__ uint32_t hr__saddr(const hr_dev &d, const hr_thr &t, uint64_t local)
 {
-    return t.sshadow + ((uint32_t)local << ((d.options & HR_OPT_SMEM32) ? 2 : 3));
+    return t.sshadow + ((uint32_t)local << (hr__opt<ABL>(d, HR_OPT_SMEM32) ? 2 : 3));
 }
 
+/* HR_OPT_SMEM32 is read only by the ABL (all options at run time) kernels; the
+ * host routes a ctx with SMEM32 to them */
+template <bool ABL>
 __device__ __forceinline__ unsigned long long hr__ld_sh(const hr_dev &d, const hr_thr &t, uint32_t a)
 {
-    if (d.options & HR_OPT_SMEM32) {
+    if (hr__opt<ABL>(d, HR_OPT_SMEM32)) {
         uint32_t v;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
         return hr__s32_unpack(v, t.tid(), d.wc_bits, d.epoch_tag << 28);
@@ -254,10 +258,11 @@ __device__ __forceinline__ unsigned long long hr__ld_sh(const hr_dev &d, const h
     return hr__ld_s(a);
 }
 
+template <bool ABL>
 __device__ __forceinline__ unsigned long long hr__cas_sh(const hr_dev &d, const hr_thr &t, uint32_t a,
                                                          unsigned long long cmp, unsigned long long val)
 {
-    if (d.options & HR_OPT_SMEM32) {
+    if (hr__opt<ABL>(d, HR_OPT_SMEM32)) {
         const uint32_t c = hr__s32_pack(cmp, d.wc_bits), v = hr__s32_pack(val, d.wc_bits);
         uint32_t r;
         HR_JITTER();
@@ -345,7 +350,7 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
     const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
     const uint32_t kcol = kind << 4;
     while (true) {
-        const unsigned long long lv = hr__live(d, old);
+        const unsigned long long lv = is_shared ? old : hr__live(d, old);   /* shared words are this kernel's */
         const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
         const uint32_t rel = hr__rel(t.tid(), (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu);
         const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)lv, d.wc_bits);
@@ -360,7 +365,7 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
             if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
             if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
         }
-        const unsigned long long prev = is_shared ? hr__cas_sh(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+        const unsigned long long prev = is_shared ? hr__cas_sh<ABL>(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
         if (prev == old) {                                                /* a8 committed */
             if (cur >= HR_RACE_BLOCK && cur != os)
                 return HR_EI_EMIT | (hr__laneid() << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID);
@@ -383,7 +388,7 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
     const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
     const unsigned long long nmeta = hr__nmeta(t, peers);
     while (true) {
-        const unsigned long long lv = hr__live(d, old);
+        const unsigned long long lv = is_shared ? old : hr__live(d, old);   /* shared words are this kernel's */
         const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
         uint32_t rinfo, rel;
         const uint32_t cur = hr__transition(d, t, lv, kind, lane, peers, kb0, kb1, rinfo, rel);
@@ -397,7 +402,7 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
             if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
             if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
         }
-        const unsigned long long prev = is_shared ? hr__cas_sh(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
+        const unsigned long long prev = is_shared ? hr__cas_sh<ABL>(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
         if (prev == old)                                                  /* a8 committed */
             return rinfo ? (rinfo | (cur == HR_RACE_GRID ? 1u : 0u)) : 0u;
         old = prev;
@@ -416,7 +421,7 @@ __device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, const h
                                                         uint32_t sh_addr, const unsigned long long *gp, uint32_t kind,
                                                         uint32_t &fresh)
 {
-    if (is_shared) { fresh = HR_OLD_FRESH; return hr__ld_sh(d, t, sh_addr); }
+    if (is_shared) { fresh = HR_OLD_FRESH; return hr__ld_sh<ABL>(d, t, sh_addr); }
     if (kind == HR_ATOMIC && !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT)) { fresh = HR_OLD_PROBE; return hr__ld_g_l1(gp); }
     if (hr__opt<ABL>(d, HR_OPT_SPECULATE)) { fresh = HR_OLD_GUESS; return 0ull; }
     fresh = HR_OLD_FRESH;
@@ -490,7 +495,7 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
 
     uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
-        const uint32_t sh_addr = hr__saddr(d, t, local);
+        const uint32_t sh_addr = hr__saddr<ABL>(d, t, local);
         unsigned long long *gp = d.gshadow + local;
         uint32_t fresh;
         const unsigned long long old = hr__first<ABL>(d, t, is_shared, sh_addr, gp, kind, fresh);
@@ -537,19 +542,24 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
 }
 
 
+/* OPTS = true reads the ablation options and HR_OPT_SMEM32 at run time; a
+ * kernel instantiated with OPTS = false must only run on a ctx without them. */
+template <bool OPTS = true>
 __device__ __forceinline__ void hr_check_read(const hr_dev &d, hr_thr &t, hr_space space, uint64_t word)
 {
-    hr_check_lanes<true>(d, t, __activemask(), true, (uint32_t)space, word, HR_READ);
+    hr_check_lanes<true, OPTS>(d, t, __activemask(), true, (uint32_t)space, word, HR_READ);
 }
 
+template <bool OPTS = true>
 __device__ __forceinline__ void hr_check_write(const hr_dev &d, hr_thr &t, hr_space space, uint64_t word)
 {
-    hr_check_lanes<true>(d, t, __activemask(), true, (uint32_t)space, word, HR_WRITE);
+    hr_check_lanes<true, OPTS>(d, t, __activemask(), true, (uint32_t)space, word, HR_WRITE);
 }
 
+template <bool OPTS = true>
 __device__ __forceinline__ void hr_check_atomic(const hr_dev &d, hr_thr &t, hr_space space, uint64_t word)
 {
-    hr_check_lanes<true>(d, t, __activemask(), true, (uint32_t)space, word, HR_ATOMIC);
+    hr_check_lanes<true, OPTS>(d, t, __activemask(), true, (uint32_t)space, word, HR_ATOMIC);
 }
 
 /* __syncthreads(); ++bc.  Overflow: saturate,

@@ -17,17 +17,24 @@
 
 namespace {
 
-template <bool I>
+/* run-time options the fast (I = 2) instantiation does not read */
+inline bool rt_opts(const hr_dev &d)
+{
+    return d.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE | HR_OPT_SMEM32);
+}
+
+template <int I>
 __device__ __forceinline__ void chk(const hr_dev &d, hr_thr &t, hr_space sp, uint64_t w, int kind)
 {
     if (I) {
-        if (kind == HR_READ) hr_check_read(d, t, sp, w);
-        else if (kind == HR_WRITE) hr_check_write(d, t, sp, w);
-        else hr_check_atomic(d, t, sp, w);
+        /* I = 1: options read at run time; I = 2: a ctx without ablation / SMEM32 options */
+        if (kind == HR_READ) hr_check_read<I == 1>(d, t, sp, w);
+        else if (kind == HR_WRITE) hr_check_write<I == 1>(d, t, sp, w);
+        else hr_check_atomic<I == 1>(d, t, sp, w);
     }
 }
 
-template <bool I>
+template <int I>
 __device__ __forceinline__ void bar(const hr_dev &d, hr_thr &t)
 {
     if (I) hr_syncthreads(d, t);
@@ -35,7 +42,7 @@ __device__ __forceinline__ void bar(const hr_dev &d, hr_thr &t)
 }
 
 /* ---- C1: tree reduction, 1 block x 32 threads ---- */
-template <bool I>
+template <int I>
 __global__ void __launch_bounds__(32) c1_kernel(hr_dev d, int *data, int rounds, int removed)
 {
     __shared__ int s[256];
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(32) c1_array_kernel(hr_dev d, int *data, int r
 }
 
 /* ---- C3: 2D Jacobi stencil through two SMEM tiles ---- */
-template <bool I>
+template <int I>
 __global__ void __launch_bounds__(256) c3_kernel(hr_dev d, int *data, int n, int sweeps, int removed)
 {
     constexpr int T = 16, H = 18, TILE = H * H;
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(256) c3_kernel(hr_dev d, int *data, int n, int
 }
 
 /* ---- C4: BFS level step and degree histogram, thread per vertex ---- */
-template <bool I>
+template <int I>
 __global__ void __launch_bounds__(256) c4_level_kernel(hr_dev d, int *data, uint32_t n, const uint64_t *rp,
                                                        const uint32_t *col, const int *flevel, int L, int racy)
 {
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(256) c4_level_kernel(hr_dev d, int *data, uint
     }
 }
 
-template <bool I>
+template <int I>
 __global__ void __launch_bounds__(256) c4_hist_kernel(hr_dev d, int *data, uint32_t n, const uint64_t *rp,
                                                       int racy)
 {
@@ -297,8 +304,9 @@ extern "C" hr_status hrb_c1(hr_ctx *ctx, int instrumented, uint32_t kernel_id, i
     hr_status st = prepare(ctx, instrumented, kernel_id, stream, &d);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    if (instrumented) c1_kernel<true><<<1, 32, 0, s>>>(d, data, rounds, removed);
-    else c1_kernel<false><<<1, 32, 0, s>>>(d, data, rounds, removed);
+    if (!instrumented) c1_kernel<0><<<1, 32, 0, s>>>(d, data, rounds, removed);
+    else if (rt_opts(d)) c1_kernel<1><<<1, 32, 0, s>>>(d, data, rounds, removed);
+    else c1_kernel<2><<<1, 32, 0, s>>>(d, data, rounds, removed);
     return launched();
 }
 
@@ -321,8 +329,9 @@ extern "C" hr_status hrb_c3(hr_ctx *ctx, int instrumented, uint32_t kernel_id, i
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (unsigned)((n / 16) * (n / 16));
-    if (instrumented) c3_kernel<true><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
-    else c3_kernel<false><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
+    if (!instrumented) c3_kernel<0><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
+    else if (rt_opts(d)) c3_kernel<1><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
+    else c3_kernel<2><<<blocks, 256, 0, s>>>(d, data, n, sweeps, removed);
     return launched();
 }
 
@@ -335,8 +344,9 @@ extern "C" hr_status hrb_c4_level(hr_ctx *ctx, int instrumented, uint32_t kernel
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (n + 255) / 256;
-    if (instrumented) c4_level_kernel<true><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
-    else c4_level_kernel<false><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
+    if (!instrumented) c4_level_kernel<0><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
+    else if (rt_opts(d)) c4_level_kernel<1><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
+    else c4_level_kernel<2><<<blocks, 256, 0, s>>>(d, data, n, rp, col, flevel, level, racy);
     return launched();
 }
 
@@ -348,7 +358,8 @@ extern "C" hr_status hrb_c4_hist(hr_ctx *ctx, int instrumented, uint32_t kernel_
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (n + 255) / 256;
-    if (instrumented) c4_hist_kernel<true><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
-    else c4_hist_kernel<false><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
+    if (!instrumented) c4_hist_kernel<0><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
+    else if (rt_opts(d)) c4_hist_kernel<1><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
+    else c4_hist_kernel<2><<<blocks, 256, 0, s>>>(d, data, n, rp, racy);
     return launched();
 }

@@ -115,7 +115,7 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
     uint32_t ei = 0;
     if (valid && (__ffs(peers) - 1) == (int)lane) {
         const bool sh = space != 0u;
-        const uint32_t sa = hr__saddr(d, t, local);
+        const uint32_t sa = hr__saddr<ABL>(d, t, local);
         unsigned long long *gp = d.gshadow + local;
         const bool fastexit = !hr__opt<ABL>(d, HR_OPT_NO_FASTEXIT);
         const uint32_t last = 31u - __clz(peers);
@@ -124,7 +124,7 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
         uint32_t fresh;
         unsigned long long old = hr__first<ABL>(d, t, sh, sa, gp, kind, fresh);
         while (true) {
-            const unsigned long long lv = hr__live(d, old);
+            const unsigned long long lv = sh ? old : hr__live(d, old);
             const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
             uint32_t rinfo, rel;
             const uint32_t cur = hr__pool_transition(d, t, lv, ps, lane, peers, rinfo, rel);
@@ -138,7 +138,7 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
                 if (fresh == HR_OLD_FRESH) break;
                 if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
             }
-            const unsigned long long prv = sh ? hr__cas_sh(d, t, sa, old, nw) : hr__cas_g(gp, old, nw);
+            const unsigned long long prv = sh ? hr__cas_sh<ABL>(d, t, sa, old, nw) : hr__cas_g(gp, old, nw);
             if (prv == old) {
                 if (rinfo) ei = rinfo | (cur == HR_RACE_GRID ? 1u : 0u);
                 break;
