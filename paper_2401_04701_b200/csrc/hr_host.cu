@@ -27,6 +27,7 @@
 #include "hr_classes.cuh"
 #include "hr_pack.cuh"
 #include "hr_compact.cuh"
+#include "hr_bserial.cuh"
 #include "fsm_table.inc"
 #include "fsm_classes.inc"
 
@@ -531,6 +532,26 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     if (!pool) split = 0;
     const uint32_t nhw = (uint32_t)warps << split;
     const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE | HR_OPT_SMEM32);
+    if (kind == HR_K_POOL && t->format == HR_TRACE_U64 && (c->cfg.options & HR_OPT_BSERIAL)) {
+        const size_t bsm = hr_bserial_smem((uint32_t)smem_words, (c->cfg.options & HR_OPT_SMEM32) != 0);
+        if (bsm <= 227 * 1024) {
+            void (*bk)(hr_dev, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t) =
+                abl ? hr_replay_bserial_kernel<true> : hr_replay_bserial_kernel<false>;
+            if (bsm > 48 * 1024) CU(cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+            bool timing = c->cfg.options & HR_OPT_TIMING;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+            const uint32_t nb = (uint32_t)(b1 - b0);
+            c->launches++;
+            bk<<<(nb + HR_BS_WARPS - 1) / HR_BS_WARPS, HR_BS_WARPS * 32, bsm, s>>>(
+                d, t->rec, woff + woi + b0 * warps, nb, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
+            CU(cudaGetLastError());
+            if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
+            c->last_kernel = kid;
+            c->have_kernel = true;
+            return HR_OK;
+        }
+    }
     if (kind == HR_K_POOL_WIDE && !(c->cfg.options & HR_OPT_NO_COMPACT)) {
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;

@@ -563,3 +563,70 @@ def test_report_async_c5_planted_repeated():
     ck.close()
     assert fl == 0
     assert [(int(r["word"]), int(r["scope"])) for r in raw] == c5.planted(lb)
+
+
+# ---- HR_OPT_BSERIAL: block-serial pooled replay (hr_bserial.cuh) ----
+BS = 16384 | 32                                      # forced, with the pooled kernel choice
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("extra", [0, 1, 4096, 8192, 2048])
+def test_bserial_random_programs(seed, extra):
+    """Barriers, __syncwarp, shared and global words, full and ragged warps,
+    up to 8 warps per block: the block-serial walk gives the oracle's set."""
+    tr = _random_batch(400 + seed, 40, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12, n_words=40,
+                       spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
+    g, fl = gpu_set(tr, options=BS | extra)
+    bc, wc = (9, 8) if extra == 4096 else (16, 16)
+    o, ofl = oracle_set(tr, bc_bits=bc, wc_bits=wc)
+    assert g == o and fl == ofl
+    tr = _random_batch(500 + seed, 200, max_blocks=2, max_warps=4, max_lanes=3, max_slots=6, n_words=3,
+                       spaces=(0, 1))
+    assert gpu_set(tr, options=BS | extra) == oracle_set(tr)
+
+
+def test_bserial_suite_listings_and_shards():
+    from tracegen import suite
+    for c in suite.suite():
+        assert gpu_set(c.trace, options=BS) == oracle_set(c.trace), c.name
+    for tr in (tp.listing1(64, 8, 32), tp.listing2(3, 4, 32), tp.listing4(1, 2, 32, 40),
+               tp.c1_tree_reduction(removed=32)):
+        assert gpu_set(tr, options=BS) == oracle_set(tr)
+    h = hr()
+    tr = _random_batch(51, 20, max_blocks=4, max_warps=4, max_lanes=32, max_slots=10, n_words=3000, spaces=(0, 1))
+    gmax, smem = h.trace_extent(tr)
+    full, _ = gpu_set(tr)
+    for n, g in ((2, 9), (8, 3), (8, 0)):
+        union = []
+        for r in range(n):
+            ck = h.Checker(gmax, smem, shard=(r, n), granule_log2=g, options=BS)
+            ck.replay(h.DeviceTrace.from_trace(tr))
+            races, _, _ = ck.report()
+            ck.close()
+            union += [tuple(x) for x in races]
+        assert sorted(union) == full
+
+
+def test_bserial_clock_overflow():
+    ev = {(0, 0, 0): [tf.W(0)] + [tf.SYNCTHREADS] * 4 + [tf.W(1)],
+          (0, 0, 1): [tf.W(0)] + [tf.SYNCTHREADS] * 4 + [tf.W(1)]}
+    tr = tp.from_thread_events(1, 1, 2, ev)
+    g, fl = gpu_set(tr, bc_bits=2, wc_bits=30, options=BS)
+    o, ofl = oracle_set(tr, bc_bits=2, wc_bits=30)
+    assert g == o and fl == ofl == hr().HR_F_CLOCK_OVERFLOW
+
+
+def test_bserial_c5_planted():
+    from tracegen import c5
+    h = hr()
+    lb = 8
+    for n in (1, 8):
+        for r in ((0, n - 1) if n > 1 else (0,)):
+            rec, woff, kd = c5.gpu_trace(lb, rank=r, nshard=n)
+            ck = h.Checker(c5.total_words(lb), 0, ring_capacity=1 << 16, shard=(r, n), options=BS | h.HR_OPT_LAZY_RESET)
+            ck.replay(h.DeviceTrace(rec, woff, kd))
+            raw, fl = ck.report_raw()
+            ck.close()
+            from paper_2401_04701_b200.multigpu import shard_owner
+            want = [(w, sc) for w, sc in c5.planted(lb) if n == 1 or shard_owner(w >> 3, n) == r]
+            assert fl == 0 and [(int(x["word"]), int(x["scope"])) for x in raw] == want
