@@ -612,8 +612,10 @@ def main():
             "gpu_launches": n_launch,
             "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch,
                                     "rule": "every libhirace kernel launched in the timed region: the replay, "
-                                            "the report's key / head / emit kernels, its 2 CUB radix sorts "
-                                            "(10 kernels each) and CUB scan (2)"},
+                                            + ("the report's key / head / emit kernels, its 2 CUB radix sorts "
+                                               "(10 kernels each) and CUB scan (2)" if async_report else
+                                               "the report's key / gather kernels and its 2 CUB radix sorts "
+                                               "(10 kernels each)")},
             "slowdown": slow,
             "cpu_baseline": cpu,
             "parity_vs_closed_form": parity_ok,
