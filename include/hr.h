@@ -202,6 +202,17 @@ hr_status hr_init(const hr_config *cfg, hr_ctx **out);
  * hr_shadow_alloc.  Default: rank 0 of 1. */
 hr_status hr_set_shard(hr_ctx *ctx, uint32_t rank, uint32_t count);
 
+/* Representative threads ("the memory footprint can be reduced
+ * by tracking only representative threads for user-defined symmetric work
+ * groups instead of tracking all threads"): from the next replay or online
+ * kernel on, only threads of simulated blocks with block % block_stride == 0
+ * and warps with warp % warp_stride == 0 are checked; the others still take
+ * part in barriers.  The result is exactly the race set of the trace
+ * restricted to those threads; races that need a non-representative thread
+ * are not seen (the user asserts the symmetry).  1, 1 = every thread
+ * (default).  HR_E_ARG on a zero stride. */
+hr_status hr_set_representatives(hr_ctx *ctx, uint32_t block_stride, uint32_t warp_stride);
+
 /* Same with a shard granule of 2^granule_log2 words (0..24; hr_set_shard uses
  * 3 = 8 words, 64 B of shadow: on C5 it balances the Zipf-hot atomic words
  * best; 9 = 4 KiB leaves the hottest granule's rank 1.2x slower at N = 8).  Smaller granules spread power-law hot words over

@@ -66,6 +66,9 @@ struct hr_dev {
     uint32_t bc_max, wc_max;
     uint32_t options;             /* HR_OPT_* */
     uint32_t block_base;          /* simulated block of blockIdx 0 (chunked replay launches) */
+    uint32_t rep_bstride, rep_wstride; /* representative threads (hr_set_representatives): only
+                                          blocks % rep_bstride == 0 and warps % rep_wstride == 0
+                                          are checked; 1 = all */
     uint32_t epoch_tag;           /* HR_OPT_LAZY_RESET: kernel epoch tag 1..15 in bits [31:28] of the
                                      shadow's clock word; a global word with another tag is INIT.
                                      0 = off (the shadow is zeroed at every kernel boundary) */
@@ -270,6 +273,18 @@ __device__ __forceinline__ unsigned long long hr__cas_sh(const hr_dev &d, const 
         return r == c ? cmp : hr__s32_unpack(r, t.tid(), d.wc_bits, d.epoch_tag << 28);
     }
     return hr__cas_s(a, cmp, val);
+}
+
+/* t.off of a thread of simulated block `block`, warp `warp`: bit 1 = its block's
+ * shared instance belongs to another address shard, bit 0 = not a representative
+ * thread ("tracking only representative threads for user-defined
+ * symmetric work groups"), so its accesses are not checked. */
+__device__ __forceinline__ uint32_t hr__thread_off(const hr_dev &d, uint32_t block, uint32_t warp)
+{
+    const uint32_t sh = ((block & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
+    const bool rep = (d.rep_bstride <= 1u || block % d.rep_bstride == 0u) &&
+                     (d.rep_wstride <= 1u || warp % d.rep_wstride == 0u);
+    return sh | (rep ? 0u : 1u);
 }
 
 /* a2: shard-local shadow index; false if this ctx does not check the access. */
@@ -537,7 +552,7 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     t.sshadow = (uint32_t)__cvta_generic_to_shared(smem_shadow);
     t.swords = smem_words;
     t.fsm = (uint32_t)__cvta_generic_to_shared(smem_fsm);
-    t.off = ((block & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
+    t.off = hr__thread_off(d, block, ltid >> 5);
     return t;
 }
 

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(HR_BS_WARPS * 32, 64 / HR_BS_WARPS) hr_replay_
     t.sshadow = smem0 + sh0;
     t.swords = smem_words;
     t.fsm = smem0;
-    t.off = ((blk & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
+    t.off = hr__thread_off(d, blk, 0u) & 2u;   /* representatives: per simulated warp below */
     const uint64_t *wo = woff + (uint64_t)sb * warps;
     const uint32_t tag_hi = d.epoch_tag << 28;
     const bool active = lane < lanes;
@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(HR_BS_WARPS * 32, 64 / HR_BS_WARPS) hr_replay_
                     __syncwarp();
                     continue;
                 }
-                const bool v = !bc_off && !((wc_off >> sw) & 1u) && hr__pool_owned(d, t, x, 0u, 0u);
+                const bool v = !bc_off && !((wc_off >> sw) & 1u) && !(hr__thread_off(d, blk, sw) & 1u) &&
+                               hr__pool_owned(d, t, x, 0u, 0u);
                 const unsigned vm = __ballot_sync(0xffffffffu, v);
                 const uint32_t k = __popc(vm);
                 if (!k) continue;

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr
     hr_thr t = hr_thread_begin(d, hr_smem, sshadow, smem_words);
 #ifdef HR_FUZZ
     const uint32_t cta = gridDim.x - 1u - blockIdx.x;
-    t.off = (((d.block_base + cta) & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
+    t.off = hr__thread_off(d, d.block_base + cta, 0u);
 #else
     const uint32_t cta = blockIdx.x;
 #endif
@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr
     const uint32_t warp = hw % warps, helper = hw / warps;
     const uint32_t nhw = warps << split_log2;
     t.meta = ((unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT) | (uint32_t)t.meta;
+    t.off = hr__thread_off(d, d.block_base + cta, warp);
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const uint64_t w = (uint64_t)cta * warps + warp;
     const uint64_t nsg = segoff[w + 1] - segoff[w];

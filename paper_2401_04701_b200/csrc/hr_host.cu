@@ -46,6 +46,7 @@ struct hr_ctx {
     uint64_t launches = 0;
     uint32_t epoch_tag = 0;                      /* HR_OPT_LAZY_RESET: tag of the current kernel (1..15) */
     uint32_t sort_tmp_n = 0;                     /* cached CUB temp size of the report sort */
+    uint32_t rep_bstride = 1, rep_wstride = 1;   /* hr_set_representatives */
     size_t sort_tmp_bytes = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
@@ -142,6 +143,8 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.bc_max = (1u << c->cfg.bc_bits) - 1u;
     d.wc_max = (1u << c->cfg.wc_bits) - 1u;
     d.options = c->cfg.options;
+    d.rep_bstride = c->rep_bstride;
+    d.rep_wstride = c->rep_wstride;
     if (d.options & HR_OPT_SMEM32) {            /* the 32-bit shared word holds bc:9, wc:8 */
         d.bc_max = std::min(d.bc_max, 511u);
         d.wc_max = std::min(d.wc_max, 255u);
@@ -216,6 +219,14 @@ extern "C" hr_status hr_set_shard_ex(hr_ctx *c, uint32_t rank, uint32_t count, u
     c->shard_count = count;
     c->shard_log2 = 0;
     while ((1u << c->shard_log2) < count) c->shard_log2++;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_set_representatives(hr_ctx *c, uint32_t block_stride, uint32_t warp_stride)
+{
+    if (!c || block_stride == 0 || warp_stride == 0) return HR_E_ARG;
+    c->rep_bstride = block_stride;
+    c->rep_wstride = warp_stride;
     return HR_OK;
 }
 

@@ -264,7 +264,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
 #ifdef HR_FUZZ
     const uint32_t cta = gridDim.x - 1u - blockIdx.x;               /* reversed block mapping */
     t.meta = ((unsigned long long)(((d.block_base + cta) << 10) | (t.tid() & 1023u)) << HR_TID_SHIFT) | (uint32_t)t.meta;
-    t.off = (((d.block_base + cta) & ((1u << d.shard_log2) - 1u)) == d.shard_rank) ? 0u : 2u;
+    t.off = hr__thread_off(d, d.block_base + cta, (t.tid() >> 5) & 31u);
 #else
     const uint32_t cta = blockIdx.x;
 #endif
@@ -278,6 +278,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     if (POOL && split_log2)
         t.meta = ((unsigned long long)(((d.block_base + cta) << 10) | (warp << 5) | lane) << HR_TID_SHIFT) |
                  (uint32_t)t.meta;
+    if (POOL && split_log2) t.off = hr__thread_off(d, d.block_base + cta, warp);
     const uint64_t gw = (uint64_t)cta * warps + warp;
     const uint64_t r0 = woff[gw];
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);

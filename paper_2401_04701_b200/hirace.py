@@ -35,7 +35,7 @@ HR_OPT_SPECULATE = 2048
 HR_OPT_SMEM32 = 4096
 HR_OPT_LAZY_RESET = 8192
 HR_OPT_BSERIAL = 16384
-EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
+EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_report_async",
            "hr_report_collect", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing", "hr_launch_count",
@@ -88,6 +88,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     sig = {
         "hr_init": ([P(HrConfig), P(vp)], ctypes.c_int),
         "hr_set_shard": ([vp, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
+        "hr_set_representatives": ([vp, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
         "hr_set_shard_ex": ([vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
         "hr_shadow_alloc": ([vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, P(vp)], ctypes.c_int),
         "hr_kernel_begin": ([vp, vp], ctypes.c_int),
@@ -140,6 +141,11 @@ def hr_init(bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, 
 
 def hr_set_shard(ctx, rank: int, count: int, granule_log2: int = 3):
     _check(load().hr_set_shard_ex(ctx, rank, count, granule_log2), ctx, "hr_set_shard_ex")
+
+
+def hr_set_representatives(ctx, block_stride: int = 1, warp_stride: int = 1):
+    """Check only blocks % block_stride == 0 and warps % warp_stride == 0."""
+    _check(load().hr_set_representatives(ctx, block_stride, warp_stride), ctx, "hr_set_representatives")
 
 
 def hr_shadow_alloc(ctx, space: int, base_word: int, n_words: int) -> int:
@@ -497,7 +503,10 @@ def check_trace(trace, device: int = 0, compact: bool = False, packed: bool = Fa
     """Replay a host trace on the GPU and return (sorted racy set, flags).
     packed=True replays the hr_pack_trace encoding of it instead."""
     gmax, smem = trace_extent(trace)
+    reps = kw.pop("representatives", None)
     ck = Checker(gmax, smem, device=device, **kw)
+    if reps is not None:
+        hr_set_representatives(ck.ctx, *reps)
     dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}", compact=compact and not packed)
     if packed:
         dt = ck.pack(dt)

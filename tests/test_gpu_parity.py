@@ -630,3 +630,42 @@ def test_bserial_c5_planted():
             from paper_2401_04701_b200.multigpu import shard_owner
             want = [(w, sc) for w, sc in c5.planted(lb) if n == 1 or shard_owner(w >> 3, n) == r]
             assert fl == 0 and [(int(x["word"]), int(x["scope"])) for x in raw] == want
+
+
+# ---- representative threads (hr_set_representatives) ----
+def _only_representatives(tr, bs, ws):
+    """The trace with the access records of non-representative threads turned
+    into NOPs (their barrier records stay): what the oracle must see."""
+    import copy
+    out = copy.copy(tr)
+    rec = tr.rec.copy()
+    nop = np.uint64(3 << 62)
+    for k in range(tr.kdesc.shape[0]):
+        blocks, warps, lanes, smem, woi = (int(x) for x in tr.kdesc[k, :5])
+        for gw in range(blocks * warps):
+            b, w = gw // warps, gw % warps
+            if (bs <= 1 or b % bs == 0) and (ws <= 1 or w % ws == 0):
+                continue
+            seg = rec[int(tr.warp_off[woi + gw]) * 32: int(tr.warp_off[woi + gw + 1]) * 32]
+            seg[(seg >> np.uint64(62)) != 3] = nop
+    out.rec = rec
+    return out
+
+
+@pytest.mark.parametrize("reps", [(2, 1), (1, 2), (3, 2), (1, 1)])
+@pytest.mark.parametrize("options", [0, 16, 32, 256, 512, 16384 | 32])
+def test_representatives_equal_the_restricted_trace(reps, options):
+    tr = _random_batch(600, 30, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12, n_words=40,
+                       spaces=(0, 1), p_barrier=0.25, p_skip=0.5)
+    g = [tuple(r) for r in hr().check_trace(tr, options=options, representatives=reps)[0]]
+    want, _ = oracle_set(_only_representatives(tr, *reps))
+    assert g == want
+    if reps != (1, 1):
+        assert len(want) < len(oracle_set(tr)[0])          # the filter drops races, by design
+
+
+def test_representatives_suite():
+    from tracegen import suite
+    for c in suite.suite()[::5]:
+        g = [tuple(r) for r in hr().check_trace(c.trace, representatives=(2, 2))[0]]
+        assert g == oracle_set(_only_representatives(c.trace, 2, 2))[0], c.name
