@@ -131,10 +131,18 @@ class Clocks:
             self.p.kill()
         self.f.flush()
         self.f.seek(0)
+        out = self.parse(self.f.read(), self.t0, self.t1)
+        os.unlink(self.f.name)
+        return out
+
+    @staticmethod
+    def parse(text: str, t0=None, t1=None) -> dict:
+        """Median SM clock, max clock and throttle reasons of the nvidia-smi
+        samples stamped inside [t0, t1] (host epoch seconds; None = all)."""
         import datetime
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
+        for line in text.splitlines():
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 10:
                 continue
@@ -142,7 +150,7 @@ class Clocks:
                 ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
             except ValueError:
                 ts = None
-            if ts is not None and self.t0 is not None and not (self.t0 - 0.05 <= ts <= (self.t1 or ts) + 0.05):
+            if ts is not None and t0 is not None and not (t0 - 0.05 <= ts <= (t1 or ts) + 0.05):
                 continue
             try:
                 sm.append(float(parts[2]))
@@ -152,7 +160,6 @@ class Clocks:
             for n, v in zip(names, parts[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
