@@ -61,7 +61,7 @@ def parse():
                     help="address-shard granule (2^g words; 3 = 64 B of shadow)")
     ap.add_argument("--double-shadow", action="store_true",
                     help="HR_OPT_DOUBLE_SHADOW: reset the previous kernel's shadow on a side stream")
-    ap.add_argument("--format", default="u64", choices=["c32", "u64"],
+    ap.add_argument("--format", default="c32", choices=["c32", "u64"],
                     help="device-resident trace encoding (include/hr.h HR_TRACE_U64 = 256 B/row, C32 = 160 B/row)")
     ap.add_argument("--e2e-format", default="packed", choices=["packed", "c32", "u64"],
                     help="host-buffer trace encoding for e2e: packed (HR_TRACE_PACKED, decoded on the device), "
