@@ -210,8 +210,11 @@ __device__ __forceinline__ bool hr__pool_owned(const hr_dev &d, const hr_thr &t,
 #ifndef HR_STAGE_NB_WIDE
 #define HR_STAGE_NB_WIDE 2u
 #endif
+#ifndef HR_STAGE_NB_ROW
+#define HR_STAGE_NB_ROW 2u
+#endif
 template <bool WIDE> struct hr_stage_cfg {
-    static constexpr uint32_t NB = WIDE ? HR_STAGE_NB_WIDE : 2u;
+    static constexpr uint32_t NB = WIDE ? HR_STAGE_NB_WIDE : HR_STAGE_NB_ROW;
     static constexpr uint32_t CH = WIDE ? 8u : 4u;
 };
 
