@@ -5,9 +5,11 @@ Workload (BASELINE.json configs[4], the multi-GPU config the metric is
 quoted on): C5 — a 2^32-access global trace over a 2^32-word (16 GiB)
 address space, 2^16 blocks x 256 threads x 256 accesses, address-sharded
 across N GPUs (tracegen/c5gen.h).  One STEP = one pass of the whole hot path
-over the trace: report-ring reset, kernel-boundary shadow reset (a11), the
-replay kernel (a1-a10, a12), hr_report (a13: D2H + sort/merge) and, for
-N > 1, the NCCL allgather of the per-shard race sets.
+over the trace: report-ring reset, kernel-boundary reset (a11: epoch tags, a
+real memset every 15 kernels), the replay kernel (a1-a10, a12), the report
+(a13: at N = 1 hr_report_async, sorted and merged on the device and written
+to pinned host memory; at N > 1 hr_report plus the NCCL allgather of the
+per-shard race sets).
 
   value  device-resident: trace generated in HBM before timing; K steps timed
          with CUDA events on the launching stream, max over ranks.
