@@ -102,6 +102,7 @@ enum {
                                     DOUBLE_SHADOW; wc_bits <= 24. */
     HR_OPT_BSERIAL = 16384u,     /* sparse U64 traces (pooled replay): one CUDA warp replays a whole
                                     simulated block epoch by epoch (hr_bserial.cuh) */
+    HR_OPT_ROW_NARROW = 65536u,  /* force the 32-register row kernel (64 warps/SM) */
     HR_OPT_SPECULATE = 2048u     /* ablation: global reads/writes skip Algorithm 1's first atomic read
                                     and CAS against INIT (the CAS return is the read when it fails).
                                     Measured slower: a failed CAS costs an L2 atomic round trip that

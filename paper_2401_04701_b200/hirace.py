@@ -35,6 +35,7 @@ HR_OPT_SPECULATE = 2048
 HR_OPT_SMEM32 = 4096
 HR_OPT_LAZY_RESET = 8192
 HR_OPT_BSERIAL = 16384
+HR_OPT_ROW_NARROW = 65536
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_report_async",
            "hr_report_collect", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",

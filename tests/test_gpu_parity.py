@@ -71,7 +71,7 @@ def test_random_small_family(seed, options):
 
 
 @pytest.mark.parametrize("seed", range(4))
-@pytest.mark.parametrize("options", [16, 32, 256, 512])
+@pytest.mark.parametrize("options", [16, 32, 256, 512, 65536])
 def test_random_wide_grids(seed, options):
     """Full warps and many warps: exercises MATCH coalescing, multi-lane folds,
     CAS contention, several tiles of the shadow and ragged warp lengths, in
@@ -84,7 +84,7 @@ def test_random_wide_grids(seed, options):
     assert len(o) > 10
 
 
-@pytest.mark.parametrize("options", [16, 32, 256, 512])
+@pytest.mark.parametrize("options", [16, 32, 256, 512, 65536])
 def test_hot_words_contention(options):
     """Few words, 32 warps x 32 lanes x 16 blocks: heavy CAS retry storms."""
     tr = _random_batch(7, 10, max_blocks=16, max_warps=32, max_lanes=32, max_slots=8, n_words=3,
@@ -97,7 +97,8 @@ def test_hot_words_contention(options):
 
 @pytest.mark.parametrize("options", [1, 2, 3, 8, 2048, 16, 32, 32 | 1, 32 | 2048, 64, 64 | 32, 256, 256 | 1,
                                      256 | 2048, 512, 512 | 1, 512 | 2, 512 | 2048, 256 | 1024,
-                                     256 | 1024 | 2048, 16 | 2048 | 64])
+                                     256 | 1024 | 2048, 16 | 2048 | 64, 65536, 65536 | 1, 65536 | 2048,
+                                     65536 | 8192])
 def test_ablations_same_result(options):
     """Coalescing off / fast exits off / no speculation / forced row or pooled
     replay change the commit order and the traffic, never the result
