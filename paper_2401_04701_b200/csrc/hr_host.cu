@@ -55,6 +55,7 @@ struct hr_ctx {
     unsigned long long *counters = nullptr;
     unsigned char *fsm = nullptr;
     uint32_t last_kernel = 0;
+    uint32_t max_kernel = 0;                     /* largest kernel id replayed on this ctx (report sort range) */
     bool have_kernel = false;
     int last_kind = 0;                           /* HR_K_* of the last replay */
     /* kernel choice of the last probed device trace (a performance hint only:
@@ -496,6 +497,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
                                                       (uint32_t)lanes, (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
     c->last_kernel = kid;
+        c->max_kernel = std::max(c->max_kernel, kid);
     c->have_kernel = true;
     return HR_OK;
 }
@@ -525,6 +527,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         CU(cudaGetLastError());
         if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
         c->last_kernel = kid;
+        c->max_kernel = std::max(c->max_kernel, kid);
         c->have_kernel = true;
         return HR_OK;
     }
@@ -563,6 +566,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
             CU(cudaGetLastError());
             if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
             c->last_kernel = kid;
+        c->max_kernel = std::max(c->max_kernel, kid);
             c->have_kernel = true;
             return HR_OK;
         }
@@ -598,6 +602,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     CU(cudaGetLastError());
     if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
     c->last_kernel = kid;
+        c->max_kernel = std::max(c->max_kernel, kid);
     c->have_kernel = true;
     return HR_OK;
 }
@@ -1233,14 +1238,21 @@ extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
     c->launches++;
     hr_arep_keys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, cap, lo0, ix0);
     CU(cudaGetLastError());
-    c->launches += 10;
-    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)cap, 0, 64, s));
+    /* only the key bits that can be set: words < max(global end, shared words),
+     * hi = kernel << 33 | space << 32 | block with kernel <= last_kernel; the
+     * padding keys (~0) stay the largest within the range, and the sorts are
+     * stable, so real records still precede them (fewer radix passes) */
+    auto bits_of = [](uint64_t v) { int b = 0; while (b < 64 && (v >> b)) b++; return b; };
+    const int lo_bits = std::max(1, std::min(64, bits_of(std::max<uint64_t>(c->gbase + c->gwords, c->smem_words_max))));
+    const int hi_bits = std::min(64, 33 + bits_of((uint64_t)std::max(c->max_kernel, c->last_kernel) + 1));
+    c->launches += 2 + (lo_bits + 7) / 8;        /* onesweep: histogram + scan + one pass per 8 bits */
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)cap, 0, lo_bits, s));
     c->launches++;
     hr_arep_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix1, cap, hi0);
     CU(cudaGetLastError());
     tb = c->arep_tmp_bytes;
-    c->launches += 10;
-    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)cap, 0, 64, s));
+    c->launches += 2 + (hi_bits + 7) / 8;
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)cap, 0, hi_bits, s));
     c->launches++;
     hr_arep_heads_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, cap, head);
     CU(cudaGetLastError());
