@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c5", "c3"],
+                    help="c5 (default): the BASELINE metric's workload; c3: the shared-memory stencil "
+                         "(BASELINE configs[2]), bound by instruction issue, not HBM")
     ap.add_argument("--lb", type=int, default=16, help="log2 blocks of C5 (16 = full 2^32 accesses)")
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -253,8 +256,28 @@ def sum_over_ranks(x: int, world: int) -> int:
     return int(t.item())
 
 
-def cpu_baseline(lb: int, seed: int):
-    """The oracle as it stands, single-threaded, on a bounded C5 sample."""
+def host_cpu() -> dict:
+    """The oracle host: logical CPUs and model (SURVEY §8(d) "Oracle timing")."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"host_cpu_count": os.cpu_count(), "host_cpus_usable": usable, "host_cpu_model": model}
+
+
+def cpu_baseline(lb: int, seed: int, full_lb: int = 16):
+    """The oracle as it stands, single-threaded, on a bounded C5 sample (1/2^(16-lb)
+    of the blocks; every block has the same access mix, so the per-access rate
+    and the x2^(16-lb) extrapolated full-step time are labelled as such)."""
     import oracle
     from tracegen import c5
     tr = c5.cpu_trace(lb, seed)
@@ -262,9 +285,14 @@ def cpu_baseline(lb: int, seed: int):
     res = oracle.check(tr, mode=oracle.BUCKETED)
     dt = time.perf_counter() - t0
     ok = [(r.word, r.scope) for r in res.races] == c5.planted(lb, seed)
-    return {"value": res.n_accesses / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"C5 shape at 2^{lb} blocks ({res.n_accesses} accesses, 1/{2 ** (16 - lb)} of the "
-                      f"blocks), bucketed mode, {dt:.2f} s; racy set == planted: {ok}"}
+    scale = 2 ** (full_lb - lb)
+    out = {"value": res.n_accesses / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"C5 shape at 2^{lb} blocks ({res.n_accesses} accesses, 1/{scale} of the "
+                     f"blocks), bucketed mode, {dt:.2f} s; racy set == planted: {ok}",
+           "sample_s": dt, "extrapolated_full_step_s": dt * scale,
+           "extrapolation": f"x{scale} (EXTRAPOLATED from the 1/{scale} sample, not measured)"}
+    out.update(host_cpu())
+    return out
 
 
 def measure_slowdown(dt, kern_ms_launch: float, data_words: int, c4_lv: int):
@@ -329,10 +357,152 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": f"C5 sample: 2^{args.ref_lb} blocks x 256 threads x 256 accesses "
                                f"(same generator as the GPU arm's 2^{args.lb}-block workload)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"C5 at 2^{args.ref_lb} blocks per step, bucketed single-threaded oracle"},
+        "cpu_baseline": dict({"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                              "sample": f"C5 at 2^{args.ref_lb} blocks per step, bucketed single-threaded oracle",
+                              "extrapolated_full_step_s": dt / args.steps * 2 ** (args.lb - args.ref_lb),
+                              "extrapolation": f"x{2 ** (args.lb - args.ref_lb)} (EXTRAPOLATED, not measured)"},
+                             **host_cpu()),
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def run_c3(args):
+    """--config c3: C3 (1024 blocks x 256 threads, 2^26 accesses, SMEM shadow)
+    on one GPU.  One step = ring reset + replay of the device-resident C32
+    trace + hr_report_async.  The SMEM shadow never reaches DRAM, so the
+    roofline is instruction issue (bound "alu"): warp instructions per launch
+    (ncu smsp__inst_executed.sum of this build, profiles/c3_instructions.json)
+    / live kernel time, against 148 SMs x 4 schedulers x 1 warp-instr/clk x
+    the max SM clock (B300_MICROARCH.md issue model, B200 SM count)."""
+    import numpy as np
+    import torch
+    from paper_2401_04701_b200 import hirace as hr, online as on
+    from tracegen import stencil
+    spin = cuda_spin_wait(0) if not args.no_spin else False
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    removed, n = 20, stencil.N
+    tr = stencil.stencil_trace(removed=removed, n=n)
+    dt = hr.DeviceTrace.from_trace(tr, compact=True)
+    n_acc = int((((tr.rec >> np.uint64(62)) & np.uint64(3)) != 3).sum())
+    words, smem = 2 * n * n, 2 * stencil.TILE
+    ck = hr.Checker(words, smem, options=hr.HR_OPT_TIMING | args.options)
+    blocks = (n // stencil.T) ** 2
+    per_block = stencil.expected_racy_shared_words(removed)
+    want = [(0, 1, b, int(w), 1) for b in range(blocks) for w in per_block]
+
+    def step(replay):
+        ck.reset()
+        replay()
+        ck.report_async()
+
+    clocks = Clocks(0, args.clock_ms)
+    clocks.start()
+    dev = lambda: ck.replay(dt, stream)  # noqa: E731
+    for _ in range(max(args.warmup, 3)):
+        step(dev)
+    raw, flags = ck.collect_raw()
+    parity = [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+              for r in raw] == want and flags == 0
+    hr.hr_replay_timing(ck.ctx)
+    hr.hr_launch_count(ck.ctx)
+    steps = args.steps
+    torch.cuda.synchronize()
+    clocks.mark_start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step(dev)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks.mark_stop()
+    clk = clocks.stop()
+    ms_step = e0.elapsed_time(e1) / steps
+    _, _, kern_ms, n_kern = hr.hr_replay_timing(ck.ctx)
+    n_launch = hr.hr_launch_count(ck.ctx)
+    raw, flags = ck.collect_raw()
+    parity = parity and [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+                         for r in raw] == want
+    k_ms = kern_ms / max(n_kern, 1)
+    hbm, hbm_kind = peaks()
+    sm_max = clk.get("sm_max_mhz") or 1965.0
+    issue_peak = 148 * 4 * sm_max * 1e6 / 1e9                          # G warp-instructions/s
+    instr, achieved = None, None
+    prof = os.path.join(ROOT, "profiles", "c3_instructions.json")
+    if os.path.exists(prof):
+        pj = json.load(open(prof))
+        instr = float(pj["inst_executed_per_launch"])
+        achieved = instr / (k_ms / 1e3) / 1e9
+    # e2e: the same steps from pinned host buffers (C32 records copied H2D in every step)
+    import torch as _t
+    pinned = {}
+    for name in ("rec32", "recop"):
+        x = getattr(dt, name)
+        h = _t.empty(x.numel(), dtype=x.dtype, pin_memory=True)
+        h.copy_(x)
+        pinned[name] = h
+    host = type("T", (), {})()
+    host.kdesc, host.warp_off, host.rec = dt.kdesc, dt.warp_off.cpu().numpy().view(np.uint64), None
+    host.rec32, host.recop = pinned["rec32"].numpy().view(np.uint32), pinned["recop"].numpy()
+    h2d = int(host.rec32.nbytes + host.recop.nbytes + host.warp_off.nbytes)
+    hrep = lambda: ck.replay_host(host, stream)  # noqa: E731
+    for _ in range(2):
+        step(hrep)
+    ck.collect_raw()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(steps):
+        step(hrep)
+    f1.record()
+    torch.cuda.synchronize()
+    raw_e, _ = ck.collect_raw()
+    e2e_ms = f0.elapsed_time(f1) / steps
+    parity = parity and len(raw_e) == len(want)
+    slow = None
+    if not args.no_slowdown:
+        d3 = torch.randint(0, 100, (words,), dtype=torch.int32, device="cuda")
+        ck3 = hr.Checker(words, smem)
+        slow = {"c3_online": on.slowdown(lambda: on.c3(None, d3, False), lambda: on.c3(ck3.ctx, d3, True), reps=10)}
+        ck3.close()
+        data = torch.zeros(words, dtype=torch.int32, device="cuda")
+        raw_ms = on.time_ms(lambda: on.raw_replay(dt, data, words), reps=5, warmup=2)
+        slow["c3_replay"] = {"checked_kernel_ms": k_ms, "raw_replay_ms": raw_ms, "slowdown": k_ms / raw_ms}
+    cpu = None
+    if not args.no_cpu:
+        import oracle
+        small = stencil.stencil_trace(removed=removed, n=64)
+        t0 = time.perf_counter()
+        res = oracle.check(small, mode=oracle.BUCKETED)
+        dtc = time.perf_counter() - t0
+        cpu = dict({"value": res.n_accesses / dtc, "unit": UNIT, "cores": 1, "kind": "oracle",
+                    "sample": f"C3 at n=64 (16 of the 1024 blocks, {res.n_accesses} accesses), bucketed, "
+                              f"{dtc:.2f} s", "extrapolated_full_step_s": dtc * n_acc / res.n_accesses,
+                    "extrapolation": "x64 by access count (EXTRAPOLATED, not measured)"}, **host_cpu())
+    out = {
+        "metric": METRIC, "value": n_acc / (ms_step / 1e3), "unit": UNIT, "n_gpus": 1, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"C3: shared-memory 2D stencil {n}x{n}, {blocks} blocks x 256 threads, 42 sweeps, "
+                               f"barrier after sweep {removed} removed, {n_acc} checked accesses",
+                   "trace_format": "c32", "host_wait": "spin" if spin else "default",
+                   "report": "hr_report_async every step", "l2": "trace (0.34 GB) > L2 is streamed; the SMEM "
+                   "shadow is per block; no flush needed"},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": issue_peak, "unit": "G warp-instr/s",
+                     "frac": (achieved / issue_peak) if achieved else None, "traffic": None,
+                     "kernel": "hr_replay_kernel", "kernel_ms": k_ms,
+                     "inst_executed_per_launch": instr,
+                     "inst_per_warp_row": (instr / (dt.n_rows)) if instr else None,
+                     "peak_rule": "148 SMs x 4 SMSPs x 1 warp-instruction/clk x sm_max_mhz",
+                     "literal_frac": 8 * n_acc / (k_ms / 1e3) / 1e9 / hbm, "literal_peak_kind": hbm_kind},
+        "clocks": clk,
+        "e2e": {"value": n_acc / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 16 + 24 * len(raw_e), "ms_per_step": e2e_ms, "format": "c32"},
+        "gpu_launches": n_launch,
+        "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch},
+        "slowdown": slow, "cpu_baseline": cpu, "parity_vs_closed_form": parity,
+    }
+    print(json.dumps(out), flush=True)
 
 
 def main():
@@ -340,10 +510,13 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.config == "c3":
+        run_c3(args)
+        return
     import numpy as np
     import torch
     from paper_2401_04701_b200 import hirace as hr
-    from paper_2401_04701_b200.multigpu import exchange_races, shard_owner
+    from paper_2401_04701_b200.multigpu import DeviceExchange, exchange_races, shard_owner
     from tracegen import c5
 
     spin = cuda_spin_wait(int(os.environ.get("LOCAL_RANK", "0"))) if not args.no_spin else False
@@ -393,7 +566,10 @@ def main():
                     granule_log2=args.granule_log2)
 
     step_log = [] if os.environ.get("HR_BENCH_STEPLOG") else None
-    async_report = world == 1 and not args.sync_report       # N > 1: the allgather needs the set per step
+    # N > 1: device report + allgather of the fixed-size per-rank buffers inside the step, merged
+    # on collect; N = 1: device report into pinned host memory
+    exchange = DeviceExchange(ck.ctx, 1 << 17) if world > 1 and not args.sync_report else None
+    async_report = world == 1 and not args.sync_report
 
     def step(replay_fn):
         if step_log is not None:                    # diagnostic: where a slow step spends its time
@@ -410,6 +586,11 @@ def main():
             t3 = time.perf_counter()
             step_log.append({"issue": round(1e3 * (t1 - t0), 2), "gpu_replay": round(ga.elapsed_time(gb), 2),
                              "wait": round(1e3 * (t2 - t1), 2), "report": round(1e3 * (t3 - t2), 2)})
+        elif exchange is not None:
+            ck.reset()
+            replay_fn()
+            exchange.step(stream)                   # a13 on the device + NCCL allgather, no host wait
+            return None, None
         elif async_report:
             ck.reset()
             replay_fn()
@@ -423,6 +604,12 @@ def main():
             raw, flags = exchange_races(raw, flags)
         return raw, flags
 
+    def collect():
+        """The last step's global set (after the loop: off the step's critical path)."""
+        if exchange is not None:
+            return exchange.collect(fallback_raw=lambda: ck.report_raw())
+        return ck.collect_raw()
+
     dev_replay = lambda: ck.replay(dt, stream)  # noqa: E731
 
     # clock sampler first: its start-up must not land in the timed region
@@ -431,8 +618,8 @@ def main():
     # warm-up + correctness of this run against the closed form (planted set)
     for _ in range(max(args.warmup, 1)):
         raw, flags = step(dev_replay)
-    if async_report and step_log is None:
-        raw, flags = ck.collect_raw()
+    if (async_report or exchange is not None) and step_log is None:
+        raw, flags = collect()
 
     def expected():
         pl = c5.planted(lb, seed)
@@ -470,8 +657,8 @@ def main():
         print("steplog:", json.dumps(step_log[-args.steps:]), file=sys.stderr)
     reset_ms, n_resets, kern_ms, n_kern = hr.hr_replay_timing(ck.ctx)
     n_launch = hr.hr_launch_count(ck.ctx)
-    if async_report and step_log is None:
-        raw, flags = ck.collect_raw()               # the last step's result, already in pinned host memory
+    if (async_report or exchange is not None) and step_log is None:
+        raw, flags = collect()                      # the last step's result (pinned host memory / gathered)
     parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw] == expected()
 
     ms_step = max_over_ranks(ms_total / args.steps, world)
@@ -485,19 +672,33 @@ def main():
     algo_bytes = dt.record_bytes() + BYTES_PER_ACCESS_ALGO * n_acc_rank
     achieved = algo_bytes / (kern_ms / max(n_kern, 1) / 1e3) / 1e9
     traffic = None
+    l2_atomic = None
     prof = os.path.join(ROOT, "profiles", "replay_dram_bytes.json")
+    rates_path = os.path.join(ROOT, "profiles", "b200_access_rates.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if world == 1 and int(pj.get("lb", -1)) == lb and pj.get("format", "u64") == args.format:
+            if world == 1 and int(pj.get("lb", -1)) == lb and pj.get("format", "u64") == args.format \
+                    and not emulated:
                 traffic = float(pj["dram_bytes_per_launch"])
+                if "l2_atom_cas_requests_per_launch" in pj and os.path.exists(rates_path):
+                    # north_star: "L2 atomic throughput against the chip's peak" — committed + failed
+                    # CAS requests the L2 served per second of the live launch, against the measured
+                    # L2 atomic unit rate (random 64-bit CAS on an L2-resident set)
+                    ops = float(pj["l2_atom_cas_requests_per_launch"])
+                    rl2 = json.load(open(rates_path))["random_cas_l2_per_s"]
+                    ach = ops / (kern_ms / max(n_kern, 1) / 1e3)
+                    l2_atomic = {"ops_per_launch": ops, "achieved_per_s": ach, "peak_per_s": rl2,
+                                 "frac": ach / rl2, "unit": "CAS/s",
+                                 "source": "ncu lts__t_requests_srcunit_tex_op_atom_dot_cas.sum of the same "
+                                           "launch (profiles/replay_dram_bytes.json); peak = measured random "
+                                           "64-bit CAS rate on an L2-resident set (profiles/b200_access_rates.json)"}
         except Exception:
             traffic = None
     literal = BYTES_PER_ACCESS_LITERAL * total_acc / (ms_step / 1e3) / 1e9 / (peak * world)
     # the floor that actually binds C5: random 8-byte RMWs on cold HBM words run at
     # the measured DRAM random-access rate, the rest streams at the copy peak
     ceiling = None
-    rates_path = os.path.join(ROOT, "profiles", "b200_access_rates.json")
     if os.path.exists(rates_path):
         rates = json.load(open(rates_path))
         floor_ms = 1e3 * (n_gather / rates["random_cas_hbm_per_s"] +
@@ -570,8 +771,8 @@ def main():
             raw_e, _ = step(host_replay)
         f1.record()
         torch.cuda.synchronize()
-        if async_report and step_log is None:
-            raw_e, _ = ck.collect_raw()
+        if (async_report or exchange is not None) and step_log is None:
+            raw_e, _ = collect()
         barrier(world)
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world)
         parity_ok = parity_ok and [(int(r["word"]), int(r["scope"])) for r in raw_e] == expected()
@@ -595,6 +796,9 @@ def main():
                        "trace_format": args.format, "host_wait": "spin" if spin else "default",
                        "report": ("hr_report_async: device sort/merge, result written to pinned host memory "
                                   "every step, collected after the loop" if async_report else
+                                  "hr_report_async_to into a device buffer + NCCL all_gather_into_tensor of the "
+                                  "2^17-record per-rank buffers every step (no host round trip); merged with "
+                                  "hr_merge_races after the loop" if exchange is not None else
                                   "hr_report: host round trip per step"),
                        "kernel_boundary_reset": ("memset per kernel" if (args.no_lazy_reset or args.double_shadow)
                                                  else "lazy: epoch-tagged shadow words, a real memset every 15 "
@@ -607,7 +811,13 @@ def main():
                          "kernel": "hr_replay_kernel", "kernel_ms": kern_ms / max(n_kern, 1),
                          "algo_bytes_per_launch": algo_bytes,
                          "algo_bytes_rule": f"records ({args.format}: {dt.record_bytes() // max(n_rows, 1)} B/row) "
-                                            "+ 16 B shadow RMW per checked access"},
+                                            "+ 16 B shadow RMW per checked access",
+                         "l2_atomic": l2_atomic},
+            "paper_context": {
+                "note": "the paper's own numbers on its RTX 2070 Super (PAPER.md:796-803): context, not targets",
+                "speedup_vs_iguard": ">10x faster on average than iGUARD over 580 kernels (PAPER.md:86)",
+                "memory_overhead": "8 B of shadow per monitored word vs iGUARD's 16 B: half (PAPER.md:725, 927)",
+                "slowdown": "7.5x average, 1.08x median over 5,105 executions (PAPER.md:898)"},
             "literal_roofline_frac": literal,
             "ceiling": ceiling,
             "step_breakdown_ms": {"replay_kernel": kern_ms_launch,
@@ -621,8 +831,11 @@ def main():
             "gpu_launches": n_launch,
             "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch,
                                     "rule": "every libhirace kernel launched in the timed region: the replay, "
+                                            "the end-of-kernel spill scan (a9 overflow recovery; returns at once "
+                                            "unless the ring overflowed), "
                                             + ("the report's key / head / emit kernels, its 2 CUB radix sorts "
-                                               "(10 kernels each) and CUB scan (2)" if async_report else
+                                               "(2 + one pass per 8 key bits that can be set) and CUB scan (2)"
+                                               if (async_report or exchange is not None) else
                                                "the report's key / gather kernels and its 2 CUB radix sorts "
                                                "(10 kernels each)")},
             "slowdown": slow,

@@ -40,7 +40,11 @@ typedef enum {
     HR_E_ARG = -1,     /* invalid argument (NULL, widths, sizes, grid too large) */
     HR_E_NOMEM = -2,   /* device or host allocation failed */
     HR_E_CUDA = -3,    /* CUDA runtime error; see hr_last_error */
-    HR_E_STATE = -4    /* call out of order (e.g. replay before hr_shadow_alloc) */
+    HR_E_STATE = -4,   /* call out of order (e.g. replay before hr_shadow_alloc) */
+    HR_E_INCOMPLETE = -5 /* hr_report / hr_report_collect: the racy set written is NOT complete —
+                            the spill store (hr_config.spill_capacity) overflowed, or a block whose
+                            shared race records the full ring dropped never called hr_thread_end
+                            (flags carry HR_F_INCOMPLETE; n_out counts what was recovered) */
 } hr_status;
 
 typedef enum { HR_GLOBAL = 0, HR_SHARED = 1 } hr_space;          /* PAPER.md:257 memory spaces */
@@ -51,21 +55,39 @@ typedef enum { HR_SCOPE_BLOCK = 1, HR_SCOPE_GRID = 2 } hr_scope;  /* DESIGN.md r
 enum {
     HR_F_CLOCK_OVERFLOW = 1u,      /* a BC/WC clock overflowed: later checks of that thread
                                       skipped, earlier races kept (PAPER.md:540 footnote) */
-    HR_F_RING_OVERFLOW = 2u,       /* report ring full: hr_report falls back to a shadow scan */
+    HR_F_RING_OVERFLOW = 2u,       /* report ring full (a warning): the dropped records were recovered
+                                      into the spill store (end-of-kernel global shadow scan, end-of-block
+                                      shared instance scan), so the set is still exact unless
+                                      HR_F_INCOMPLETE is also set */
     HR_F_MODEL_VIOLATION = 4u,     /* unknown control record / sub-warp sync */
     HR_F_BARRIER_DIVERGENCE = 8u,  /* barrier record not uniform across a warp's lanes */
-    HR_F_UNMONITORED = 16u         /* global access outside the registered shadow region */
+    HR_F_UNMONITORED = 16u,        /* global access outside the registered shadow region */
+    HR_F_INCOMPLETE = 32u          /* overflow recovery failed: the spill store was full, or (as
+                                      HR_E_INCOMPLETE) a dropped shared record was never spilled */
 };
 
 /* Shadow word layout ("5 bits ... 8 bytes of memory per address"):
  *   [63:59] state  [58:32] tid = block:17 | warp:5 | lane:5  [31:wc_bits] bc  [wc_bits-1:0] wc
  * state_bits must be 5 and tid_bits 27; bc_bits + wc_bits must be 32.
- * Defaults (hr_init with cfg == NULL): 5/27/16/16, ring 1<<20 records, device 0. */
+ * Defaults (hr_init with cfg == NULL): 5/27/16/16, ring 1<<20 records, device 0,
+ * spill capacity automatic.
+ *
+ * Report storage (a9, "report races on unique memory addresses"):
+ * racy words are appended to the ring as they are found.  When the ring is
+ * full, dropped records are recovered into the spill store: after each kernel
+ * (before its global shadow is reset) a device-side scan copies every RACE word
+ * of that kernel's global shadow there if the kernel dropped a global record,
+ * and each block that dropped a shared record copies its instance's RACE words
+ * there at block end.  The report is the sorted union of ring and spill, so it
+ * stays exact until the spill itself is full (HR_F_INCOMPLETE, HR_E_INCOMPLETE).
+ * spill_capacity 0 = automatic: max(2^16, min(2^24, local global shadow words)),
+ * fixed when hr_shadow_alloc registers the global region (24 B per record). */
 typedef struct {
     uint8_t state_bits, tid_bits, bc_bits, wc_bits;
     uint32_t ring_capacity;   /* race records the device ring holds (>= 1) */
     int device;               /* CUDA device ordinal */
     uint32_t options;         /* HR_OPT_* bits */
+    uint32_t spill_capacity;  /* records of the overflow spill store; 0 = automatic (above) */
 } hr_config;
 
 enum {
@@ -235,9 +257,12 @@ hr_status hr_shadow_alloc(hr_ctx *ctx, hr_space space, uint64_t base_word, uint6
 
 /* New kernel epoch: a kernel boundary orders everything, so the global shadow
  * is reset to INIT (all-zero words) on `stream`; skipped if
- * no kernel used it since the last reset.  With HR_OPT_DOUBLE_SHADOW the other
- * (already zero) buffer becomes current and the used one is zeroed on a side
- * stream after its kernel completes. */
+ * no kernel used it since the last reset.  Before that, the end-of-kernel spill
+ * scan of the previous kernel is enqueued (one launch; it returns at once
+ * unless that kernel's ring records overflowed).  With HR_OPT_DOUBLE_SHADOW the
+ * other (already zero) buffer becomes current and the used one is zeroed on a
+ * side stream after its kernel completes.  Online kernels: call it BEFORE
+ * hr_device_view for the kernel (the view carries the buffer and epoch tag). */
 hr_status hr_kernel_begin(hr_ctx *ctx, void *stream);
 
 /* Replay every kernel of `t` on `stream`: for each kernel, hr_kernel_begin then
@@ -275,8 +300,12 @@ hr_status hr_unpack_trace(hr_ctx *ctx, const hr_trace *in, uint64_t *rec_out, vo
  * sorted by (kernel, space, block, word), one record per address with the
  * widest scope observed.  n_out receives the number of races (may exceed cap:
  * then only cap are written and HR_E_ARG is returned).  flags_out (may be NULL)
- * receives the sticky HR_F_* word.  If the ring overflowed, the current global
- * shadow is scanned for RACE words of the last replayed kernel instead. */
+ * receives the sticky HR_F_* word.  Enqueues the end-of-kernel spill scan of
+ * the last kernel first (a no-op on the device unless it dropped a record).
+ * The result is the union of the ring and the spill store (see hr_config);
+ * HR_E_INCOMPLETE (after writing what was recovered) if that is not the whole
+ * racy set.  Witness fields (first_tid, first_kind, prev_state) of a record
+ * recovered by a scan are the stored accessor and 0xff. */
 hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out);
 
 /* hr_report without a host round trip (a13 on the device, "report races
@@ -287,6 +316,18 @@ hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32
  * caller can enqueue the next kernel's checks behind it.  Each call replaces
  * the previous result.  Cost: two radix sorts of ring_capacity keys. */
 hr_status hr_report_async(hr_ctx *ctx, void *stream);
+
+/* The same device-side report into caller-owned DEVICE memory, for a
+ * device-resident exchange (the race-set allgather of the
+ * address-sharded replay runs on these buffers, no host round trip):
+ *   out  DEVICE, out_cap hr_race records: the sorted unique set (the first
+ *        out_cap of it);
+ *   hdr  DEVICE, 4 uint32: [0] unique count (may exceed out_cap), [1] sticky
+ *        flags, [2] raw ring records, [3] non-zero if the ring overflowed (the
+ *        set then lives partly in the spill store: call hr_report).
+ * Enqueued on `stream` (NULL = the ctx's last stream); returns at once.  The
+ * buffers must stay valid until the stream reaches the report. */
+hr_status hr_report_async_to(hr_ctx *ctx, void *stream, hr_race *out, uint32_t out_cap, uint32_t *hdr);
 
 /* Wait for the last hr_report_async and copy its result out, with the same
  * contract as hr_report.  If the ring had overflowed it runs hr_report (the
@@ -326,7 +367,8 @@ hr_status hr_replay_timing(hr_ctx *ctx, double *reset_ms, uint64_t *n_resets, do
 
 /* Number of device kernels this ctx launched since the last call (every
  * __global__ launch of libhirace, including the kernels of its CUB scans (2)
- * and 64-bit radix sorts (10: histogram, scan, 8 onesweep passes)),
+ * and radix sorts (2 + one onesweep pass per 8 key bits: 10 for the 64-bit
+ * sorts of hr_report; hr_report_async sorts only the key bits that can be set)),
  * then clear it.  Host only, no CUDA call; lets a harness state how many
  * kernels ran inside a timed region. */
 hr_status hr_launch_count(hr_ctx *ctx, uint64_t *n_launches);
@@ -335,8 +377,12 @@ hr_status hr_launch_count(hr_ctx *ctx, uint64_t *n_launches);
  * and per-state flags (32 bytes).  Either pointer may be NULL. */
 hr_status hr_fsm_table(uint8_t *table2048, uint8_t *flags32);
 
-/* The device pointer of the packed device context (struct hr_dev in
- * hr_device.cuh) for user kernels instrumented online; valid until hr_destroy. */
+/* Copy the packed device context (struct hr_dev in hr_device.cuh, by value)
+ * for a user kernel instrumented online into hr_dev_out (size >= sizeof(hr_dev)).
+ * Take it after hr_kernel_begin for that kernel: it holds the current global
+ * shadow buffer and epoch tag.  The kernel's id (hr_dev.kernel_id) may be set
+ * by the caller; every thread must call hr_thread_begin first and
+ * hr_thread_end last (ring-overflow recovery of shared races). */
 hr_status hr_device_view(hr_ctx *ctx, void *hr_dev_out, size_t size);
 
 const char *hr_last_error(hr_ctx *ctx);

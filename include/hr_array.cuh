@@ -18,6 +18,7 @@
  *     a[j] += 2;            // read then write (two checked accesses)
  *     hr_atomic_add(a, k, 1);   // hr_check_atomic, then atomicAdd
  *     ctx.syncthreads();        // hr_syncthreads: barrier + block clock
+ *     ctx.end();                // hr_thread_end: last statement of every thread
  *
  * All checks run the same device core as the replay (hr_device.cuh).
  */
@@ -35,6 +36,8 @@ struct hr_ctx_dev {
         : d(dev), t(hr_thread_begin(dev, smem_fsm, smem_shadow, smem_words)) {}
     __device__ __forceinline__ void syncthreads() { hr_syncthreads(d, t); }
     __device__ __forceinline__ void syncwarp() { hr_syncwarp(d, t); }
+    /* end of the block's checks (hr_thread_end): every thread, after its last access */
+    __device__ __forceinline__ void end() { hr_thread_end(d, t); }
 };
 
 template <typename T>

@@ -38,7 +38,11 @@
 #include "hr.h"
 
 #define HR_FSM_BYTES 2048
-#define HR_FSM_SMEM_BYTES (HR_FSM_BYTES + 32)   /* table + per-state flags */
+/* table + per-state flags + a 16-byte block scratch (zero in the global copy):
+ * [HR_FSM_DROP_OFF] counts this block's shared-space race records the full
+ * ring dropped (a9 overflow; hr_thread_end spills the instance when non-zero) */
+#define HR_FSM_DROP_OFF (HR_FSM_BYTES + 32)
+#define HR_FSM_SMEM_BYTES (HR_FSM_BYTES + 48)
 #define HR_STATE_SHIFT 59
 #define HR_TID_SHIFT 32
 #define HR_RACE_BLOCK 30u
@@ -56,6 +60,11 @@ struct hr_dev {
     hr_race *ring;
     unsigned int *ring_tail;
     unsigned int *flags;
+    hr_race *spill;               /* a9 overflow store (right after the ring: ring + ring_cap) */
+    unsigned int *ovf;            /* [0] spill tail [1] shared drops not yet spilled [2] global drop:
+                                     kernel id + 1 of a kernel whose global race record the full ring
+                                     dropped (0 = none) [3] spill-scan completion counter */
+    uint32_t spill_cap;
     unsigned long long *counters; /* [0] checks [1] CAS retries [2] fast exits */
     const unsigned char *fsm;     /* HR_FSM_SMEM_BYTES in global memory */
     uint32_t ring_cap;
@@ -175,6 +184,15 @@ __device__ __forceinline__ uint32_t hr__laneid()
     uint32_t l;
     asm("mov.u32 %0, %%laneid;" : "=r"(l));
     return l;
+}
+
+/* A control row is divergent unless every active lane holds the same control
+ * record (replay: the trace format's warp-aligned barriers, tracegen/format.py). */
+__device__ __forceinline__ bool hr__ctrl_divergent(uint64_t x, unsigned ctrl, unsigned lane_mask)
+{
+    const bool is_ctrl = (x >> 62) == 3u && (x & HR_WORD_MASK) != 0u;
+    const unsigned same = __match_any_sync(0xffffffffu, is_ctrl ? x : 0ull);
+    return ctrl != lane_mask || __any_sync(0xffffffffu, is_ctrl && same != ctrl);
 }
 
 /* ---------------- labels ---------------- */
@@ -443,6 +461,97 @@ __device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, const h
     return hr__ld_g(gp);
 }
 
+/* a9 overflow: the ring is full and this race record is dropped.  Every drop
+ * is recovered exactly ("ring overflow"):
+ *   global: the kernel's id is latched in ovf[2]; hr_spill_scan_kernel, which
+ *     the host enqueues after the kernel (before its shadow is reset), copies
+ *     every RACE word of that kernel's global shadow into the spill;
+ *   shared: the block's drop count (shared address `drop_sa`) and ovf[1] are raised;
+ *     hr_thread_end spills every RACE word of the block's instance and lowers
+ *     ovf[1] again.  ovf[1] != 0 at report time = a block that never spilled.
+ * The finite-history baseline has no FSM shadow to scan: its drops are lost. */
+/* (scalar arguments: a rare path kept out of line without copying hr_dev to the stack) */
+static __device__ __noinline__ void hr__ring_drop_x(unsigned int *flags, unsigned int *ovf, uint32_t options,
+                                                   uint32_t kernel_id, uint32_t drop_sa, uint32_t space)
+{
+    if ((*(volatile unsigned int *)flags & HR_F_RING_OVERFLOW) == 0u) atomicOr(flags, HR_F_RING_OVERFLOW);
+    if (options & HR_OPT_FINITE_HISTORY) {
+        atomicAdd(&ovf[1], 1u);
+    } else if (space) {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(drop_sa) : "memory");
+        atomicAdd(&ovf[1], 1u);
+    } else if (*(volatile unsigned int *)&ovf[2] != kernel_id + 1u) {
+        *(volatile unsigned int *)&ovf[2] = kernel_id + 1u;
+    }
+}
+
+__device__ __forceinline__ void hr__ring_drop(const hr_dev &d, uint32_t drop_sa, uint32_t space)
+{
+    hr__ring_drop_x(d.flags, d.ovf, d.options, d.kernel_id, drop_sa, space);
+}
+
+/* Append one record to the spill (warp-aggregated over the lanes of `mask`
+ * with want = true); past spill_cap the set is incomplete (HR_F_INCOMPLETE). */
+__device__ __forceinline__ void hr__spill_put(hr_race *spill, unsigned int *ovf, uint32_t spill_cap,
+                                              unsigned int *flags, unsigned mask, bool want, const hr_race &r)
+{
+    const unsigned m = __ballot_sync(mask, want);
+    if (!m) return;
+    const uint32_t lane = hr__laneid(), leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&ovf[0], (unsigned)__popc(m));
+    base = __shfl_sync(mask, base, leader);
+    if (want) {
+        const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+        if (slot < spill_cap) spill[slot] = r;
+        else atomicOr(flags, HR_F_INCOMPLETE);
+    }
+}
+
+/* The RACE words of one shared instance (`words` words at shared address
+ * `sa`, 64-bit or HR_OPT_SMEM32 layout) into the spill, by the `nthr` threads
+ * of the caller (ltid = 0..nthr-1: whole warps, or nthr < 32 lanes of one). */
+static __device__ __noinline__ void hr__spill_instance_x(hr_race *spill, unsigned int *ovf, uint32_t spill_cap,
+                                                         unsigned int *flags, uint32_t options, uint32_t kernel_id,
+                                                         uint32_t sa, uint32_t words, uint32_t block, uint32_t ltid,
+                                                         uint32_t nthr)
+{
+    const bool s32 = (options & HR_OPT_SMEM32) != 0u;
+    const unsigned mask = nthr >= 32u ? 0xffffffffu : ((1u << nthr) - 1u);
+    for (uint32_t i0 = ltid & ~31u; i0 < words; i0 += nthr) {
+        const uint32_t i = i0 + (ltid & 31u);
+        uint32_t st = 0, tid = 0;
+        if (i < words) {
+            if (s32) {
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sa + 4u * i) : "memory");
+                st = v >> HR_S32_STATE_SHIFT;
+                tid = (block << 10) | ((v >> 17) & 1023u);
+            } else {
+                const unsigned long long v = hr__ld_s(sa + 8u * i);
+                st = (uint32_t)(v >> HR_STATE_SHIFT);
+                tid = (uint32_t)(v >> HR_TID_SHIFT) & 0x7ffffffu;
+            }
+        }
+        hr_race r;
+        r.word = i;
+        r.block = block;
+        r.kernel = kernel_id;
+        r.first_tid = tid;
+        r.space = HR_SHARED;
+        r.scope = (uint8_t)(st == HR_RACE_GRID ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
+        r.first_kind = 0xff;                      /* witness unknown: diagnostic fields only */
+        r.prev_state = 0xff;
+        hr__spill_put(spill, ovf, spill_cap, flags, mask, i < words && st >= HR_RACE_BLOCK, r);
+    }
+}
+
+__device__ __forceinline__ void hr__spill_instance(const hr_dev &d, uint32_t sa, uint32_t words, uint32_t block,
+                                                   uint32_t ltid, uint32_t nthr)
+{
+    hr__spill_instance_x(d.spill, d.ovf, d.spill_cap, d.flags, d.options, d.kernel_id, sa, words, block, ltid, nthr);
+}
+
 __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t, uint32_t slot, uint32_t space,
                                                uint64_t word, uint32_t ei)
 {
@@ -458,7 +567,7 @@ __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t,
         rr.prev_state = (uint8_t)((ei >> 19) & 31u);
         d.ring[slot] = rr;
     } else {
-        hr__set_flag(d, HR_F_RING_OVERFLOW);
+        hr__ring_drop(d, t.fsm + HR_FSM_DROP_OFF, space);
     }
 }
 
@@ -529,6 +638,65 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
     }
 }
 
+/*
+ * Shared-space row (a2-a9 specialised): every lane of the warp holds a
+ * shared-space access to its own word (the caller checked: 32 valid lanes,
+ * strictly increasing words < swords, t.off clear, a kernel without run-time
+ * options).  Algorithm 1 exactly as in hr__commit_single, with what the
+ * shared space fixes folded in (DESIGN.md §5 "shared row"):
+ *   - the instance is this block's: the relation is never Global, so it is
+ *     the XOR of the low 10 tid bits (Self / Warp / Block), and Bs needs only
+ *     bc > oBC (an INIT word ignores relation and sync, any value indexes
+ *     the same table row);
+ *   - no epoch tag (the instance is zeroed at block start), no probe;
+ *   - a7: the unchanged word (i), and RACE_BLOCK under a non-Global relation
+ *     (iii) — always non-Global here; (ii)'s insensitive states are GREAD,
+ *     GATOMIC, RACE_GRID, which need another block and never occur.
+ */
+__device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind)
+{
+    const uint32_t sa = t.sshadow + (word << 3);
+    const uint32_t lo = (uint32_t)t.meta, tid_lo = (uint32_t)(t.meta >> HR_TID_SHIFT) & 1023u;
+    const uint32_t bc = lo >> d.wc_bits, wc = lo & ((1u << d.wc_bits) - 1u);
+    const uint32_t kcol = t.fsm + (kind << 4);
+    unsigned long long old = hr__ld_s(sa);
+    uint32_t ei = 0;
+    while (true) {
+        const uint32_t ohi = (uint32_t)(old >> 32), olo = (uint32_t)old;
+        const uint32_t os = ohi >> (HR_STATE_SHIFT - 32);
+        const uint32_t x = (tid_lo ^ ohi) & 1023u;
+        const uint32_t rel = (x != 0u) + (x >= 32u);
+        const uint32_t sync = (bc > (olo >> d.wc_bits)) ? 2u
+                              : ((rel <= 1u && wc > (olo & ((1u << d.wc_bits) - 1u))) ? 1u : 0u);
+        const uint32_t cur = hr__lds_u8(kcol + ((os << 6) | (sync << 2) | rel));
+        const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
+        if (nw == old || (cur == os && os == HR_RACE_BLOCK)) break;      /* a7 (i), (iii) */
+        const unsigned long long prev = hr__cas_s(sa, old, nw);
+        if (prev == old) {                                                /* a8 committed */
+            if (cur >= HR_RACE_BLOCK && cur != os)
+                ei = HR_EI_EMIT | (hr__laneid() << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID);
+            break;
+        }
+        old = prev;
+    }
+    const unsigned em = __ballot_sync(0xffffffffu, ei != 0u);              /* a9 */
+    if (em) {
+        const uint32_t lane = hr__laneid(), leader = __ffs(em) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(em));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (ei) hr__write_race(d, t, base + __popc(em & ((1u << lane) - 1u)), 1u, word, ei);
+    }
+}
+
+/* The test for hr__check_shared_row (warp-uniform result). */
+__device__ __forceinline__ bool hr__shared_row_ok(const hr_thr &t, uint32_t op, uint32_t space, uint64_t word)
+{
+    const unsigned long long prevw = __shfl_up_sync(0xffffffffu, (unsigned long long)word, 1);
+    return __all_sync(0xffffffffu, op != 3u && space != 0u && word < t.swords && !(t.off & 3u) &&
+                                       (hr__laneid() == 0u || word > prevw));
+}
+
 /* ---------------- online instrumentation API ---------------- */
 
 /* Copy the FSM table into `smem_fsm` (HR_FSM_SMEM_BYTES, 16-B aligned), zero the
@@ -556,6 +724,25 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     return t;
 }
 
+/* End of a block: if the full ring dropped a race record of
+ * this block's shared instance, copy every RACE word of the instance into the
+ * spill before the instance dies with the block (a9 overflow recovery).  Every
+ * thread of the block must call it (it holds a __syncthreads) after its last
+ * check; a kernel that cannot (an early return) must keep the ring large
+ * enough, else hr_report returns HR_E_INCOMPLETE. */
+__device__ __forceinline__ void hr_thread_end(const hr_dev &d, const hr_thr &t)
+{
+    if (t.swords == 0u) return;                   /* block-uniform */
+    __syncthreads();
+    uint32_t drops;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(drops) : "r"(t.fsm + HR_FSM_DROP_OFF) : "memory");
+    if (drops == 0u) return;                      /* block-uniform: read after the barrier */
+    const uint32_t nthr = blockDim.x * blockDim.y * blockDim.z;
+    const uint32_t ltid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const uint32_t nscan = (nthr & 31u) ? min(nthr, 32u) : nthr;   /* whole warps, or one (partial) warp */
+    if (ltid < nscan) hr__spill_instance(d, t.sshadow, t.swords, t.tid() >> 10, ltid, nscan);
+    if (ltid == 0u) atomicSub(&d.ovf[1], drops);
+}
 
 /* OPTS = true reads the ablation options and HR_OPT_SMEM32 at run time; a
  * kernel instantiated with OPTS = false must only run on a ctx without them. */

@@ -37,6 +37,8 @@ struct hr_bs_smem {
     uint16_t tag[32];                  /* simulated warp << 5 | lane */
     uint32_t wc[32];
     uint32_t cur[32];
+    uint32_t drops;                    /* shared race records of this block the full ring dropped */
+    uint32_t pad[3];
 };
 
 __device__ __forceinline__ uint32_t hr__lds_u32(uint32_t a)
@@ -148,7 +150,7 @@ __device__ __forceinline__ void hr__check_bpool(const hr_dev &d, const hr_thr &t
                 rr.prev_state = (uint8_t)((ei >> 14) & 31u);
                 d.ring[slot] = rr;
             } else {
-                hr__set_flag(d, HR_F_RING_OVERFLOW);
+                hr__ring_drop(d, ps + (uint32_t)offsetof(hr_bs_smem, drops), space);
             }
         }
     }
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(HR_BS_WARPS * 32, 64 / HR_BS_WARPS) hr_replay_
     hr_bs_smem *me = reinterpret_cast<hr_bs_smem *>(hr_smem + HR_FSM_SMEM_BYTES + hw * sizeof(hr_bs_smem));
     me->wc[lane] = 0u;
     me->cur[lane] = 0u;
+    if (lane == 0) me->drops = 0u;
     __syncthreads();                                   /* the only CTA barrier: setup */
     const uint32_t sb = blockIdx.x * HR_BS_WARPS + hw; /* simulated block of this warp (launch-relative) */
     if (sb >= n_blocks) return;
@@ -223,13 +226,11 @@ __global__ void __launch_bounds__(HR_BS_WARPS * 32, 64 / HR_BS_WARPS) hr_replay_
                 if (ctrl) {
                     /* as hr__barrier_row: divergence and mixed barrier kinds are flagged */
                     const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
-                    if ((bst && bst != lane_mask) || ctrl != lane_mask)
-                        if (lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
-                    if (ctrl & ~bst) {
-                        const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
-                        if (bsw != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
-                    }
+                    if (hr__ctrl_divergent(x, ctrl, lane_mask) && lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+                    const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
+                    if ((bst | bsw) != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
                     if (bst) break;                              /* this warp's block epoch ends */
+                    if (!bsw) continue;                          /* undefined control code: no barrier */
                     /* __syncwarp of simulated warp sw: close the pool, advance its clock */
                     flush();
                     const uint32_t wc = me->wc[sw];
@@ -283,6 +284,13 @@ __global__ void __launch_bounds__(HR_BS_WARPS * 32, 64 / HR_BS_WARPS) hr_replay_
                 bc++;
             }
         }
+    }
+    /* a12 + a9: the block's shared instance dies here; spill it if the ring dropped one of its races */
+    __syncwarp();
+    const uint32_t drops = *(volatile uint32_t *)&me->drops;
+    if (drops) {
+        hr__spill_instance(d, t.sshadow, smem_words, blk, lane, 32u);
+        if (lane == 0) atomicSub(&d.ovf[1], drops);
     }
 }
 

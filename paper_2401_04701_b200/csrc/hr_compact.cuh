@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr
             src.bulk(buf, c0 + (c + NB) * CH, rows2, CH, bar0 + 8u * b);
         }
     }
+    hr_thread_end(d, t);                                             /* a9: spill a dropped shared race */
 }
 
 #endif /* HR_COMPACT_CUH_ */

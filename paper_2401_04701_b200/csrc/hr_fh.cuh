@@ -111,10 +111,11 @@ __global__ void __launch_bounds__(1024, 1) hr_fh_replay_kernel(hr_dev d, SRC src
         const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
         if (ctrl) {
             const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
-            if ((bst && bst != lane_mask) || ctrl != lane_mask)
-                if (lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+            if (hr__ctrl_divergent(x, ctrl, lane_mask) && lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+            const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
+            if ((bst | bsw) != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
             if (bst) hr_syncthreads(d, t);
-            else hr_syncwarp(d, t);
+            else if (bsw) hr_syncwarp(d, t);
             continue;
         }
         const uint32_t space = (uint32_t)(x >> 61) & 1u;

@@ -50,8 +50,14 @@ struct hr_ctx {
     size_t sort_tmp_bytes = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
-    hr_race *ring = nullptr;
-    unsigned int *tail = nullptr;     /* [0] ring tail, [1] flags, [2] scan count */
+    hr_race *ring = nullptr;                     /* ring_capacity records, then spill_cap spill records */
+    uint32_t spill_cap = 0;
+    bool scan_pending = false;                   /* a kernel used the current global shadow since its
+                                                    end-of-kernel spill scan was enqueued */
+    bool online_used = false;                    /* hr_device_view since the last hr_reset_report: ring
+                                                    records may carry any kernel id / shared word */
+    unsigned int *tail = nullptr;     /* [0] ring tail, [1] flags, [2..5] hr_dev.ovf (spill tail,
+                                         unspilled shared drops, global drop kernel + 1, scan counter) */
     unsigned long long *counters = nullptr;
     unsigned char *fsm = nullptr;
     uint32_t last_kernel = 0;
@@ -123,6 +129,11 @@ static uint32_t smem_u64(const hr_ctx *c, uint64_t smem_words)
     return (c->cfg.options & HR_OPT_SMEM32) ? (uint32_t)((smem_words + 1) / 2) : (uint32_t)smem_words;
 }
 
+/* spill store: automatic capacity (hr.h, hr_config) and the tail words */
+#define HR_SPILL_MIN (1u << 16)
+#define HR_SPILL_AUTO_MAX (1u << 24)
+#define HR_TAIL_WORDS 8
+
 static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
 {
     hr_dev d;
@@ -133,6 +144,9 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.ring = c->ring;
     d.ring_tail = c->tail;
     d.flags = c->tail + 1;
+    d.spill = c->ring + c->cfg.ring_capacity;
+    d.ovf = c->tail + 2;
+    d.spill_cap = c->spill_cap;
     d.counters = c->counters;
     d.fsm = c->fsm;
     d.ring_cap = c->cfg.ring_capacity;
@@ -169,6 +183,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
     def.ring_capacity = 1u << 20;
     def.device = 0;
     def.options = 0;
+    def.spill_capacity = 0;
     const hr_config &k = cfg ? *cfg : def;
     if (k.state_bits != 5 || k.tid_bits != 27 || k.bc_bits < 1 || k.wc_bits < 1 ||
         k.bc_bits + k.wc_bits != 32 || k.ring_capacity < 1 ||
@@ -184,18 +199,20 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
     do {
         cudaError_t e = cudaSetDevice(c->device);
         if (e != cudaSuccess) { st = fail(c, HR_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e)); break; }
+        c->spill_cap = k.spill_capacity ? k.spill_capacity : HR_SPILL_MIN;
         if (cudaMalloc(&c->fsm, HR_FSM_SMEM_BYTES) != cudaSuccess ||
-            cudaMalloc(&c->ring, sizeof(hr_race) * (size_t)k.ring_capacity) != cudaSuccess ||
-            cudaMalloc(&c->tail, 4 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMalloc(&c->ring, sizeof(hr_race) * ((size_t)k.ring_capacity + c->spill_cap)) != cudaSuccess ||
+            cudaMalloc(&c->tail, HR_TAIL_WORDS * sizeof(unsigned int)) != cudaSuccess ||
             cudaMalloc(&c->counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_NOMEM, "device allocation failed in hr_init");
             break;
         }
         unsigned char host[HR_FSM_SMEM_BYTES];
+        memset(host, 0, sizeof host);                /* the block scratch (HR_FSM_DROP_OFF) starts at 0 */
         memcpy(host, hr_fsm_table_init, HR_FSM_BYTES);
         memcpy(host + HR_FSM_BYTES, hr_fsm_flags_init, 32);
         if (cudaMemcpy(c->fsm, host, HR_FSM_SMEM_BYTES, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemset(c->tail, 0, 4 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMemset(c->tail, 0, HR_TAIL_WORDS * sizeof(unsigned int)) != cudaSuccess ||
             cudaMemset(c->counters, 0, 16 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_CUDA, "hr_init upload failed");
             break;
@@ -275,6 +292,23 @@ extern "C" hr_status hr_shadow_alloc(hr_ctx *c, hr_space space, uint64_t base_wo
             CU(cudaEventRecord(c->reset_done[b], c->side));
         }
     }
+    if (!c->cfg.spill_capacity) {
+        /* automatic spill: one record per local shadow word, within [2^16, 2^24] */
+        const uint32_t want = (uint32_t)std::min<uint64_t>(HR_SPILL_AUTO_MAX, std::max<uint64_t>(HR_SPILL_MIN, local));
+        if (want > c->spill_cap) {
+            hr_race *nr = nullptr;
+            const size_t ring_bytes = sizeof(hr_race) * (size_t)c->cfg.ring_capacity;
+            if (cudaMalloc(&nr, ring_bytes + sizeof(hr_race) * (size_t)want) != cudaSuccess)
+                return fail(c, HR_E_NOMEM, "spill store of %u records failed", want);
+            CU(cudaDeviceSynchronize());
+            /* keep what the ring and spill hold (hr_shadow_alloc is normally called before any kernel) */
+            CU(cudaMemcpy(nr, c->ring, ring_bytes + sizeof(hr_race) * (size_t)c->spill_cap, cudaMemcpyDeviceToDevice));
+            cudaFree(c->ring);
+            c->ring = nr;
+            c->spill_cap = want;
+        }
+    }
+    c->scan_pending = false;
     c->gcur = 0;
     c->epoch_tag = 0;
     c->gshadow = c->gbuf[0];
@@ -297,12 +331,29 @@ static hr_status reset_buffer(hr_ctx *c, int b, cudaStream_t s)
     return HR_OK;
 }
 
+/* a9 overflow recovery of the kernel that used the current global shadow:
+ * one launch, ordered after that kernel and before the shadow is reset or its
+ * epoch tag retired; on the device it returns at once unless the kernel
+ * dropped a global race record (hr_spill_scan_kernel). */
+static hr_status enqueue_spill_scan(hr_ctx *c, cudaStream_t s)
+{
+    if (!c->scan_pending || !c->gshadow || c->shadow_bytes != 8) return HR_OK;
+    c->scan_pending = false;
+    const uint64_t blocks = std::min<uint64_t>(148ull * 4ull, (c->glocal + 255) / 256);
+    c->launches++;
+    hr_spill_scan_kernel<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, s>>>(
+        make_dev(c, c->last_kernel), c->gshadow, c->glocal, (c->cfg.options & HR_OPT_LAZY_RESET) ? c->epoch_tag : 0u);
+    CU(cudaGetLastError());
+    return HR_OK;
+}
+
 extern "C" hr_status hr_kernel_begin(hr_ctx *c, void *stream)
 {
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
     if (!c->gshadow) return HR_OK;
+    if (hr_status st = enqueue_spill_scan(c, c->stream)) return st;
     if (c->cfg.options & HR_OPT_LAZY_RESET) {
         /* epoch tags 1..15: words of earlier kernels read as INIT (hr__live);
          * the shadow is zeroed for real only before a tag would be reused */
@@ -426,6 +477,15 @@ static hr_status check_kernel(hr_ctx *c, const hr_trace *t, uint32_t k)
 
 static hr_status reserve(hr_ctx *c, int i, size_t bytes);
 
+/* A replay kernel with id `kid` was enqueued on the current global shadow. */
+static void note_kernel(hr_ctx *c, uint32_t kid)
+{
+    c->last_kernel = kid;
+    c->max_kernel = std::max(c->max_kernel, kid);
+    c->have_kernel = true;
+    c->scan_pending = true;                      /* its end-of-kernel spill scan is due */
+}
+
 /* Compacted replay of blocks [b0, b1) of kernel k (hr_compact.cuh): count and
  * scan the packed rows of every (warp, helper) stream, write them, replay them.
  * Two small synchronous reads size the buffers. */
@@ -496,9 +556,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     kern<<<(unsigned)(b1 - b0), nhw * 32u, smem, s>>>(d, hr_src_cmp{orec, otag}, segoff, rowoff, (uint32_t)warps,
                                                       (uint32_t)lanes, (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
-    c->last_kernel = kid;
-        c->max_kernel = std::max(c->max_kernel, kid);
-    c->have_kernel = true;
+    note_kernel(c, kid);
     return HR_OK;
 }
 
@@ -526,9 +584,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
             d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
         CU(cudaGetLastError());
         if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
-        c->last_kernel = kid;
-        c->max_kernel = std::max(c->max_kernel, kid);
-        c->have_kernel = true;
+        note_kernel(c, kid);
         return HR_OK;
     }
     const bool pool = kind == HR_K_POOL || kind == HR_K_POOL_WIDE;
@@ -565,9 +621,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
                 d, t->rec, woff + woi + b0 * warps, nb, (uint32_t)warps, (uint32_t)lanes, (uint32_t)smem_words);
             CU(cudaGetLastError());
             if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
-            c->last_kernel = kid;
-        c->max_kernel = std::max(c->max_kernel, kid);
-            c->have_kernel = true;
+            note_kernel(c, kid);
             return HR_OK;
         }
     }
@@ -601,9 +655,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
                                                        (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
     if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
-    c->last_kernel = kid;
-        c->max_kernel = std::max(c->max_kernel, kid);
-    c->have_kernel = true;
+    note_kernel(c, kid);
     return HR_OK;
 }
 
@@ -1105,10 +1157,6 @@ static hr_status sort_races_device(hr_ctx *c, uint32_t n, std::vector<hr_race> &
     HR_PROF_MARK();
     if (n > c->rep_cap) {
         if (c->rep_host) cudaFreeHost(c->rep_host);
-    if (c->arep_host) cudaFreeHost(c->arep_host);
-    if (c->arep_hdr_host) cudaFreeHost(c->arep_hdr_host);
-    if (c->arep_scratch) cudaFree(c->arep_scratch);
-    if (c->arep_ev) cudaEventDestroy(c->arep_ev);
         c->rep_host = nullptr;
         c->rep_cap = 0;
         if (cudaHostAlloc((void **)&c->rep_host, nb * sizeof(hr_race), cudaHostAllocDefault) != cudaSuccess)
@@ -1168,7 +1216,8 @@ __global__ void hr_arep_heads_kernel(const hr_race *__restrict__ r, const unsign
  * the run (as unique_races on the host) */
 __global__ void hr_arep_emit_kernel(const hr_race *__restrict__ r, const unsigned int *__restrict__ tail,
                                     const uint32_t *__restrict__ idx, const uint32_t *__restrict__ head,
-                                    const uint32_t *__restrict__ pos, uint32_t cap, hr_race *out, uint32_t *hdr)
+                                    const uint32_t *__restrict__ pos, uint32_t cap, hr_race *out, uint32_t out_cap,
+                                    uint32_t *hdr)
 {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = min(*tail, cap);
@@ -1176,8 +1225,9 @@ __global__ void hr_arep_emit_kernel(const hr_race *__restrict__ r, const unsigne
         hdr[0] = n ? pos[n - 1] + head[n - 1] : 0u;
         hdr[1] = tail[1];
         hdr[2] = *tail;
+        hdr[3] = tail[2] | tail[3];             /* spill records or unspilled drops: collect -> hr_report */
     }
-    if (p >= n || !head[p]) return;
+    if (p >= n || !head[p] || pos[p] >= out_cap) return;
     hr_race x = r[idx[p]];
     for (uint32_t q = p + 1; q < n && !head[q]; q++) {
         const hr_race &y = r[idx[q]];
@@ -1190,14 +1240,15 @@ __global__ void hr_arep_emit_kernel(const hr_race *__restrict__ r, const unsigne
     out[pos[p]] = x;
 }
 
+static hr_status report_async(hr_ctx *c, cudaStream_t s, hr_race *out, uint32_t out_cap, uint32_t *hdr);
+
 extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
 {
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-    const uint32_t cap = c->cfg.ring_capacity;
     if (!c->arep_host) {
-        const size_t bytes = (size_t)cap * sizeof(hr_race);
+        const size_t bytes = (size_t)c->cfg.ring_capacity * sizeof(hr_race);
         if (cudaHostAlloc((void **)&c->arep_host, bytes, cudaHostAllocMapped) != cudaSuccess)
             return fail(c, HR_E_NOMEM, "pinned mapped report buffer of %zu bytes failed", bytes);
         CU(cudaHostGetDevicePointer((void **)&c->arep_dev, c->arep_host, 0));
@@ -1206,6 +1257,26 @@ extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
         CU(cudaHostGetDevicePointer((void **)&c->arep_hdr_dev, c->arep_hdr_host, 0));
         CU(cudaEventCreateWithFlags(&c->arep_ev, cudaEventDisableTiming));
     }
+    if (hr_status st = report_async(c, s, c->arep_dev, c->cfg.ring_capacity, c->arep_hdr_dev)) return st;
+    CU(cudaEventRecord(c->arep_ev, s));
+    c->arep_pending = true;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_report_async_to(hr_ctx *c, void *stream, hr_race *out, uint32_t out_cap, uint32_t *hdr)
+{
+    if (!c || !hdr || (out_cap && !out)) return fail(c, HR_E_ARG, "hr_report_async_to: bad arguments");
+    CU(cudaSetDevice(c->device));
+    return report_async(c, stream ? (cudaStream_t)stream : c->stream, out, out_cap, hdr);
+}
+
+/* a13 on the device (hr_report_async / hr_report_async_to): enqueue on `s` the
+ * end-of-kernel spill scan, the sorts, the run-head merge and the emit into
+ * out[0, out_cap) + hdr[4]. */
+static hr_status report_async(hr_ctx *c, cudaStream_t s, hr_race *out, uint32_t out_cap, uint32_t *hdr)
+{
+    const uint32_t cap = c->cfg.ring_capacity;
+    if (hr_status st = enqueue_spill_scan(c, s)) return st;
     /* scratch: lo keys x2, hi keys x2, idx x2, head flags, positions, CUB temp */
     const size_t nb = cap;
     size_t off[9], tot = 0;
@@ -1243,8 +1314,9 @@ extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
      * padding keys (~0) stay the largest within the range, and the sorts are
      * stable, so real records still precede them (fewer radix passes) */
     auto bits_of = [](uint64_t v) { int b = 0; while (b < 64 && (v >> b)) b++; return b; };
-    const int lo_bits = std::max(1, std::min(64, bits_of(std::max<uint64_t>(c->gbase + c->gwords, c->smem_words_max))));
-    const int hi_bits = std::min(64, 33 + bits_of((uint64_t)std::max(c->max_kernel, c->last_kernel) + 1));
+    int lo_bits = std::max(1, std::min(64, bits_of(std::max<uint64_t>(c->gbase + c->gwords, c->smem_words_max))));
+    int hi_bits = std::min(64, 33 + bits_of((uint64_t)std::max(c->max_kernel, c->last_kernel) + 1));
+    if (c->online_used) lo_bits = hi_bits = 64;  /* online kernels: caller-chosen ids and instance sizes */
     c->launches += 2 + (lo_bits + 7) / 8;        /* onesweep: histogram + scan + one pass per 8 bits */
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)cap, 0, lo_bits, s));
     c->launches++;
@@ -1260,10 +1332,8 @@ extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
     c->launches += 2;
     CU(cub::DeviceScan::ExclusiveSum(tmp, tb, head, pos, (int)cap, s));
     c->launches++;
-    hr_arep_emit_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, head, pos, cap, c->arep_dev, c->arep_hdr_dev);
+    hr_arep_emit_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, head, pos, cap, out, out_cap, hdr);
     CU(cudaGetLastError());
-    CU(cudaEventRecord(c->arep_ev, s));
-    c->arep_pending = true;
     return HR_OK;
 }
 
@@ -1275,7 +1345,7 @@ extern "C" hr_status hr_report_collect(hr_ctx *c, hr_race *out, size_t cap, size
     CU(cudaEventSynchronize(c->arep_ev));
     c->arep_pending = false;
     const uint32_t m = c->arep_hdr_host[0], flags = c->arep_hdr_host[1];
-    if (flags & HR_F_RING_OVERFLOW)                      /* the shadow scan needs the synchronous path */
+    if (c->arep_hdr_host[3])                             /* ring overflow: the spill needs the full path */
         return hr_report(c, out, cap, n_out, flags_out);
     *n_out = m;
     if (flags_out) *flags_out = flags;
@@ -1292,43 +1362,33 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
     hr__prof_n = 0;
     HR_PROF_MARK();
     CU(cudaSetDevice(c->device));
+    if (hr_status st = enqueue_spill_scan(c, c->stream)) return st;
     CU(cudaStreamSynchronize(c->stream));
     HR_PROF_MARK();
-    unsigned int hdr[4];
+    unsigned int hdr[HR_TAIL_WORDS];
     CU(cudaMemcpy(hdr, c->tail, sizeof hdr, cudaMemcpyDeviceToHost));
     HR_PROF_MARK();
-    uint32_t n = std::min<uint32_t>(hdr[0], c->cfg.ring_capacity);
+    /* ring [0, n_ring) then spill [ring_capacity, ring_capacity + n_spill): the spill is
+     * only written after a drop, i.e. with a full ring, so the two are contiguous */
+    const uint32_t n_ring = std::min<uint32_t>(hdr[0], c->cfg.ring_capacity);
+    const uint32_t n_spill = std::min<uint32_t>(hdr[2], c->spill_cap);
+    if (n_spill && n_ring != c->cfg.ring_capacity)
+        return fail(c, HR_E_STATE, "hr_report: spill records with a ring that is not full (%u of %u)", n_ring,
+                    c->cfg.ring_capacity);
+    const uint32_t n = n_ring + n_spill;
     uint32_t flags = hdr[1];
+    const bool incomplete = (flags & HR_F_INCOMPLETE) || hdr[3] != 0u;
+    if (hdr[3] != 0u) flags |= HR_F_INCOMPLETE;
     std::vector<hr_race> &v = c->rep;
     v.clear();
-    const bool scan = (flags & HR_F_RING_OVERFLOW) && c->have_kernel && c->gshadow && c->shadow_bytes == 8;
     bool sorted = false;
-    if (n >= 4096 && !scan) {                   /* large report: sort on the device */
+    if (n >= 4096) {                            /* large report: sort on the device */
         hr_status st = sort_races_device(c, n, v);
         if (st) return st;
         sorted = true;
     } else {
         v.resize(n);
         if (n) CU(cudaMemcpy(v.data(), c->ring, n * sizeof(hr_race), cudaMemcpyDeviceToHost));
-    }
-    if (scan) {
-        /* fallback: scan the last kernel's global shadow (shared instances are gone) */
-        uint32_t scap = 1u << 22;
-        hr_race *tmp = nullptr;
-        CU(cudaMalloc(&tmp, sizeof(hr_race) * (size_t)scap));
-        CU(cudaMemset(c->tail + 2, 0, sizeof(unsigned int)));
-        c->launches++;
-        hr_scan_kernel<<<148 * 8, 256>>>(c->gshadow, c->glocal, c->gbase, c->shard_rank, c->shard_log2, c->gran_log2,
-                                         c->last_kernel, (c->cfg.options & HR_OPT_LAZY_RESET) ? c->epoch_tag : 0u,
-                                         tmp, c->tail + 2, scap);
-        CU(cudaGetLastError());
-        unsigned int cnt = 0;
-        CU(cudaMemcpy(&cnt, c->tail + 2, sizeof cnt, cudaMemcpyDeviceToHost));
-        cnt = std::min(cnt, scap);
-        size_t off = v.size();
-        v.resize(off + cnt);
-        if (cnt) CU(cudaMemcpy(v.data() + off, tmp, cnt * sizeof(hr_race), cudaMemcpyDeviceToHost));
-        cudaFree(tmp);
     }
     HR_PROF_MARK();
     if (!sorted) sort_races(v);
@@ -1344,7 +1404,12 @@ extern "C" hr_status hr_report(hr_ctx *c, hr_race *out, size_t cap, size_t *n_ou
         for (int i = 1; i < hr__prof_n; i++) fprintf(stderr, " %.2f", hr__prof[i] - hr__prof[i - 1]);
         fprintf(stderr, " ms (sync, hdr, reserve, keys, sort1, hikeys, sort2, gather, d2h-enq, d2h-sync, unique, copy-out)\n");
     }
-    return m > cap ? fail(c, HR_E_ARG, "hr_report: %zu races, capacity %zu", m, cap) : HR_OK;
+    if (m > cap) return fail(c, HR_E_ARG, "hr_report: %zu races, capacity %zu", m, cap);
+    if (incomplete)
+        return fail(c, HR_E_INCOMPLETE, "hr_report: racy set incomplete (%s)",
+                    hdr[3] ? "a block's dropped shared race records were never spilled (hr_thread_end missing)"
+                           : "spill store full: raise hr_config.spill_capacity");
+    return HR_OK;
 }
 
 /* Merge of per-shard race sets (include/hr.h): host only, no CUDA call. */
@@ -1459,9 +1524,10 @@ extern "C" hr_status hr_reset_report(hr_ctx *c)
 {
     if (!c) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
-    CU(cudaMemsetAsync(c->tail, 0, 4 * sizeof(unsigned int), c->stream));
+    CU(cudaMemsetAsync(c->tail, 0, HR_TAIL_WORDS * sizeof(unsigned int), c->stream));
     CU(cudaMemsetAsync(c->counters, 0, 4 * sizeof(unsigned long long), c->stream));
     c->have_kernel = false;
+    c->online_used = false;
     return HR_OK;
 }
 
@@ -1520,6 +1586,9 @@ extern "C" hr_status hr_device_view(hr_ctx *c, void *out, size_t size)
     if (!c || !out || size < sizeof(hr_dev)) return fail(c, HR_E_ARG, "hr_device_view: need %zu bytes", sizeof(hr_dev));
     hr_dev d = make_dev(c, c->last_kernel);
     memcpy(out, &d, sizeof d);
+    c->online_used = true;                      /* a user kernel will run on this view */
+    c->scan_pending = true;
+    c->have_kernel = true;
     return HR_OK;
 }
 

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(32) c1_kernel(hr_dev d, int *data, int rounds,
         }
         bar<I>(d, t);
     }
+    if (I) hr_thread_end(d, t);
 }
 
 /* ---- C1 again, written against the transparent wrapper (hr_array.cuh):
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(32) c1_array_kernel(hr_dev d, int *data, int r
         if (lane == 0) g[out + r] = s[0];
         ctx.syncthreads();
     }
+    ctx.end();
 }
 
 /* ---- C3: 2D Jacobi stencil through two SMEM tiles ---- */
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(256) c3_kernel(hr_dev d, int *data, int n, int
     int v = tile[src][c];
     chk<I>(d, t, HR_GLOBAL, (uint64_t)n * n + (uint64_t)gy * n + gx, HR_WRITE);
     data[n * n + gy * n + gx] = v;
+    if (I) hr_thread_end(d, t);
 }
 
 /* ---- C4: BFS level step and degree histogram, thread per vertex ---- */
@@ -264,10 +267,14 @@ hr_status prepare(hr_ctx *ctx, int instrumented, uint32_t kernel_id, void *strea
     memset(d, 0, sizeof *d);
     if (!instrumented) return HR_OK;
     if (!ctx) return HR_E_ARG;
-    hr_status st = hr_device_view(ctx, d, sizeof *d);
+    /* kernel boundary first (fresh global shadow / next epoch tag, and the end-of-kernel
+     * spill scan of the previous kernel), then the view of the state this kernel uses */
+    hr_status st = hr_kernel_begin(ctx, stream);
+    if (st) return st;
+    st = hr_device_view(ctx, d, sizeof *d);
     if (st) return st;
     d->kernel_id = kernel_id;
-    return hr_kernel_begin(ctx, stream);          /* kernel boundary: fresh global shadow */
+    return HR_OK;
 }
 
 hr_status launched()

@@ -2,7 +2,8 @@
  * hr_records.cuh — record sources of the replay kernels: row r of a warp for
  * one lane, decoded to the u64 record of tracegen/format.py (HR_TRACE_U64
  * stored as is; HR_TRACE_C32 split into a u32 word and a byte op | space<<2).
- * Streamed with ld.global.cs (read once).
+ * The replay kernels stage rows in shared memory with TMA bulk copies (below);
+ * the probes and the block-serial replay read them with ld.global.cs.
  */
 #ifndef HR_RECORDS_CUH_
 #define HR_RECORDS_CUH_

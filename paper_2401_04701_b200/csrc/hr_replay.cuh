@@ -11,9 +11,9 @@
  * driven by a synthetic access stream instead of a user
  * kernel's own loads and stores.
  *
- * Record rows are streamed with ld.global.cs (read once, evict-first) and
- * prefetched two rows ahead so the record latency is off the shadow-update
- * critical path.
+ * Record rows reach each warp through a per-warp ring of TMA bulk copies
+ * (cp.async.bulk on an mbarrier, hr_records.cuh) issued NB chunks ahead, so the
+ * record latency is off the shadow-update critical path.
  */
 #ifndef HR_REPLAY_CUH_
 #define HR_REPLAY_CUH_
@@ -157,20 +157,23 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
     }
 }
 
+/* A row holding control records (a10).  Uniform rows: __syncthreads advances
+ * bc, __syncwarp wc; a control code the trace format does not define (word > 2)
+ * is no barrier at all — HR_F_MODEL_VIOLATION, no clock moves (as the oracle,
+ * oracle/hr_oracle.c materialize).  A row whose lanes disagree is flagged
+ * HR_F_BARRIER_DIVERGENCE (undefined in CUDA; its racy set is unspecified). */
 __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint64_t x, unsigned lane_mask)
 {
     const uint32_t op = (uint32_t)(x >> 62);
     const uint64_t w = x & HR_WORD_MASK;
     const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
     const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
-    if ((bst && bst != lane_mask) || (ctrl != lane_mask))
-        if ((threadIdx.x & 31u) == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+    const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
+    if (hr__ctrl_divergent(x, ctrl, lane_mask) && (threadIdx.x & 31u) == 0)
+        hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+    if ((bst | bsw) != ctrl && (threadIdx.x & 31u) == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
     if (bst) hr_syncthreads(d, t);
-    else hr_syncwarp(d, t);
-    if (ctrl & ~bst) {
-        const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
-        if (bsw != ctrl && (threadIdx.x & 31u) == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
-    }
+    else if (bsw) hr_syncwarp(d, t);
 }
 
 /* Helper warp of a word when a simulated warp is split over 2^split_log2 CUDA
@@ -365,7 +368,9 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 continue;
             }
             if (!POOL) {
-                hr_check_lanes<false, ABL>(d, t, 0xffffffffu, op != 3u, (uint32_t)(x >> 61) & 1u, w, op);
+                const uint32_t space = (uint32_t)(x >> 61) & 1u;
+                if (!ABL && hr__shared_row_ok(t, op, space, w)) hr__check_shared_row(d, t, (uint32_t)w, op);
+                else hr_check_lanes<false, ABL>(d, t, 0xffffffffu, op != 3u, space, w, op);
                 continue;
             }
             insert(hr__pool_owned(d, t, x, split_log2, helper), x);
@@ -378,6 +383,7 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
         }
     }
     if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); __syncwarp(); }
+    hr_thread_end(d, t);                                             /* a9: spill a dropped shared race */
 }
 
 /* Probe for the kernel choice (one block): out[0..1] = access records / records
@@ -421,35 +427,49 @@ __global__ void hr_density_kernel(SRC src, uint64_t n_rows, uint32_t samples, co
     if (threadIdx.x < 5) out[threadIdx.x] = acc[threadIdx.x];
 }
 
-/* Overflow fallback / cross-check: every RACE word of the (local) global
- * shadow becomes one record in `out` (a9 "end-of-kernel shadow scan"). */
-__global__ void hr_scan_kernel(const unsigned long long *__restrict__ sh, uint64_t n_local, uint64_t gbase,
-                               uint32_t shard_rank, uint32_t shard_log2, uint32_t gran_log2, uint32_t kernel_id,
-                               uint32_t epoch_tag, hr_race *out,
-                               unsigned int *count, uint32_t cap)
+/* a9 overflow recovery, global space (enqueued by the host after every kernel,
+ * before its shadow is reset, and before a report): if the kernel latched a
+ * dropped global race record in ovf[2] (hr__ring_drop), every RACE word of its
+ * epoch in the (local) global shadow becomes one spill record — a superset of
+ * the dropped ones, exact because the shadow word of a racy address stays in
+ * RACE_* for the rest of the kernel.  Otherwise each CTA only reads one word.
+ * The last CTA to finish clears ovf[2] (all CTAs read it before counting). */
+__global__ void __launch_bounds__(256) hr_spill_scan_kernel(hr_dev d, const unsigned long long *__restrict__ sh,
+                                                            uint64_t n_local, uint32_t epoch_tag)
 {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        unsigned long long v = sh[i];
-        if (epoch_tag && (((uint32_t)v >> 28) & 15u) != epoch_tag) continue;   /* an earlier kernel's word */
-        uint32_t st = (uint32_t)(v >> HR_STATE_SHIFT);
-        if (st >= HR_RACE_BLOCK) {
-            uint32_t slot = atomicAdd(count, 1u);
-            if (slot < cap) {
-                uint64_t gran_local = i >> gran_log2;
-                uint64_t g = (hr_shard_granule(gran_local, shard_rank, shard_log2) << gran_log2) |
-                             (i & ((1ull << gran_log2) - 1u));
-                hr_race r;
-                r.word = gbase + g;
-                r.block = 0xffffffffu;
-                r.kernel = kernel_id;
-                r.first_tid = (uint32_t)(v >> HR_TID_SHIFT) & 0x7ffffffu;
-                r.space = HR_GLOBAL;
-                r.scope = (uint8_t)(st == HR_RACE_GRID ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
-                r.first_kind = 0xff;
-                r.prev_state = 0xff;
-                out[slot] = r;
-            }
+    __shared__ uint32_t kid1;
+    if (threadIdx.x == 0) kid1 = *(volatile unsigned int *)&d.ovf[2];
+    __syncthreads();
+    if (kid1) {
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+        for (uint64_t i0 = first; i0 < n_local; i0 += stride) {       /* warp-uniform trip count */
+            const uint64_t i = i0 + (threadIdx.x & 31u);
+            const unsigned long long v = i < n_local ? sh[i] : 0ull;
+            const uint32_t st = (uint32_t)(v >> HR_STATE_SHIFT);
+            /* lazy reset: a word of another epoch tag belongs to an earlier kernel */
+            const bool mine = !epoch_tag || (((uint32_t)v >> 28) & 15u) == epoch_tag;
+            const uint64_t gran = i >> d.gran_log2;
+            hr_race r;
+            r.word = d.gbase + ((hr_shard_granule(gran, d.shard_rank, d.shard_log2) << d.gran_log2) |
+                                (i & ((1ull << d.gran_log2) - 1u)));
+            r.block = 0xffffffffu;
+            r.kernel = kid1 - 1u;
+            r.first_tid = (uint32_t)(v >> HR_TID_SHIFT) & 0x7ffffffu;
+            r.space = HR_GLOBAL;
+            r.scope = (uint8_t)(st == HR_RACE_GRID ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
+            r.first_kind = 0xff;
+            r.prev_state = 0xff;
+            hr__spill_put(d.spill, d.ovf, d.spill_cap, d.flags, 0xffffffffu, i < n_local && mine && st >= HR_RACE_BLOCK, r);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&d.ovf[3], 1u) == gridDim.x - 1u) {
+            *(volatile unsigned int *)&d.ovf[2] = 0u;
+            *(volatile unsigned int *)&d.ovf[3] = 0u;
+            __threadfence();
         }
     }
 }

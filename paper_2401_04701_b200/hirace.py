@@ -20,10 +20,10 @@ import numpy as np
 
 from . import build as _build
 
-HR_OK, HR_E_ARG, HR_E_NOMEM, HR_E_CUDA, HR_E_STATE = 0, -1, -2, -3, -4
+HR_OK, HR_E_ARG, HR_E_NOMEM, HR_E_CUDA, HR_E_STATE, HR_E_INCOMPLETE = 0, -1, -2, -3, -4, -5
 HR_GLOBAL, HR_SHARED = 0, 1
 HR_F_CLOCK_OVERFLOW, HR_F_RING_OVERFLOW, HR_F_MODEL_VIOLATION = 1, 2, 4
-HR_F_BARRIER_DIVERGENCE, HR_F_UNMONITORED = 8, 16
+HR_F_BARRIER_DIVERGENCE, HR_F_UNMONITORED, HR_F_INCOMPLETE = 8, 16, 32
 HR_OPT_NO_COALESCE, HR_OPT_NO_FASTEXIT, HR_OPT_TIMING, HR_OPT_NO_SPECULATE, HR_OPT_NO_POOL, HR_OPT_POOL = \
     1, 2, 4, 8, 16, 32
 HR_OPT_DOUBLE_SHADOW = 64
@@ -38,6 +38,7 @@ HR_OPT_BSERIAL = 16384
 HR_OPT_ROW_NARROW = 65536
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_report_async",
+           "hr_report_async_to",
            "hr_report_collect", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing", "hr_launch_count",
            "hr_fsm_table",
@@ -47,7 +48,7 @@ EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives
 class HrConfig(ctypes.Structure):
     _fields_ = [("state_bits", ctypes.c_uint8), ("tid_bits", ctypes.c_uint8), ("bc_bits", ctypes.c_uint8),
                 ("wc_bits", ctypes.c_uint8), ("ring_capacity", ctypes.c_uint32), ("device", ctypes.c_int),
-                ("options", ctypes.c_uint32)]
+                ("options", ctypes.c_uint32), ("spill_capacity", ctypes.c_uint32)]
 
 
 class HrRace(ctypes.Structure):
@@ -100,6 +101,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_merge_races": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, P(ctypes.c_size_t)], ctypes.c_int),
         "hr_report_async": ([vp, vp], ctypes.c_int),
+        "hr_report_async_to": ([vp, vp, vp, ctypes.c_uint32, vp], ctypes.c_int),
         "hr_report_collect": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_race_classes": ([vp, P(HrTrace), vp, ctypes.c_size_t, vp, vp], ctypes.c_int),
         "hr_reset_report": ([vp], ctypes.c_int),
@@ -121,20 +123,23 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
 
 
 class HiraceError(RuntimeError):
-    pass
+    def __init__(self, msg: str, status: int = 0):
+        super().__init__(msg)
+        self.status = status
 
 
 def _check(rc: int, ctx=None, what: str = ""):
     if rc != HR_OK:
         msg = load().hr_last_error(ctx).decode() if ctx else ""
-        raise HiraceError(f"{what} failed with status {rc}: {msg}")
+        raise HiraceError(f"{what} failed with status {rc}: {msg}", rc)
 
 
 # ---- C-ABI mirrors -------------------------------------------------------------
 
 def hr_init(bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, device: int = 0,
-            options: int = 0):
-    cfg = HrConfig(5, 27, bc_bits, wc_bits, ring_capacity, device, options)
+            options: int = 0, spill_capacity: int = 0):
+    """spill_capacity 0 = automatic (include/hr.h, hr_config)."""
+    cfg = HrConfig(5, 27, bc_bits, wc_bits, ring_capacity, device, options, spill_capacity)
     ctx = ctypes.c_void_p()
     _check(load().hr_init(ctypes.byref(cfg), ctypes.byref(ctx)), None, "hr_init")
     return ctx
@@ -229,6 +234,14 @@ def hr_report_raw(ctx, cap: int = 1 << 17, copy: bool = True) -> Tuple[np.ndarra
 def hr_report_async(ctx, stream: Optional[int] = None):
     """Enqueue the device-side report (hr_report_async); no host wait."""
     _check(load().hr_report_async(ctx, stream or None), ctx, "hr_report_async")
+
+
+def hr_report_async_to(ctx, out_ptr: int, out_cap: int, hdr_ptr: int, stream: Optional[int] = None):
+    """Enqueue the device-side report into caller DEVICE buffers: out (out_cap
+    hr_race records) and hdr (4 uint32: unique count, flags, raw count,
+    overflow).  No host wait (include/hr.h)."""
+    _check(load().hr_report_async_to(ctx, stream or None, ctypes.c_void_p(out_ptr), out_cap,
+                                     ctypes.c_void_p(hdr_ptr)), ctx, "hr_report_async_to")
 
 
 def hr_report_collect(ctx, cap: int = 1 << 17, copy: bool = True) -> Tuple[np.ndarray, int]:
@@ -432,8 +445,8 @@ class Checker:
 
     def __init__(self, global_words: int, smem_words: int = 0, base_word: int = 0, device: int = 0,
                  bc_bits: int = 16, wc_bits: int = 16, ring_capacity: int = 1 << 20, options: int = 0,
-                 shard: Optional[Tuple[int, int]] = None, granule_log2: int = 3):
-        self.ctx = hr_init(bc_bits, wc_bits, ring_capacity, device, options)
+                 shard: Optional[Tuple[int, int]] = None, granule_log2: int = 3, spill_capacity: int = 0):
+        self.ctx = hr_init(bc_bits, wc_bits, ring_capacity, device, options, spill_capacity)
         if shard is not None:
             hr_set_shard(self.ctx, shard[0], shard[1], granule_log2)
         self.shadow_ptr = hr_shadow_alloc(self.ctx, HR_GLOBAL, base_word, max(1, global_words))

@@ -9,9 +9,11 @@ with block % N == r.  Each rank replays every
 simulated thread but only its own records, keeping all barrier records so the
 per-word commit order stays happens-before consistent; its shadow is 1/N.
 The ONE exchange is the race-set allgather (NCCL over NVLink on GPUs, gloo
-in the CPU tests) followed by a concatenate-and-sort merge in libhirace
-(hr_merge_races, host C) — shards are address-disjoint, so the merge only
-interleaves the per-rank sorted lists.
+in the CPU tests): each rank's device report (hr_report_async_to) goes into
+a fixed-size device buffer that all_gather_into_tensor moves to every rank
+inside the step (DeviceExchange); the concatenate-and-merge in libhirace
+(hr_merge_races, host C) runs when the set is collected — shards are
+address-disjoint, so the merge only interleaves the per-rank sorted lists.
 
 torch.distributed provides the process group only; the check runs in
 libhirace.so.
@@ -122,9 +124,95 @@ def exchange_races(raw: np.ndarray, flags: int = 0, group=None, device=None) -> 
     return hr_merge_races(flat.view(RACE_DTYPE)), all_flags
 
 
-def replay_sharded(trace, group=None, device: Optional[int] = None, base_word: int = 0, **checker_kw):
+class DeviceExchange:
+    """The per-step race-set exchange with no host round trip (SURVEY §8(e)
+    step 5): each rank's sorted unique set is written by hr_report_async_to
+    into a fixed-size DEVICE buffer (cap records + a 4-word header), and one
+    all_gather_into_tensor moves every rank's buffer to every rank (NCCL over
+    NVLink: on the launching stream, ordered after the report).  The merge of
+    the N address-disjoint sorted lists (hr_merge_races) runs only in
+    collect(), off the step's critical path.
+
+    With a gloo group (CPU tests; several ranks sharing one GPU) the buffers
+    are staged through host memory for the collective: same result, not the
+    device path."""
+
+    def __init__(self, ctx, cap: int = 1 << 17, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.ctx, self.cap, self.group = ctx, int(cap), group
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+        dev = device
+        self.buf = torch.empty(self.cap * RACE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.hdr = torch.zeros(4, dtype=torch.int32, device=dev)
+        gdev = dev if self.nccl else "cpu"
+        self.gbuf = torch.empty(self.world * self.buf.numel(), dtype=torch.uint8, device=gdev)
+        self.ghdr = torch.empty(self.world * 4, dtype=torch.int32, device=gdev)
+
+    def step(self, stream: Optional[int] = None):
+        """Enqueue this rank's report and the allgather (asynchronous on NCCL)."""
+        import torch
+        import torch.distributed as dist
+        from .hirace import hr_report_async_to
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        hr_report_async_to(self.ctx, self.buf.data_ptr(), self.cap, self.hdr.data_ptr(), stream)
+        if self.nccl:
+            dist.all_gather_into_tensor(self.ghdr, self.hdr, group=self.group)
+            dist.all_gather_into_tensor(self.gbuf, self.buf, group=self.group)
+        else:
+            dist.all_gather_into_tensor(self.ghdr, self.hdr.cpu(), group=self.group)
+            dist.all_gather_into_tensor(self.gbuf, self.buf.cpu(), group=self.group)
+
+    def step_from_host(self, raw: np.ndarray, flags: int = 0):
+        """Same exchange for a set already on the host (e.g. a CPU-side test of
+        the gather / merge logic): the set is written into the device (or, on
+        gloo, host) buffer and header, then gathered as in step()."""
+        import torch
+        import torch.distributed as dist
+        raw = np.ascontiguousarray(raw, dtype=RACE_DTYPE)
+        n = min(len(raw), self.cap)
+        hdr = torch.tensor([len(raw), flags, len(raw), 0], dtype=torch.int32)
+        buf = torch.zeros(self.buf.numel(), dtype=torch.uint8)
+        if n:
+            buf[: n * RACE_DTYPE.itemsize] = torch.from_numpy(raw[:n].view(np.uint8).copy())
+        if self.nccl:
+            self.hdr.copy_(hdr)
+            self.buf.copy_(buf)
+            hdr, buf = self.hdr, self.buf
+        dist.all_gather_into_tensor(self.ghdr, hdr, group=self.group)
+        dist.all_gather_into_tensor(self.gbuf, buf, group=self.group)
+
+    def collect(self, fallback_raw=None) -> Tuple[np.ndarray, int]:
+        """(sorted global set, OR of the ranks' flags) of the last step; identical
+        on every rank.  A rank whose set overflowed `cap` or whose ring
+        overflowed (spill store) is re-read with the full hr_report path
+        (`fallback_raw` = that rank's (raw, flags) getter) and re-exchanged."""
+        from .hirace import hr_merge_races
+        hdr = self.ghdr.cpu().numpy().reshape(self.world, 4).astype(np.int64)
+        if np.any(hdr[:, 0] > self.cap) or np.any(hdr[:, 3] != 0):
+            if fallback_raw is None:
+                raise RuntimeError("race-set exchange overflow: raise DeviceExchange cap or pass fallback_raw")
+            raw, flags = fallback_raw()
+            return exchange_races(raw, flags, self.group)
+        allb = self.gbuf.cpu().numpy().reshape(self.world, -1)
+        parts = [allb[r].view(RACE_DTYPE)[: int(hdr[r, 0])] for r in range(self.world)]
+        flags = 0
+        for f in hdr[:, 1]:
+            flags |= int(f)
+        flat = np.concatenate(parts) if parts else np.zeros(0, RACE_DTYPE)
+        return hr_merge_races(flat), flags
+
+
+def replay_sharded(trace, group=None, device: Optional[int] = None, base_word: int = 0, cap: int = 1 << 17,
+                   **checker_kw):
     """Replay a host trace address-sharded over the ranks of `group` (one GPU per
-    rank) and return the global sorted race set (hr_race records) and flags."""
+    rank) and return the global sorted race set (hr_race records) and flags,
+    identical on every rank: shard (host), replay (libhirace), device report,
+    allgather (DeviceExchange), merge."""
     import torch
     import torch.distributed as dist
     from . import hirace
@@ -135,6 +223,8 @@ def replay_sharded(trace, group=None, device: Optional[int] = None, base_word: i
     ck = hirace.Checker(gmax - base_word, smem, base_word=base_word, device=dev, shard=(rank, world),
                         **checker_kw)
     ck.replay(hirace.DeviceTrace.from_trace(local, device=f"cuda:{dev}"))
-    raw, flags = ck.report_raw()
+    ex = DeviceExchange(ck.ctx, cap, group, device=torch.device("cuda", dev))
+    ex.step()
+    out = ex.collect(fallback_raw=ck.report_raw)
     ck.close()
-    return exchange_races(raw, flags, group)
+    return out

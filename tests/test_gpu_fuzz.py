@@ -72,7 +72,9 @@ def _witness(tr):
 def test_fuzzed_schedules_match_oracle():
     from paper_2401_04701_b200 import build
     lib = build.build_fuzz()
-    env = dict(os.environ, HIRACE_LIB=lib, PYTHONPATH=ROOT)
+    # additive PYTHONPATH: the driver's load-recording hook (sitecustomize) must stay on the path
+    pp = os.environ.get("PYTHONPATH", "")
+    env = dict(os.environ, HIRACE_LIB=lib, PYTHONPATH=ROOT + (os.pathsep + pp if pp else ""))
     out = subprocess.run([sys.executable, "-c", "import tests.test_gpu_fuzz as m; m.worker()"], cwd=ROOT, env=env,
                          capture_output=True, text=True, timeout=1200)
     assert out.returncode == 0, out.stderr[-3000:]

@@ -32,6 +32,27 @@ def _to_raw(races):
     return a
 
 
+def _worker_device_exchange(rank, world, port, path, out_dir):
+    """Same as _worker through multigpu.DeviceExchange (fixed-size buffers +
+    all_gather_into_tensor, merged on collect), with a small cap so one rank's
+    set overflows it once and the full-path fallback is exercised too."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    trace = np.load(path, allow_pickle=True)["t"].item()
+    res = oracle.check(multigpu.shard_trace(trace, rank, world))
+    raw = _to_raw(res.races)
+    ex = multigpu.DeviceExchange(None, cap=1 << 12, device="cpu")
+    ex.step_from_host(raw, res.flags)
+    merged, flags = ex.collect()
+    small = multigpu.DeviceExchange(None, cap=2, device="cpu")
+    small.step_from_host(raw, res.flags)
+    merged2, _ = small.collect(fallback_raw=lambda: (raw, res.flags))
+    assert np.array_equal(merged, merged2)
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), merged)
+    dist.destroy_process_group()
+
+
 def _worker(rank, world, port, path, out_dir):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -50,11 +71,11 @@ def _worker(rank, world, port, path, out_dir):
     dist.destroy_process_group()
 
 
-def _run(trace, world=2):
+def _run(trace, world=2, worker=None):
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "t.npz")
         np.savez(path, t=np.array(trace, dtype=object))
-        mp.spawn(_worker, args=(world, _free_port(), path, d), nprocs=world, join=True)
+        mp.spawn(worker or _worker, args=(world, _free_port(), path, d), nprocs=world, join=True)
         outs = [np.load(os.path.join(d, f"r{r}.npy")) for r in range(world)]
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])          # identical on every rank
@@ -81,6 +102,15 @@ def test_gloo_sharded_random_programs():
     want = [tuple(r) for r in oracle.check(trace).races]
     assert len(want) > 5
     assert _run(trace, 2) == want
+
+
+def test_gloo_device_exchange_c5_and_random():
+    trace = c5.cpu_trace(3)
+    want = [tuple(r) for r in oracle.check(trace).races]
+    assert _run(trace, 2, _worker_device_exchange) == want
+    rng = random.Random(9)
+    t = tp.random_program(rng, max_slots=12, n_words=4000, spaces=(0, 1), grid=(4, 2, 32))
+    assert _run(t, 2, _worker_device_exchange) == [tuple(r) for r in oracle.check(t).races]
 
 
 def test_gloo_sharded_c5():

@@ -261,3 +261,31 @@ def test_barrier_divergence_flag():
     assert oracle.check(tr).flags & oracle.F_BARRIER_DIVERGENCE
     with pytest.raises(tf.BarrierDivergence):
         tp.from_thread_events(1, 1, 2, {(0, 0, 0): [tf.SYNCTHREADS], (0, 0, 1): [tf.W(0)]})
+
+
+def test_undefined_control_code_is_no_barrier():
+    """The oracle's model-violation branch (reading R12 in DESIGN.md): the trace
+    format defines control words 0 NOP, 1 __syncthreads, 2 __syncwarp; any
+    other code is flagged and is NOT a barrier.  Pinned by the barrier
+    semantics (§II-B): lane 0 writes word 0, then every lane
+    holds the code, then lane 1 reads word 0.  Had the code been a __syncwarp
+    the two accesses would be ordered (same warp, later warp epoch) and there
+    would be no race; as no barrier they are unordered and word 0 races,
+    BLOCK scope (one block)."""
+    import numpy as np
+    for code in (3, 7, 12345):
+        rows = np.full((1, 3, 32), tf.NOP, dtype=np.uint64)
+        rows[0, 0, 0] = tf.W(0)
+        rows[0, 1, :] = tf.encode(tf.OP_CTRL, 0, code)
+        rows[0, 2, 1] = tf.R(0)
+        tr = tf.make_trace([tf.kernel_from_rows(1, 1, 2, rows)])
+        for mode in (oracle.PAIRWISE, oracle.BUCKETED):
+            res = oracle.check(tr, mode=mode)
+            assert res.flags == oracle.F_MODEL_VIOLATION
+            assert [(r.word, r.scope) for r in res.races] == [(0, oracle.SCOPE_BLOCK)]
+        rows[0, 1, :] = tf.SYNCWARP
+        res = oracle.check(tf.make_trace([tf.kernel_from_rows(1, 1, 2, rows)]))
+        assert res.races == [] and res.flags == 0
+        # an undefined code orders nothing: the set equals that of the same trace with a NOP there
+        rows[0, 1, :] = tf.NOP
+        assert [r.word for r in oracle.check(tf.make_trace([tf.kernel_from_rows(1, 1, 2, rows)])).races] == [0]
