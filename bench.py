@@ -66,8 +66,10 @@ def parse():
                     help="address-shard granule (2^g words; 3 = 64 B of shadow)")
     ap.add_argument("--double-shadow", action="store_true",
                     help="HR_OPT_DOUBLE_SHADOW: reset the previous kernel's shadow on a side stream")
-    ap.add_argument("--format", default="c32", choices=["c32", "u64"],
-                    help="device-resident trace encoding (include/hr.h HR_TRACE_U64 = 256 B/row, C32 = 160 B/row)")
+    ap.add_argument("--format", default="c32", choices=["c32", "u64", "pooled"],
+                    help="device-resident trace encoding (include/hr.h HR_TRACE_U64 = 256 B/row, C32 = 160 B/row, "
+                         "POOLED = the C32 trace re-laid out as warp pools by hr_pool_trace, untimed: for sparse "
+                         "address shards)")
     ap.add_argument("--e2e-format", default="packed", choices=["packed", "c32", "u64"],
                     help="host-buffer trace encoding for e2e: packed (HR_TRACE_PACKED, decoded on the device), "
                          "c32 (160 B/row) or u64 (256 B/row)")
@@ -313,11 +315,15 @@ def measure_slowdown(dt, kern_ms_launch: float, data_words: int, c4_lv: int):
     # C1 (1 block), C3 (1024 blocks), C4 (BFS levels + histogram) online
     d1 = torch.arange(8 * 256 + 8, dtype=torch.int32, device="cuda")
     ck1 = hr.Checker(8 * 256 + 8, 256)
-    out["c1_online"] = on.slowdown(lambda: on.c1(None, d1, False), lambda: on.c1(ck1.ctx, d1, True), reps=20)
+    # instrumented runs reset the report ring each time (a racy kernel would otherwise fill it
+    # and every further run would pay the overflow recovery)
+    out["c1_online"] = on.slowdown(lambda: on.c1(None, d1, False),
+                                   lambda: (hr.hr_reset_report(ck1.ctx), on.c1(ck1.ctx, d1, True)), reps=20)
     ck1.close()
     d3 = torch.randint(0, 100, (2 * 512 * 512,), dtype=torch.int32, device="cuda")
     ck3 = hr.Checker(2 * 512 * 512, 648)
-    out["c3_online"] = on.slowdown(lambda: on.c3(None, d3, False), lambda: on.c3(ck3.ctx, d3, True), reps=10)
+    out["c3_online"] = on.slowdown(lambda: on.c3(None, d3, False),
+                                   lambda: (hr.hr_reset_report(ck3.ctx), on.c3(ck3.ctx, d3, True)), reps=10)
     ck3.close()
     g = c4.Graph(c4_lv)
     dev = on.C4Device(g)
@@ -325,7 +331,8 @@ def measure_slowdown(dt, kern_ms_launch: float, data_words: int, c4_lv: int):
     ck4 = hr.Checker(g.n + 1024, 0, ring_capacity=1 << 24)
     for racy in (False, True):
         out[f"c4_online_{'racy' if racy else 'atomic'}_2^{c4_lv}"] = on.slowdown(
-            lambda: dev.run(None, d4, False, racy), lambda: dev.run(ck4.ctx, d4, True, racy), reps=5)
+            lambda: dev.run(None, d4, False, racy),
+            lambda: (hr.hr_reset_report(ck4.ctx), dev.run(ck4.ctx, d4, True, racy)), reps=5)
     ck4.close()
     for v in out.values():
         for k in list(v):
@@ -381,15 +388,14 @@ def run_c3(args):
     spin = cuda_spin_wait(0) if not args.no_spin else False
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream().cuda_stream
-    removed, n = 20, stencil.N
+    removed, n = None, stencil.N                           # the race-free stencil; racy variant below
     tr = stencil.stencil_trace(removed=removed, n=n)
     dt = hr.DeviceTrace.from_trace(tr, compact=True)
     n_acc = int((((tr.rec >> np.uint64(62)) & np.uint64(3)) != 3).sum())
     words, smem = 2 * n * n, 2 * stencil.TILE
     ck = hr.Checker(words, smem, options=hr.HR_OPT_TIMING | args.options)
     blocks = (n // stencil.T) ** 2
-    per_block = stencil.expected_racy_shared_words(removed)
-    want = [(0, 1, b, int(w), 1) for b in range(blocks) for w in per_block]
+    want = []
 
     def step(replay):
         ck.reset()
@@ -424,6 +430,31 @@ def run_c3(args):
     parity = parity and [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
                          for r in raw] == want
     k_ms = kern_ms / max(n_kern, 1)
+    # racy variant (barrier after sweep 20 removed: 524,288 racy shared words per step, so the
+    # report — device sort of the ring + 12.6 MB written to pinned host memory — weighs in)
+    tr_r = stencil.stencil_trace(removed=20, n=n)
+    dt_r = hr.DeviceTrace.from_trace(tr_r, compact=True)
+    want_r = [(0, 1, b, int(w), 1) for b in range(blocks) for w in stencil.expected_racy_shared_words(20)]
+    rr = lambda: ck.replay(dt_r, stream)  # noqa: E731
+    for _ in range(3):
+        step(rr)
+    ck.collect_raw()
+    hr.hr_replay_timing(ck.ctx)
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    for _ in range(steps):
+        step(rr)
+    g1.record()
+    torch.cuda.synchronize()
+    raw_r, _ = ck.collect_raw()
+    _, _, kr_ms, nkr = hr.hr_replay_timing(ck.ctx)
+    racy = {"workload": "same stencil, barrier after sweep 20 removed", "ms_per_step": g0.elapsed_time(g1) / steps,
+            "value": n_acc / (g0.elapsed_time(g1) / steps / 1e3), "kernel_ms": kr_ms / max(nkr, 1),
+            "races_per_step": len(raw_r),
+            "parity_vs_closed_form": [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]),
+                                       int(r["scope"])) for r in raw_r] == want_r}
+    del dt_r
     hbm, hbm_kind = peaks()
     sm_max = clk.get("sm_max_mhz") or 1965.0
     issue_peak = 148 * 4 * sm_max * 1e6 / 1e9                          # G warp-instructions/s
@@ -463,7 +494,8 @@ def run_c3(args):
     if not args.no_slowdown:
         d3 = torch.randint(0, 100, (words,), dtype=torch.int32, device="cuda")
         ck3 = hr.Checker(words, smem)
-        slow = {"c3_online": on.slowdown(lambda: on.c3(None, d3, False), lambda: on.c3(ck3.ctx, d3, True), reps=10)}
+        slow = {"c3_online": on.slowdown(lambda: on.c3(None, d3, False, removed=None),
+                                         lambda: on.c3(ck3.ctx, d3, True, removed=None), reps=10)}
         ck3.close()
         data = torch.zeros(words, dtype=torch.int32, device="cuda")
         raw_ms = on.time_ms(lambda: on.raw_replay(dt, data, words), reps=5, warmup=2)
@@ -471,12 +503,12 @@ def run_c3(args):
     cpu = None
     if not args.no_cpu:
         import oracle
-        small = stencil.stencil_trace(removed=removed, n=64)
+        small = stencil.stencil_trace(removed=20, n=64)
         t0 = time.perf_counter()
         res = oracle.check(small, mode=oracle.BUCKETED)
         dtc = time.perf_counter() - t0
         cpu = dict({"value": res.n_accesses / dtc, "unit": UNIT, "cores": 1, "kind": "oracle",
-                    "sample": f"C3 at n=64 (16 of the 1024 blocks, {res.n_accesses} accesses), bucketed, "
+                    "sample": f"C3 racy variant at n=64 (16 of the 1024 blocks, {res.n_accesses} accesses), bucketed, "
                               f"{dtc:.2f} s", "extrapolated_full_step_s": dtc * n_acc / res.n_accesses,
                     "extrapolation": "x64 by access count (EXTRAPOLATED, not measured)"}, **host_cpu())
     out = {
@@ -484,7 +516,7 @@ def run_c3(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"C3: shared-memory 2D stencil {n}x{n}, {blocks} blocks x 256 threads, 42 sweeps, "
-                               f"barrier after sweep {removed} removed, {n_acc} checked accesses",
+                               f"race-free (racy variant in racy_variant), {n_acc} checked accesses",
                    "trace_format": "c32", "host_wait": "spin" if spin else "default",
                    "report": "hr_report_async every step", "l2": "trace (0.34 GB) > L2 is streamed; the SMEM "
                    "shadow is per block; no flush needed"},
@@ -500,6 +532,7 @@ def run_c3(args):
                 "d2h_bytes_per_step": 16 + 24 * len(raw_e), "ms_per_step": e2e_ms, "format": "c32"},
         "gpu_launches": n_launch,
         "gpu_launches_detail": {"replay_kernel": n_kern, "all_libhirace": n_launch},
+        "racy_variant": racy,
         "slowdown": slow, "cpu_baseline": cpu, "parity_vs_closed_form": parity,
     }
     print(json.dumps(out), flush=True)
@@ -533,7 +566,7 @@ def main():
 
     shard_rank, shard_n = emulated if emulated else (rank, world)
     # --- input: this rank's shard of the trace, generated in HBM (untimed) ---
-    if args.format == "c32":
+    if args.format in ("c32", "pooled"):
         rec32, recop, woff, kd = c5.gpu_trace_c32(lb, seed, rank=shard_rank, nshard=shard_n,
                                                   granule_log2=args.granule_log2)
         dt = hr.DeviceTrace(None, woff, kd, rec32, recop)
@@ -564,6 +597,14 @@ def main():
         opts |= hr.HR_OPT_LAZY_RESET
     ck = hr.Checker(c5.total_words(lb), 0, shard=(shard_rank, shard_n), options=opts, ring_capacity=1 << 21,
                     granule_log2=args.granule_log2)
+    if args.format == "pooled":
+        pooled = ck.pool(dt, stream)                      # untimed input re-layout (hr_pool_trace)
+        dt.rec32 = dt.recop = None
+        rec32 = recop = None  # noqa: F841
+        dt = pooled
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        n_rows = dt.n_rows
 
     step_log = [] if os.environ.get("HR_BENCH_STEPLOG") else None
     # N > 1: device report + allgather of the fixed-size per-rank buffers inside the step, merged

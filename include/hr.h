@@ -125,6 +125,10 @@ enum {
     HR_OPT_BSERIAL = 16384u,     /* sparse U64 traces (pooled replay): one CUDA warp replays a whole
                                     simulated block epoch by epoch (hr_bserial.cuh) */
     HR_OPT_ROW_NARROW = 65536u,  /* force the 32-register row kernel (64 warps/SM) */
+    HR_OPT_NO_STREAMS = 131072u, /* long-tailed barrier-free kernels without shared shadow: use the
+                                    per-block compacted replay instead of the stream-scheduled one
+                                    (hr_streams.cuh: hub warps fanned out over helper streams that
+                                    any CUDA warp of any CTA replays, longest first) */
     HR_OPT_SPECULATE = 2048u     /* ablation: global reads/writes skip Algorithm 1's first atomic read
                                     and CAS against INIT (the CAS return is the read when it fails).
                                     Measured slower: a failed CAS costs an L2 atomic round trip that
@@ -150,8 +154,21 @@ typedef struct {
 enum {
     HR_TRACE_U64 = 0,   /* rec: one u64 record per lane and row (any word < 2^61) */
     HR_TRACE_C32 = 1,   /* rec32 + recop: 160 B per row instead of 256 (words < 2^32) */
-    HR_TRACE_PACKED = 2 /* packed + pack_off: lossless variable-length rows (below), made by hr_pack_trace */
+    HR_TRACE_PACKED = 2, /* packed + pack_off: lossless variable-length rows (below), made by hr_pack_trace */
+    HR_TRACE_POOLED = 3  /* rec + recop: pooled rows (below), made by hr_pool_trace */
 };
+
+/* HR_TRACE_POOLED: the same access streams re-laid out as warp pools (not in
+ * the paper: a replay input layout for sparse traces, e.g. address shards,
+ * whose rows carry few accesses).  Row r holds 32 entries: rec[r*32 + i] a
+ * U64-layout record and recop[r*32 + i] (u8) the simulated lane it belongs
+ * to.  A row is either a barrier row copied verbatim (tags = lanes) or up to
+ * 32 accesses of ONE simulated warp inside one epoch, in record order (row-
+ * major, lanes ascending), NOP-padded at its end; warp_off gives each warp's
+ * rows as for U64.  Lanes of one row are unordered by happens-before (same
+ * warp, same epochs) and each thread's accesses keep program order, so a row
+ * is checked as one pool (same-word entries folded in order).  Device only
+ * (hr_replay_trace); not for hr_replay_trace_host / hr_race_classes. */
 
 /* HR_TRACE_PACKED: a lossless, transfer-oriented encoding of the U64 rows
  * (not in the paper: it shrinks the host->device bytes of hr_replay_trace_host).
@@ -290,6 +307,16 @@ hr_status hr_replay_trace_host(hr_ctx *ctx, const hr_trace *t, void *stream);
  * other fields (kdesc, warp_off, n_rows) are shared with the packed trace. */
 hr_status hr_pack_trace(hr_ctx *ctx, const hr_trace *in, uint8_t *out, uint64_t cap, uint64_t *pack_off,
                         uint64_t *bytes, void *stream);
+
+/* Re-lay a DEVICE trace `in` (U64 or C32) out as HR_TRACE_POOLED on `stream`:
+ *   rec_out == NULL: size query, *rows receives the pooled row count;
+ *   otherwise rec_out (DEVICE, cap_rows*32 u64), tag_out (DEVICE, cap_rows*32
+ *   u8) and warp_off_out (DEVICE, in->n_warp_off u64; warp offsets for the
+ *   same kdesc) receive the pooled trace; HR_E_ARG if cap_rows < *rows.
+ * Accesses this ctx's address shard does not own are dropped (an unsharded
+ * ctx keeps all).  Synchronises `stream`. */
+hr_status hr_pool_trace(hr_ctx *ctx, const hr_trace *in, uint64_t *rec_out, uint8_t *tag_out, uint64_t cap_rows,
+                        uint64_t *warp_off_out, uint64_t *rows, void *stream);
 
 /* Decode a DEVICE HR_TRACE_PACKED trace `in` into U64 rows: rec_out (DEVICE,
  * in->n_rows*32 u64) receives row r of every segment at rec_out[r*32..];

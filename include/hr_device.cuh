@@ -587,8 +587,13 @@ __device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, 
     }
     peers = __match_any_sync(mask, key);
     if (ONLINE && __any_sync(mask, peers != (1u << lane))) {
-        const unsigned same_epoch = __match_any_sync(mask, (unsigned long long)(uint32_t)t.meta);
-        if (peers & ~same_epoch) peers = 1u << lane;
+        /* a fold needs one epoch: true in any program with uniform barriers (one SHFL +
+         * VOTE to confirm); otherwise split the groups by epoch with a second MATCH */
+        const uint32_t lo = (uint32_t)t.meta;
+        if (!__all_sync(mask, lo == __shfl_sync(mask, lo, __ffs(mask) - 1))) {
+            const unsigned same_epoch = __match_any_sync(mask, (unsigned long long)lo);
+            if (peers & ~same_epoch) peers = 1u << lane;
+        }
     }
     kb0 = __ballot_sync(mask, kind & 1u);
     kb1 = __ballot_sync(mask, (kind >> 1) & 1u);
@@ -604,10 +609,19 @@ __device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, 
  * access is committed (the final ballot is the warp's convergence point), so a
  * lane never runs ahead of an access folded into another lane (program order).
  */
+__device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind);
+__device__ __forceinline__ bool hr__shared_row_ok(const hr_thr &t, uint32_t op, uint32_t space, uint64_t word);
+
 template <bool ONLINE, bool ABL = true>
 __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t, unsigned mask, bool valid,
                                                uint32_t space, uint64_t word, uint32_t kind)
 {
+    /* online, full warp of distinct shared words (a stencil / tile access): the specialised
+     * shared row (no grouping needed, clocks per lane) */
+    if (ONLINE && !ABL && mask == 0xffffffffu && hr__shared_row_ok(t, valid ? kind : 3u, space, word)) {
+        hr__check_shared_row(d, t, (uint32_t)word, kind);
+        return;
+    }
     const uint32_t lane = hr__laneid();
     const bool is_shared = space != 0u;
     uint64_t local = 0;

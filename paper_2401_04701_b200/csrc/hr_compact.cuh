@@ -177,8 +177,9 @@ __global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr
     t.off = hr__thread_off(d, d.block_base + cta, warp);
     const unsigned lane_mask = lanes >= 32u ? 0xffffffffu : ((1u << lanes) - 1u);
     const uint64_t w = (uint64_t)cta * warps + warp;
-    const uint64_t nsg = segoff[w + 1] - segoff[w];
-    const uint64_t bi = segoff[w] << split_log2;
+    /* segoff == NULL: one stream per warp with rows [rowoff[w], rowoff[w+1]) (HR_TRACE_POOLED) */
+    const uint64_t nsg = segoff ? segoff[w + 1] - segoff[w] : 1u;
+    const uint64_t bi = (segoff ? segoff[w] : w) << split_log2;
     const uint64_t c0 = rowoff[bi + helper * nsg], c1 = rowoff[bi + (helper + 1) * nsg];
     const uint32_t n = (uint32_t)(c1 - c0);
     const uint32_t smem0 = (uint32_t)__cvta_generic_to_shared(hr_smem);

@@ -28,6 +28,7 @@
 #include "hr_pack.cuh"
 #include "hr_compact.cuh"
 #include "hr_bserial.cuh"
+#include "hr_streams.cuh"
 #include "fsm_table.inc"
 #include "fsm_classes.inc"
 
@@ -73,9 +74,12 @@ struct hr_ctx {
     /* staging: 0 warp_off, 1 rec|rec32|packed, 2 recop|decoded chunk, 3 pack_off,
      * 4 hr_pack_trace segment sizes + error word, 5 scan temporaries,
      * compacted replay: 6 segment counts, 7 segment offsets, 8 row counts,
-     * 9 row offsets, 10 packed records, 11 packed tags */
-    void *stage[12] = {};
-    size_t stage_cap[12] = {};
+     * 9 row offsets, 10 packed records, 11 packed tags,
+     * stream-scheduled replay (hr_streams.cuh): 12 per-warp units/streams/slots (3 x nw+1),
+     * 13 their scans (3 x nw+1), 14 helper log2, 15 slot counts, 16 slot offsets, 17 stream
+     * lengths / bases, 18 stream warp / key / id / total, 19 sorted keys / order, 20 counters */
+    void *stage[24] = {};
+    size_t stage_cap[24] = {};
     hr_race *rep_host = nullptr;                 /* pinned staging of the sorted report (D2H) */
     size_t rep_cap = 0;
     std::vector<hr_race> rep;                    /* report scratch, kept across calls */
@@ -560,6 +564,122 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     return HR_OK;
 }
 
+/* Stream-scheduled replay of blocks [b0, b1) of a barrier-free kernel k
+ * without shared shadow (hr_streams.cuh).  Two small synchronous reads size
+ * the buffers.  *fallback = true (nothing replayed) if the kernel holds a
+ * barrier record. */
+template <typename SRC>
+static hr_status launch_streams(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const uint64_t *woff,
+                                cudaStream_t s, uint64_t b0, uint64_t b1, bool abl, bool *fallback)
+{
+    *fallback = false;
+    const uint64_t *kd = t->kdesc + 8ull * k;
+    const uint64_t warps = kd[1], lanes = kd[2], woi = kd[4];
+    const uint32_t kid = t->kernel_base + k;
+    hr_dev d = make_dev(c, kid);
+    d.block_base = (uint32_t)b0;
+    const uint64_t nw = (b1 - b0) * warps;
+    const uint64_t *wk = woff + woi + b0 * warps;
+    hr_status st;
+    const size_t n1 = (size_t)(nw + 1);
+    if ((st = reserve(c, 12, 3 * n1 * 8)) || (st = reserve(c, 13, 3 * n1 * 8)) || (st = reserve(c, 14, n1)) ||
+        (st = reserve(c, 20, 64)))
+        return st;
+    uint64_t *cntw = (uint64_t *)c->stage[12], *offw = (uint64_t *)c->stage[13];
+    uint64_t *nunit = cntw, *nstream = cntw + n1, *nslot = cntw + 2 * n1;
+    uint64_t *unitoff = offw, *streamoff = offw + n1, *slotoff = offw + 2 * n1;
+    uint8_t *hlog2 = (uint8_t *)c->stage[14];
+    unsigned int *ctr = (unsigned int *)c->stage[20];   /* [0] barrier flag, [1] next stream */
+    c->launches++;
+    hr_st_plan_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(wk, nw, nunit, nstream, nslot, hlog2);
+    CU(cudaGetLastError());
+    size_t tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nunit, unitoff, (int64_t)n1, s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    for (int i = 0; i < 3; i++) {
+        size_t tb = tmp;
+        c->launches += 2;
+        CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tb, cntw + i * n1, offw + i * n1, (int64_t)n1, s));
+    }
+    uint64_t tot[3];
+    for (int i = 0; i < 3; i++) CU(cudaMemcpyAsync(&tot[i], offw + i * n1 + nw, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemsetAsync(ctr, 0, 8, s));
+    CU(cudaStreamSynchronize(s));
+    const uint64_t nunits = tot[0], ns = tot[1], nslots = tot[2];
+    if (ns >= 0xffffffffull) { *fallback = true; return HR_OK; }
+    if ((st = reserve(c, 15, (size_t)(nslots + 1) * 8)) || (st = reserve(c, 16, (size_t)(nslots + 1) * 8)) ||
+        (st = reserve(c, 17, (size_t)(ns + 1) * 16)) || (st = reserve(c, 18, (size_t)(ns + 1) * 16)) ||
+        (st = reserve(c, 19, (size_t)(ns + 1) * 8)))
+        return st;
+    uint64_t *cnt = (uint64_t *)c->stage[15], *eoff = (uint64_t *)c->stage[16];
+    uint64_t *plen = (uint64_t *)c->stage[17], *sbase = plen + (ns + 1);
+    uint32_t *swarp = (uint32_t *)c->stage[18], *skey = swarp + (ns + 1), *sid = skey + (ns + 1),
+             *stot = sid + (ns + 1);
+    uint32_t *skey2 = (uint32_t *)c->stage[19], *order = skey2 + (ns + 1);
+    CU(cudaMemsetAsync(cnt + nslots, 0, 8, s));
+    const unsigned ugrid = (unsigned)((nunits * 32 + HR_ST_WALK_WARPS * 32 - 1) / (HR_ST_WALK_WARPS * 32));
+    if (nunits) {
+        c->launches++;
+        hr_st_walk_kernel<false, SRC><<<ugrid, HR_ST_WALK_WARPS * 32, 0, s>>>(
+            d, src, wk, nw, unitoff, slotoff, streamoff, hlog2, (uint32_t)lanes, cnt, nullptr, nullptr, nullptr,
+            nullptr, ctr);
+        CU(cudaGetLastError());
+    }
+    tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, eoff, (int64_t)(nslots + 1), s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches += 2;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, eoff, (int64_t)(nslots + 1), s));
+    c->launches++;
+    hr_st_stream_kernel<<<(unsigned)((ns + 1 + 255) / 256), 256, 0, s>>>(streamoff, unitoff, slotoff, nw, ns, eoff,
+                                                                         plen, swarp, skey, sid, stot);
+    CU(cudaGetLastError());
+    tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, plen, sbase, (int64_t)(ns + 1), s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches += 2;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, plen, sbase, (int64_t)(ns + 1), s));
+    uint64_t entries = 0;
+    unsigned int barrier = 0;
+    CU(cudaMemcpyAsync(&entries, sbase + ns, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&barrier, ctr, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (barrier) { *fallback = true; return HR_OK; }
+    if ((st = reserve(c, 10, (size_t)std::max<uint64_t>(entries, 32) * 8)) ||
+        (st = reserve(c, 11, (size_t)std::max<uint64_t>(entries, 32))))
+        return st;
+    uint64_t *orec = (uint64_t *)c->stage[10];
+    uint8_t *otag = (uint8_t *)c->stage[11];
+    /* longest stream first */
+    tmp = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp, skey, skey2, sid, order, (int)ns, 0, 32, s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches += 2 + 4;
+    CU(cub::DeviceRadixSort::SortPairs(c->stage[5], tmp, skey, skey2, sid, order, (int)ns, 0, 32, s));
+    if (nunits) {
+        c->launches++;
+        hr_st_walk_kernel<true, SRC><<<ugrid, HR_ST_WALK_WARPS * 32, 0, s>>>(
+            d, src, wk, nw, unitoff, slotoff, streamoff, hlog2, (uint32_t)lanes, nullptr, eoff, sbase, orec, otag,
+            ctr);
+        CU(cudaGetLastError());
+    }
+    c->launches++;
+    hr_st_pad_kernel<<<(unsigned)((ns * 32 + 255) / 256), 256, 0, s>>>(sbase, stot, ns, orec, otag);
+    CU(cudaGetLastError());
+    const size_t smem = hr_streams_smem();
+    void (*kern)(hr_dev, hr_src_cmp, const uint64_t *, const uint32_t *, const uint32_t *, uint32_t, uint32_t,
+                 unsigned int *) = abl ? hr_replay_streams_kernel<true> : hr_replay_streams_kernel<false>;
+    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->launches++;
+    kern<<<(unsigned)(dev_sms * 2), HR_ST_WARPS * 32, smem, s>>>(d, hr_src_cmp{orec, otag}, sbase, order, swarp,
+                                                                (uint32_t)ns, (uint32_t)warps, ctr + 1);
+    CU(cudaGetLastError());
+    note_kernel(c, kid);
+    return HR_OK;
+}
+
 /* One launch over simulated blocks [b0, b1) of kernel k (the whole kernel in
  * one launch for device traces; block-range chunks for host traces — blocks
  * are unordered by happens-before, so chunked launches replay the same kernel). */
@@ -629,7 +749,11 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
-        hr_status st = launch_compact(c, t, k, src, woff, s, b0, b1, split, abl);
+        bool fallback = true;
+        hr_status st = HR_OK;
+        if (smem_words == 0 && !(c->cfg.options & HR_OPT_NO_STREAMS))
+            st = launch_streams(c, t, k, src, woff, s, b0, b1, abl, &fallback);
+        if (!st && fallback) st = launch_compact(c, t, k, src, woff, s, b0, b1, split, abl);
         if (st) return st;
         if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
         return HR_OK;
@@ -684,6 +808,7 @@ static bool trace_ok(const hr_trace *t)
     if (t->format == HR_TRACE_U64) return t->rec != nullptr;
     if (t->format == HR_TRACE_C32) return t->rec32 && t->recop;
     if (t->format == HR_TRACE_PACKED) return t->packed && t->pack_off;
+    if (t->format == HR_TRACE_POOLED) return t->rec && t->recop;
     return false;
 }
 
@@ -700,12 +825,139 @@ static hr_status dispatch(hr_ctx *c, const hr_trace *t, const uint64_t *rec, con
 
 static hr_status replay_packed(hr_ctx *c, const hr_trace *t, bool host);
 
+/* HR_TRACE_POOLED (include/hr.h): every kernel through the compacted replay
+ * kernel, one stream per simulated warp (rows = the warp's pools). */
+static hr_status replay_pooled(hr_ctx *c, const hr_trace *t)
+{
+    const hr_src_cmp src{t->rec, (const uint8_t *)t->recop};
+    if (!src.aligned_ok()) return fail(c, HR_E_ARG, "pooled trace records must be 16-byte aligned (TMA staging)");
+    const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE | HR_OPT_SMEM32);
+    c->last_kind = HR_K_POOL;
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        hr_status st = check_kernel(c, t, k);
+        if (st) return st;
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        const uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
+        if (!blocks) continue;
+        if ((st = hr_kernel_begin(c, c->stream))) return st;
+        const uint32_t kid = t->kernel_base + k;
+        hr_dev d = make_dev(c, kid);
+        const uint32_t nhw = (uint32_t)warps;
+        const uint32_t stage_off = hr_stage_offset(false, nhw, smem_u64(c, smem_words));
+        const size_t smem = (size_t)stage_off + hr_stage_bytes(nhw, 2u, 8u, hr_src_cmp::ROW_BYTES);
+        if (smem > 227 * 1024) return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block", k, smem);
+        void (*kern)(hr_dev, hr_src_cmp, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t,
+                     uint32_t) = abl ? hr_replay_compact_kernel<true> : hr_replay_compact_kernel<false>;
+        if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const bool timing = c->cfg.options & HR_OPT_TIMING;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, c->stream)); }
+        c->launches++;
+        kern<<<(unsigned)blocks, nhw * 32u, smem, c->stream>>>(d, src, nullptr, t->warp_off + woi, (uint32_t)warps,
+                                                                (uint32_t)lanes, (uint32_t)smem_words, stage_off, 0u);
+        CU(cudaGetLastError());
+        if (timing) { CU(cudaEventRecord(e1, c->stream)); c->ev_kernel.push_back({e0, e1}); }
+        note_kernel(c, kid);
+    }
+    return HR_OK;
+}
+
+__global__ void hr_pool_woff_kernel(const uint64_t *__restrict__ segoff, const uint64_t *__restrict__ rowoff,
+                                    uint64_t nw, uint64_t base, uint64_t *__restrict__ out)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= nw) out[i] = base + rowoff[segoff[i]];
+}
+
+template <typename SRC>
+static hr_status pool_trace(hr_ctx *c, const hr_trace *t, SRC src, uint64_t *rec_out, uint8_t *tag_out,
+                            uint64_t cap_rows, uint64_t *woff_out, uint64_t *rows, cudaStream_t s)
+{
+    uint64_t base = 0;
+    hr_status st;
+    for (uint32_t k = 0; k < t->n_kernels; k++) {
+        const uint64_t *kd = t->kdesc + 8ull * k;
+        const uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], woi = kd[4];
+        if (!blocks) continue;
+        if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32 ||
+            woi + blocks * warps + 1 > t->n_warp_off)
+            return fail(c, HR_E_ARG, "hr_pool_trace: kernel %u: bad grid or warp_off range", k);
+        hr_dev d = make_dev(c, t->kernel_base + k);
+        const uint64_t nw = blocks * warps;
+        const uint64_t *wk = t->warp_off + woi;
+        if ((st = reserve(c, 6, (nw + 1) * 8)) || (st = reserve(c, 7, (nw + 1) * 8))) return st;
+        uint64_t *nseg = (uint64_t *)c->stage[6], *segoff = (uint64_t *)c->stage[7];
+        c->launches++;
+        hr_cmp_nseg_kernel<<<(unsigned)((nw + 1 + 255) / 256), 256, 0, s>>>(wk, nw, nseg);
+        CU(cudaGetLastError());
+        size_t tmp = 0;
+        CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg, segoff, (int64_t)(nw + 1), s));
+        if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+        c->launches += 2;
+        CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, nseg, segoff, (int64_t)(nw + 1), s));
+        uint64_t nsegs = 0;
+        CU(cudaMemcpyAsync(&nsegs, segoff + nw, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if ((st = reserve(c, 8, (nsegs + 1) * 8)) || (st = reserve(c, 9, (nsegs + 1) * 8))) return st;
+        uint64_t *cnt = (uint64_t *)c->stage[8], *rowoff = (uint64_t *)c->stage[9];
+        CU(cudaMemsetAsync(cnt + nsegs, 0, 8, s));
+        const unsigned wgrid = (unsigned)((nsegs * 32 + 255) / 256);
+        if (nsegs) {
+            c->launches++;
+            hr_cmp_walk_kernel<false, SRC><<<wgrid, 256, 0, s>>>(d, src, wk, segoff, nw, (uint32_t)lanes, 0u, cnt,
+                                                                 nullptr, nullptr);
+            CU(cudaGetLastError());
+        }
+        tmp = 0;
+        CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, rowoff, (int64_t)(nsegs + 1), s));
+        if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+        c->launches += 2;
+        CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, rowoff, (int64_t)(nsegs + 1), s));
+        uint64_t nrows = 0;
+        CU(cudaMemcpyAsync(&nrows, rowoff + nsegs, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (rec_out) {
+            if (base + nrows > cap_rows) return fail(c, HR_E_ARG, "hr_pool_trace: %llu rows > cap %llu",
+                                                     (unsigned long long)(base + nrows), (unsigned long long)cap_rows);
+            if (nsegs) {
+                c->launches++;
+                hr_cmp_walk_kernel<true, SRC><<<wgrid, 256, 0, s>>>(d, src, wk, segoff, nw, (uint32_t)lanes, 0u, rowoff,
+                                                                    rec_out + base * 32, tag_out + base * 32);
+                CU(cudaGetLastError());
+            }
+            c->launches++;
+            hr_pool_woff_kernel<<<(unsigned)((nw + 1 + 255) / 256), 256, 0, s>>>(segoff, rowoff, nw, base,
+                                                                                 woff_out + woi);
+            CU(cudaGetLastError());
+            CU(cudaStreamSynchronize(s));
+        }
+        base += nrows;
+    }
+    *rows = base;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_pool_trace(hr_ctx *c, const hr_trace *in, uint64_t *rec_out, uint8_t *tag_out,
+                                   uint64_t cap_rows, uint64_t *warp_off_out, uint64_t *rows, void *stream)
+{
+    if (!c || !in || !rows || !trace_ok(in) || (in->format != HR_TRACE_U64 && in->format != HR_TRACE_C32) ||
+        (rec_out && (!tag_out || !warp_off_out)))
+        return fail(c, HR_E_ARG, "hr_pool_trace: bad arguments (U64 or C32 device trace required)");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    c->stream = s;
+    if (in->format == HR_TRACE_C32)
+        return pool_trace(c, in, hr_src_c32{in->rec32, in->recop}, rec_out, tag_out, cap_rows, warp_off_out, rows, s);
+    return pool_trace(c, in, hr_src_u64{in->rec}, rec_out, tag_out, cap_rows, warp_off_out, rows, s);
+}
+
 extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
 {
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
     if (t->format == HR_TRACE_PACKED) return replay_packed(c, t, false);
+    if (t->format == HR_TRACE_POOLED) return replay_pooled(c, t);
     return dispatch(c, t, t->rec, t->rec32, t->recop, t->warp_off);
 }
 
@@ -947,6 +1199,7 @@ extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *st
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
     if (t->format == HR_TRACE_PACKED) return replay_packed(c, t, true);
+    if (t->format == HR_TRACE_POOLED) return fail(c, HR_E_ARG, "hr_replay_trace_host: POOLED traces are device only");
     const bool c32 = t->format == HR_TRACE_C32;
     hr_status st;
     if ((st = reserve(c, 0, (size_t)t->n_warp_off * 8))) return st;
@@ -1472,7 +1725,8 @@ extern "C" hr_status hr_race_classes(hr_ctx *c, const hr_trace *t, const hr_race
                                      uint8_t *classes_out, void *stream)
 {
     if (!c || !trace_ok(t) || (n && (!races || !classes_out))) return fail(c, HR_E_ARG, "hr_race_classes: bad arguments");
-    if (t->format == HR_TRACE_PACKED) return fail(c, HR_E_ARG, "hr_race_classes: U64 or C32 traces only");
+    if (t->format == HR_TRACE_PACKED || t->format == HR_TRACE_POOLED)
+        return fail(c, HR_E_ARG, "hr_race_classes: U64 or C32 traces only");
     CU(cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     if (n == 0) return HR_OK;
@@ -1610,7 +1864,7 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->tail) cudaFree(c->tail);
     if (c->counters) cudaFree(c->counters);
     if (c->fsm) cudaFree(c->fsm);
-    for (int i = 0; i < 12; i++)
+    for (int i = 0; i < 24; i++)
         if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->rep_host) cudaFreeHost(c->rep_host);
     if (c->arep_host) cudaFreeHost(c->arep_host);

@@ -36,8 +36,9 @@ HR_OPT_SMEM32 = 4096
 HR_OPT_LAZY_RESET = 8192
 HR_OPT_BSERIAL = 16384
 HR_OPT_ROW_NARROW = 65536
+HR_OPT_NO_STREAMS = 131072
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
-           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_report", "hr_report_async",
+           "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_pool_trace", "hr_report", "hr_report_async",
            "hr_report_async_to",
            "hr_report_collect", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
            "hr_replay_timing", "hr_launch_count",
@@ -57,7 +58,7 @@ class HrRace(ctypes.Structure):
                 ("first_kind", ctypes.c_uint8), ("prev_state", ctypes.c_uint8)]
 
 
-HR_TRACE_U64, HR_TRACE_C32, HR_TRACE_PACKED = 0, 1, 2
+HR_TRACE_U64, HR_TRACE_C32, HR_TRACE_PACKED, HR_TRACE_POOLED = 0, 1, 2, 3
 
 
 class HrTrace(ctypes.Structure):
@@ -98,6 +99,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_replay_trace_host": ([vp, P(HrTrace), vp], ctypes.c_int),
         "hr_pack_trace": ([vp, P(HrTrace), vp, ctypes.c_uint64, vp, P(ctypes.c_uint64), vp], ctypes.c_int),
         "hr_unpack_trace": ([vp, P(HrTrace), vp, vp], ctypes.c_int),
+        "hr_pool_trace": ([vp, P(HrTrace), vp, vp, ctypes.c_uint64, vp, P(ctypes.c_uint64), vp], ctypes.c_int),
         "hr_report": ([vp, P(HrRace), ctypes.c_size_t, P(ctypes.c_size_t), P(ctypes.c_uint32)], ctypes.c_int),
         "hr_merge_races": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, P(ctypes.c_size_t)], ctypes.c_int),
         "hr_report_async": ([vp, vp], ctypes.c_int),
@@ -180,6 +182,17 @@ def hr_pack_trace(ctx, t: HrTrace, out: int, cap: int, pack_off: int, stream: in
     n = ctypes.c_uint64()
     _check(load().hr_pack_trace(ctx, ctypes.byref(t), ctypes.c_void_p(out or None), cap, ctypes.c_void_p(pack_off),
                                 ctypes.byref(n), ctypes.c_void_p(stream)), ctx, "hr_pack_trace")
+    return int(n.value)
+
+
+def hr_pool_trace(ctx, t: HrTrace, rec_out: int, tag_out: int, cap_rows: int, woff_out: int,
+                  stream: int = 0) -> int:
+    """Re-lay a device U64/C32 trace as HR_TRACE_POOLED; rec_out == 0 is the
+    size query.  Returns the pooled row count."""
+    n = ctypes.c_uint64()
+    _check(load().hr_pool_trace(ctx, ctypes.byref(t), ctypes.c_void_p(rec_out or None), ctypes.c_void_p(tag_out or None),
+                                cap_rows, ctypes.c_void_p(woff_out or None), ctypes.byref(n), ctypes.c_void_p(stream)),
+           ctx, "hr_pool_trace")
     return int(n.value)
 
 
@@ -329,12 +342,15 @@ class DeviceTrace:
     ``packed`` uint8 and ``pack_off`` int64 (made by ``Checker.pack``)."""
 
     def __init__(self, rec, warp_off, kdesc: np.ndarray, rec32=None, recop=None, packed=None, pack_off=None,
-                 n_rows: Optional[int] = None):
+                 n_rows: Optional[int] = None, pooled: bool = False):
         self.rec, self.rec32, self.recop = rec, rec32, recop
         self.packed, self.pack_off = packed, pack_off
         self.warp_off = warp_off
         self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
-        if packed is not None:
+        if pooled:                              # rec: pooled entries, recop: their simulated lanes
+            self.format = HR_TRACE_POOLED
+            self.n_rows = rec.numel() // 32
+        elif packed is not None:
             self.format = HR_TRACE_PACKED
             self.n_rows = int(n_rows)
         else:
@@ -356,6 +372,8 @@ class DeviceTrace:
     def record_bytes(self) -> int:
         if self.format == HR_TRACE_PACKED:
             return int(self.packed.numel())
+        if self.format == HR_TRACE_POOLED:
+            return self.n_rows * 288
         return self.n_rows * (160 if self.format == HR_TRACE_C32 else 256)
 
     def to_host(self) -> "HostTrace":
@@ -385,6 +403,8 @@ class DeviceTrace:
         t.format = self.format
         if self.format == HR_TRACE_C32:
             t.rec32, t.recop = self.rec32.data_ptr(), self.recop.data_ptr()
+        elif self.format == HR_TRACE_POOLED:
+            t.rec, t.recop = self.rec.data_ptr(), self.recop.data_ptr()
         elif self.format == HR_TRACE_PACKED:
             t.packed, t.pack_off = self.packed.data_ptr(), self.pack_off.data_ptr()
         else:
@@ -479,6 +499,21 @@ class Checker:
         hr_pack_trace(self.ctx, t, out.data_ptr(), n, pack_off.data_ptr(), stream)
         return DeviceTrace(None, dtrace.warp_off, dtrace.kdesc, packed=out, pack_off=pack_off, n_rows=dtrace.n_rows)
 
+    def pool(self, dtrace: DeviceTrace, stream: Optional[int] = None) -> DeviceTrace:
+        """HR_TRACE_POOLED copy of a device U64 / C32 trace (hr_pool_trace): this
+        ctx's shard only, accesses packed 32 per row per warp epoch."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        dev = dtrace.warp_off.device
+        t = dtrace.c()
+        n = hr_pool_trace(self.ctx, t, 0, 0, 0, 0, stream)
+        rec = torch.empty(max(n, 1) * 32, dtype=torch.int64, device=dev)
+        tag = torch.empty(max(n, 1) * 32, dtype=torch.uint8, device=dev)
+        woff = torch.zeros_like(dtrace.warp_off)
+        hr_pool_trace(self.ctx, t, rec.data_ptr(), tag.data_ptr(), max(n, 1), woff.data_ptr(), stream)
+        return DeviceTrace(rec[: n * 32], woff, dtrace.kdesc, recop=tag[: n * 32], pooled=True)
+
     def report(self):
         return hr_report(self.ctx)
 
@@ -513,9 +548,11 @@ class Checker:
             pass
 
 
-def check_trace(trace, device: int = 0, compact: bool = False, packed: bool = False, **kw) -> Tuple[List[Race], int]:
+def check_trace(trace, device: int = 0, compact: bool = False, packed: bool = False, pooled: bool = False,
+                **kw) -> Tuple[List[Race], int]:
     """Replay a host trace on the GPU and return (sorted racy set, flags).
-    packed=True replays the hr_pack_trace encoding of it instead."""
+    packed=True replays the hr_pack_trace encoding of it instead, pooled=True
+    the hr_pool_trace layout."""
     gmax, smem = trace_extent(trace)
     reps = kw.pop("representatives", None)
     ck = Checker(gmax, smem, device=device, **kw)
@@ -524,6 +561,8 @@ def check_trace(trace, device: int = 0, compact: bool = False, packed: bool = Fa
     dt = DeviceTrace.from_trace(trace, device=f"cuda:{device}", compact=compact and not packed)
     if packed:
         dt = ck.pack(dt)
+    if pooled:
+        dt = ck.pool(dt)
     ck.replay(dt)
     races, flags, _ = ck.report()
     ck.close()

@@ -9,14 +9,17 @@ ap.add_argument("config", choices=["c3", "c4"])
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--lv", type=int, default=20, help="C4 graph: 2^lv vertices")
 ap.add_argument("--atomic", action="store_true", help="C4 race-free (atomic) variant")
+ap.add_argument("--u64", action="store_true", help="U64 records (default: C32, as bench.py)")
+ap.add_argument("--racefree", action="store_true", help="C3 race-free variant")
+ap.add_argument("--options", type=int, default=0)
 a = ap.parse_args()
 if a.config == "c3":
-    tr, words, smem = stencil.stencil_trace(removed=20), 2 * 512 * 512, 648
+    tr, words, smem = stencil.stencil_trace(removed=None if a.racefree else 20), 2 * 512 * 512, 648
 else:
     g = c4.Graph(a.lv)
     tr, words, smem = g.trace(not a.atomic), c4.total_words(a.lv), 0
-dt = hr.DeviceTrace.from_trace(tr)
-ck = hr.Checker(words, smem, ring_capacity=1 << 22, options=hr.HR_OPT_TIMING)
+dt = hr.DeviceTrace.from_trace(tr, compact=not a.u64)
+ck = hr.Checker(words, smem, ring_capacity=1 << 24, options=hr.HR_OPT_TIMING | a.options)
 for _ in range(a.reps):
     ck.reset(); ck.replay(dt); raw, fl = ck.report_raw()
 print("races", len(raw), "flags", fl, hr.hr_replay_timing(ck.ctx))
