@@ -55,6 +55,12 @@ hr_status hrb_c4_level(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int ra
 hr_status hrb_c4_hist(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int racy, uint32_t n,
                       const uint64_t *rp, int *data, void *stream);
 
+/* Sub-warp __syncwarp(mask) online (hr_syncwarp_mask): 1 block x
+ * 32 threads; lane l writes data[l]; lanes 0..15 call __syncwarp(0x0000ffff);
+ * lane l reads data[(l & 16) | ((l + 1) & 15)] and writes data[32 + l]
+ * (unmonitored).  Monitored words [0, 32). */
+hr_status hrb_masked_sync(hr_ctx *ctx, uint32_t kernel_id, int *data, void *stream);
+
 /* Uninstrumented replay of a device trace (hr.h's hr_trace): the same grid,
  * record walk and barriers as hr_replay_trace, but each global record performs
  * only the raw 4-byte data access (read / write / atomicAdd on data[word] for

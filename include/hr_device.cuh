@@ -59,9 +59,9 @@ struct hr_dev {
     uint64_t gwords;              /* monitored global words (whole region, all shards) */
     hr_race *ring;
     unsigned int *ring_tail;
-    unsigned int *flags;
+    unsigned int *flags;          /* = ring_tail + 1 */
     hr_race *spill;               /* a9 overflow store (right after the ring: ring + ring_cap) */
-    unsigned int *ovf;            /* [0] spill tail [1] shared drops not yet spilled [2] global drop:
+    unsigned int *ovf;            /* = ring_tail + 2: [0] spill tail [1] shared drops not yet spilled [2] global drop:
                                      kernel id + 1 of a kernel whose global race record the full ring
                                      dropped (0 = none) [3] spill-scan completion counter */
     uint32_t spill_cap;
@@ -186,13 +186,21 @@ __device__ __forceinline__ uint32_t hr__laneid()
     return l;
 }
 
-/* A control row is divergent unless every active lane holds the same control
- * record (replay: the trace format's warp-aligned barriers, tracegen/format.py). */
-__device__ __forceinline__ bool hr__ctrl_divergent(uint64_t x, unsigned ctrl, unsigned lane_mask)
+/* Control rows (replay: the trace format's warp-aligned barriers,
+ * tracegen/format.py): do the lanes holding a control record disagree on it? */
+__device__ __forceinline__ bool hr__ctrl_mixed(uint64_t x, unsigned ctrl)
 {
     const bool is_ctrl = (x >> 62) == 3u && (x & HR_WORD_MASK) != 0u;
     const unsigned same = __match_any_sync(0xffffffffu, is_ctrl ? x : 0ull);
-    return ctrl != lane_mask || __any_sync(0xffffffffu, is_ctrl && same != ctrl);
+    return __any_sync(0xffffffffu, is_ctrl && same != ctrl);
+}
+
+/* Divergent control row, except a sub-warp __syncwarp (every control lane holds
+ * the same __syncwarp record, but not every active lane): that one is
+ * __syncwarp(mask), see hr__barrier_row. */
+__device__ __forceinline__ bool hr__ctrl_divergent(uint64_t x, unsigned ctrl, unsigned lane_mask)
+{
+    return ctrl != lane_mask || hr__ctrl_mixed(x, ctrl);
 }
 
 /* ---------------- labels ---------------- */
@@ -470,12 +478,15 @@ __device__ __forceinline__ unsigned long long hr__first(const hr_dev &d, const h
  *     hr_thread_end spills every RACE word of the block's instance and lowers
  *     ovf[1] again.  ovf[1] != 0 at report time = a block that never spilled.
  * The finite-history baseline has no FSM shadow to scan: its drops are lost. */
-/* (scalar arguments: a rare path kept out of line without copying hr_dev to the stack) */
-static __device__ __noinline__ void hr__ring_drop_x(unsigned int *flags, unsigned int *ovf, uint32_t options,
-                                                   uint32_t kernel_id, uint32_t drop_sa, uint32_t space)
+/* (scalar arguments: a rare path kept out of line without copying hr_dev to the
+ * stack; flags and ovf are found from the ring tail: make_dev lays them out as
+ * tail[1] and tail[2..5], so the hot loop keeps no extra constants live) */
+static __device__ __noinline__ void hr__ring_drop_x(unsigned int *tail, bool fh, uint32_t kernel_id, uint32_t drop_sa,
+                                                   uint32_t space)
 {
+    unsigned int *flags = tail + 1, *ovf = tail + 2;
     if ((*(volatile unsigned int *)flags & HR_F_RING_OVERFLOW) == 0u) atomicOr(flags, HR_F_RING_OVERFLOW);
-    if (options & HR_OPT_FINITE_HISTORY) {
+    if (fh) {
         atomicAdd(&ovf[1], 1u);
     } else if (space) {
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(drop_sa) : "memory");
@@ -485,9 +496,10 @@ static __device__ __noinline__ void hr__ring_drop_x(unsigned int *flags, unsigne
     }
 }
 
+template <bool FH = false>
 __device__ __forceinline__ void hr__ring_drop(const hr_dev &d, uint32_t drop_sa, uint32_t space)
 {
-    hr__ring_drop_x(d.flags, d.ovf, d.options, d.kernel_id, drop_sa, space);
+    hr__ring_drop_x(d.ring_tail, FH, d.kernel_id, drop_sa, space);
 }
 
 /* Append one record to the spill (warp-aggregated over the lanes of `mask`
@@ -552,6 +564,7 @@ __device__ __forceinline__ void hr__spill_instance(const hr_dev &d, uint32_t sa,
     hr__spill_instance_x(d.spill, d.ovf, d.spill_cap, d.flags, d.options, d.kernel_id, sa, words, block, ltid, nthr);
 }
 
+template <bool FH = false>
 __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t, uint32_t slot, uint32_t space,
                                                uint64_t word, uint32_t ei)
 {
@@ -567,7 +580,7 @@ __device__ __forceinline__ void hr__write_race(const hr_dev &d, const hr_thr &t,
         rr.prev_state = (uint8_t)((ei >> 19) & 31u);
         d.ring[slot] = rr;
     } else {
-        hr__ring_drop(d, t.fsm + HR_FSM_DROP_OFF, space);
+        hr__ring_drop<FH>(d, t.fsm + HR_FSM_DROP_OFF, space);
     }
 }
 
@@ -680,8 +693,8 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
         const uint32_t os = ohi >> (HR_STATE_SHIFT - 32);
         const uint32_t x = (tid_lo ^ ohi) & 1023u;
         const uint32_t rel = (x != 0u) + (x >= 32u);
-        const uint32_t sync = (bc > (olo >> d.wc_bits)) ? 2u
-                              : ((rel <= 1u && wc > (olo & ((1u << d.wc_bits) - 1u))) ? 1u : 0u);
+        const uint32_t ws = (rel <= 1u) & (wc > (olo & ((1u << d.wc_bits) - 1u)));
+        const uint32_t sync = (bc > (olo >> d.wc_bits)) ? 2u : ws;
         const uint32_t cur = hr__lds_u8(kcol + ((os << 6) | (sync << 2) | rel));
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
         if (nw == old || (cur == os && os == HR_RACE_BLOCK)) break;      /* a7 (i), (iii) */
@@ -789,12 +802,28 @@ __device__ __forceinline__ void hr_syncthreads(const hr_dev &d, hr_thr &t)
     else t.meta += 1ull << d.wc_bits;
 }
 
-/* __syncwarp(); ++wc (full warp only; sub-warp masks are future work). */
+/* __syncwarp(mask) for a sub-warp mask ("takes a mask argument";
+ * PAPER.md:1054 lists sub-warp support as future work).  A thread's scalar warp
+ * clock cannot say that only some lanes synchronised, so (reading R8 in
+ * DESIGN.md, the same rule as the replay and the oracle) the call synchronises
+ * the lanes for real but adds NO happens-before edge: no clock moves and
+ * HR_F_MODEL_VIOLATION is latched.  Races the masked barrier would order are
+ * therefore still reported (sound, not precise).  A full mask is hr_syncwarp. */
+__device__ __forceinline__ void hr_syncwarp_mask(const hr_dev &d, hr_thr &t, unsigned mask);
+
+/* __syncwarp(); ++wc (full warp; see hr_syncwarp_mask for sub-warp masks). */
 __device__ __forceinline__ void hr_syncwarp(const hr_dev &d, hr_thr &t)
 {
     __syncwarp();
     if (((uint32_t)t.meta & d.wc_max) >= d.wc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
     else t.meta += 1ull;
+}
+
+__device__ __forceinline__ void hr_syncwarp_mask(const hr_dev &d, hr_thr &t, unsigned mask)
+{
+    if (mask == 0xffffffffu) { hr_syncwarp(d, t); return; }
+    __syncwarp(mask);
+    if (hr__laneid() == (uint32_t)(__ffs(mask) - 1)) hr__set_flag(d, HR_F_MODEL_VIOLATION);
 }
 
 #endif /* HR_DEVICE_CUH_ */

@@ -130,13 +130,21 @@ static int materialize(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_ke
                             nbar++;
                         }
                     }
-                    if (nbar != 0 && (nbar != (int)lanes || !same)) *flags |= HRO_F_BARRIER_DIVERGENCE;
+                    /* a __syncwarp that only some active lanes hold is __syncwarp(mask) with a
+                     * sub-warp mask ("takes a mask argument"): reading R8 —
+                     * model violation, and conservatively NO happens-before edge (no clock
+                     * moves), so every race the masked barrier would hide is still reported */
+                    const int partial_ws = nbar != 0 && nbar != (int)lanes && same &&
+                                           (first_bar & ((1ull << 61) - 1)) == 2;
+                    if (partial_ws) *flags |= HRO_F_MODEL_VIOLATION;
+                    else if (nbar != 0 && (nbar != (int)lanes || !same)) *flags |= HRO_F_BARRIER_DIVERGENCE;
                     for (uint64_t l = 0; l < lanes; l++) {
                         uint64_t x = row[l];
                         uint32_t op = (uint32_t)(x >> 62);
                         uint32_t space = (uint32_t)((x >> 61) & 1);
                         uint64_t word = x & ((1ull << 61) - 1);
                         if (op == 3) {
+                            if (partial_ws) continue;   /* sub-warp __syncwarp: no edge (above) */
                             if (word == 1) {            /* __syncthreads: bc + 1 */
                                 if (bc[l] + 1 > bc_max) { dead[l] = 1; *flags |= HRO_F_CLOCK_OVERFLOW; }
                                 else bc[l]++;

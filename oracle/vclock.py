@@ -11,7 +11,10 @@ one event of one runnable thread executes.  A thread reaching
 ``__syncthreads`` (``__syncwarp``) blocks until every thread of its block
 (warp) has reached it; then all are released together and their vector
 clocks are joined (the barrier's happens-before edges).
-Accesses do not synchronise (atomics included, reading R1).
+Accesses do not synchronise (atomics included, reading R1).  A ``__syncwarp``
+record held by only some lanes of a warp row is ``__syncwarp(mask)`` (PAPER.md:264
+"takes a mask argument"): here it synchronises exactly those lanes — the
+precise semantics the conservative oracle reading R8 over-approximates.
 
 Decodes the trace records itself (shares no code with the CUDA path).
 """
@@ -23,7 +26,7 @@ from typing import Dict, Iterator, List, Optional, Set, Tuple
 import numpy as np
 
 Thread = Tuple[int, int, int]          # (block, warp, lane)
-Event = Tuple                          # ("acc", space, word, kind) | ("S",) | ("WS",)
+Event = Tuple                          # ("acc", space, word, kind) | ("S",) | ("WS",) | ("WS", lanes)
 
 
 def thread_events(trace) -> List[Dict[Thread, List[Event]]]:
@@ -37,6 +40,13 @@ def thread_events(trace) -> List[Dict[Thread, List[Event]]]:
             for w in range(warps):
                 gw = b * warps + w
                 r0, r1 = int(trace.warp_off[woi + gw]), int(trace.warp_off[woi + gw + 1])
+                # per row: the lanes holding a __syncwarp record (the barrier's mask)
+                ws_mask = {}
+                for r in range(r0, r1):
+                    m = frozenset(l for l in range(lanes)
+                                  if int(rec[r * 32 + l]) & ~(1 << 61) == (3 << 62) | 2)
+                    if m and len(m) < lanes:
+                        ws_mask[r] = m
                 for l in range(lanes):
                     ev: List[Event] = []
                     for r in range(r0, r1):
@@ -46,7 +56,7 @@ def thread_events(trace) -> List[Dict[Thread, List[Event]]]:
                             if word == 1:
                                 ev.append(("S",))
                             elif word == 2:
-                                ev.append(("WS",))
+                                ev.append(("WS", ws_mask[r]) if r in ws_mask else ("WS",))
                         else:
                             ev.append(("acc", space, word, op))
                     th[(b, w, l)] = ev
@@ -66,10 +76,12 @@ class _Run:
     def runnable(self) -> List[Thread]:
         return [t for t in self.ids if t not in self.waiting and self.pc[t] < len(self.th[t])]
 
-    def members(self, t: Thread, kind: str) -> List[Thread]:
+    def members(self, t: Thread, e: Event) -> List[Thread]:
         b, w, _ = t
-        if kind == "S":
+        if e[0] == "S":
             return [u for u in self.ids if u[0] == b]
+        if len(e) > 1:                                  # __syncwarp(mask): the masked lanes
+            return [u for u in self.ids if u[0] == b and u[1] == w and u[2] in e[1]]
         return [u for u in self.ids if u[0] == b and u[1] == w]
 
     def exec(self, t: Thread):
@@ -77,7 +89,7 @@ class _Run:
         e = self.th[t][self.pc[t]]
         if e[0] in ("S", "WS"):
             self.waiting[t] = e
-            grp = self.members(t, e[0])
+            grp = self.members(t, e)
             if all(self.waiting.get(u) == e for u in grp):
                 for u in grp:
                     del self.waiting[u]

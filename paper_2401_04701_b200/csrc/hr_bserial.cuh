@@ -226,9 +226,15 @@ __global__ void __launch_bounds__(HR_BS_WARPS * 32, 64 / HR_BS_WARPS) hr_replay_
                 if (ctrl) {
                     /* as hr__barrier_row: divergence and mixed barrier kinds are flagged */
                     const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
-                    if (hr__ctrl_divergent(x, ctrl, lane_mask) && lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
                     const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
-                    if ((bst | bsw) != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+                    const bool mixed = hr__ctrl_mixed(x, ctrl);
+                    const bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
+                    if (lane == 0) {
+                        if (partial_ws) hr__set_flag(d, HR_F_MODEL_VIOLATION);   /* sub-warp mask: no edge */
+                        else if (ctrl != lane_mask || mixed) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+                        if ((bst | bsw) != ctrl) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+                    }
+                    if (partial_ws) continue;
                     if (bst) break;                              /* this warp's block epoch ends */
                     if (!bsw) continue;                          /* undefined control code: no barrier */
                     /* __syncwarp of simulated warp sw: close the pool, advance its clock */

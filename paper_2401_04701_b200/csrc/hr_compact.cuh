@@ -56,6 +56,8 @@ struct hr_src_cmp {
         hr__bulk_g2s(dst + ch * 256u, tag + row * 32, nrows * 32u, bar);
     }
     __host__ bool aligned_ok() const { return (((uintptr_t)rec | (uintptr_t)tag) & 15u) == 0; }
+    static constexpr bool C32 = false;
+    __device__ __forceinline__ static void sld2(uint32_t, uint32_t, uint32_t, uint32_t, uint32_t &, uint32_t &) {}
 };
 
 /* Walk one (warp, segment) unit: count (WRITE = false) or write the packed rows
@@ -151,8 +153,10 @@ __global__ void __launch_bounds__(256) hr_cmp_walk_kernel(hr_dev d, SRC src, con
 #ifndef HR_CMP_MINB
 #define HR_CMP_MINB 1
 #endif
-template <bool ABL>
-__global__ void __launch_bounds__(1024, HR_CMP_MINB) hr_replay_compact_kernel(hr_dev d, hr_src_cmp src,
+/* NARROW = true: at most 32 registers (64 warps/SM: memory-level parallelism for
+ * random-DRAM-bound pooled shards), else up to 64 */
+template <bool ABL, bool NARROW = false>
+__global__ void __launch_bounds__(1024, NARROW ? 2 : HR_CMP_MINB) hr_replay_compact_kernel(hr_dev d, hr_src_cmp src,
                                                                     const uint64_t *__restrict__ segoff,
                                                                     const uint64_t *__restrict__ rowoff,
                                                                     uint32_t warps, uint32_t lanes,

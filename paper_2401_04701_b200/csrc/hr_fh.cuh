@@ -111,9 +111,15 @@ __global__ void __launch_bounds__(1024, 1) hr_fh_replay_kernel(hr_dev d, SRC src
         const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
         if (ctrl) {
             const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
-            if (hr__ctrl_divergent(x, ctrl, lane_mask) && lane == 0) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
             const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
-            if ((bst | bsw) != ctrl && lane == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+            const bool mixed = hr__ctrl_mixed(x, ctrl);
+            const bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
+            if (lane == 0) {
+                if (partial_ws) hr__set_flag(d, HR_F_MODEL_VIOLATION);           /* sub-warp mask: no edge */
+                else if (ctrl != lane_mask || mixed) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+                if ((bst | bsw) != ctrl) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+            }
+            if (partial_ws) continue;
             if (bst) hr_syncthreads(d, t);
             else if (bsw) hr_syncwarp(d, t);
             continue;
@@ -130,7 +136,7 @@ __global__ void __launch_bounds__(1024, 1) hr_fh_replay_kernel(hr_dev d, SRC src
             if (lane == leader) b = atomicAdd(d.ring_tail, (unsigned)__popc(em));
             b = __shfl_sync(0xffffffffu, b, leader);
             if (scope)
-                hr__write_race(d, t, b + __popc(em & ((1u << lane) - 1u)), space, w,
+                hr__write_race<true>(d, t, b + __popc(em & ((1u << lane) - 1u)), space, w,
                                HR_EI_EMIT | (lane << 26) | (op << 24) | (scope == 2u ? 1u : 0u));
         }
     }

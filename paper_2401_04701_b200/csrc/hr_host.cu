@@ -846,8 +846,11 @@ static hr_status replay_pooled(hr_ctx *c, const hr_trace *t)
         const uint32_t stage_off = hr_stage_offset(false, nhw, smem_u64(c, smem_words));
         const size_t smem = (size_t)stage_off + hr_stage_bytes(nhw, 2u, 8u, hr_src_cmp::ROW_BYTES);
         if (smem > 227 * 1024) return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block", k, smem);
+        /* 32-register variant unless HR_OPT_ROW_WIDE (measured on C5 shards) */
+        const bool narrow = !(c->cfg.options & HR_OPT_ROW_WIDE);
         void (*kern)(hr_dev, hr_src_cmp, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t,
-                     uint32_t) = abl ? hr_replay_compact_kernel<true> : hr_replay_compact_kernel<false>;
+                     uint32_t) = abl ? (narrow ? hr_replay_compact_kernel<true, true> : hr_replay_compact_kernel<true>)
+                                     : (narrow ? hr_replay_compact_kernel<false, true> : hr_replay_compact_kernel<false>);
         if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;

@@ -218,6 +218,24 @@ __global__ void __launch_bounds__(256) c4_hist_kernel(hr_dev d, int *data, uint3
     }
 }
 
+/* ---- sub-warp __syncwarp(mask), online: lane l writes word l,
+ * lanes 0..15 meet a __syncwarp(0x0000ffff) (hr_syncwarp_mask: no happens-before
+ * edge, HR_F_MODEL_VIOLATION), then lane l reads its tile neighbour's word ---- */
+__global__ void __launch_bounds__(32) masked_sync_kernel(hr_dev d, int *data)
+{
+    __shared__ __align__(16) unsigned char fsm[HR_FSM_SMEM_BYTES];
+    __shared__ unsigned long long sh[1];
+    hr_thr t = hr_thread_begin(d, fsm, sh, 0);
+    const uint32_t lane = threadIdx.x;
+    hr_check_write(d, t, HR_GLOBAL, lane);
+    data[lane] = (int)lane;
+    if (lane < 16u) hr_syncwarp_mask(d, t, 0x0000ffffu);
+    const uint32_t r = (lane & 16u) | ((lane + 1u) & 15u);
+    hr_check_read(d, t, HR_GLOBAL, r);
+    data[32 + lane] = data[r];
+    hr_thread_end(d, t);
+}
+
 /* ---- uninstrumented replay: the same record walk and barriers as
  * hr_replay_kernel, but each access is the raw data access (4-byte word) ---- */
 template <typename SRC>
@@ -302,6 +320,15 @@ extern "C" hr_status hrb_raw_replay(const hr_trace *t, int *data, uint64_t data_
         if (cudaGetLastError() != cudaSuccess) return HR_E_CUDA;
     }
     return HR_OK;
+}
+
+extern "C" hr_status hrb_masked_sync(hr_ctx *ctx, uint32_t kernel_id, int *data, void *stream)
+{
+    hr_dev d;
+    hr_status st = prepare(ctx, 1, kernel_id, stream, &d);
+    if (st) return st;
+    masked_sync_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d, data);
+    return launched();
 }
 
 extern "C" hr_status hrb_c1(hr_ctx *ctx, int instrumented, uint32_t kernel_id, int rounds, int removed, int *data,

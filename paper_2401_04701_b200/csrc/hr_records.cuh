@@ -84,6 +84,8 @@ struct hr_src_u64 {
         return v;
     }
     __host__ bool aligned_ok() const { return ((uintptr_t)rec & 15u) == 0; }
+    static constexpr bool C32 = false;
+    __device__ __forceinline__ static void sld2(uint32_t, uint32_t, uint32_t, uint32_t, uint32_t &, uint32_t &) {}
     __device__ __forceinline__ static uint64_t decode(raw_t x) { return x; }
     __device__ __forceinline__ uint64_t row(uint64_t r, uint32_t lane) const { return load(r, lane); }
 };
@@ -126,6 +128,14 @@ struct hr_src_c32 {
         return decode(x);
     }
     __host__ bool aligned_ok() const { return (((uintptr_t)rec32 | (uintptr_t)recop) & 15u) == 0; }
+    /* the staged (word, op byte) pair undecoded (the row kernel's shared-row test) */
+    static constexpr bool C32 = true;
+    __device__ __forceinline__ static void sld2(uint32_t buf, uint32_t j, uint32_t lane, uint32_t ch, uint32_t &w,
+                                                uint32_t &b)
+    {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(buf + (j * 32u + lane) * 4u) : "memory");
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(buf + ch * 128u + j * 32u + lane) : "memory");
+    }
     __device__ __forceinline__ static uint64_t decode(raw_t x)
     {
         return ((uint64_t)(x.b & 3u) << 62) | ((uint64_t)((x.b >> 2) & 1u) << 61) | x.w;

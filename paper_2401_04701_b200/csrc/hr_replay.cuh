@@ -160,8 +160,11 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
 /* A row holding control records (a10).  Uniform rows: __syncthreads advances
  * bc, __syncwarp wc; a control code the trace format does not define (word > 2)
  * is no barrier at all — HR_F_MODEL_VIOLATION, no clock moves (as the oracle,
- * oracle/hr_oracle.c materialize).  A row whose lanes disagree is flagged
- * HR_F_BARRIER_DIVERGENCE (undefined in CUDA; its racy set is unspecified). */
+ * oracle/hr_oracle.c materialize).  A __syncwarp record held by only some of
+ * the warp's lanes is __syncwarp(mask) with a sub-warp mask:
+ * HR_F_MODEL_VIOLATION and, conservatively, no happens-before edge (reading
+ * R8: the races it would order are still reported).  Any other disagreement
+ * is HR_F_BARRIER_DIVERGENCE (undefined in CUDA; racy set unspecified). */
 __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint64_t x, unsigned lane_mask)
 {
     const uint32_t op = (uint32_t)(x >> 62);
@@ -169,9 +172,15 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
     const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
     const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
     const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
-    if (hr__ctrl_divergent(x, ctrl, lane_mask) && (threadIdx.x & 31u) == 0)
-        hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
-    if ((bst | bsw) != ctrl && (threadIdx.x & 31u) == 0) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+    const bool mixed = hr__ctrl_mixed(x, ctrl);
+    const bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
+    const bool div = ctrl != lane_mask || mixed;
+    if ((threadIdx.x & 31u) == 0) {
+        if (partial_ws) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+        else if (div) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+        if ((bst | bsw) != ctrl) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+    }
+    if (partial_ws) return;
     if (bst) hr_syncthreads(d, t);
     else if (bsw) hr_syncwarp(d, t);
 }
@@ -357,6 +366,28 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 for (uint32_t j = 0; j < CH; j++) insert(vs[j], xs[j]);
                 j0 = rows;
             }
+        }
+        if (!POOL && !ABL && SRC::C32) {
+            /* C32 rows read undecoded: barrier test, then the shared-row fast path
+             * (hr__check_shared_row) on the raw (word, op | space << 2) pair */
+            for (uint32_t j = 0; j < rows; j++) {
+                uint32_t w32 = 0u, ob = 3u;
+                if (active) SRC::sld2(buf, j, lane, CH, w32, ob);
+                const bool ctl = (ob & 3u) == 3u;
+                if (__any_sync(0xffffffffu, ctl && w32 != 0u)) {
+                    hr__barrier_row(d, t, ((uint64_t)(ob & 3u) << 62) | ((uint64_t)((ob >> 2) & 1u) << 61) | w32,
+                                    lane_mask);
+                    continue;
+                }
+                const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
+                if (__all_sync(0xffffffffu, !ctl && (ob & 4u) && w32 < t.swords && !(t.off & 3u) &&
+                                                (lane == 0u || w32 > wprev))) {
+                    hr__check_shared_row(d, t, w32, ob & 3u);
+                    continue;
+                }
+                hr_check_lanes<false, ABL>(d, t, 0xffffffffu, !ctl, (ob >> 2) & 1u, w32, ob & 3u);
+            }
+            j0 = rows;
         }
         for (uint32_t j = j0; j < rows; j++) {
             const uint64_t x = active ? SRC::sld(buf, j, lane, CH) : HR_NOP_REC;

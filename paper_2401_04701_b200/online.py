@@ -11,7 +11,7 @@ import numpy as np
 
 from . import hirace
 
-EXPORTS = ("hrb_c1", "hrb_c1_array", "hrb_c3", "hrb_c4_level", "hrb_c4_hist", "hrb_raw_replay")
+EXPORTS = ("hrb_c1", "hrb_c1_array", "hrb_c3", "hrb_c4_level", "hrb_c4_hist", "hrb_raw_replay", "hrb_masked_sync")
 
 
 def _lib():
@@ -24,6 +24,7 @@ def _lib():
         lib.hrb_c4_level.argtypes = [vp, i, u32, i, u32, vp, vp, vp, i, vp, vp]
         lib.hrb_c4_hist.argtypes = [vp, i, u32, i, u32, vp, vp, vp]
         lib.hrb_raw_replay.argtypes = [ctypes.POINTER(hirace.HrTrace), vp, ctypes.c_uint64, vp]
+        lib.hrb_masked_sync.argtypes = [vp, u32, vp, vp]
         for n in EXPORTS:
             getattr(lib, n).restype = ctypes.c_int
         lib._hrb_ready = True
@@ -57,6 +58,11 @@ def c3(ctx, data, instrumented: bool, n: int = 512, sweeps: int = 42, removed: O
        kernel_id: int = 0):
     r = -1 if removed is None else removed
     _ok(_lib().hrb_c3(ctx, int(instrumented), kernel_id, n, sweeps, r, data.data_ptr(), _stream()), ctx, "hrb_c3")
+
+
+def masked_sync(ctx, data, kernel_id: int = 0):
+    """The sub-warp __syncwarp(mask) kernel (include/hr_bench.h hrb_masked_sync)."""
+    _ok(_lib().hrb_masked_sync(ctx, kernel_id, data.data_ptr(), _stream()), ctx, "hrb_masked_sync")
 
 
 def raw_replay(dtrace, data, data_words: int):

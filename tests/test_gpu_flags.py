@@ -113,3 +113,61 @@ def test_mixed_barrier_and_undefined_row_flags():
     assert wfl == h.HR_F_MODEL_VIOLATION | h.HR_F_BARRIER_DIVERGENCE
     for options in KERNELS:
         assert gpu_set(tr, options=options)[1] == wfl
+
+
+# ---- sub-warp __syncwarp(mask) (reading R8: model violation, no happens-before edge) ----
+
+def _masked_rows_trace(seed):
+    """Random single-warp-row programs where some __syncwarp rows are held by
+    a random subset of lanes (a sub-warp mask)."""
+    import random
+    rng = random.Random(seed)
+    nw, nrows = 4, 10
+    rows = np.full((2 * nw, nrows, 32), tf.NOP, dtype=np.uint64)
+    for w in range(2 * nw):
+        for r in range(nrows):
+            if rng.random() < 0.3:
+                lanes = [l for l in range(32) if rng.random() < 0.5] if rng.random() < 0.6 else list(range(32))
+                for l in lanes:
+                    rows[w, r, l] = tf.SYNCWARP
+            else:
+                for l in range(32):
+                    if rng.random() < 0.6:
+                        rows[w, r, l] = rng.choice([tf.R, tf.W, tf.A])(rng.randrange(40), rng.randrange(2))
+    return tf.make_trace([tf.kernel_from_rows(2, nw, 32, rows, smem_words=40)])
+
+
+@pytest.mark.parametrize("options", KERNELS)
+def test_masked_syncwarp_replay_matches_oracle(options):
+    from tests.test_oracle_pins import _masked_syncwarp_trace
+    tr = _masked_syncwarp_trace()
+    want = oracle_set(tr)
+    assert want[1] == hr().HR_F_MODEL_VIOLATION and len(want[0]) == 2
+    assert gpu_set(tr, options=options) == want
+    for seed in range(3):
+        tr = _masked_rows_trace(seed)
+        want = oracle_set(tr)
+        assert want[1] & hr().HR_F_MODEL_VIOLATION
+        assert gpu_set(tr, options=options) == want, seed
+
+
+def test_masked_syncwarp_online():
+    """hr_syncwarp_mask in a real kernel: the racy set equals the oracle's on
+    the same access stream (lanes 0..15 hold the masked __syncwarp row)."""
+    import torch
+    from paper_2401_04701_b200 import online
+    h = hr()
+    rows = np.full((1, 3, 32), tf.NOP, dtype=np.uint64)
+    for l in range(32):
+        rows[0, 0, l] = tf.W(l)
+        rows[0, 2, l] = tf.R((l & 16) | ((l + 1) & 15))
+    rows[0, 1, :16] = tf.SYNCWARP
+    tr = tf.make_trace([tf.kernel_from_rows(1, 1, 32, rows)])
+    want = oracle_set(tr)
+    assert want[1] == h.HR_F_MODEL_VIOLATION and len(want[0]) == 32
+    data = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ck = h.Checker(32, 0)
+    online.masked_sync(ck.ctx, data)
+    races, flags, _ = ck.report()
+    ck.close()
+    assert ([tuple(r) for r in races], flags) == want

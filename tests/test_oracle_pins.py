@@ -289,3 +289,49 @@ def test_undefined_control_code_is_no_barrier():
         # an undefined code orders nothing: the set equals that of the same trace with a NOP there
         rows[0, 1, :] = tf.NOP
         assert [r.word for r in oracle.check(tf.make_trace([tf.kernel_from_rows(1, 1, 2, rows)])).races] == [0]
+
+
+def _masked_syncwarp_trace(barrier=tf.SYNCWARP, lanes_in=(0, 1)):
+    """1 block, 1 warp, 3 active lanes.  The lanes `lanes_in` hold a __syncwarp
+    record on row 2 (lanes (0, 1): a __syncwarp(0b011) in CUDA terms).  Lane 0
+    writes words 1 and 0 before it; after it lane 1 reads word 0 and lane 2
+    reads word 1."""
+    import numpy as np
+    rows = np.full((1, 4, 32), tf.NOP, dtype=np.uint64)
+    rows[0, 0, 0] = tf.W(1)
+    rows[0, 1, 0] = tf.W(0)
+    for l in lanes_in:
+        rows[0, 2, l] = barrier
+    rows[0, 3, 1] = tf.R(0)
+    rows[0, 3, 2] = tf.R(1)
+    return tf.make_trace([tf.kernel_from_rows(1, 1, 3, rows)])
+
+
+def test_masked_syncwarp_conservative_reading():
+    """Reading R8: a __syncwarp that only some lanes hold is
+    __syncwarp(mask) with a sub-warp mask ("takes a mask
+    argument"); a scalar warp clock cannot express it, so the oracle flags a
+    model violation and adds no happens-before edge.  Pins:
+      * exact semantics (vector clocks where the barrier joins exactly the
+        masked lanes, over every interleaving): word 0 is ordered (lanes 0
+        and 1 are both in the mask), word 1 races (lane 2 is not);
+      * the oracle's set is a superset of the exact one (sound), and equals
+        the set of the same trace with the masked barrier removed;
+      * a full-warp __syncwarp in the same place orders both."""
+    tr = _masked_syncwarp_trace()
+    th = vclock.thread_events(tr)[0]
+    exact = set()
+    n = 0
+    for sched in vclock.enumerate_schedules(th):
+        exact |= set(vclock.vclock_races(th, sched))
+        n += 1
+    assert n > 1 and exact == {(0, 0xFFFFFFFF, 1)}
+    for mode in (oracle.PAIRWISE, oracle.BUCKETED):
+        res = oracle.check(tr, mode=mode)
+        assert res.flags == oracle.F_MODEL_VIOLATION
+        got = {(r.space, r.block, r.word) for r in res.races}
+        assert got >= exact and got == {(0, 0xFFFFFFFF, 0), (0, 0xFFFFFFFF, 1)}
+    nop = _masked_syncwarp_trace(barrier=tf.NOP)
+    assert [tuple(r) for r in oracle.check(nop).races] == [tuple(r) for r in oracle.check(tr).races]
+    full = oracle.check(_masked_syncwarp_trace(lanes_in=(0, 1, 2)))
+    assert full.races == [] and full.flags == 0
