@@ -379,11 +379,12 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                                     lane_mask);
                     continue;
                 }
-                const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
-                if (__all_sync(0xffffffffu, !ctl && (ob & 4u) && w32 < t.swords && !(t.off & 3u) &&
-                                                (lane == 0u || w32 > wprev))) {
-                    hr__check_shared_row(d, t, w32, ob & 3u);
-                    continue;
+                if (__all_sync(0xffffffffu, (ob & 7u) >= 4u && (ob & 3u) != 3u)) {     /* all shared accesses */
+                    const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
+                    if (__all_sync(0xffffffffu, w32 < t.swords && !(t.off & 3u) && (lane == 0u || w32 > wprev))) {
+                        hr__check_shared_row(d, t, w32, ob & 3u);
+                        continue;
+                    }
                 }
                 hr_check_lanes<false, ABL>(d, t, 0xffffffffu, !ctl, (ob >> 2) & 1u, w32, ob & 3u);
             }
