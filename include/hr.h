@@ -125,6 +125,12 @@ enum {
     HR_OPT_BSERIAL = 16384u,     /* sparse U64 traces (pooled replay): one CUDA warp replays a whole
                                     simulated block epoch by epoch (hr_bserial.cuh) */
     HR_OPT_ROW_NARROW = 65536u,  /* force the 32-register row kernel (64 warps/SM) */
+    HR_OPT_BINNED = 262144u,     /* address-binned replay (hr_binned.cuh) for kernels without shared
+                                    shadow: accesses regrouped per (shadow bucket of 64 MB, block) in
+                                    happens-before order and checked bucket by bucket so the random
+                                    shadow RMWs hit L2.  Opt-in: exact, but measured slower than the
+                                    row replay on C5 (161 vs 90 ms, DESIGN.md §5 item 17) */
+    HR_OPT_NO_BINNED = 524288u,  /* never use the binned replay (the default) */
     HR_OPT_NO_STREAMS = 131072u, /* long-tailed barrier-free kernels without shared shadow: use the
                                     per-block compacted replay instead of the stream-scheduled one
                                     (hr_streams.cuh: hub warps fanned out over helper streams that

@@ -11,7 +11,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libhirace.so")
 LIB_FUZZ = os.path.join(PKG, "libhirace_fuzz.so")   # -DHR_FUZZ schedule-fuzzing variant (tests only)
 SOURCES = [os.path.join(CSRC, "hr_host.cu"), os.path.join(CSRC, "hr_online.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("hr_replay.cuh", "hr_records.cuh", "hr_fh.cuh", "hr_classes.cuh", "hr_pack.cuh", "hr_compact.cuh", "hr_streams.cuh", "hr_bserial.cuh", "fsm_table.inc",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("hr_replay.cuh", "hr_records.cuh", "hr_fh.cuh", "hr_classes.cuh", "hr_pack.cuh", "hr_compact.cuh", "hr_streams.cuh", "hr_binned.cuh", "hr_bserial.cuh", "fsm_table.inc",
                                             "fsm_classes.inc")] + \
     [os.path.join(INCLUDE, f) for f in ("hr.h", "hr_device.cuh", "hr_bench.h", "hr_array.cuh")]
 

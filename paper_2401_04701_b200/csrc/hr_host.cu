@@ -29,6 +29,7 @@
 #include "hr_compact.cuh"
 #include "hr_bserial.cuh"
 #include "hr_streams.cuh"
+#include "hr_binned.cuh"
 #include "fsm_table.inc"
 #include "fsm_classes.inc"
 
@@ -77,7 +78,8 @@ struct hr_ctx {
      * 9 row offsets, 10 packed records, 11 packed tags,
      * stream-scheduled replay (hr_streams.cuh): 12 per-warp units/streams/slots (3 x nw+1),
      * 13 their scans (3 x nw+1), 14 helper log2, 15 slot counts, 16 slot offsets, 17 stream
-     * lengths / bases, 18 stream warp / key / id / total, 19 sorted keys / order, 20 counters */
+     * lengths / bases, 18 stream warp / key / id / total, 19 sorted keys / order, 20 counters,
+     * binned replay (hr_binned.cuh): 21 entries, 22 per-(bucket, block) counts, 23 their offsets */
     void *stage[24] = {};
     size_t stage_cap[24] = {};
     hr_race *rep_host = nullptr;                 /* pinned staging of the sorted report (D2H) */
@@ -680,6 +682,92 @@ static hr_status launch_streams(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     return HR_OK;
 }
 
+/* Address-binned replay of blocks [b0, b1) of kernel k (hr_binned.cuh): count
+ * walk, scan, write walk, bucket-major persistent replay.  One synchronous
+ * read sizes the entry buffer.  *fallback = true (nothing replayed) if an
+ * entry cannot hold the clocks. */
+template <typename SRC>
+static hr_status launch_binned(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const uint64_t *woff,
+                               cudaStream_t s, uint64_t b0, uint64_t b1, bool abl, bool *fallback)
+{
+    *fallback = false;
+    const uint64_t *kd = t->kdesc + 8ull * k;
+    const uint64_t warps = kd[1], lanes = kd[2], woi = kd[4];
+    const uint32_t kid = t->kernel_base + k;
+    hr_dev d = make_dev(c, kid);
+    d.block_base = (uint32_t)b0;
+    const uint32_t nb = (uint32_t)(b1 - b0);
+    const uint32_t nbk = (uint32_t)((c->glocal + (1ull << HR_BN_BITS) - 1) >> HR_BN_BITS);
+    const uint64_t ns = (uint64_t)nbk * nb;
+    hr_status st;
+    /* 64-bit counts: the scan's sum type is the input's, and C5 has 2^32 entries */
+    if ((st = reserve(c, 22, (size_t)(ns + 1) * 8)) || (st = reserve(c, 23, (size_t)(ns + 1) * 8)) ||
+        (st = reserve(c, 20, 64)))
+        return st;
+    uint64_t *cnt = (uint64_t *)c->stage[22];
+    uint64_t *off = (uint64_t *)c->stage[23];
+    unsigned int *status = (unsigned int *)c->stage[20];
+    unsigned long long *next = (unsigned long long *)((char *)c->stage[20] + 8);
+    CU(cudaMemsetAsync(c->stage[20], 0, 16, s));
+    CU(cudaMemsetAsync(cnt + ns, 0, 8, s));
+    const size_t wsm = hr_bn_walk_smem(nbk);
+    void (*wk0)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t, uint64_t *, const uint64_t *,
+                uint64_t *, unsigned int *) = hr_bn_walk_kernel<false, SRC>;
+    void (*wk1)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t, uint64_t *, const uint64_t *,
+                uint64_t *, unsigned int *) = hr_bn_walk_kernel<true, SRC>;
+    if (wsm > 48 * 1024) {
+        CU(cudaFuncSetAttribute(wk0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+        CU(cudaFuncSetAttribute(wk1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    }
+    const unsigned wgrid = (nb + HR_BN_WALK_WARPS - 1) / HR_BN_WALK_WARPS;
+    const uint64_t *wkoff = woff + woi + b0 * warps;
+    c->launches++;
+    wk0<<<wgrid, HR_BN_WALK_WARPS * 32, wsm, s>>>(d, src, wkoff, nb, (uint32_t)warps, (uint32_t)lanes, nbk, cnt,
+                                                   nullptr, nullptr, status);
+    CU(cudaGetLastError());
+    size_t tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int64_t)(ns + 1), s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches += 2;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, off, (int64_t)(ns + 1), s));
+    uint64_t entries = 0;
+    unsigned int hst = 0;
+    CU(cudaMemcpyAsync(&entries, off + ns, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (hst & HR_BN_ST_CANCEL) { *fallback = true; return HR_OK; }
+    if ((st = reserve(c, 21, (size_t)std::max<uint64_t>(entries, 1) * 8))) return st;
+    uint64_t *ent = (uint64_t *)c->stage[21];
+    c->launches++;
+    wk1<<<wgrid, HR_BN_WALK_WARPS * 32, wsm, s>>>(d, src, wkoff, nb, (uint32_t)warps, (uint32_t)lanes, nbk, cnt, off,
+                                                   ent, status);
+    CU(cudaGetLastError());
+    const size_t rsm = hr_bn_replay_smem();
+    void (*rk)(hr_dev, const uint64_t *, const uint64_t *, uint32_t, uint64_t, unsigned long long *) =
+        abl ? hr_bn_replay_kernel<true> : hr_bn_replay_kernel<false>;
+    if (rsm > 48 * 1024) CU(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->launches++;
+    rk<<<(unsigned)(dev_sms * 2), HR_BN_WARPS * 32, rsm, s>>>(d, ent, off, nb, ns, next);
+    CU(cudaGetLastError());
+    note_kernel(c, kid);
+    return HR_OK;
+}
+
+/* Binned replay (HR_OPT_BINNED) for kernels without shared shadow and at most
+ * HR_BN_MAXBK shadow buckets. */
+static bool use_binned(const hr_ctx *c, int kind, uint64_t smem_words)
+{
+    const uint32_t o = c->cfg.options;
+    if (smem_words != 0 || c->shadow_bytes != 8 || !c->gshadow || (o & HR_OPT_NO_BINNED)) return false;
+    const uint64_t nbk = (c->glocal + (1ull << HR_BN_BITS) - 1) >> HR_BN_BITS;
+    if (nbk > HR_BN_MAXBK) return false;
+    /* opt-in: measured slower than the row replay on C5 (DESIGN.md §5 item 17) */
+    (void)kind;
+    return (o & HR_OPT_BINNED) != 0;
+}
+
 /* One launch over simulated blocks [b0, b1) of kernel k (the whole kernel in
  * one launch for device traces; block-range chunks for host traces — blocks
  * are unordered by happens-before, so chunked launches replay the same kernel). */
@@ -708,6 +796,20 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         return HR_OK;
     }
     const bool pool = kind == HR_K_POOL || kind == HR_K_POOL_WIDE;
+    const bool abl0 = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE | HR_OPT_SMEM32);
+    if (use_binned(c, kind, smem_words) && !(c->cfg.options & HR_OPT_BSERIAL)) {
+        bool timing = c->cfg.options & HR_OPT_TIMING;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
+        bool fallback = true;
+        hr_status st = launch_binned(c, t, k, src, woff, s, b0, b1, abl0, &fallback);
+        if (st) return st;
+        if (!fallback) {
+            if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
+            return HR_OK;
+        }
+        if (timing) { c->ev_pool.push_back(e0); c->ev_pool.push_back(e1); }
+    }
     if (!src.aligned_ok()) return fail(c, HR_E_ARG, "trace records must be 16-byte aligned (TMA staging)");
     const bool wide = kind == HR_K_POOL_WIDE || kind == HR_K_ROW_WIDE;
     const uint32_t nb = wide ? hr_stage_cfg<true>::NB : hr_stage_cfg<false>::NB;
