@@ -45,17 +45,8 @@
 #define HR_BN_BITS 23u                /* bucket = 2^23 shadow words = 64 MB */
 #define HR_BN_MAXBK 2048u             /* buckets per launch (SMEM counters of the walk) */
 #define HR_BN_WALK_WARPS 4u
-#define HR_BN_PF 8u                   /* rows a walk warp loads ahead */
 #define HR_BN_CLOCK_MAX 4095u
 #define HR_BN_ST_CANCEL 1u            /* status: clocks too wide for an entry: fall back */
-
-#define HR_BN_NOENT (~0ull)           /* no entry (kind bits 3 never occur in an entry) */
-
-/* u64 words of a walk warp's SMEM: positions, clocks / cursors, sector buffers */
-__host__ __device__ __forceinline__ uint32_t hr_bn_walk_words(uint32_t nbk, bool write)
-{
-    return nbk + 32u + (write ? 4u * nbk : 0u);
-}
 
 __device__ __forceinline__ uint64_t hr__bn_entry(uint32_t off, uint32_t kind, uint32_t warp, uint32_t lane,
                                                  uint32_t bc, uint32_t wc)
@@ -75,20 +66,11 @@ __global__ void __launch_bounds__(HR_BN_WALK_WARPS * 32) hr_bn_walk_kernel(
     extern __shared__ __align__(16) unsigned char hr_smem[];
     const uint32_t hw = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t sb = blockIdx.x * HR_BN_WALK_WARPS + hw;    /* simulated block (launch-relative) */
-    /* per CUDA warp: stream positions [nbk] (u64), wc[32] and cur[32] of its simulated warps,
-     * and (write pass) one 32-byte sector buffer per stream: entries are written to global
-     * memory in whole sectors (a row's gathers go to up to 32 different streams; 8-byte
-     * scattered stores would leave partial sectors for L2 to evict) */
-    uint64_t *pos = reinterpret_cast<uint64_t *>(hr_smem) + (size_t)hw * hr_bn_walk_words(nbk, WRITE);
+    /* per CUDA warp: stream positions [nbk] (u64), then wc[32] and cur[32] of its simulated warps */
+    uint64_t *pos = reinterpret_cast<uint64_t *>(hr_smem) + (size_t)hw * (nbk + 32u);
     uint32_t *wcs = reinterpret_cast<uint32_t *>(pos + nbk), *cur = wcs + 32;
-    uint64_t *sbuf = pos + nbk + 32u;                            /* [nbk][4], write pass only */
     if (sb >= n_blocks) return;                                  /* warp-uniform */
-    for (uint32_t b = lane; b < nbk; b += 32u) {
-        const uint64_t p0 = WRITE ? off[(uint64_t)b * n_blocks + sb] : 0ull;
-        pos[b] = p0;
-        if (WRITE)
-            for (uint32_t q = 0; q < 4u; q++) sbuf[4u * b + q] = HR_BN_NOENT;   /* slots before the stream */
-    }
+    for (uint32_t b = lane; b < nbk; b += 32u) pos[b] = WRITE ? off[(uint64_t)b * n_blocks + sb] : 0ull;
     wcs[lane] = 0u;
     cur[lane] = 0u;
     __syncwarp();
@@ -108,18 +90,8 @@ __global__ void __launch_bounds__(HR_BN_WALK_WARPS * 32) hr_bn_walk_kernel(
             uint32_t p = cur[sw];
             if (p >= n) continue;
             const bool rep = !(hr__thread_off(d, blk, sw) & 1u);
-            bool brk = false;
-            while (p < n && !brk) {
-              /* HR_BN_PF rows loaded ahead (independent loads: the walk is latency bound
-               * otherwise); rows past a __syncthreads are re-read in the next epoch */
-              uint64_t xs[HR_BN_PF];
-#pragma unroll
-              for (uint32_t q = 0; q < HR_BN_PF; q++)
-                  xs[q] = (active && p + q < n) ? src.row(r0 + p + q, lane) : HR_NOP_REC;
-#pragma unroll
-              for (uint32_t q = 0; q < HR_BN_PF; q++) {
-                if (brk || p >= n) break;
-                const uint64_t x = xs[q];
+            while (p < n) {
+                const uint64_t x = active ? src.row(r0 + p, lane) : HR_NOP_REC;
                 p++;
                 const uint32_t op = (uint32_t)(x >> 62);
                 const uint64_t w = x & HR_WORD_MASK;
@@ -136,7 +108,7 @@ __global__ void __launch_bounds__(HR_BN_WALK_WARPS * 32) hr_bn_walk_kernel(
                         if ((bst | bsw) != ctrl) hr__set_flag(d, HR_F_MODEL_VIOLATION);
                     }
                     if (partial_ws) continue;
-                    if (bst) { brk = true; break; }                    /* this warp's block epoch ends */
+                    if (bst) break;                                    /* this warp's block epoch ends */
                     if (!bsw) continue;
                     /* __syncwarp of simulated warp sw (hr_syncwarp: saturate, stop, flag) */
                     const uint32_t wcv = wcs[sw];
@@ -182,34 +154,10 @@ __global__ void __launch_bounds__(HR_BN_WALK_WARPS * 32) hr_bn_walk_kernel(
                     pos[bk] = base + __popc(grp);
                 }
                 base = __shfl_sync(0xffffffffu, base, leader);
-                if (WRITE) {
-                    /* sectors of 4 entries: a sector this group fills alone is stored directly
-                     * (the group's lanes in one instruction: one sector write); entries of a
-                     * sector it only starts or only continues go to the stream's SMEM buffer,
-                     * and the leader stores the buffer once it is complete */
-                    const uint32_t g = __popc(grp);
-                    const uint64_t P = base + __popc(grp & ((1u << lane) - 1u));
-                    const uint64_t S = P >> 2, gend = base + g;           /* group covers [base, gend) */
-                    const bool whole = (S << 2) >= base && (S << 2) + 4u <= gend;
-                    if (v) {
-                        const uint64_t ent = hr__bn_entry((uint32_t)(local & ((1ull << HR_BN_BITS) - 1u)), op, sw,
-                                                          lane, bc, wcv);
-                        if (whole) out[P] = ent;
-                        else sbuf[4u * bk + (uint32_t)(P & 3u)] = ent;
-                    }
-                    __syncwarp();
-                    /* the buffered sector the group continued and completed: store it */
-                    if (v && lane == leader && (base & 3u) && ((base >> 2) << 2) + 4u <= gend) {
-                        const uint64_t s0 = (base >> 2) << 2;
-                        for (uint32_t q = 0; q < 4u; q++) {
-                            const uint64_t e = sbuf[4u * bk + q];
-                            if (e != HR_BN_NOENT) out[s0 + q] = e;
-                            sbuf[4u * bk + q] = HR_BN_NOENT;
-                        }
-                    }
-                }
+                if (WRITE && v)
+                    out[base + __popc(grp & ((1u << lane) - 1u))] =
+                        hr__bn_entry((uint32_t)(local & ((1ull << HR_BN_BITS) - 1u)), op, sw, lane, bc, wcv);
                 __syncwarp();
-              }
             }
             if (lane == 0) cur[sw] = p;
             __syncwarp();
@@ -227,15 +175,6 @@ __global__ void __launch_bounds__(HR_BN_WALK_WARPS * 32) hr_bn_walk_kernel(
     }
     if (!WRITE)
         for (uint32_t b = lane; b < nbk; b += 32u) cnt[(uint64_t)b * n_blocks + sb] = pos[b];
-    if (WRITE)                                                     /* the streams' last, partial sectors */
-        for (uint32_t b = lane; b < nbk; b += 32u)
-            if (pos[b] & 3u) {
-                const uint64_t s0 = (pos[b] >> 2) << 2;
-                for (uint32_t q = 0; q < (uint32_t)(pos[b] & 3u); q++) {
-                    const uint64_t e = sbuf[4u * b + q];
-                    if (e != HR_BN_NOENT) out[s0 + q] = e;
-                }
-            }
 }
 
 /* One pool of up to 32 entries (lane i: entry i) of the streams in
@@ -365,54 +304,15 @@ __device__ __forceinline__ void hr__bn_check(const hr_dev &d, const hr_thr &t, u
     }
 }
 
-/* Non-empty streams, in stream (bucket-major) order: ne[s] = 1 if stream s has
- * entries; after the scan, list[pos[s]] = s and lst[pos[s]] = off[s]. */
-__global__ void hr_bn_nonempty_kernel(const uint64_t *__restrict__ off, uint64_t ns, uint32_t *__restrict__ ne)
-{
-    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < ns) ne[s] = off[s + 1] > off[s] ? 1u : 0u;
-    else if (s == ns) ne[s] = 0u;
-}
-
-__global__ void hr_bn_list_kernel(const uint64_t *__restrict__ off, uint64_t ns, const uint32_t *__restrict__ ne,
-                                  const uint32_t *__restrict__ pos, uint32_t *__restrict__ list,
-                                  uint64_t *__restrict__ lst)
-{
-    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < ns && ne[s]) {
-        list[pos[s]] = (uint32_t)s;
-        lst[pos[s]] = off[s];
-    } else if (s == ns) {
-        lst[pos[ns]] = off[ns];                      /* end of the last stream */
-    }
-}
-
-/* cs[c] = the first listed stream starting at or after entry c * HR_BN_CHUNK */
-#define HR_BN_CHUNK 2048u
-__global__ void hr_bn_chunk_kernel(const uint64_t *__restrict__ lst, uint32_t nl, uint64_t nchunks,
-                                   uint32_t *__restrict__ cs)
-{
-    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > nchunks) return;
-    const uint64_t target = c * HR_BN_CHUNK;
-    uint32_t lo = 0, hi = nl;                         /* first i in [0, nl] with lst[i] >= target */
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (lst[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    cs[c] = lo;
-}
-
-/* Persistent replay, bucket-major: a warp takes the next chunk of HR_BN_CHUNK
- * entries and checks, whole, every non-empty stream that STARTS in it (so no
- * stream is split between warps; a long stream is one warp's work), 32
- * entries per pool, the next pool's entries loaded ahead.  Each lane finds
- * its entry's stream among the (at most 32) listed streams the pool spans. */
+/* Persistent replay of the streams, bucket-major: a warp takes the next
+ * HR_BN_GRAB streams (whole streams, so no stream is split between warps)
+ * and checks their concatenated entries 32 at a time. */
 #define HR_BN_WARPS 16u
+#define HR_BN_GRAB 4u
 template <bool ABL>
 __global__ void __launch_bounds__(HR_BN_WARPS * 32, 2) hr_bn_replay_kernel(
-    hr_dev d, const uint64_t *__restrict__ ent, const uint32_t *__restrict__ list, const uint64_t *__restrict__ lst,
-    uint32_t nl, const uint32_t *__restrict__ cs, uint32_t nchunks, uint32_t n_blocks, unsigned int *__restrict__ next)
+    hr_dev d, const uint64_t *__restrict__ ent, const uint64_t *__restrict__ off, uint32_t n_blocks, uint64_t nstreams,
+    unsigned long long *__restrict__ next)
 {
     extern __shared__ __align__(16) unsigned char hr_smem[];
     for (uint32_t i = threadIdx.x; i < HR_FSM_SMEM_BYTES / 16; i += blockDim.x)
@@ -427,36 +327,26 @@ __global__ void __launch_bounds__(HR_BN_WARPS * 32, 2) hr_bn_replay_kernel(
     t.off = 0;
     const uint32_t pool_sa = t.fsm + ((HR_FSM_SMEM_BYTES + 15u) & ~15u) + (threadIdx.x >> 5) * 384u;
     while (true) {
-        uint32_t c = 0;
-        if (lane == 0) c = atomicAdd(next, 1u);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= nchunks) break;
-        uint32_t li = cs[c];
-        const uint32_t lend = cs[c + 1];
-        if (li >= lend) continue;
-        const uint64_t e_end = lst[lend];
-        uint64_t e0 = lst[li];
-        uint64_t xn = e0 + lane < e_end ? __ldcs(reinterpret_cast<const unsigned long long *>(ent + e0 + lane)) : 0ull;
-        for (; e0 < e_end; e0 += 32u) {
-            const uint64_t e = e0 + lane;
-            const bool valid = e < e_end;
-            const uint64_t x = xn;
-            xn = e + 32u < e_end ? __ldcs(reinterpret_cast<const unsigned long long *>(ent + e + 32u)) : 0ull;
-            /* boundaries lst[li+1 .. li+32]: this lane's stream = li + #(boundaries <= e) */
-            const uint64_t bl = lst[min(li + 1u + lane, nl)];
-            uint32_t k = 0;
+        unsigned long long s0 = 0;
+        if (lane == 0) s0 = atomicAdd(next, (unsigned long long)HR_BN_GRAB);
+        s0 = __shfl_sync(0xffffffffu, s0, 0);
+        if (s0 >= nstreams) break;
+        const uint32_t ns = (uint32_t)((nstreams - s0) < (uint64_t)HR_BN_GRAB ? (nstreams - s0) : (uint64_t)HR_BN_GRAB);
+        /* streams [s0, s0 + ns): entries [off[s0], off[s0 + ns]); stream s = bucket * n_blocks + block */
+        uint64_t bnd[HR_BN_GRAB + 1];
 #pragma unroll
-            for (uint32_t step = 16; step >= 1; step >>= 1) {
-                const uint64_t v = __shfl_sync(0xffffffffu, bl, k + step - 1u);
-                if (k + step <= 32u && v <= e) k += step;
-            }
-            const uint32_t my = min(li + k, nl - 1u);
-            const uint32_t sid = list[my];
-            const uint32_t bk = sid / n_blocks, blk = sid - bk * n_blocks;
+        for (uint32_t k = 0; k <= HR_BN_GRAB; k++) bnd[k] = off[s0 + min(k, ns)];
+        const uint32_t blk0 = (uint32_t)(s0 % n_blocks), bk0 = (uint32_t)(s0 / n_blocks);
+        for (uint64_t e0 = bnd[0]; e0 < bnd[ns]; e0 += 32u) {
+            const uint64_t e = e0 + lane;
+            const bool valid = e < bnd[ns];
+            const uint64_t x = valid ? __ldcs(reinterpret_cast<const unsigned long long *>(ent + e)) : 0ull;
+            uint32_t k = 0;                                     /* this lane's stream within the grab */
+#pragma unroll
+            for (uint32_t q = 1; q < HR_BN_GRAB; q++) k += (q < ns && e >= bnd[q]) ? 1u : 0u;
+            uint32_t blk = blk0 + k, bk = bk0;
+            if (blk >= n_blocks) { blk -= n_blocks; bk++; }
             hr__bn_check<ABL>(d, t, x, valid, d.block_base + blk, (uint64_t)bk << HR_BN_BITS, pool_sa);
-            /* next pool starts in the stream of this pool's last valid entry */
-            const uint32_t last = (uint32_t)min((uint64_t)31u, e_end - 1u - e0);
-            li = __shfl_sync(0xffffffffu, my, last);
         }
     }
 }
@@ -466,9 +356,9 @@ __host__ __forceinline__ size_t hr_bn_replay_smem()
     return ((HR_FSM_SMEM_BYTES + 15u) & ~15u) + HR_BN_WARPS * 384u;
 }
 
-__host__ __forceinline__ size_t hr_bn_walk_smem(uint32_t nbk, bool write)
+__host__ __forceinline__ size_t hr_bn_walk_smem(uint32_t nbk)
 {
-    return (size_t)HR_BN_WALK_WARPS * hr_bn_walk_words(nbk, write) * 8u;
+    return (size_t)HR_BN_WALK_WARPS * (nbk + 32u) * 8u;
 }
 
 #endif /* HR_BINNED_CUH_ */

@@ -710,14 +710,15 @@ static hr_status launch_binned(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src
     unsigned long long *next = (unsigned long long *)((char *)c->stage[20] + 8);
     CU(cudaMemsetAsync(c->stage[20], 0, 16, s));
     CU(cudaMemsetAsync(cnt + ns, 0, 8, s));
-    const size_t wsm = hr_bn_walk_smem(nbk, false), wsm1 = hr_bn_walk_smem(nbk, true);
+    const size_t wsm = hr_bn_walk_smem(nbk);
     void (*wk0)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t, uint64_t *, const uint64_t *,
                 uint64_t *, unsigned int *) = hr_bn_walk_kernel<false, SRC>;
     void (*wk1)(hr_dev, SRC, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t, uint64_t *, const uint64_t *,
                 uint64_t *, unsigned int *) = hr_bn_walk_kernel<true, SRC>;
-    if (wsm > 48 * 1024) CU(cudaFuncSetAttribute(wk0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-    if (wsm1 > 48 * 1024) CU(cudaFuncSetAttribute(wk1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm1));
-    if (wsm1 > 227 * 1024) { *fallback = true; return HR_OK; }
+    if (wsm > 48 * 1024) {
+        CU(cudaFuncSetAttribute(wk0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+        CU(cudaFuncSetAttribute(wk1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    }
     const unsigned wgrid = (nb + HR_BN_WALK_WARPS - 1) / HR_BN_WALK_WARPS;
     const uint64_t *wkoff = woff + woi + b0 * warps;
     c->launches++;
@@ -738,46 +739,17 @@ static hr_status launch_binned(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src
     if ((st = reserve(c, 21, (size_t)std::max<uint64_t>(entries, 1) * 8))) return st;
     uint64_t *ent = (uint64_t *)c->stage[21];
     c->launches++;
-    wk1<<<wgrid, HR_BN_WALK_WARPS * 32, wsm1, s>>>(d, src, wkoff, nb, (uint32_t)warps, (uint32_t)lanes, nbk, cnt, off,
+    wk1<<<wgrid, HR_BN_WALK_WARPS * 32, wsm, s>>>(d, src, wkoff, nb, (uint32_t)warps, (uint32_t)lanes, nbk, cnt, off,
                                                    ent, status);
     CU(cudaGetLastError());
-    /* the non-empty streams, listed, and the chunk -> first listed stream map */
-    if ((st = reserve(c, 15, (size_t)(ns + 1) * 4)) || (st = reserve(c, 16, (size_t)(ns + 1) * 4)) ||
-        (st = reserve(c, 17, (size_t)(ns + 1) * 4)) || (st = reserve(c, 18, (size_t)(ns + 1) * 8)))
-        return st;
-    uint32_t *ne = (uint32_t *)c->stage[15], *npos = (uint32_t *)c->stage[16], *list = (uint32_t *)c->stage[17];
-    uint64_t *lst = (uint64_t *)c->stage[18];
-    const unsigned sgrid = (unsigned)((ns + 1 + 255) / 256);
-    c->launches++;
-    hr_bn_nonempty_kernel<<<sgrid, 256, 0, s>>>(off, ns, ne);
-    CU(cudaGetLastError());
-    tmp = 0;
-    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ne, npos, (int64_t)(ns + 1), s));
-    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
-    c->launches += 2;
-    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, ne, npos, (int64_t)(ns + 1), s));
-    c->launches++;
-    hr_bn_list_kernel<<<sgrid, 256, 0, s>>>(off, ns, ne, npos, list, lst);
-    CU(cudaGetLastError());
-    uint32_t nl = 0;
-    CU(cudaMemcpyAsync(&nl, npos + ns, 4, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    const uint64_t nchunks = (entries + HR_BN_CHUNK - 1) / HR_BN_CHUNK;
-    if ((st = reserve(c, 19, (size_t)(nchunks + 1) * 4))) return st;
-    uint32_t *cs = (uint32_t *)c->stage[19];
-    c->launches++;
-    hr_bn_chunk_kernel<<<(unsigned)((nchunks + 1 + 255) / 256), 256, 0, s>>>(lst, nl, nchunks, cs);
-    CU(cudaGetLastError());
     const size_t rsm = hr_bn_replay_smem();
-    void (*rk)(hr_dev, const uint64_t *, const uint32_t *, const uint64_t *, uint32_t, const uint32_t *, uint32_t,
-               uint32_t, unsigned int *) = abl ? hr_bn_replay_kernel<true> : hr_bn_replay_kernel<false>;
+    void (*rk)(hr_dev, const uint64_t *, const uint64_t *, uint32_t, uint64_t, unsigned long long *) =
+        abl ? hr_bn_replay_kernel<true> : hr_bn_replay_kernel<false>;
     if (rsm > 48 * 1024) CU(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     c->launches++;
-    if (nl)
-        rk<<<(unsigned)(dev_sms * 2), HR_BN_WARPS * 32, rsm, s>>>(d, ent, list, lst, nl, cs, (uint32_t)nchunks, nb,
-                                                                  (unsigned int *)next);
+    rk<<<(unsigned)(dev_sms * 2), HR_BN_WARPS * 32, rsm, s>>>(d, ent, off, nb, ns, next);
     CU(cudaGetLastError());
     note_kernel(c, kid);
     return HR_OK;
