@@ -597,6 +597,8 @@ def main():
         opts |= hr.HR_OPT_LAZY_RESET
     ck = hr.Checker(c5.total_words(lb), 0, shard=(shard_rank, shard_n), options=opts, ring_capacity=1 << 21,
                     granule_log2=args.granule_log2)
+    if shard_n > 1:
+        dt.flags = hr.HR_TRACE_F_SHARD_OWNED              # the generator kept only this rank's records
     if args.format == "pooled":
         pooled = ck.pool(dt, stream)                      # untimed input re-layout (hr_pool_trace)
         dt.rec32 = dt.recop = None

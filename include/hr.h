@@ -156,6 +156,16 @@ typedef struct {
     uint8_t space, scope, first_kind, prev_state;
 } hr_race;
 
+/* hr_trace.flags */
+enum {
+    HR_TRACE_F_SHARD_OWNED = 1u  /* every global access record of the trace targets a word of this ctx's
+                                    address shard (the trace was partitioned for this rank, as
+                                    tracegen's C5 shard generator and multigpu.shard_trace do): the
+                                    replay skips the per-access owner hash.  A record the shard does
+                                    not own would then be checked here too; the region check and the
+                                    shard-local index are unchanged.  No effect on an unsharded ctx. */
+};
+
 /* Record encodings of an hr_trace. */
 enum {
     HR_TRACE_U64 = 0,   /* rec: one u64 record per lane and row (any word < 2^61) */
@@ -220,7 +230,7 @@ typedef struct {
      *   recop  n_rows*32 u8: op | space << 2
      * decoded in the kernel to the u64 record above; same ownership rules. */
     uint32_t format;
-    uint32_t reserved;
+    uint32_t flags;           /* HR_TRACE_F_* (below) */
     const uint32_t *rec32;
     const uint8_t *recop;
     /* format HR_TRACE_PACKED (rec, rec32, recop unused; n_rows and warp_off as

@@ -78,6 +78,7 @@ struct hr_dev {
     uint32_t rep_bstride, rep_wstride; /* representative threads (hr_set_representatives): only
                                           blocks % rep_bstride == 0 and warps % rep_wstride == 0
                                           are checked; 1 = all */
+    uint32_t owned_only;          /* the replayed trace is HR_TRACE_F_SHARD_OWNED: no owner test */
     uint32_t epoch_tag;           /* HR_OPT_LAZY_RESET: kernel epoch tag 1..15 in bits [31:28] of the
                                      shadow's clock word; a global word with another tag is INIT.
                                      0 = off (the shadow is zeroed at every kernel boundary) */
@@ -326,7 +327,7 @@ __device__ __forceinline__ bool hr__locate(const hr_dev &d, const hr_thr &t, uin
     if (word < d.gbase || g >= d.gwords) { hr__set_flag(d, HR_F_UNMONITORED); return false; }
     const uint64_t gran = g >> d.gran_log2;
     local = ((gran >> d.shard_log2) << d.gran_log2) | (g & ((1ull << d.gran_log2) - 1u));
-    return hr_shard_owner(gran, d.shard_log2) == d.shard_rank;
+    return d.owned_only || hr_shard_owner(gran, d.shard_log2) == d.shard_rank;
 }
 
 /* a5 + a6 (+ a3 fold): the state after this lane's access from `old`, then the
@@ -684,31 +685,36 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
 {
     const uint32_t sa = t.sshadow + (word << 3);
     const uint32_t lo = (uint32_t)t.meta, tid_lo = (uint32_t)(t.meta >> HR_TID_SHIFT) & 1023u;
-    const uint32_t bc = lo >> d.wc_bits, wc = lo & ((1u << d.wc_bits) - 1u);
     const uint32_t kcol = t.fsm + (kind << 4);
     unsigned long long old = hr__ld_s(sa);
-    uint32_t ei = 0;
+    uint32_t os = 0, cur = 0;
+    bool racy = false;
     while (true) {
-        const uint32_t ohi = (uint32_t)(old >> 32), olo = (uint32_t)old;
-        const uint32_t os = ohi >> (HR_STATE_SHIFT - 32);
+        const uint32_t ohi = (uint32_t)(old >> 32);
+        os = ohi >> (HR_STATE_SHIFT - 32);
         const uint32_t x = (tid_lo ^ ohi) & 1023u;
         const uint32_t rel = (x != 0u) + (x >= 32u);
-        const uint32_t ws = (rel <= 1u) & (wc > (olo & ((1u << d.wc_bits) - 1u)));
-        const uint32_t sync = (bc > (olo >> d.wc_bits)) ? 2u : ws;
-        const uint32_t cur = hr__lds_u8(kcol + ((os << 6) | (sync << 2) | rel));
+        /* checkSync by XOR: in a happens-before consistent commit order the stored
+         * access of this block is never in a later block epoch (oBC <= BC), nor, in
+         * this warp and block epoch, in a later warp epoch (oWC <= WC), so "advanced"
+         * is "differs" (an INIT word ignores the label) */
+        const uint32_t dlo = (uint32_t)old ^ lo;
+        const uint32_t sync = (dlo >> d.wc_bits) ? 2u : ((rel <= 1u) & ((dlo << (32u - d.wc_bits)) != 0u));
+        cur = hr__lds_u8(kcol + ((os << 6) | (sync << 2) | rel));
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
         if (nw == old || (cur == os && os == HR_RACE_BLOCK)) break;      /* a7 (i), (iii) */
         const unsigned long long prev = hr__cas_s(sa, old, nw);
         if (prev == old) {                                                /* a8 committed */
-            if (cur >= HR_RACE_BLOCK && cur != os)
-                ei = HR_EI_EMIT | (hr__laneid() << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID);
+            racy = cur >= HR_RACE_BLOCK && cur != os;
             break;
         }
         old = prev;
     }
-    const unsigned em = __ballot_sync(0xffffffffu, ei != 0u);              /* a9 */
+    const unsigned em = __ballot_sync(0xffffffffu, racy);                  /* a9 */
     if (em) {
         const uint32_t lane = hr__laneid(), leader = __ffs(em) - 1;
+        const uint32_t ei =
+            racy ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u)) : 0u;
         uint32_t base = 0;
         if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(em));
         base = __shfl_sync(0xffffffffu, base, leader);

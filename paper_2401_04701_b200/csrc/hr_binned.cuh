@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(HR_BN_WALK_WARPS * 32) hr_bn_walk_kernel(
                         } else {
                             const uint64_t gran = g >> d.gran_log2;
                             local = ((gran >> d.shard_log2) << d.gran_log2) | (g & ((1ull << d.gran_log2) - 1u));
-                            v = hr_shard_owner(gran, d.shard_log2) == d.shard_rank;
+                            v = d.owned_only || hr_shard_owner(gran, d.shard_log2) == d.shard_rank;
                         }
                     }
                 }

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) hr_cmp_walk_kernel(hr_dev d, SRC src, con
             continue;
         }
         bool v = op != 3u;
-        if (v && !((x >> 61) & 1u) && d.shard_log2) {
+        if (v && !((x >> 61) & 1u) && d.shard_log2 && !d.owned_only) {
             const uint64_t g = wd - d.gbase;
             const bool in = wd >= d.gbase && g < d.gwords;
             v = !in || hr_shard_owner(g >> d.gran_log2, d.shard_log2) == d.shard_rank;

@@ -49,6 +49,7 @@ struct hr_ctx {
     uint32_t epoch_tag = 0;                      /* HR_OPT_LAZY_RESET: tag of the current kernel (1..15) */
     uint32_t sort_tmp_n = 0;                     /* cached CUB temp size of the report sort */
     uint32_t rep_bstride = 1, rep_wstride = 1;   /* hr_set_representatives */
+    bool cur_owned_only = false;                 /* the trace being replayed is HR_TRACE_F_SHARD_OWNED */
     size_t sort_tmp_bytes = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
@@ -165,6 +166,7 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.wc_max = (1u << c->cfg.wc_bits) - 1u;
     d.options = c->cfg.options;
     d.rep_bstride = c->rep_bstride;
+    d.owned_only = c->cur_owned_only ? 1u : 0u;
     d.rep_wstride = c->rep_wstride;
     if (d.options & HR_OPT_SMEM32) {            /* the 32-bit shared word holds bc:9, wc:8 */
         d.bc_max = std::min(d.bc_max, 511u);
@@ -1056,11 +1058,19 @@ extern "C" hr_status hr_pool_trace(hr_ctx *c, const hr_trace *in, uint64_t *rec_
     return pool_trace(c, in, hr_src_u64{in->rec}, rec_out, tag_out, cap_rows, warp_off_out, rows, s);
 }
 
+/* HR_TRACE_F_SHARD_OWNED for the duration of one replay call */
+struct owned_scope {
+    hr_ctx *c;
+    owned_scope(hr_ctx *ctx, const hr_trace *t) : c(ctx) { c->cur_owned_only = (t->flags & HR_TRACE_F_SHARD_OWNED) != 0; }
+    ~owned_scope() { c->cur_owned_only = false; }
+};
+
 extern "C" hr_status hr_replay_trace(hr_ctx *c, const hr_trace *t, void *stream)
 {
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
+    owned_scope own(c, t);
     if (t->format == HR_TRACE_PACKED) return replay_packed(c, t, false);
     if (t->format == HR_TRACE_POOLED) return replay_pooled(c, t);
     return dispatch(c, t, t->rec, t->rec32, t->recop, t->warp_off);
@@ -1303,6 +1313,7 @@ extern "C" hr_status hr_replay_trace_host(hr_ctx *c, const hr_trace *t, void *st
     if (!c || !trace_ok(t)) return fail(c, HR_E_ARG, "null or malformed trace");
     CU(cudaSetDevice(c->device));
     c->stream = (cudaStream_t)stream;
+    owned_scope own(c, t);
     if (t->format == HR_TRACE_PACKED) return replay_packed(c, t, true);
     if (t->format == HR_TRACE_POOLED) return fail(c, HR_E_ARG, "hr_replay_trace_host: POOLED traces are device only");
     const bool c32 = t->format == HR_TRACE_C32;

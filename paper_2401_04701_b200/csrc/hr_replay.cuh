@@ -205,7 +205,7 @@ __device__ __forceinline__ bool hr__pool_owned(const hr_dev &d, const hr_thr &t,
     const uint64_t w = x & HR_WORD_MASK;
     bool v = op != 3u && !(t.off & 1u);
     if (sp) v = v && !(t.off & 2u);
-    else if (d.shard_log2) {
+    else if (d.shard_log2 && !d.owned_only) {
         /* words outside the region go on to hr__locate on every shard, which flags them */
         const uint64_t g = w - d.gbase;
         const bool in = w >= d.gbase && g < d.gwords;

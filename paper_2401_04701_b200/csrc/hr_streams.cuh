@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(HR_ST_WALK_WARPS * 32) hr_st_walk_kernel(
             return;                                           /* the plan is discarded */
         }
         bool v = op != 3u;
-        if (v && !((x >> 61) & 1u) && d.shard_log2) {
+        if (v && !((x >> 61) & 1u) && d.shard_log2 && !d.owned_only) {
             const uint64_t g = wd - d.gbase;
             const bool in = wd >= d.gbase && g < d.gwords;
             v = !in || hr_shard_owner(g >> d.gran_log2, d.shard_log2) == d.shard_rank;

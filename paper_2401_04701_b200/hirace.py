@@ -61,13 +61,14 @@ class HrRace(ctypes.Structure):
 
 
 HR_TRACE_U64, HR_TRACE_C32, HR_TRACE_PACKED, HR_TRACE_POOLED = 0, 1, 2, 3
+HR_TRACE_F_SHARD_OWNED = 1
 
 
 class HrTrace(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("n_rows", ctypes.c_uint64), ("kdesc", ctypes.c_void_p),
                 ("n_kernels", ctypes.c_uint32), ("kernel_base", ctypes.c_uint32),
                 ("warp_off", ctypes.c_void_p), ("n_warp_off", ctypes.c_uint64),
-                ("format", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("format", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("rec32", ctypes.c_void_p), ("recop", ctypes.c_void_p),
                 ("packed", ctypes.c_void_p), ("pack_off", ctypes.c_void_p)]
 
@@ -349,6 +350,7 @@ class DeviceTrace:
         self.packed, self.pack_off = packed, pack_off
         self.warp_off = warp_off
         self.kdesc = np.ascontiguousarray(kdesc, dtype=np.uint64)
+        self.flags = 0                          # HR_TRACE_F_* (e.g. SHARD_OWNED for a per-rank shard)
         if pooled:                              # rec: pooled entries, recop: their simulated lanes
             self.format = HR_TRACE_POOLED
             self.n_rows = rec.numel() // 32
@@ -403,6 +405,7 @@ class DeviceTrace:
         t.warp_off = self.warp_off.data_ptr()
         t.n_warp_off = self.warp_off.numel()
         t.format = self.format
+        t.flags = self.flags
         if self.format == HR_TRACE_C32:
             t.rec32, t.recop = self.rec32.data_ptr(), self.recop.data_ptr()
         elif self.format == HR_TRACE_POOLED:
@@ -514,7 +517,9 @@ class Checker:
         tag = torch.empty(max(n, 1) * 32, dtype=torch.uint8, device=dev)
         woff = torch.zeros_like(dtrace.warp_off)
         hr_pool_trace(self.ctx, t, rec.data_ptr(), tag.data_ptr(), max(n, 1), woff.data_ptr(), stream)
-        return DeviceTrace(rec[: n * 32], woff, dtrace.kdesc, recop=tag[: n * 32], pooled=True)
+        out = DeviceTrace(rec[: n * 32], woff, dtrace.kdesc, recop=tag[: n * 32], pooled=True)
+        out.flags = dtrace.flags
+        return out
 
     def report(self):
         return hr_report(self.ctx)

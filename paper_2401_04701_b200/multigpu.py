@@ -222,7 +222,9 @@ def replay_sharded(trace, group=None, device: Optional[int] = None, base_word: i
     local = shard_trace(trace, rank, world, base_word)
     ck = hirace.Checker(gmax - base_word, smem, base_word=base_word, device=dev, shard=(rank, world),
                         **checker_kw)
-    ck.replay(hirace.DeviceTrace.from_trace(local, device=f"cuda:{dev}"))
+    dt = hirace.DeviceTrace.from_trace(local, device=f"cuda:{dev}")
+    dt.flags = hirace.HR_TRACE_F_SHARD_OWNED       # shard_trace kept only this rank's records
+    ck.replay(dt)
     ex = DeviceExchange(ck.ctx, cap, group, device=torch.device("cuda", dev))
     ex.step()
     out = ex.collect(fallback_raw=ck.report_raw)

@@ -78,3 +78,40 @@ def test_pooled_shards_union_and_c5_planted():
         union += [(int(x["word"]), int(x["scope"])) for x in raw]
         ck.close()
     assert sorted(union) == c5.planted(lb)
+
+
+@pytest.mark.parametrize("options", [0, 16, 32, 256, 16384 | 32])
+def test_shard_owned_flag_same_result(options):
+    """HR_TRACE_F_SHARD_OWNED (the per-access owner hash skipped for traces
+    partitioned for this rank): same per-rank sets as the owner test, on C5
+    shards from the generator and on host-sharded random programs."""
+    from paper_2401_04701_b200 import multigpu
+    h = hr()
+    lb, n = 8, 8
+    union = []
+    for r in range(n):
+        r32, rop, woff, kd = c5.gpu_trace_c32(lb, rank=r, nshard=n)
+        ck = h.Checker(c5.total_words(lb), 0, shard=(r, n), options=options | h.HR_OPT_LAZY_RESET)
+        dt = h.DeviceTrace(None, woff, kd, r32, rop)
+        ck.replay(dt)
+        plain = [tuple(x) for x in ck.report()[0]]
+        ck.reset()
+        dt.flags = h.HR_TRACE_F_SHARD_OWNED
+        ck.replay(dt)
+        owned = [tuple(x) for x in ck.report()[0]]
+        ck.close()
+        assert owned == plain
+        union += owned
+    assert sorted((x[3], x[4]) for x in union) == c5.planted(lb)
+    tr = _random_batch(61, 8, max_blocks=4, max_warps=8, max_lanes=32, max_slots=10, n_words=3000, spaces=(0, 1))
+    want, _ = oracle_set(tr)
+    gmax, smem = h.trace_extent(tr)
+    union = []
+    for r in range(4):
+        ck = h.Checker(gmax, smem, shard=(r, 4), options=options)
+        dt = h.DeviceTrace.from_trace(multigpu.shard_trace(tr, r, 4))
+        dt.flags = h.HR_TRACE_F_SHARD_OWNED
+        ck.replay(dt)
+        union += [tuple(x) for x in ck.report()[0]]
+        ck.close()
+    assert sorted(union) == want
