@@ -124,7 +124,7 @@ enum {
                                     DOUBLE_SHADOW; wc_bits <= 24. */
     HR_OPT_BSERIAL = 16384u,     /* sparse U64 traces (pooled replay): one CUDA warp replays a whole
                                     simulated block epoch by epoch (hr_bserial.cuh) */
-    HR_OPT_ROW_NARROW = 65536u,  /* force the 32-register row kernel (64 warps/SM) */
+    HR_OPT_ROW_NARROW = 65536u,  /* force the 48-register row kernel (the default for dense global traces) */
     HR_OPT_BINNED = 262144u,     /* address-binned replay (hr_binned.cuh) for kernels without shared
                                     shadow: accesses regrouped per (shadow bucket of 64 MB, block) in
                                     happens-before order and checked bucket by bucket so the random

@@ -429,10 +429,11 @@ static int kernel_choice_rule(hr_ctx *c, double acc, double tot, double maxw, do
     if (o & HR_OPT_ROW_WIDE) return HR_K_ROW_WIDE;
     if (o & HR_OPT_ROW_NARROW) return HR_K_ROW;
     const bool small = nwarps < 2048;
-    /* dense traces: the 64-register row kernel.  With the load-first a4 it also
-     * beats the 32-register one on the random-DRAM-bound C5 (88.6 vs 90.3 ms
-     * C32, 91.1 vs 93.0 ms u64), where the wider occupancy used to win */
-    const int row = HR_K_ROW_WIDE;
+    /* dense traces: the 64-register row kernel when issue or latency bound (a
+     * shared-shadow majority, or a small grid), else the 48-register one, which
+     * beats the 64-register kernel on the random-DRAM-bound C5 (88.6 vs 90.2 ms,
+     * round 2; in round 1 the 32-register one lost to 64 through spills) */
+    const int row = (tot > 0 && shared >= 0.5 * acc) || small ? HR_K_ROW_WIDE : HR_K_ROW;
     if (o & HR_OPT_NO_POOL) return row;
     if (o & HR_OPT_POOL_WIDE) return HR_K_POOL_WIDE;
     const bool tail = nwarps > 0 && maxw > 16.0 * (sumw / nwarps);

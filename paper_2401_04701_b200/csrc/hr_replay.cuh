@@ -243,7 +243,7 @@ __host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint
     return warps * nb * (ch * row_bytes + 8u);
 }
 
-/* POOL = false, WIDE = false: row-by-row at 32 registers, 64 warps/SM (dense
+/* POOL = false, WIDE = false: row-by-row at 48 registers, 40 warps/SM (dense
  *   global traces: occupancy hides the random-DRAM latency).
  * POOL = false, WIDE = true: row-by-row at up to 64 registers (shared-shadow
  *   heavy or small grids: issue and latency bound, spills cost more than warps).
@@ -253,10 +253,16 @@ __host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint
  *   very long warps, e.g. power-law BFS hubs: per-warp latency decides).
  * Rows reach the warp through its TMA staging ring (hr_records.cuh). */
 #ifdef HR_ROW_REGS
-/* register-cap experiments: the 32-register kernels get __maxnreg__ instead */
+/* register-cap experiments: the narrow kernels get __maxnreg__(HR_ROW_REGS) instead */
 #define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : HR_ROW_REGS)
 #else
-#define HR_REPLAY_BOUNDS(POOL, WIDE) __launch_bounds__(1024, (WIDE) ? 1 : 2)
+/* narrow row kernel at 48 registers: on C5 (dense, random-DRAM bound) it beats both the
+ * 64-register kernel (fewer warps) and the 32-register one (spills): 88.6 vs 90.2 ms,
+ * round 2; the narrow pooled kernel stays at 32 (C5 shards: 32 < 40 < 48) */
+#ifndef HR_ROW_NARROW_REGS
+#define HR_ROW_NARROW_REGS 48
+#endif
+#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : ((POOL) ? 32 : HR_ROW_NARROW_REGS))
 #endif
 template <bool POOL, bool WIDE, bool ABL, typename SRC>
 __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
