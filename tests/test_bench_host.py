@@ -35,3 +35,8 @@ def test_reference_arm_line():
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["unit"] == "accesses/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    cb = d["cpu_baseline"]
+    # SURVEY §8(d) "Oracle timing": the host's core count and model, and the labelled extrapolation
+    assert cb["host_cpu_count"] == os.cpu_count() and cb["cores"] == 1
+    assert "host_cpu_model" in cb and "EXTRAPOLATED" in cb["extrapolation"]
+    assert cb["extrapolated_full_step_s"] > 0
