@@ -678,7 +678,7 @@ static hr_status launch_streams(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     c->launches++;
-    kern<<<(unsigned)(dev_sms * 2), HR_ST_WARPS * 32, smem, s>>>(d, hr_src_cmp{orec, otag}, sbase, order, swarp,
+    kern<<<(unsigned)(dev_sms * HR_ST_CTAS), HR_ST_WARPS * 32, smem, s>>>(d, hr_src_cmp{orec, otag}, sbase, order, swarp,
                                                                 (uint32_t)ns, (uint32_t)warps, ctr + 1);
     CU(cudaGetLastError());
     note_kernel(c, kid);

@@ -42,6 +42,9 @@
 #define HR_ST_HMAX_LOG2 8u            /* at most 256 helper streams per simulated warp */
 #define HR_ST_TARGET 8192u            /* aim: total rows / L >= this many streams of length <= L */
 #define HR_ST_WALK_WARPS 8u
+#ifndef HR_ST_PF
+#define HR_ST_PF 8u                   /* rows a walk warp loads ahead */
+#endif
 
 __device__ __forceinline__ uint32_t hr__st_hlog2(uint64_t len, uint64_t L)
 {
@@ -110,8 +113,16 @@ __global__ void __launch_bounds__(HR_ST_WALK_WARPS * 32) hr_st_walk_kernel(
     }
     __syncwarp();
     const bool active = lane < lanes;
-    for (uint64_t r = r0; r < r1; r++) {
-        const uint64_t x = active ? src.row(r, lane) : HR_NOP_REC;
+    for (uint64_t rb = r0; rb < r1; rb += HR_ST_PF) {
+      /* HR_ST_PF rows loaded ahead: the walk is a chain of dependent row steps,
+       * so independent loads are what keeps it off the latency floor */
+      uint64_t xs[HR_ST_PF];
+#pragma unroll
+      for (uint32_t q = 0; q < HR_ST_PF; q++) xs[q] = (active && rb + q < r1) ? src.row(rb + q, lane) : HR_NOP_REC;
+#pragma unroll
+      for (uint32_t q = 0; q < HR_ST_PF; q++) {
+        if (rb + q >= r1) break;
+        const uint64_t x = xs[q];
         const uint32_t op = (uint32_t)(x >> 62);
         const uint64_t wd = x & HR_WORD_MASK;
         if (__any_sync(0xffffffffu, op == 3u && wd != 0u)) {
@@ -139,6 +150,7 @@ __global__ void __launch_bounds__(HR_ST_WALK_WARPS * 32) hr_st_walk_kernel(
             out_tag[o] = (uint8_t)lane;
         }
         __syncwarp();
+      }
     }
     if (!WRITE)
         for (uint32_t h = lane; h < H; h += 32u) cnt[slotoff[w] + (uint64_t)h * nseg + seg] = pos[h];
@@ -188,8 +200,11 @@ __global__ void hr_st_pad_kernel(const uint64_t *__restrict__ sbase, const uint3
  * SMEM by TMA bulk copies (NB x CH rows per warp, phases continuing across
  * streams).  No shared shadow and no clocks (barrier-free kernel). */
 #define HR_ST_WARPS 16u
+#ifndef HR_ST_CTAS
+#define HR_ST_CTAS 3u                 /* CTAs per SM (<= 42 registers, 48 warps/SM) */
+#endif
 template <bool ABL>
-__global__ void __launch_bounds__(HR_ST_WARPS * 32, 2) hr_replay_streams_kernel(
+__global__ void __launch_bounds__(HR_ST_WARPS * 32, HR_ST_CTAS) hr_replay_streams_kernel(
     hr_dev d, hr_src_cmp src, const uint64_t *__restrict__ sbase, const uint32_t *__restrict__ order,
     const uint32_t *__restrict__ swarp, uint32_t ns, uint32_t warps, unsigned int *__restrict__ next)
 {
