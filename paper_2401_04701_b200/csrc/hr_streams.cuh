@@ -43,7 +43,8 @@
 #define HR_ST_TARGET 8192u            /* aim: total rows / L >= this many streams of length <= L */
 #define HR_ST_WALK_WARPS 8u
 #ifndef HR_ST_PF
-#define HR_ST_PF 8u                   /* rows a walk warp loads ahead */
+#define HR_ST_PF 1u                   /* rows a walk warp loads ahead (C4 2^24: 1 -> 24.8 ms, 4 -> 24.7, 8 -> 26.7: the
+                                         unrolled body costs more than the overlap gains) */
 #endif
 
 __device__ __forceinline__ uint32_t hr__st_hlog2(uint64_t len, uint64_t L)
