@@ -398,8 +398,10 @@ hr_status hr_race_classes(hr_ctx *ctx, const hr_trace *t, const hr_race *races, 
 /* Clear the ring, its counter and the flags word (asynchronous on the last stream). */
 hr_status hr_reset_report(hr_ctx *ctx);
 
-/* Device-side counters of the last replay: [0] checked accesses, [1] CAS
- * retries, [2] fast exits (only maintained when built with HR_COUNTERS). */
+/* Device-side counters since the last hr_reset_report: [0] checked accesses,
+ * [1] failed CAS (Algorithm 1 retries), [2] a7 fast exits (no atomic), [3]
+ * committed CAS.  Maintained only by builds with -DHR_COUNTERS (a diagnostic
+ * build: per-access atomics); zero otherwise.  Synchronises. */
 hr_status hr_counters(hr_ctx *ctx, uint64_t out[4]);
 
 /* With HR_OPT_TIMING: synchronise and return the summed device time (ms) and

@@ -187,6 +187,24 @@ __device__ __forceinline__ uint32_t hr__laneid()
     return l;
 }
 
+/* Diagnostic counters (only in builds with -DHR_COUNTERS; hr_counters):
+ * [0] checked accesses [1] failed CAS (Algorithm 1 retries) [2] a7 fast exits
+ * [3] committed CAS.  Slices per SM (HR_CNT_BASE + slice * 4 + i) keep the
+ * atomics of a diagnostic run from serialising on one word. */
+#define HR_CNT_BASE 32u
+#define HR_CNT_SLICES 32u
+#ifdef HR_COUNTERS
+__device__ __forceinline__ uint32_t hr__smid()
+{
+    uint32_t s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
+}
+#define HR_COUNT(d, i) atomicAdd(&(d).counters[HR_CNT_BASE + ((hr__smid() % HR_CNT_SLICES) << 2) + (i)], 1ull)
+#else
+#define HR_COUNT(d, i) ((void)0)
+#endif
+
 /* Control rows (replay: the trace format's warp-aligned barriers,
  * tracegen/format.py): do the lanes holding a control record disagree on it? */
 __device__ __forceinline__ bool hr__ctrl_mixed(uint64_t x, unsigned ctrl)
@@ -400,19 +418,23 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
         if (cur == os && fresh != HR_OLD_GUESS && fastexit) {
             const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
-            if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+            if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH)) {
+                HR_COUNT(d, 2);
                 return 0u;                                                /* a7 (ii), (iii) */
+            }
         }
         if (nw == old) {
-            if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
+            if (fresh == HR_OLD_FRESH) { HR_COUNT(d, 2); return 0u; }     /* a7 (i) */
             if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
         }
         const unsigned long long prev = is_shared ? hr__cas_sh<ABL>(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
         if (prev == old) {                                                /* a8 committed */
+            HR_COUNT(d, 3);
             if (cur >= HR_RACE_BLOCK && cur != os)
                 return HR_EI_EMIT | (hr__laneid() << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID);
             return 0u;
         }
+        HR_COUNT(d, 1);
         old = prev;
         fresh = HR_OLD_FRESH;
     }
@@ -437,21 +459,23 @@ __device__ __forceinline__ uint32_t hr__commit(const hr_dev &d, const hr_thr &t,
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
         if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
             const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
-            if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+            if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH)) {
+                HR_COUNT(d, 2);
                 return 0u;                                                /* a7 (ii), (iii) */
+            }
         }
         if (nw == old) {
-            if (fresh == HR_OLD_FRESH) return 0u;                         /* a7 (i) */
+            if (fresh == HR_OLD_FRESH) { HR_COUNT(d, 2); return 0u; }     /* a7 (i) */
             if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
         }
         const unsigned long long prev = is_shared ? hr__cas_sh<ABL>(d, t, sh_addr, old, nw) : hr__cas_g(gp, old, nw);
-        if (prev == old)                                                  /* a8 committed */
+        if (prev == old) {                                                /* a8 committed */
+            HR_COUNT(d, 3);
             return rinfo ? (rinfo | (cur == HR_RACE_GRID ? 1u : 0u)) : 0u;
+        }
+        HR_COUNT(d, 1);
         old = prev;
         fresh = HR_OLD_FRESH;
-#ifdef HR_COUNTERS
-        atomicAdd(&d.counters[1], 1ull);
-#endif
     }
 }
 
@@ -640,6 +664,7 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
     const bool is_shared = space != 0u;
     uint64_t local = 0;
     valid = valid && !(t.off & 1u) && hr__locate(d, t, space, word, local);
+    if (valid) HR_COUNT(d, 0);
     /* match key: 0 = no access on this lane (filtered lanes must not alias owned words) */
     const uint64_t key = valid ? ((local << 2) | (is_shared ? 2u : 0u) | 1u) : 0ull;
     unsigned kb0, kb1;
@@ -689,6 +714,7 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
     unsigned long long old = hr__ld_s(sa);
     uint32_t os = 0, cur = 0;
     bool racy = false;
+    HR_COUNT(d, 0);
     while (true) {
         const uint32_t ohi = (uint32_t)(old >> 32);
         os = ohi >> (HR_STATE_SHIFT - 32);
@@ -702,12 +728,14 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
         const uint32_t sync = (dlo >> d.wc_bits) ? 2u : ((rel <= 1u) & ((dlo << (32u - d.wc_bits)) != 0u));
         cur = hr__lds_u8(kcol + ((os << 6) | (sync << 2) | rel));
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
-        if (nw == old || (cur == os && os == HR_RACE_BLOCK)) break;      /* a7 (i), (iii) */
+        if (nw == old || (cur == os && os == HR_RACE_BLOCK)) { HR_COUNT(d, 2); break; }   /* a7 (i), (iii) */
         const unsigned long long prev = hr__cas_s(sa, old, nw);
         if (prev == old) {                                                /* a8 committed */
+            HR_COUNT(d, 3);
             racy = cur >= HR_RACE_BLOCK && cur != os;
             break;
         }
+        HR_COUNT(d, 1);
         old = prev;
     }
     const unsigned em = __ballot_sync(0xffffffffu, racy);                  /* a9 */

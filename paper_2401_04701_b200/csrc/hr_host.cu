@@ -211,7 +211,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         if (cudaMalloc(&c->fsm, HR_FSM_SMEM_BYTES) != cudaSuccess ||
             cudaMalloc(&c->ring, sizeof(hr_race) * ((size_t)k.ring_capacity + c->spill_cap)) != cudaSuccess ||
             cudaMalloc(&c->tail, HR_TAIL_WORDS * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMalloc(&c->counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMalloc(&c->counters, 256 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_NOMEM, "device allocation failed in hr_init");
             break;
         }
@@ -221,7 +221,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         memcpy(host + HR_FSM_BYTES, hr_fsm_flags_init, 32);
         if (cudaMemcpy(c->fsm, host, HR_FSM_SMEM_BYTES, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemset(c->tail, 0, HR_TAIL_WORDS * sizeof(unsigned int)) != cudaSuccess ||
-            cudaMemset(c->counters, 0, 16 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMemset(c->counters, 0, 256 * sizeof(unsigned long long)) != cudaSuccess) {
             st = fail(c, HR_E_CUDA, "hr_init upload failed");
             break;
         }
@@ -1897,6 +1897,7 @@ extern "C" hr_status hr_reset_report(hr_ctx *c)
     CU(cudaSetDevice(c->device));
     CU(cudaMemsetAsync(c->tail, 0, HR_TAIL_WORDS * sizeof(unsigned int), c->stream));
     CU(cudaMemsetAsync(c->counters, 0, 4 * sizeof(unsigned long long), c->stream));
+    CU(cudaMemsetAsync(c->counters + HR_CNT_BASE, 0, 4 * HR_CNT_SLICES * sizeof(unsigned long long), c->stream));
     c->have_kernel = false;
     c->online_used = false;
     return HR_OK;
@@ -1907,7 +1908,12 @@ extern "C" hr_status hr_counters(hr_ctx *c, uint64_t out[4])
     if (!c || !out) return HR_E_ARG;
     CU(cudaSetDevice(c->device));
     CU(cudaStreamSynchronize(c->stream));
-    CU(cudaMemcpy(out, c->counters, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    uint64_t sl[4 * HR_CNT_SLICES];
+    CU(cudaMemcpy(sl, c->counters + HR_CNT_BASE, sizeof sl, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; i++) {
+        out[i] = 0;
+        for (uint32_t k = 0; k < HR_CNT_SLICES; k++) out[i] += sl[4 * k + i];
+    }
     return HR_OK;
 }
 

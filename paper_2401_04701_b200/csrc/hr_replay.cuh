@@ -109,6 +109,7 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
     /* pooled entries passed only the cheap owner test (hr__pool_owned): the
      * region check (HR_F_UNMONITORED) and the shard-local index happen here */
     const bool valid = lane < n && hr__locate(d, t, space, word, local);
+    if (valid) HR_COUNT(d, 0);
     const uint64_t key = valid ? ((local << 2) | (space << 1) | 1u) : 0ull;
     unsigned kb0, kb1;
     const unsigned peers = hr__group<false, ABL>(d, t, 0xffffffffu, lane, key, kind, kb0, kb1);
@@ -131,18 +132,22 @@ __device__ __forceinline__ void hr__check_pool(const hr_dev &d, const hr_thr &t,
             const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
             if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
                 const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
-                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH)) {
+                    HR_COUNT(d, 2);
                     break;
+                }
             }
             if (nw == old) {
-                if (fresh == HR_OLD_FRESH) break;
+                if (fresh == HR_OLD_FRESH) { HR_COUNT(d, 2); break; }
                 if (fresh == HR_OLD_PROBE) { old = hr__ld_g(gp); fresh = HR_OLD_FRESH; continue; }
             }
             const unsigned long long prv = sh ? hr__cas_sh<ABL>(d, t, sa, old, nw) : hr__cas_g(gp, old, nw);
             if (prv == old) {
+                HR_COUNT(d, 3);
                 if (rinfo) ei = rinfo | (cur == HR_RACE_GRID ? 1u : 0u);
                 break;
             }
+            HR_COUNT(d, 1);
             old = prv;
             fresh = HR_OLD_FRESH;
         }
