@@ -42,6 +42,11 @@
  *                   for hub addresses with 10^5..10^6 accesses.
  *   tests/test_oracle_pins.py checks both modes equal on random traces.
  *
+ * Control records (readings R8 and R12 in DESIGN.md): 1 = __syncthreads, 2 =
+ * __syncwarp; a __syncwarp only some active lanes of a warp row hold is a
+ * sub-warp __syncwarp(mask) and any other code is undefined —
+ * both flag a model violation and order nothing (no clock moves).
+ *
  * Clock overflow (PAPER.md:540 footnote: "race detection is discontinued with
  * a warning if a clock overflows (after reporting any previously identified
  * races)"): reading R6 — a thread whose bc (wc) would exceed bc_max (wc_max)
