@@ -212,7 +212,12 @@ enum {
  *             [63:62] op (0 R, 1 W, 2 A, 3 control) [61] space [60:0] word;
  *             control words: 0 NOP, 1 __syncthreads, 2 __syncwarp
  *   kdesc     HOST, n_kernels x 8 uint64: blocks, warps, lanes(<=32), smem_words,
- *             warp_off_index, 0, 0, 0
+ *             warp_off_index, tile_log2, 0, 0 — tile_log2 (0..4): 0 = whole-warp
+ *             __syncwarp records; 1..4 = the kernel's warp-level barriers are tiles
+ *             of 2^tile_log2 lanes (a __syncwarp record held by whole tiles is one
+ *             barrier per tile; reading R8 in DESIGN.md).  Tile
+ *             kernels are replayed by the row kernel (one clock per lane);
+ *             HR_TRACE_POOLED / hr_pool_trace reject them (HR_E_ARG)
  *   warp_off  DEVICE, uint64 absolute row offsets; warp w of kernel k owns rows
  *             [warp_off[woi+w], warp_off[woi+w+1]) with woi = kdesc[k][4]
  *   The ctx never takes ownership.  For hr_replay_trace_host, rec and warp_off are
@@ -268,6 +273,13 @@ hr_status hr_set_shard(hr_ctx *ctx, uint32_t rank, uint32_t count);
  * are not seen (the user asserts the symmetry).  1, 1 = every thread
  * (default).  HR_E_ARG on a zero stride. */
 hr_status hr_set_representatives(hr_ctx *ctx, uint32_t block_stride, uint32_t warp_stride);
+
+/* Warp tiles of online kernels (PAPER.md:264 __syncwarp's mask; cooperative
+ * groups tiled_partition<2^tile_log2>): from the next hr_device_view on, the
+ * kernel's warp-level barriers are hr_syncwarp_mask calls over whole tiles of
+ * 2^tile_log2 lanes, each ordering exactly its tile.  0 or 5 = whole warps
+ * (default).  Replayed traces declare their tile in kdesc[5] instead. */
+hr_status hr_set_warp_tile(hr_ctx *ctx, uint32_t tile_log2);
 
 /* Same with a shard granule of 2^granule_log2 words (0..24; hr_set_shard uses
  * 3 = 8 words, 64 B of shadow: on C5 it balances the Zipf-hot atomic words

@@ -79,6 +79,8 @@ struct hr_dev {
                                           blocks % rep_bstride == 0 and warps % rep_wstride == 0
                                           are checked; 1 = all */
     uint32_t owned_only;          /* the replayed trace is HR_TRACE_F_SHARD_OWNED: no owner test */
+    uint32_t tile_log2;           /* warp-level barriers order tiles of 2^tile_log2 lanes (5 = whole
+                                     warps): the "Warp" relation is "same tile" (reading R8) */
     uint32_t epoch_tag;           /* HR_OPT_LAZY_RESET: kernel epoch tag 1..15 in bits [31:28] of the
                                      shadow's clock word; a global word with another tag is INIT.
                                      0 = off (the shadow is zeroed at every kernel boundary) */
@@ -224,11 +226,14 @@ __device__ __forceinline__ bool hr__ctrl_divergent(uint64_t x, unsigned ctrl, un
 
 /* ---------------- labels ---------------- */
 
-/* compareTids: Self 0, Warp 1, Block 2, Global 3 from the packed-tid XOR. */
-__device__ __forceinline__ uint32_t hr__rel(uint32_t tid, uint32_t otid)
+/* compareTids: Self 0, Warp 1, Block 2, Global 3 from the packed-tid XOR.  With
+ * warp tiles of 2^tl lanes the packed tid block:17 | warp:5 | lane:5 is also
+ * block:17 | tile:(10-tl) | lane-in-tile:tl, and "Warp" means "same tile" (the
+ * unit a warp-level barrier orders); tl = 5: whole warps. */
+__device__ __forceinline__ uint32_t hr__rel(uint32_t tid, uint32_t otid, uint32_t tl = 5u)
 {
     uint32_t x = tid ^ otid;
-    return (x != 0u) + (x >= 32u) + (x >= 1024u);
+    return (x != 0u) + (x >= (1u << tl)) + (x >= 1024u);
 }
 
 /* checkSync: Bs 2 if same block and bc advanced; else Ws 1 if same warp and wc
@@ -368,11 +373,12 @@ __device__ __forceinline__ uint32_t hr__transition(const hr_dev &d, const hr_thr
 #else
     const uint32_t ftid = t.tid();
 #endif
-    rel = hr__rel(ftid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+    rel = hr__rel(ftid, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu, d.tile_log2);
     const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
     uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
     rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19)) : 0u;
     unsigned r = peers & ~(1u << lane);
+    uint32_t prev = lane;
     while (r) {
 #ifdef HR_FUZZ
         const uint32_t j = 31u - __clz(r);
@@ -382,7 +388,10 @@ __device__ __forceinline__ uint32_t hr__transition(const hr_dev &d, const hr_thr
         r &= r - 1;
 #endif
         const uint32_t kj = ((kb0 >> j) & 1u) | (((kb1 >> j) & 1u) << 1);
-        const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | 1u));
+        /* lanes of one row: same epochs (Us); Warp inside a tile, Block across tiles */
+        const uint32_t rj = ((j ^ prev) >> d.tile_log2) ? 2u : 1u;
+        prev = j;
+        const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | rj));
         if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
             rinfo = HR_EI_EMIT | (j << 26) | (kj << 24) | (cur << 19);
         cur = nx;
@@ -412,7 +421,7 @@ __device__ __forceinline__ uint32_t hr__commit_single(const hr_dev &d, const hr_
     while (true) {
         const unsigned long long lv = is_shared ? old : hr__live(d, old);   /* shared words are this kernel's */
         const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
-        const uint32_t rel = hr__rel(t.tid(), (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu);
+        const uint32_t rel = hr__rel(t.tid(), (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu, d.tile_log2);
         const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)lv, d.wc_bits);
         const uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | kcol | (sync << 2) | rel));
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
@@ -624,9 +633,10 @@ __device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, 
         if (__all_sync(mask, lane == 0 || key > prev)) return peers;
     }
     peers = __match_any_sync(mask, key);
-    if (ONLINE && __any_sync(mask, peers != (1u << lane))) {
+    if ((ONLINE || d.tile_log2 < 5u) && __any_sync(mask, peers != (1u << lane))) {
         /* a fold needs one epoch: true in any program with uniform barriers (one SHFL +
-         * VOTE to confirm); otherwise split the groups by epoch with a second MATCH */
+         * VOTE to confirm); otherwise (online code, or warp tiles whose barriers move
+         * the tiles' clocks apart) split the groups by epoch with a second MATCH */
         const uint32_t lo = (uint32_t)t.meta;
         if (!__all_sync(mask, lo == __shfl_sync(mask, lo, __ffs(mask) - 1))) {
             const unsigned same_epoch = __match_any_sync(mask, (unsigned long long)lo);
@@ -719,7 +729,7 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
         const uint32_t ohi = (uint32_t)(old >> 32);
         os = ohi >> (HR_STATE_SHIFT - 32);
         const uint32_t x = (tid_lo ^ ohi) & 1023u;
-        const uint32_t rel = (x != 0u) + (x >= 32u);
+        const uint32_t rel = (x != 0u) + (x >= (1u << d.tile_log2));
         /* checkSync by XOR: in a happens-before consistent commit order the stored
          * access of this block is never in a later block epoch (oBC <= BC), nor, in
          * this warp and block epoch, in a later warp epoch (oWC <= WC), so "advanced"
@@ -836,6 +846,16 @@ __device__ __forceinline__ void hr_syncthreads(const hr_dev &d, hr_thr &t)
     else t.meta += 1ull << d.wc_bits;
 }
 
+/* Do the lanes of `held` (a __syncwarp record on those lanes of a row) form whole
+ * warp tiles of 2^tl lanes within the active `lane_mask`?  Convergent call. */
+__device__ __forceinline__ bool hr__tile_aligned(unsigned held, unsigned lane_mask, uint32_t tl)
+{
+    const uint32_t T = 1u << tl, lane = hr__laneid();
+    const unsigned tm = (T >= 32u ? 0xffffffffu : (((1u << T) - 1u) << (lane & ~(T - 1u)))) & lane_mask;
+    const unsigned h = held & tm;
+    return __all_sync(0xffffffffu, h == 0u || h == tm);
+}
+
 /* __syncwarp(mask) for a sub-warp mask ("takes a mask argument";
  * PAPER.md:1054 lists sub-warp support as future work).  A thread's scalar warp
  * clock cannot say that only some lanes synchronised, so (reading R8 in
@@ -855,9 +875,32 @@ __device__ __forceinline__ void hr_syncwarp(const hr_dev &d, hr_thr &t)
 
 __device__ __forceinline__ void hr_syncwarp_mask(const hr_dev &d, hr_thr &t, unsigned mask)
 {
-    if (mask == 0xffffffffu) { hr_syncwarp(d, t); return; }
+    if (mask == 0xffffffffu && d.tile_log2 >= 5u) { hr_syncwarp(d, t); return; }
     __syncwarp(mask);
-    if (hr__laneid() == (uint32_t)(__ffs(mask) - 1)) hr__set_flag(d, HR_F_MODEL_VIOLATION);
+    /* a kernel with warp tiles (hr_set_warp_tile): a mask of whole tiles holding this
+     * lane is that tile's barrier: this lane's warp-tile clock advances (exact) */
+    bool whole = d.tile_log2 < 5u;
+    if (whole) {
+        const uint32_t T = 1u << d.tile_log2, lane = hr__laneid();
+        const unsigned tm = T >= 32u ? 0xffffffffu : (((1u << T) - 1u) << (lane & ~(T - 1u)));
+        whole = (mask & tm) == tm;
+    }
+    if (whole) {
+        if (((uint32_t)t.meta & d.wc_max) >= d.wc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+        else t.meta += 1ull;
+    } else if (hr__laneid() == (uint32_t)(__ffs(mask) - 1)) {
+        hr__set_flag(d, HR_F_MODEL_VIOLATION);
+    }
+}
+
+/* The lanes of `held` take a warp-tile barrier (replay of a tile row): a real
+ * __syncwarp for the converged warp, and each holding lane's clock advances. */
+__device__ __forceinline__ void hr_syncwarp_lanes(const hr_dev &d, hr_thr &t, unsigned held)
+{
+    __syncwarp();
+    if (!((held >> hr__laneid()) & 1u)) return;
+    if (((uint32_t)t.meta & d.wc_max) >= d.wc_max) { t.off |= 1u; hr__set_flag(d, HR_F_CLOCK_OVERFLOW); }
+    else t.meta += 1ull;
 }
 
 #endif /* HR_DEVICE_CUH_ */

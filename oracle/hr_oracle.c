@@ -114,7 +114,13 @@ static int materialize(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_ke
     for (uint64_t k = 0; k < n_kernels; k++) {
         const uint64_t *kd = kdesc + 8 * k;
         uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], woi = kd[4];
-        if (lanes < 1 || lanes > 32) { free(a); return -1; }
+        /* kdesc[5]: the kernel's warp tile, log2 of its lanes (0 = whole warps).  With
+         * tiles of T lanes, an aligned __syncwarp(tile mask) orders exactly the tile's
+         * lanes (reading R8 in DESIGN.md), so a tile plays the role of a
+         * warp: threads are (block, tile = warp*32/T + lane/T, lane%T) below */
+        const uint64_t tl = kd[5];
+        if (lanes < 1 || lanes > 32 || tl > 4) { free(a); return -1; }
+        const uint64_t T = tl ? (1ull << tl) : 32;
         for (uint64_t b = 0; b < blocks; b++) {
             int64_t block_sync_count = -1;
             for (uint64_t w = 0; w < warps; w++) {
@@ -139,10 +145,26 @@ static int materialize(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_ke
                      * sub-warp mask ("takes a mask argument"): reading R8 —
                      * model violation, and conservatively NO happens-before edge (no clock
                      * moves), so every race the masked barrier would hide is still reported */
-                    const int partial_ws = nbar != 0 && nbar != (int)lanes && same &&
-                                           (first_bar & ((1ull << 61) - 1)) == 2;
+                    int partial_ws = nbar != 0 && nbar != (int)lanes && same &&
+                                     (first_bar & ((1ull << 61) - 1)) == 2;
+                    /* tile kernels: a __syncwarp held by whole tiles (every active lane of
+                     * each tile it touches) is one tile barrier per such tile: exact */
+                    int tile_ws = 0;
+                    if (partial_ws && tl) {
+                        tile_ws = 1;
+                        for (uint64_t t0 = 0; t0 < lanes; t0 += T) {
+                            int held = 0, n_in = 0;
+                            for (uint64_t l = t0; l < t0 + T && l < lanes; l++) {
+                                n_in++;
+                                held += (row[l] & ~(1ull << 61)) == ((3ull << 62) | 2);
+                            }
+                            if (held != 0 && held != n_in) tile_ws = 0;
+                        }
+                        if (tile_ws) partial_ws = 0;
+                    }
                     if (partial_ws) *flags |= HRO_F_MODEL_VIOLATION;
-                    else if (nbar != 0 && (nbar != (int)lanes || !same)) *flags |= HRO_F_BARRIER_DIVERGENCE;
+                    else if (!tile_ws && nbar != 0 && (nbar != (int)lanes || !same))
+                        *flags |= HRO_F_BARRIER_DIVERGENCE;
                     for (uint64_t l = 0; l < lanes; l++) {
                         uint64_t x = row[l];
                         uint32_t op = (uint32_t)(x >> 62);
@@ -150,6 +172,7 @@ static int materialize(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_ke
                         uint64_t word = x & ((1ull << 61) - 1);
                         if (op == 3) {
                             if (partial_ws) continue;   /* sub-warp __syncwarp: no edge (above) */
+                            (void)tile_ws;              /* tile barrier: advances its lanes' wc below */
                             if (word == 1) {            /* __syncthreads: bc + 1 */
                                 if (bc[l] + 1 > bc_max) { dead[l] = 1; *flags |= HRO_F_CLOCK_OVERFLOW; }
                                 else bc[l]++;
@@ -175,8 +198,8 @@ static int materialize(const uint64_t *rec, const uint64_t *kdesc, uint64_t n_ke
                         e->space = (uint8_t)space;
                         e->ablock = space ? (uint32_t)b : GLOBAL_BLOCK;
                         e->tblock = (uint32_t)b;
-                        e->twarp = (uint16_t)w;
-                        e->tlane = (uint8_t)l;
+                        e->twarp = (uint16_t)(w * (32 / T) + l / T);   /* the tile (= the warp without tiles) */
+                        e->tlane = (uint8_t)(l % T);
                         e->bc = bc[l];
                         e->wc = wc[l];
                         e->kind = (uint8_t)op;

@@ -35,18 +35,23 @@ def thread_events(trace) -> List[Dict[Thread, List[Event]]]:
     rec = np.asarray(trace.rec, dtype=np.uint64)
     for k in range(trace.kdesc.shape[0]):
         blocks, warps, lanes, _smem, woi = (int(x) for x in trace.kdesc[k, :5])
+        tl = int(trace.kdesc[k, 5])              # warp tile (log2 lanes), 0 = whole warps
         th: Dict[Thread, List[Event]] = {}
         for b in range(blocks):
             for w in range(warps):
                 gw = b * warps + w
                 r0, r1 = int(trace.warp_off[woi + gw]), int(trace.warp_off[woi + gw + 1])
-                # per row: the lanes holding a __syncwarp record (the barrier's mask)
+                # per row: the lanes holding a __syncwarp record (the barrier's mask); in a
+                # tile kernel each tile's lanes form their own barrier (one __syncwarp(tile
+                # mask) per tile)
                 ws_mask = {}
                 for r in range(r0, r1):
                     m = frozenset(l for l in range(lanes)
                                   if int(rec[r * 32 + l]) & ~(1 << 61) == (3 << 62) | 2)
                     if m and len(m) < lanes:
                         ws_mask[r] = m
+                    if m and tl:
+                        ws_mask[r] = {l: frozenset(x for x in m if x >> tl == l >> tl) for l in m}
                 for l in range(lanes):
                     ev: List[Event] = []
                     for r in range(r0, r1):
@@ -56,7 +61,10 @@ def thread_events(trace) -> List[Dict[Thread, List[Event]]]:
                             if word == 1:
                                 ev.append(("S",))
                             elif word == 2:
-                                ev.append(("WS", ws_mask[r]) if r in ws_mask else ("WS",))
+                                msk = ws_mask.get(r)
+                                if isinstance(msk, dict):
+                                    msk = msk[l]
+                                ev.append(("WS", msk) if msk is not None else ("WS",))
                         else:
                             ev.append(("acc", space, word, op))
                     th[(b, w, l)] = ev

@@ -228,7 +228,7 @@ __device__ __forceinline__ void hr__bn_check(const hr_dev &d, const hr_thr &t, u
         while (true) {
             const unsigned long long lv = hr__live(d, old);
             const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
-            const uint32_t rel = hr__rel(tid, (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu);
+            const uint32_t rel = hr__rel(tid, (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu, d.tile_log2);
             const uint32_t sync = hr__sync(rel, lo, (uint32_t)lv, d.wc_bits);
             uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
             uint32_t rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19))
@@ -242,7 +242,7 @@ __device__ __forceinline__ void hr__bn_check(const hr_dev &d, const hr_thr &t, u
                 uint32_t tj, lj, kj;
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ej) : "r"(pool_sa + 8u * j) : "memory");
                 hr__bn_decode(ej, hr__lds_u32(pool_sa + 256u + 4u * j), tag_hi, d.wc_bits, tj, lj, kj);
-                const uint32_t rj = hr__rel(tj, ptid);
+                const uint32_t rj = hr__rel(tj, ptid, d.tile_log2);
                 const uint32_t sj = hr__sync(rj, lj, plo, d.wc_bits);
                 const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | (sj << 2) | rj));
                 if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)

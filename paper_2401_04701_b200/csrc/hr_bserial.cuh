@@ -90,7 +90,7 @@ __device__ __forceinline__ void hr__check_bpool(const hr_dev &d, const hr_thr &t
         while (true) {
             const unsigned long long lv = sh ? old : hr__live(d, old);
             const uint32_t os = (uint32_t)(lv >> HR_STATE_SHIFT);
-            const uint32_t rel = hr__rel(base | tag0, (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu);
+            const uint32_t rel = hr__rel(base | tag0, (uint32_t)(lv >> HR_TID_SHIFT) & 0x7ffffffu, d.tile_log2);
             const uint32_t sync = hr__sync(rel, lo0, (uint32_t)lv, d.wc_bits);
             uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind << 4) | (sync << 2) | rel));
             uint32_t rinfo = (cur >= HR_RACE_BLOCK && cur != os)
@@ -104,7 +104,7 @@ __device__ __forceinline__ void hr__check_bpool(const hr_dev &d, const hr_thr &t
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(xj) : "r"(rec_sa + 8u * j) : "memory");
                 const uint32_t tj = hr__lds_u16(tag_sa + 2u * j);
                 const uint32_t kj = (uint32_t)(xj >> 62);
-                const uint32_t rj = hr__rel(tj, prev);             /* Self / Warp / Block, same epochs: Us */
+                const uint32_t rj = hr__rel(tj, prev, d.tile_log2); /* Self / Warp / Block, same epochs: Us */
                 const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | rj));
                 if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
                     rinfo = HR_EI_EMIT | (tj << 21) | (kj << 19) | (cur << 14);

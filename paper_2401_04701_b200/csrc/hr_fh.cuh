@@ -42,14 +42,15 @@ __device__ __forceinline__ bool hr_fh__conflict(uint32_t a, uint32_t b)
 }
 
 /* unordered (and distinct threads): 0 = ordered/same thread, 1 = same block, 2 = other block */
-__device__ __forceinline__ uint32_t hr_fh__unordered(uint64_t p, uint32_t tid, uint32_t lo, uint32_t wc_bits)
+__device__ __forceinline__ uint32_t hr_fh__unordered(uint64_t p, uint32_t tid, uint32_t lo, uint32_t wc_bits,
+                                                     uint32_t tl)
 {
     const uint32_t ptid = (uint32_t)(p >> 32) & 0x7ffffffu;
     if (ptid == tid) return 0;
     if ((ptid >> 10) != (tid >> 10)) return 2;
     const uint32_t plo = (uint32_t)p;
     if ((plo >> wc_bits) != (lo >> wc_bits)) return 0;                 /* a __syncthreads separates */
-    if (((ptid >> 5) & 31u) != ((tid >> 5) & 31u)) return 1;          /* same block epoch, other warp */
+    if (((ptid ^ tid) & 1023u) >> tl) return 1;                        /* same block epoch, other warp (tile) */
     const uint32_t m = (1u << wc_bits) - 1u;
     return (plo & m) == (lo & m) ? 1u : 0u;                           /* same warp: warp epoch */
 }
@@ -70,11 +71,11 @@ __device__ __forceinline__ uint32_t hr_fh__access(const hr_dev &d, const hr_thr 
         uint32_t scope = 0;
         if (!(rd & HR_FH_REPORTED)) {
             if ((wr & HR_FH_VALID) && hr_fh__conflict(kind, (uint32_t)(wr >> 59) & 3u)) {
-                const uint32_t u = hr_fh__unordered(wr, t.tid(), lo, d.wc_bits);
+                const uint32_t u = hr_fh__unordered(wr, t.tid(), lo, d.wc_bits, d.tile_log2);
                 scope = u > scope ? u : scope;
             }
             if ((rd & HR_FH_VALID) && kind != HR_READ) {
-                const uint32_t u = hr_fh__unordered(rd, t.tid(), lo, d.wc_bits);
+                const uint32_t u = hr_fh__unordered(rd, t.tid(), lo, d.wc_bits, d.tile_log2);
                 scope = u > scope ? u : scope;
             }
         }
@@ -113,13 +114,16 @@ __global__ void __launch_bounds__(1024, 1) hr_fh_replay_kernel(hr_dev d, SRC src
             const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
             const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
             const bool mixed = hr__ctrl_mixed(x, ctrl);
-            const bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
+            bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
+            const bool tile_ws = partial_ws && d.tile_log2 < 5u && hr__tile_aligned(bsw, lane_mask, d.tile_log2);
+            partial_ws = partial_ws && !tile_ws;
             if (lane == 0) {
                 if (partial_ws) hr__set_flag(d, HR_F_MODEL_VIOLATION);           /* sub-warp mask: no edge */
-                else if (ctrl != lane_mask || mixed) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
+                else if (!tile_ws && (ctrl != lane_mask || mixed)) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
                 if ((bst | bsw) != ctrl) hr__set_flag(d, HR_F_MODEL_VIOLATION);
             }
             if (partial_ws) continue;
+            if (tile_ws) { hr_syncwarp_lanes(d, t, bsw); continue; }
             if (bst) hr_syncthreads(d, t);
             else if (bsw) hr_syncwarp(d, t);
             continue;

@@ -50,6 +50,7 @@ struct hr_ctx {
     uint32_t sort_tmp_n = 0;                     /* cached CUB temp size of the report sort */
     uint32_t rep_bstride = 1, rep_wstride = 1;   /* hr_set_representatives */
     bool cur_owned_only = false;                 /* the trace being replayed is HR_TRACE_F_SHARD_OWNED */
+    uint32_t online_tile_log2 = 5;               /* hr_set_warp_tile: warp tile of online kernels */
     size_t sort_tmp_bytes = 0;                       /* kernels launched (1 per CUB call), hr_launch_count */
     uint32_t shadow_bytes = 8;                   /* per word: 8 (HiRace) or 16 (finite-history baseline) */
     uint32_t smem_words_max = 0;
@@ -141,6 +142,17 @@ static uint32_t smem_u64(const hr_ctx *c, uint64_t smem_words)
 #define HR_SPILL_AUTO_MAX (1u << 24)
 #define HR_TAIL_WORDS 8
 
+static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id);
+
+/* the device view for replaying kernel k of t: kdesc[5] is its warp tile */
+static hr_dev make_kdev(hr_ctx *c, const hr_trace *t, uint32_t k)
+{
+    hr_dev d = make_dev(c, t->kernel_base + k);
+    const uint64_t tl = t->kdesc[8ull * k + 5];
+    d.tile_log2 = tl ? (uint32_t)tl : 5u;
+    return d;
+}
+
 static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
 {
     hr_dev d;
@@ -167,6 +179,7 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.options = c->cfg.options;
     d.rep_bstride = c->rep_bstride;
     d.owned_only = c->cur_owned_only ? 1u : 0u;
+    d.tile_log2 = c->online_tile_log2;
     d.rep_wstride = c->rep_wstride;
     if (d.options & HR_OPT_SMEM32) {            /* the 32-bit shared word holds bc:9, wc:8 */
         d.bc_max = std::min(d.bc_max, 511u);
@@ -245,6 +258,13 @@ extern "C" hr_status hr_set_shard_ex(hr_ctx *c, uint32_t rank, uint32_t count, u
     c->shard_count = count;
     c->shard_log2 = 0;
     while ((1u << c->shard_log2) < count) c->shard_log2++;
+    return HR_OK;
+}
+
+extern "C" hr_status hr_set_warp_tile(hr_ctx *c, uint32_t tile_log2)
+{
+    if (!c || tile_log2 > 5) return fail(c, HR_E_ARG, "hr_set_warp_tile: tile_log2 must be 0..5");
+    c->online_tile_log2 = tile_log2 ? tile_log2 : 5u;
     return HR_OK;
 }
 
@@ -474,7 +494,7 @@ static hr_status check_kernel(hr_ctx *c, const hr_trace *t, uint32_t k)
     const uint64_t *kd = t->kdesc + 8ull * k;
     uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
     if (blocks == 0) return HR_OK;
-    if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32)
+    if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32 || kd[5] > 4)
         return fail(c, HR_E_ARG, "kernel %u: grid %llux%llux%llu outside the 17/5/5-bit tid", k,
                     (unsigned long long)blocks, (unsigned long long)warps, (unsigned long long)lanes);
     if (smem_words > c->smem_words_max)
@@ -505,7 +525,7 @@ static hr_status launch_compact(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     const uint64_t *kd = t->kdesc + 8ull * k;
     const uint64_t warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
     const uint32_t kid = t->kernel_base + k;
-    hr_dev d = make_dev(c, kid);
+    hr_dev d = make_kdev(c, t, k);
     d.block_base = (uint32_t)b0;
     const uint64_t nw = (b1 - b0) * warps;
     const uint64_t *wk = woff + woi + b0 * warps;
@@ -581,7 +601,7 @@ static hr_status launch_streams(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     const uint64_t *kd = t->kdesc + 8ull * k;
     const uint64_t warps = kd[1], lanes = kd[2], woi = kd[4];
     const uint32_t kid = t->kernel_base + k;
-    hr_dev d = make_dev(c, kid);
+    hr_dev d = make_kdev(c, t, k);
     d.block_base = (uint32_t)b0;
     const uint64_t nw = (b1 - b0) * warps;
     const uint64_t *wk = woff + woi + b0 * warps;
@@ -697,7 +717,7 @@ static hr_status launch_binned(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src
     const uint64_t *kd = t->kdesc + 8ull * k;
     const uint64_t warps = kd[1], lanes = kd[2], woi = kd[4];
     const uint32_t kid = t->kernel_base + k;
-    hr_dev d = make_dev(c, kid);
+    hr_dev d = make_kdev(c, t, k);
     d.block_base = (uint32_t)b0;
     const uint32_t nb = (uint32_t)(b1 - b0);
     const uint32_t nbk = (uint32_t)((c->glocal + (1ull << HR_BN_BITS) - 1) >> HR_BN_BITS);
@@ -781,7 +801,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     const uint64_t *kd = t->kdesc + 8ull * k;
     uint64_t warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
     uint32_t kid = t->kernel_base + k;
-    hr_dev d = make_dev(c, kid);
+    hr_dev d = make_kdev(c, t, k);
     d.block_base = (uint32_t)b0;
     if (c->shadow_bytes == 16) {                               /* finite-history baseline */
         size_t smem = HR_FSM_SMEM_BYTES + smem_words * 16;
@@ -798,9 +818,14 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         note_kernel(c, kid);
         return HR_OK;
     }
+    /* the pooled and block-serial walks (pooled, compacted, streams, binned, bserial)
+     * keep one warp clock per simulated warp: tile kernels, whose tiles carry their
+     * own clocks, take the row kernel (64 registers) */
+    const bool tiles = kd[5] != 0;
+    if (tiles && (kind == HR_K_POOL || kind == HR_K_POOL_WIDE)) kind = HR_K_ROW_WIDE;
     const bool pool = kind == HR_K_POOL || kind == HR_K_POOL_WIDE;
     const bool abl0 = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE | HR_OPT_SMEM32);
-    if (use_binned(c, kind, smem_words) && !(c->cfg.options & HR_OPT_BSERIAL)) {
+    if (use_binned(c, kind, smem_words) && !(c->cfg.options & HR_OPT_BSERIAL) && !tiles) {
         bool timing = c->cfg.options & HR_OPT_TIMING;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
@@ -831,7 +856,7 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
     if (!pool) split = 0;
     const uint32_t nhw = (uint32_t)warps << split;
     const bool abl = c->cfg.options & (HR_OPT_NO_COALESCE | HR_OPT_NO_FASTEXIT | HR_OPT_SPECULATE | HR_OPT_SMEM32);
-    if (kind == HR_K_POOL && t->format == HR_TRACE_U64 && (c->cfg.options & HR_OPT_BSERIAL)) {
+    if (kind == HR_K_POOL && t->format == HR_TRACE_U64 && (c->cfg.options & HR_OPT_BSERIAL) && !tiles) {
         const size_t bsm = hr_bserial_smem((uint32_t)smem_words, (c->cfg.options & HR_OPT_SMEM32) != 0);
         if (bsm <= 227 * 1024) {
             void (*bk)(hr_dev, const uint64_t *, const uint64_t *, uint32_t, uint32_t, uint32_t, uint32_t) =
@@ -944,9 +969,10 @@ static hr_status replay_pooled(hr_ctx *c, const hr_trace *t)
         const uint64_t *kd = t->kdesc + 8ull * k;
         const uint64_t blocks = kd[0], warps = kd[1], lanes = kd[2], smem_words = kd[3], woi = kd[4];
         if (!blocks) continue;
+        if (kd[5]) return fail(c, HR_E_ARG, "pooled trace: kernel %u declares warp tiles (one clock per warp)", k);
         if ((st = hr_kernel_begin(c, c->stream))) return st;
         const uint32_t kid = t->kernel_base + k;
-        hr_dev d = make_dev(c, kid);
+        hr_dev d = make_kdev(c, t, k);
         const uint32_t nhw = (uint32_t)warps;
         const uint32_t stage_off = hr_stage_offset(false, nhw, smem_u64(c, smem_words));
         const size_t smem = (size_t)stage_off + hr_stage_bytes(nhw, 2u, 8u, hr_src_cmp::ROW_BYTES);
@@ -990,7 +1016,8 @@ static hr_status pool_trace(hr_ctx *c, const hr_trace *t, SRC src, uint64_t *rec
         if (blocks > (1ull << 17) || warps < 1 || warps > 32 || lanes < 1 || lanes > 32 ||
             woi + blocks * warps + 1 > t->n_warp_off)
             return fail(c, HR_E_ARG, "hr_pool_trace: kernel %u: bad grid or warp_off range", k);
-        hr_dev d = make_dev(c, t->kernel_base + k);
+        if (kd[5]) return fail(c, HR_E_ARG, "hr_pool_trace: kernel %u declares warp tiles (replay it as rows)", k);
+        hr_dev d = make_kdev(c, t, k);
         const uint64_t nw = blocks * warps;
         const uint64_t *wk = t->warp_off + woi;
         if ((st = reserve(c, 6, (nw + 1) * 8)) || (st = reserve(c, 7, (nw + 1) * 8))) return st;
@@ -1828,7 +1855,7 @@ static hr_status classes_launch(hr_ctx *c, const hr_trace *t, SRC src, const uns
         if (st) return st;
         const uint64_t *kd = t->kdesc + 8ull * k;
         if (!kd[0]) continue;
-        hr_dev d = make_dev(c, t->kernel_base + k);
+        hr_dev d = make_kdev(c, t, k);
         size_t smem = HR_FSM_SMEM_BYTES + HR_CLASS_TABLES_BYTES;
         c->launches++;
         hr_classes_kernel<SRC><<<(unsigned)kd[0], (unsigned)(kd[1] * 32), smem, s>>>(

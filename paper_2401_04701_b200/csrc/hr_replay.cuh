@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
     const uint32_t os = (uint32_t)(old >> HR_STATE_SHIFT);
     const uint32_t src0 = ps.src_at(lane);
     const uint32_t kind0 = (uint32_t)(ps.rec_at(lane) >> 62);
-    rel = hr__rel(base | src0, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu);
+    rel = hr__rel(base | src0, (uint32_t)(old >> HR_TID_SHIFT) & 0x7ffffffu, d.tile_log2);
     const uint32_t sync = hr__sync(rel, (uint32_t)t.meta, (uint32_t)old, d.wc_bits);
     uint32_t cur = hr__lds_u8(t.fsm + ((os << 6) | (kind0 << 4) | (sync << 2) | rel));
     rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (src0 << 26) | (kind0 << 24) | (os << 19)) : 0u;
@@ -86,7 +86,8 @@ __device__ __forceinline__ uint32_t hr__pool_transition(const hr_dev &d, const h
         r &= r - 1;
         const uint32_t sj = ps.src_at(j);
         const uint32_t kj = (uint32_t)(ps.rec_at(j) >> 62);
-        const uint32_t rj = sj == prev_src ? 0u : 1u;                 /* Self / Warp, same epochs: Us */
+        /* Self / Warp (same tile) / Block (another tile), same epochs: Us */
+        const uint32_t rj = sj == prev_src ? 0u : (((sj ^ prev_src) >> d.tile_log2) ? 2u : 1u);
         const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | rj));
         if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
             rinfo = HR_EI_EMIT | (sj << 26) | (kj << 24) | (cur << 19);
@@ -178,8 +179,11 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
     const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
     const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
     const bool mixed = hr__ctrl_mixed(x, ctrl);
-    const bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
-    const bool div = ctrl != lane_mask || mixed;
+    bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
+    /* a tile kernel: a __syncwarp row held by whole tiles is one barrier per tile (exact) */
+    const bool tile_ws = partial_ws && d.tile_log2 < 5u && hr__tile_aligned(bsw, lane_mask, d.tile_log2);
+    partial_ws = partial_ws && !tile_ws;
+    const bool div = !tile_ws && (ctrl != lane_mask || mixed);
     if ((threadIdx.x & 31u) == 0) {
         if (partial_ws) hr__set_flag(d, HR_F_MODEL_VIOLATION);
         else if (div) hr__set_flag(d, HR_F_BARRIER_DIVERGENCE);
@@ -187,6 +191,7 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
     }
     if (partial_ws) return;
     if (bst) hr_syncthreads(d, t);
+    else if (tile_ws) hr_syncwarp_lanes(d, t, bsw);
     else if (bsw) hr_syncwarp(d, t);
 }
 

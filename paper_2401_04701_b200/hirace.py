@@ -39,7 +39,7 @@ HR_OPT_ROW_NARROW = 65536
 HR_OPT_NO_STREAMS = 131072
 HR_OPT_BINNED = 262144
 HR_OPT_NO_BINNED = 524288
-EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
+EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_set_warp_tile", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_pool_trace", "hr_report", "hr_report_async",
            "hr_report_async_to",
            "hr_report_collect", "hr_merge_races", "hr_race_classes", "hr_reset_report", "hr_counters",
@@ -95,6 +95,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "hr_init": ([P(HrConfig), P(vp)], ctypes.c_int),
         "hr_set_shard": ([vp, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
         "hr_set_representatives": ([vp, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
+        "hr_set_warp_tile": ([vp, ctypes.c_uint32], ctypes.c_int),
         "hr_set_shard_ex": ([vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32], ctypes.c_int),
         "hr_shadow_alloc": ([vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, P(vp)], ctypes.c_int),
         "hr_kernel_begin": ([vp, vp], ctypes.c_int),
@@ -157,6 +158,11 @@ def hr_set_shard(ctx, rank: int, count: int, granule_log2: int = 3):
 def hr_set_representatives(ctx, block_stride: int = 1, warp_stride: int = 1):
     """Check only blocks % block_stride == 0 and warps % warp_stride == 0."""
     _check(load().hr_set_representatives(ctx, block_stride, warp_stride), ctx, "hr_set_representatives")
+
+
+def hr_set_warp_tile(ctx, tile_log2: int):
+    """Online kernels' warp-level barriers are tiles of 2^tile_log2 lanes (0/5 = whole warps; reading R8)."""
+    _check(load().hr_set_warp_tile(ctx, tile_log2), ctx, "hr_set_warp_tile")
 
 
 def hr_shadow_alloc(ctx, space: int, base_word: int, n_words: int) -> int:

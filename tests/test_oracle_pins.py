@@ -335,3 +335,67 @@ def test_masked_syncwarp_conservative_reading():
     assert [tuple(r) for r in oracle.check(nop).races] == [tuple(r) for r in oracle.check(tr).races]
     full = oracle.check(_masked_syncwarp_trace(lanes_in=(0, 1, 2)))
     assert full.races == [] and full.flags == 0
+
+
+def _tile_example(declared: bool):
+    """T = 2 lanes per tile (tiles {0,1}, {2,3}).  Lane 0 writes word 0 and
+    lane 2 word 1; tile 0 then meets a tile barrier (lanes 0 and 1 hold the
+    __syncwarp record), tile 1 does not; then lane 1 reads word 0 and lane 3
+    reads word 1."""
+    import numpy as np
+    rows = np.full((1, 3, 32), tf.NOP, dtype=np.uint64)
+    rows[0, 0, 0] = tf.W(0)
+    rows[0, 0, 2] = tf.W(1)
+    rows[0, 1, 0] = tf.SYNCWARP
+    rows[0, 1, 1] = tf.SYNCWARP
+    rows[0, 2, 1] = tf.R(0)
+    rows[0, 2, 3] = tf.R(1)
+    k = tf.kernel_from_rows(1, 1, 4, rows)
+    k.tile_log2 = 1 if declared else 0
+    return tf.make_trace([k])
+
+
+def test_tile_barriers_exact():
+    """Warp tiles (PAPER.md:264 __syncwarp's mask; the paper's future work,
+    PAPER.md:1054): a kernel that declares T-lane tiles treats an aligned
+    partial __syncwarp row as one barrier per tile, exactly (reading R8).
+    Pinned by hand (word 0 is ordered by tile 0's barrier, word 1 is not:
+    tile 1 never synchronised) and by vector clocks whose tile barriers join
+    exactly the tile's lanes over every interleaving; undeclared, the same row
+    is a sub-warp mask handled conservatively (both words, model violation)."""
+    tr = _tile_example(True)
+    th = vclock.thread_events(tr)[0]
+    exact = set()
+    for sched in vclock.enumerate_schedules(th):
+        exact |= set(vclock.vclock_races(th, sched))
+    assert exact == {(0, 0xFFFFFFFF, 1)}
+    for mode in (oracle.PAIRWISE, oracle.BUCKETED):
+        res = oracle.check(tr, mode=mode)
+        assert res.flags == 0
+        assert {(r.space, r.block, r.word) for r in res.races} == exact
+    und = oracle.check(_tile_example(False))
+    assert und.flags == oracle.F_MODEL_VIOLATION and [r.word for r in und.races] == [0, 1]
+
+
+@pytest.mark.slow
+def test_tile_programs_vector_clocks_and_modes():
+    """Random tile programs (tiny: every interleaving enumerated) — the
+    oracle's static set equals the vector-clock set on every interleaving;
+    larger ones — pairwise == bucketed."""
+    rng = random.Random(91)
+    n_checked = 0
+    for _ in range(60):
+        tr = tp.random_tile_program(rng, blocks=rng.randint(1, 2), warps=1, lanes=4, tile_log2=rng.choice([1, 2]),
+                                    slots=rng.randint(2, 4), n_words=2, p_tile=0.35, p_sync=0.1)
+        th = vclock.thread_events(tr)[0]
+        want = {(r.space, r.block, r.word) for r in oracle.check(tr, mode=oracle.PAIRWISE).races}
+        for i, sched in enumerate(vclock.enumerate_schedules(th, cap=400)):
+            assert set(vclock.vclock_races(th, sched)) == want
+            n_checked += 1
+    assert n_checked > 1000
+    for _ in range(30):
+        tr = tp.random_tile_program(rng, blocks=3, warps=2, lanes=32, tile_log2=rng.choice([1, 2, 3, 4]), slots=14,
+                                    n_words=20, spaces=(0, 1))
+        a = oracle.check(tr, mode=oracle.PAIRWISE)
+        b = oracle.check(tr, mode=oracle.BUCKETED)
+        assert [tuple(r) for r in a.races] == [tuple(r) for r in b.races] and a.flags == b.flags == 0

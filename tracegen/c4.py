@@ -52,7 +52,7 @@ class Graph:
         nr, nk, nw = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint64()
         self.lib.c4_sizes(self.h, int(racy), ctypes.byref(nr), ctypes.byref(nk), ctypes.byref(nw))
         rec = np.empty(nr.value * 32, dtype=np.uint64)
-        kd = np.empty((nk.value, 8), dtype=np.uint64)
+        kd = np.zeros((nk.value, 8), dtype=np.uint64)
         wo = np.empty(nw.value, dtype=np.uint64)
         self.lib.c4_fill(self.h, int(racy), rec.ctypes.data, kd.ctypes.data, wo.ctypes.data)
         return Trace(rec, kd, wo)

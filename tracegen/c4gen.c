@@ -168,7 +168,7 @@ void c4_fill(void *h, int racy, uint64_t *rec, uint64_t *kdesc, uint64_t *woff)
     for (uint32_t k = 0; k <= g->n_levels; k++) {
         uint64_t *kd = kdesc + 8 * k;
         memset(kd, 0, 64);
-        kd[0] = g->n / 256; kd[1] = 8; kd[2] = 32; kd[3] = 0; kd[4] = wo;
+        kd[0] = g->n / 256; kd[1] = 8; kd[2] = 32; kd[3] = 0; kd[4] = wo; kd[5] = kd[6] = kd[7] = 0;
         for (uint64_t w = 0; w < nw; w++) {
             woff[wo++] = row;
             uint64_t nr = warp_rows(g, k, w, racy);

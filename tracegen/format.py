@@ -28,7 +28,11 @@ warp-aligned: when one active lane holds a barrier at some row, every active
 lane of that warp holds the same barrier at that row.
 
 ``kdesc`` is an (n_kernels, 8) uint64 array:
-    [blocks, warps, lanes, smem_words, warp_off_index, 0, 0, 0]
+    [blocks, warps, lanes, smem_words, warp_off_index, tile_log2, 0, 0]
+``tile_log2`` (1..4) declares that the kernel's warp-level barriers are tiles of
+2^tile_log2 lanes (cooperative-groups ``tiled_partition<T>().sync()``, i.e.
+``__syncwarp(tile mask)``): a ``__syncwarp`` record held by whole tiles is one
+barrier per tile.  0 = whole-warp ``__syncwarp`` only.
 ``warp_off`` is a uint64 array of absolute row indices.
 """
 from __future__ import annotations
@@ -83,6 +87,7 @@ class Kernel:
     lanes: int
     smem_words: int
     rows: List[np.ndarray] = field(default_factory=list)  # per warp: (n_rows, 32) uint64
+    tile_log2: int = 0     # warp-level barriers are tiles of 2^tile_log2 lanes (0 = whole warps)
 
     @property
     def n_warps(self) -> int:
@@ -219,7 +224,7 @@ def make_trace(kernels: Sequence[Kernel]) -> Trace:
                 recs.append(r.reshape(-1))
             row += int(sum(lens))
         offs.append(o)
-        kd.append([k.blocks, k.warps, k.lanes, k.smem_words, woi, 0, 0, 0])
+        kd.append([k.blocks, k.warps, k.lanes, k.smem_words, woi, k.tile_log2, 0, 0])
     rec = np.concatenate(recs) if recs else np.zeros(0, dtype=np.uint64)
     return Trace(np.ascontiguousarray(rec, dtype=np.uint64),
                  np.array(kd, dtype=np.uint64).reshape(-1, KDESC_FIELDS),

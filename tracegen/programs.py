@@ -14,7 +14,7 @@ import random
 from typing import List, Optional, Sequence
 
 from .format import (A, R, W, NOP, SYNCTHREADS, SYNCWARP, SPACE_GLOBAL, SPACE_SHARED,
-                     Trace, build_kernel, make_trace, single_kernel)
+                     Trace, build_kernel, kernel_from_rows, make_trace, single_kernel)
 
 # ---------------------------------------------------------------------------
 # Paper listings
@@ -157,3 +157,35 @@ def from_thread_events(blocks: int, warps: int, lanes: int, events: dict,
     """Trace from an explicit ``{(block, warp, lane): [records]}`` map (missing = empty)."""
     return single_kernel(blocks, warps, lanes, lambda b, w, l: events.get((b, w, l), []),
                          smem_words)
+
+
+def random_tile_program(rng: random.Random, blocks: int = 2, warps: int = 2, lanes: int = 32, tile_log2: int = 2,
+                        slots: int = 12, n_words: int = 16, spaces: Sequence[int] = (SPACE_GLOBAL,),
+                        p_tile: float = 0.3, p_sync: float = 0.08, p_skip: float = 0.3,
+                        kinds: Sequence[str] = "RWA"):
+    """A kernel whose warp-level barriers are tiles of 2^tile_log2 lanes
+    (cooperative-groups ``tiled_partition<T>().sync()``): each slot is an
+    access row (lanes skip at random), a ``__syncthreads`` row (every lane of
+    the block), or a tile-barrier row in which every tile of every warp
+    independently does or does not hold a ``__syncwarp`` record."""
+    import numpy as np
+    kmap = {"R": R, "W": W, "A": A}
+    T = 1 << tile_log2
+    rows = np.full((blocks * warps, slots, 32), NOP, dtype=np.uint64)
+    for s in range(slots):
+        u = rng.random()
+        if u < p_sync:
+            rows[:, s, :lanes] = SYNCTHREADS
+        elif u < p_sync + p_tile:
+            for gw in range(blocks * warps):
+                for t0 in range(0, lanes, T):
+                    if rng.random() < 0.5:
+                        rows[gw, s, t0:min(t0 + T, lanes)] = SYNCWARP
+        else:
+            for gw in range(blocks * warps):
+                for l in range(lanes):
+                    if rng.random() >= p_skip:
+                        rows[gw, s, l] = kmap[rng.choice(list(kinds))](rng.randrange(n_words), rng.choice(list(spaces)))
+    k = kernel_from_rows(blocks, warps, lanes, rows, smem_words=n_words if SPACE_SHARED in spaces else 0)
+    k.tile_log2 = tile_log2
+    return make_trace([k])
