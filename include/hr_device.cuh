@@ -716,11 +716,21 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
  *     (iii) — always non-Global here; (ii)'s insensitive states are GREAD,
  *     GATOMIC, RACE_GRID, which need another block and never occur.
  */
+/* min(v, 1) as one VIMNMX (inline PTX: the compiler would otherwise turn it into a
+ * compare and a select/add pair per term) */
+__device__ __forceinline__ uint32_t hr__min1(uint32_t v)
+{
+    uint32_t r;
+    asm("min.u32 %0, %1, 1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind)
 {
     const uint32_t sa = t.sshadow + (word << 3);
     const uint32_t lo = (uint32_t)t.meta, tid_lo = (uint32_t)(t.meta >> HR_TID_SHIFT) & 1023u;
     const uint32_t kcol = t.fsm + (kind << 4);
+    const uint32_t wsh = 32u - d.wc_bits;
     unsigned long long old = hr__ld_s(sa);
     uint32_t os = 0, cur = 0;
     bool racy = false;
@@ -729,14 +739,17 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
         const uint32_t ohi = (uint32_t)(old >> 32);
         os = ohi >> (HR_STATE_SHIFT - 32);
         const uint32_t x = (tid_lo ^ ohi) & 1023u;
-        const uint32_t rel = (x != 0u) + (x >= (1u << d.tile_log2));
         /* checkSync by XOR: in a happens-before consistent commit order the stored
          * access of this block is never in a later block epoch (oBC <= BC), nor, in
          * this warp and block epoch, in a later warp epoch (oWC <= WC), so "advanced"
-         * is "differs" (an INIT word ignores the label) */
+         * is "differs".  The two sync bits are set independently (bit 1: bc differs,
+         * bit 0: wc differs); the table maps index 3 to Bs and Ws under a Block
+         * relation to Us (fsm/generate.py), and an INIT word ignores the label.
+         * Each 0/1 term as a min (one VIMNMX) so the index folds into LEA/IADD3. */
         const uint32_t dlo = (uint32_t)old ^ lo;
-        const uint32_t sync = (dlo >> d.wc_bits) ? 2u : ((rel <= 1u) & ((dlo << (32u - d.wc_bits)) != 0u));
-        cur = hr__lds_u8(kcol + ((os << 6) | (sync << 2) | rel));
+        const uint32_t idx = (os << 6) + (hr__min1(dlo >> d.wc_bits) << 3) + (hr__min1(dlo << wsh) << 2) +
+                             hr__min1(x) + hr__min1(x >> d.tile_log2);        /* + rel: Self / Warp / Block */
+        cur = hr__lds_u8(kcol + idx);
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
         if (nw == old || (cur == os && os == HR_RACE_BLOCK)) { HR_COUNT(d, 2); break; }   /* a7 (i), (iii) */
         const unsigned long long prev = hr__cas_s(sa, old, nw);
@@ -748,15 +761,16 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
         HR_COUNT(d, 1);
         old = prev;
     }
-    const unsigned em = __ballot_sync(0xffffffffu, racy);                  /* a9 */
-    if (em) {
-        const uint32_t lane = hr__laneid(), leader = __ffs(em) - 1;
-        const uint32_t ei =
-            racy ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u)) : 0u;
+    /* a9: rare here, so no warp vote on the common path; the racy lanes that arrive
+     * together share one ring reservation (warp-aggregated over __activemask) */
+    if (racy) {
+        const unsigned m = __activemask();
+        const uint32_t lane = hr__laneid(), leader = __ffs(m) - 1;
         uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(em));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (ei) hr__write_race(d, t, base + __popc(em & ((1u << lane) - 1u)), 1u, word, ei);
+        if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(m));
+        base = __shfl_sync(m, base, leader);
+        const uint32_t ei = HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u);
+        hr__write_race(d, t, base + __popc(m & ((1u << lane) - 1u)), 1u, word, ei);
     }
 }
 

@@ -175,8 +175,11 @@ __device__ __forceinline__ void hr__barrier_row(const hr_dev &d, hr_thr &t, uint
 {
     const uint32_t op = (uint32_t)(x >> 62);
     const uint64_t w = x & HR_WORD_MASK;
-    const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
+    /* the common row: every active lane holds a __syncthreads (inactive lanes hold
+     * NOP), so nothing is mixed, divergent or undefined */
     const unsigned bst = __ballot_sync(0xffffffffu, op == 3u && w == 1u);
+    if (bst == lane_mask) { hr_syncthreads(d, t); return; }
+    const unsigned ctrl = __ballot_sync(0xffffffffu, op == 3u && w != 0u);
     const unsigned bsw = __ballot_sync(0xffffffffu, op == 3u && w == 2u);
     const bool mixed = hr__ctrl_mixed(x, ctrl);
     bool partial_ws = bsw != 0u && bsw == ctrl && ctrl != lane_mask && !mixed;
@@ -390,17 +393,18 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 uint32_t w32 = 0u, ob = 3u;
                 if (active) SRC::sld2(buf, j, lane, CH, w32, ob);
                 const bool ctl = (ob & 3u) == 3u;
+                /* one vote classifies a shared row: every lane a shared-space access
+                 * (op | space << 2 in 4..6) to strictly increasing in-range words */
+                const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
+                if (__all_sync(0xffffffffu, (ob & 7u) - 4u < 3u && w32 < t.swords && !(t.off & 3u) &&
+                                                (lane == 0u || w32 > wprev))) {
+                    hr__check_shared_row(d, t, w32, ob & 3u);
+                    continue;
+                }
                 if (__any_sync(0xffffffffu, ctl && w32 != 0u)) {
                     hr__barrier_row(d, t, ((uint64_t)(ob & 3u) << 62) | ((uint64_t)((ob >> 2) & 1u) << 61) | w32,
                                     lane_mask);
                     continue;
-                }
-                if (__all_sync(0xffffffffu, (ob & 7u) >= 4u && (ob & 3u) != 3u)) {     /* all shared accesses */
-                    const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
-                    if (__all_sync(0xffffffffu, w32 < t.swords && !(t.off & 3u) && (lane == 0u || w32 > wprev))) {
-                        hr__check_shared_row(d, t, w32, ob & 3u);
-                        continue;
-                    }
                 }
                 hr_check_lanes<false, ABL>(d, t, 0xffffffffu, !ctl, (ob >> 2) & 1u, w32, ob & 3u);
             }

@@ -37,7 +37,11 @@ Encoding:
     kind  R=0 W=1 A=2      sync  Us=0 Ws=1 Bs=2      rel  Self=0 Warp=1 Block=2 Global=3
     INIT = 0 (the all-zero shadow word), RACE_BLOCK = 30, RACE_GRID = 31.
 Infeasible labels (Bs with Global, Ws with Block/Global) are
-never produced by the label computation; their entries repeat the Us entry.
+never produced by hr__sync; their entries repeat the Us entry.  Sync index 3
+(both bits: "bc and wc both differ") repeats the Bs entry (Bs dominates Ws,
+SPEC.md:244), so a label computation may set the two bits independently
+(bit 1 "block epoch differs", bit 0 "warp epoch differs") and let the table
+resolve dominance and feasibility (hr__check_shared_row).
 Per-state flag byte: bit0 race, bit1 label-insensitive closure (the stored
 tid/clocks are dead: skip the write when the state is unchanged), bit2
 block-only closure (only the stored block id is live: skip the write when the
@@ -274,7 +278,8 @@ def build_table(machine: Optional[Machine] = None):
                     if c not in inv or kind == 3:
                         table[idx] = c
                         continue
-                    ss = s if (s < 3 and feasible(s, t)) else S_US
+                    ss = S_BS if s == 3 else s              # both bits set: Bs dominates Ws
+                    ss = ss if feasible(ss, t) else S_US
                     table[idx] = mc.next_code(c, kind, ss, t)
     flags = bytearray(N_CODES)
     for c in mc.codes():

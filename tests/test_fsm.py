@@ -92,6 +92,20 @@ def test_totality():
                     assert TABLE[(c << 6) | (m << 4) | (s << 2) | t] in MC.codes()
 
 
+def test_independent_sync_bits():
+    """hr__check_shared_row sets the two sync bits independently (bit 1: block
+    epoch differs, bit 0: warp epoch differs): index 3 must act as Bs (Bs
+    dominates Ws) and Ws with a Block relation as Us (a warp
+    clock says nothing across warps), so the table resolves the label."""
+    for c in MC.codes():
+        for m in range(3):
+            row = lambda s, t: TABLE[(c << 6) | (m << 4) | (s << 2) | t]
+            for t in range(3):
+                assert row(3, t) == row(2, t)
+            assert row(3, 3) == row(0, 3)
+            assert row(1, 2) == row(0, 2)
+
+
 def test_fig1_restriction_is_five_states():
     """Fig. 1: reads/writes, no barriers, relations
     Self/Global -> exactly INIT, READ, GREAD, WRITE, RACE, with unmentioned
