@@ -79,6 +79,7 @@ struct hr_dev {
                                           blocks % rep_bstride == 0 and warps % rep_wstride == 0
                                           are checked; 1 = all */
     uint32_t owned_only;          /* the replayed trace is HR_TRACE_F_SHARD_OWNED: no owner test */
+    uint32_t wc_lsh;              /* 32 - wc_bits (shifts the wc field to the top) */
     uint32_t tile_log2;           /* warp-level barriers order tiles of 2^tile_log2 lanes (5 = whole
                                      warps): the "Warp" relation is "same tile" (reading R8) */
     uint32_t epoch_tag;           /* HR_OPT_LAZY_RESET: kernel epoch tag 1..15 in bits [31:28] of the
@@ -716,6 +717,36 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
  *     (iii) — always non-Global here; (ii)'s insensitive states are GREAD,
  *     GATOMIC, RACE_GRID, which need another block and never occur.
  */
+/* The racy lanes of a shared row that arrive together share one ring
+ * reservation (warp-aggregated over __activemask); a full ring drops the
+ * record into the block's shared spill count (hr__ring_drop_x).  Out of line:
+ * the common path keeps no ring constants live. */
+static __device__ __noinline__ void hr__emit_shared_x(hr_race *ring, unsigned int *tail, uint32_t ring_cap,
+                                                      uint32_t kernel_id, uint32_t fsm_sa, uint32_t tid,
+                                                      uint32_t word, uint32_t ei)
+{
+    const unsigned m = __activemask();
+    const uint32_t lane = hr__laneid(), leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(tail, (unsigned)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+    if (slot < ring_cap) {
+        hr_race rr;
+        rr.word = word;
+        rr.block = tid >> 10;
+        rr.kernel = kernel_id;
+        rr.first_tid = tid;
+        rr.space = (uint8_t)HR_SHARED;
+        rr.scope = (uint8_t)((ei & 1u) ? HR_SCOPE_GRID : HR_SCOPE_BLOCK);
+        rr.first_kind = (uint8_t)((ei >> 24) & 3u);
+        rr.prev_state = (uint8_t)((ei >> 19) & 31u);
+        ring[slot] = rr;
+    } else {
+        hr__ring_drop_x(tail, false, kernel_id, fsm_sa + HR_FSM_DROP_OFF, 1u);
+    }
+}
+
 /* min(v, 1) as one VIMNMX (inline PTX: the compiler would otherwise turn it into a
  * compare and a select/add pair per term) */
 __device__ __forceinline__ uint32_t hr__min1(uint32_t v)
@@ -730,7 +761,7 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
     const uint32_t sa = t.sshadow + (word << 3);
     const uint32_t lo = (uint32_t)t.meta, tid_lo = (uint32_t)(t.meta >> HR_TID_SHIFT) & 1023u;
     const uint32_t kcol = t.fsm + (kind << 4);
-    const uint32_t wsh = 32u - d.wc_bits;
+    const uint32_t wsh = d.wc_lsh;                                        /* 32 - wc_bits */
     unsigned long long old = hr__ld_s(sa);
     uint32_t os = 0, cur = 0;
     bool racy = false;
@@ -761,25 +792,18 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
         HR_COUNT(d, 1);
         old = prev;
     }
-    /* a9: rare here, so no warp vote on the common path; the racy lanes that arrive
-     * together share one ring reservation (warp-aggregated over __activemask) */
-    if (racy) {
-        const unsigned m = __activemask();
-        const uint32_t lane = hr__laneid(), leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(d.ring_tail, (unsigned)__popc(m));
-        base = __shfl_sync(m, base, leader);
-        const uint32_t ei = HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u);
-        hr__write_race(d, t, base + __popc(m & ((1u << lane) - 1u)), 1u, word, ei);
-    }
+    /* a9: rare here, so no warp vote on the common path and the emit out of line */
+    if (racy)
+        hr__emit_shared_x(d.ring, d.ring_tail, d.ring_cap, d.kernel_id, t.fsm, t.tid(), word,
+                          HR_EI_EMIT | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u));
 }
 
 /* The test for hr__check_shared_row (warp-uniform result). */
 __device__ __forceinline__ bool hr__shared_row_ok(const hr_thr &t, uint32_t op, uint32_t space, uint64_t word)
 {
-    const unsigned long long prevw = __shfl_up_sync(0xffffffffu, (unsigned long long)word, 1);
+    const uint32_t w32 = (uint32_t)word, prevw = __shfl_up_sync(0xffffffffu, w32, 1);   /* word < swords < 2^32 */
     return __all_sync(0xffffffffu, op != 3u && space != 0u && word < t.swords && !(t.off & 3u) &&
-                                       (hr__laneid() == 0u || word > prevw));
+                                       (hr__laneid() == 0u || w32 > prevw));
 }
 
 /* ---------------- online instrumentation API ---------------- */
@@ -802,9 +826,13 @@ __device__ __forceinline__ hr_thr hr_thread_begin(const hr_dev &d, unsigned char
     uint32_t block = d.block_base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const uint32_t tid = (block << 10) | ((ltid >> 5) << 5) | (ltid & 31u);
     t.meta = ((unsigned long long)tid << HR_TID_SHIFT) | ((unsigned long long)d.epoch_tag << 28);
-    t.sshadow = (uint32_t)__cvta_generic_to_shared(smem_shadow);
+    /* the two shared-space bases pass through a SHFL, which ptxas does not
+     * rematerialise: they stay in registers instead of an S2R SR_CgaCtaId + LEA
+     * chain before every check (every thread of the block is here) */
+    const unsigned am = __activemask();
+    t.sshadow = __shfl_sync(am, (uint32_t)__cvta_generic_to_shared(smem_shadow), __ffs(am) - 1);
     t.swords = smem_words;
-    t.fsm = (uint32_t)__cvta_generic_to_shared(smem_fsm);
+    t.fsm = __shfl_sync(am, (uint32_t)__cvta_generic_to_shared(smem_fsm), __ffs(am) - 1);
     t.off = hr__thread_off(d, block, ltid >> 5);
     return t;
 }

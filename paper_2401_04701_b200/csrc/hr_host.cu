@@ -174,6 +174,7 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.shard_log2 = c->shard_log2;
     d.gran_log2 = c->gran_log2;
     d.wc_bits = c->cfg.wc_bits;
+    d.wc_lsh = 32u - c->cfg.wc_bits;
     d.bc_max = (1u << c->cfg.bc_bits) - 1u;
     d.wc_max = (1u << c->cfg.wc_bits) - 1u;
     d.options = c->cfg.options;
@@ -839,9 +840,18 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         if (timing) { c->ev_pool.push_back(e0); c->ev_pool.push_back(e1); }
     }
     if (!src.aligned_ok()) return fail(c, HR_E_ARG, "trace records must be 16-byte aligned (TMA staging)");
+    /* the wide row kernel stages 16-row C32 chunks: if that and the shadow do not
+     * fit one block's shared memory, the narrow row kernel (4-row chunks) runs */
+    if (kind == HR_K_ROW_WIDE &&
+        (size_t)hr_stage_offset(false, (uint32_t)warps, smem_u64(c, smem_words)) +
+                hr_stage_bytes((uint32_t)warps, hr_stage_cfg<true, false, SRC::ROW_BYTES>::NB,
+                               hr_stage_cfg<true, false, SRC::ROW_BYTES>::CH, SRC::ROW_BYTES) > 227 * 1024)
+        kind = HR_K_ROW;
     const bool wide = kind == HR_K_POOL_WIDE || kind == HR_K_ROW_WIDE;
     const uint32_t nb = wide ? hr_stage_cfg<true>::NB : hr_stage_cfg<false>::NB;
-    const uint32_t ch = wide ? hr_stage_cfg<true>::CH : hr_stage_cfg<false>::CH;
+    const uint32_t ch = kind == HR_K_ROW_WIDE ? hr_stage_cfg<true, false, SRC::ROW_BYTES>::CH
+                        : wide               ? hr_stage_cfg<true, true, SRC::ROW_BYTES>::CH
+                                             : hr_stage_cfg<false>::CH;
     /* long-tailed grids (wide pooled kernel): split each simulated warp over up
      * to 4 CUDA warps of the block (hr_replay_kernel); HR_SPLIT_LOG2 overrides */
     uint32_t split = 0;

@@ -238,9 +238,11 @@ __device__ __forceinline__ bool hr__pool_owned(const hr_dev &d, const hr_thr &t,
 #ifndef HR_STAGE_NB_ROW
 #define HR_STAGE_NB_ROW 2u
 #endif
-template <bool WIDE> struct hr_stage_cfg {
+template <bool WIDE, bool POOL = false, uint32_t ROW_BYTES = 256u> struct hr_stage_cfg {
     static constexpr uint32_t NB = WIDE ? HR_STAGE_NB_WIDE : HR_STAGE_NB_ROW;
-    static constexpr uint32_t CH = WIDE ? 8u : 4u;
+    /* the 64-register row kernel on C32 rows (160 B): 16-row chunks, which halve the
+     * per-chunk refill work of the issue-bound shared-shadow traces (C3) */
+    static constexpr uint32_t CH = WIDE ? ((!POOL && ROW_BYTES == 160u) ? 16u : 8u) : 4u;
 };
 
 /* Dynamic shared memory of a replay launch: FSM table, warp pools, the shared
@@ -303,7 +305,8 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     const uint32_t cta = blockIdx.x;
 #endif
 
-    constexpr uint32_t NB = hr_stage_cfg<WIDE>::NB, CH = hr_stage_cfg<WIDE>::CH;
+    constexpr uint32_t NB = hr_stage_cfg<WIDE, POOL, SRC::ROW_BYTES>::NB;
+    constexpr uint32_t CH = hr_stage_cfg<WIDE, POOL, SRC::ROW_BYTES>::CH;
     constexpr uint32_t CHB = CH * SRC::ROW_BYTES;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t hw = threadIdx.x >> 5;                            /* CUDA warp */
@@ -389,21 +392,26 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
         if (!POOL && !ABL && SRC::C32) {
             /* C32 rows read undecoded: barrier test, then the shared-row fast path
              * (hr__check_shared_row) on the raw (word, op | space << 2) pair */
-            for (uint32_t j = 0; j < rows; j++) {
-                uint32_t w32 = 0u, ob = 3u;
-                if (active) SRC::sld2(buf, j, lane, CH, w32, ob);
+            /* the shared-row word limit: 0 while this lane is off (t.off changes only at barriers) */
+            uint32_t swl = (t.off & 3u) ? 0u : t.swords;
+            uint32_t pw = buf + lane * 4u, pb = buf + CH * 128u + lane;       /* this lane's word / op byte */
+            for (uint32_t j = 0; j < rows; j++, pw += 128u, pb += 32u) {
+                uint32_t w32, ob;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w32) : "r"(pw) : "memory");
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(ob) : "r"(pb) : "memory");
+                if (!active) { w32 = 0u; ob = 3u; }                        /* lanes beyond the grid: NOP */
                 const bool ctl = (ob & 3u) == 3u;
                 /* one vote classifies a shared row: every lane a shared-space access
                  * (op | space << 2 in 4..6) to strictly increasing in-range words */
                 const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
-                if (__all_sync(0xffffffffu, (ob & 7u) - 4u < 3u && w32 < t.swords && !(t.off & 3u) &&
-                                                (lane == 0u || w32 > wprev))) {
+                if (__all_sync(0xffffffffu, (ob & 7u) - 4u < 3u && w32 < swl && (lane == 0u || w32 > wprev))) {
                     hr__check_shared_row(d, t, w32, ob & 3u);
                     continue;
                 }
                 if (__any_sync(0xffffffffu, ctl && w32 != 0u)) {
                     hr__barrier_row(d, t, ((uint64_t)(ob & 3u) << 62) | ((uint64_t)((ob >> 2) & 1u) << 61) | w32,
                                     lane_mask);
+                    swl = (t.off & 3u) ? 0u : t.swords;
                     continue;
                 }
                 hr_check_lanes<false, ABL>(d, t, 0xffffffffu, !ctl, (ob >> 2) & 1u, w32, ob & 3u);
