@@ -43,6 +43,9 @@
  * ring dropped (a9 overflow; hr_thread_end spills the instance when non-zero) */
 #define HR_FSM_DROP_OFF (HR_FSM_BYTES + 32)
 #define HR_FSM_SMEM_BYTES (HR_FSM_BYTES + 48)
+/* a NOP C32 record in the global table copy (word 0 at +0, op byte 3 at +4):
+ * the row loop points lanes beyond the grid at it instead of testing them */
+#define HR_FSM_NOP_OFF (HR_FSM_BYTES + 40)
 #define HR_STATE_SHIFT 59
 #define HR_TID_SHIFT 32
 #define HR_RACE_BLOCK 30u
@@ -713,9 +716,10 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
  *     bc > oBC (an INIT word ignores relation and sync, any value indexes
  *     the same table row);
  *   - no epoch tag (the instance is zeroed at block start), no probe;
- *   - a7: the unchanged word (i), and RACE_BLOCK under a non-Global relation
- *     (iii) — always non-Global here; (ii)'s insensitive states are GREAD,
- *     GATOMIC, RACE_GRID, which need another block and never occur.
+ *   - a7: RACE_BLOCK under a non-Global relation (iii) — always non-Global
+ *     here; (ii)'s insensitive states are GREAD, GATOMIC, RACE_GRID, which
+ *     need another block and never occur; the unchanged word (i) goes to the
+ *     CAS, which rewrites the same value.
  */
 /* The racy lanes of a shared row that arrive together share one ring
  * reservation (warp-aggregated over __activemask); a full ring drops the
@@ -782,7 +786,10 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
                              hr__min1(x) + hr__min1(x >> d.tile_log2);        /* + rel: Self / Warp / Block */
         cur = hr__lds_u8(kcol + idx);
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
-        if (nw == old || (cur == os && os == HR_RACE_BLOCK)) { HR_COUNT(d, 2); break; }   /* a7 (i), (iii) */
+        /* a7 (iii) only: a RACE word stays RACE (the stored tid is diagnostic).  (i), the
+         * unchanged word, is left to the CAS, which then writes the same value: in a
+         * shared row the clocks or the tid nearly always differ (C3: never equal) */
+        if (cur == os && os >= HR_RACE_BLOCK) { HR_COUNT(d, 2); break; }
         const unsigned long long prev = hr__cas_s(sa, old, nw);
         if (prev == old) {                                                /* a8 committed */
             HR_COUNT(d, 3);

@@ -231,6 +231,7 @@ extern "C" hr_status hr_init(const hr_config *cfg, hr_ctx **out)
         }
         unsigned char host[HR_FSM_SMEM_BYTES];
         memset(host, 0, sizeof host);                /* the block scratch (HR_FSM_DROP_OFF) starts at 0 */
+        host[HR_FSM_NOP_OFF + 4] = 3;                /* the NOP C32 record: word 0, op byte 3 */
         memcpy(host, hr_fsm_table_init, HR_FSM_BYTES);
         memcpy(host + HR_FSM_BYTES, hr_fsm_flags_init, 32);
         if (cudaMemcpy(c->fsm, host, HR_FSM_SMEM_BYTES, cudaMemcpyHostToDevice) != cudaSuccess ||

@@ -394,17 +394,23 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
              * (hr__check_shared_row) on the raw (word, op | space << 2) pair */
             /* the shared-row word limit: 0 while this lane is off (t.off changes only at barriers) */
             uint32_t swl = (t.off & 3u) ? 0u : t.swords;
-            uint32_t pw = buf + lane * 4u, pb = buf + CH * 128u + lane;       /* this lane's word / op byte */
-            for (uint32_t j = 0; j < rows; j++, pw += 128u, pb += 32u) {
+            /* this lane's word / op byte; lanes beyond the grid read the NOP record of
+             * the table copy (HR_FSM_NOP_OFF) on every row */
+            uint32_t pw = active ? buf + lane * 4u : t.fsm + HR_FSM_NOP_OFF;
+            uint32_t pb = active ? buf + CH * 128u + lane : t.fsm + HR_FSM_NOP_OFF + 4u;
+            const uint32_t dw = active ? 128u : 0u, db = active ? 32u : 0u;
+            const uint32_t l0 = lane == 0u ? 1u : 0u;
+            for (uint32_t j = 0; j < rows; j++, pw += dw, pb += db) {
                 uint32_t w32, ob;
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w32) : "r"(pw) : "memory");
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(ob) : "r"(pb) : "memory");
-                if (!active) { w32 = 0u; ob = 3u; }                        /* lanes beyond the grid: NOP */
                 const bool ctl = (ob & 3u) == 3u;
                 /* one vote classifies a shared row: every lane a shared-space access
-                 * (op | space << 2 in 4..6) to strictly increasing in-range words */
+                 * (op | space << 2 in 4..6; a byte with other bits set takes the general
+                 * path, which masks them) to strictly increasing in-range words (lane 0
+                 * compares with itself: + 1) */
                 const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
-                if (__all_sync(0xffffffffu, (ob & 7u) - 4u < 3u && w32 < swl && (lane == 0u || w32 > wprev))) {
+                if (__all_sync(0xffffffffu, (ob - 4u < 3u) & (w32 < swl) & (w32 + l0 > wprev))) {
                     hr__check_shared_row(d, t, w32, ob & 3u);
                     continue;
                 }
