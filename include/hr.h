@@ -365,11 +365,14 @@ hr_status hr_report(hr_ctx *ctx, hr_race *out, size_t cap, size_t *n_out, uint32
 
 /* hr_report without a host round trip (a13 on the device, "report races
  * on unique memory addresses"): enqueue on `stream` (NULL = the ctx's last
- * stream) a sort of the whole ring at its capacity, the merge of equal
- * addresses (widest scope) and the write of the result into pinned host
- * memory owned by the ctx.  Returns at once; nothing waits for the GPU, so a
- * caller can enqueue the next kernel's checks behind it.  Each call replaces
- * the previous result.  Cost: two radix sorts of ring_capacity keys. */
+ * stream) the sort of the ring's records, the merge of equal addresses
+ * (widest scope) and the write of the result into pinned host memory owned by
+ * the ctx.  Returns at once; nothing waits for the GPU, so a caller can
+ * enqueue the next kernel's checks behind it.  Each call replaces the previous
+ * result.  Runs as one CUDA graph whose first kernel reads the record count on
+ * the device: up to 8192 records are sorted and merged by that one CTA in
+ * shared memory; more take the graph's conditional branch, two radix sorts of
+ * ring_capacity keys (the host never learns the count). */
 hr_status hr_report_async(hr_ctx *ctx, void *stream);
 
 /* The same device-side report into caller-owned DEVICE memory, for a
@@ -425,8 +428,11 @@ hr_status hr_replay_timing(hr_ctx *ctx, double *reset_ms, uint64_t *n_resets, do
 /* Number of device kernels this ctx launched since the last call (every
  * __global__ launch of libhirace, including the kernels of its CUB scans (2)
  * and radix sorts (2 + one onesweep pass per 8 key bits: 10 for the 64-bit
- * sorts of hr_report; hr_report_async sorts only the key bits that can be set)),
- * then clear it.  Host only, no CUDA call; lets a harness state how many
+ * sorts of hr_report)), then clear it.  hr_report_async runs as one CUDA graph:
+ * its small-set kernel always, the full-capacity sort path (keys, 2 sorts over
+ * the key bits that can be set, heads, scan, emit) only when the ring held more
+ * than 8192 records — that path counts its own kernels on the device, so this
+ * call synchronises the device to read them.  Lets a harness state how many
  * kernels ran inside a timed region. */
 hr_status hr_launch_count(hr_ctx *ctx, uint64_t *n_launches);
 

@@ -95,6 +95,15 @@ struct hr_ctx {
     uint32_t *arep_hdr_host = nullptr, *arep_hdr_dev = nullptr;
     cudaEvent_t arep_ev = nullptr;
     bool arep_pending = false;
+    /* the report as one CUDA graph: the one-CTA small-set kernel, then an IF node
+     * (set by that kernel) around the full-capacity CUB path; rebuilt when its
+     * arguments change.  arep_big: kernels the IF body launched (hr_launch_count). */
+    cudaGraph_t arep_graph = nullptr;
+    cudaGraphExec_t arep_exec = nullptr;
+    cudaStream_t arep_cap = nullptr;              /* capture stream of the IF body */
+    unsigned long long *arep_big = nullptr;
+    struct { const void *out, *hdr, *scratch, *ring; uint32_t out_cap, cap; int lo_bits, hi_bits; } arep_key = {};
+    bool arep_no_graph = false;                   /* graph build failed once: direct launches */
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
     char err[512] = {0};
@@ -1648,6 +1657,112 @@ __global__ void hr_arep_emit_kernel(const hr_race *__restrict__ r, const unsigne
     out[pos[p]] = x;
 }
 
+/* The small-set report in one CTA: when the ring holds at most HR_AREP_SMALL
+ * records, sort their (hi, lo, ring index) keys — the order of the two stable
+ * CUB sorts — with a bitonic network in shared memory, flag the run heads,
+ * scan them and emit each run's merged record, as the kernels above do.  A
+ * larger ring sets the graph's conditional so that the CUB path (the IF body)
+ * runs instead; the host never learns the count.  Cost: one launch, O(n log^2 n)
+ * shared-memory work, instead of sorting the whole ring capacity every report. */
+#define HR_AREP_SMALL 8192u
+#define HR_AREP_SMALL_THREADS 1024u
+static constexpr size_t HR_AREP_SMALL_SMEM = (size_t)HR_AREP_SMALL * 20u;
+
+__global__ void __launch_bounds__(HR_AREP_SMALL_THREADS)
+    hr_arep_small_kernel(const hr_race *__restrict__ r, const unsigned int *__restrict__ tail, uint32_t cap,
+                         hr_race *out, uint32_t out_cap, uint32_t *hdr, cudaGraphConditionalHandle big,
+                         unsigned long long *big_launches, uint32_t body_launches)
+{
+    extern __shared__ __align__(16) unsigned char hr_smem[];
+    uint64_t *khi = reinterpret_cast<uint64_t *>(hr_smem), *klo = khi + HR_AREP_SMALL;
+    uint32_t *kix = reinterpret_cast<uint32_t *>(klo + HR_AREP_SMALL);
+    __shared__ uint32_t wsum[HR_AREP_SMALL_THREADS / 32u];
+    const uint32_t n = min(*tail, cap);
+    if (n > HR_AREP_SMALL) {
+        if (threadIdx.x == 0) {
+            cudaGraphSetConditional(big, 1u);
+            atomicAdd(big_launches, (unsigned long long)body_launches);
+        }
+        return;
+    }
+    uint32_t np = 1;
+    while (np < n) np <<= 1;
+    for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+        if (i < n) {
+            const hr_race &x = r[i];
+            khi[i] = ((uint64_t)x.kernel << 33) | ((uint64_t)x.space << 32) | (uint64_t)x.block;
+            klo[i] = x.word;
+        } else {
+            khi[i] = klo[i] = ~0ull;                  /* padding: after every record */
+        }
+        kix[i] = i;
+    }
+    __syncthreads();
+    /* bitonic network over np keys; pair q of a stage compares i and i + j */
+    for (uint32_t k = 2; k <= np; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t q = threadIdx.x; q < np / 2u; q += blockDim.x) {
+                const uint32_t i = (q / j) * 2u * j + (q % j), l = i + j;
+                const uint64_t ah = khi[i], bh = khi[l], al = klo[i], bl = klo[l];
+                const uint32_t ai = kix[i], bi = kix[l];
+                const bool gt = ah > bh || (ah == bh && (al > bl || (al == bl && ai > bi)));
+                if (gt == ((i & k) == 0u)) {
+                    khi[i] = bh; khi[l] = ah;
+                    klo[i] = bl; klo[l] = al;
+                    kix[i] = bi; kix[l] = ai;
+                }
+            }
+            __syncthreads();
+        }
+    /* run heads over contiguous chunks, a block-wide exclusive scan of their counts */
+    const uint32_t ch = (n + blockDim.x - 1u) / blockDim.x;
+    const uint32_t p0 = min(n, threadIdx.x * ch), p1 = min(n, p0 + ch);
+    uint32_t heads = 0;
+    for (uint32_t p = p0; p < p1; p++) heads += (p == 0u || !hr__same_addr(r[kix[p]], r[kix[p - 1]])) ? 1u : 0u;
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    uint32_t inc = heads;
+#pragma unroll
+    for (uint32_t o = 1; o < 32u; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31u) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < blockDim.x / 32u ? wsum[lane] : 0u;
+#pragma unroll
+        for (uint32_t o = 1; o < 32u; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += v;
+        }
+        wsum[lane] = s;                               /* inclusive warp prefix */
+    }
+    __syncthreads();
+    uint32_t pos = inc - heads + (w ? wsum[w - 1] : 0u);
+    if (threadIdx.x == 0) {
+        hdr[0] = wsum[blockDim.x / 32u - 1u];
+        hdr[1] = tail[1];
+        hdr[2] = *tail;
+        hdr[3] = tail[2] | tail[3];
+    }
+    for (uint32_t p = p0; p < p1; p++) {
+        if (p != 0u && hr__same_addr(r[kix[p]], r[kix[p - 1]])) continue;
+        if (pos < out_cap) {
+            hr_race x = r[kix[p]];
+            for (uint32_t q = p + 1; q < n && hr__same_addr(r[kix[q]], x); q++) {
+                const hr_race &y = r[kix[q]];
+                if (y.scope > x.scope) {
+                    const uint8_t sc = y.scope;
+                    if (x.first_kind == 0xff) x = y;
+                    x.scope = sc;
+                }
+            }
+            out[pos] = x;
+        }
+        pos++;
+    }
+}
+
 static hr_status report_async(hr_ctx *c, cudaStream_t s, hr_race *out, uint32_t out_cap, uint32_t *hdr);
 
 extern "C" hr_status hr_report_async(hr_ctx *c, void *stream)
@@ -1676,6 +1791,114 @@ extern "C" hr_status hr_report_async_to(hr_ctx *c, void *stream, hr_race *out, u
     if (!c || !hdr || (out_cap && !out)) return fail(c, HR_E_ARG, "hr_report_async_to: bad arguments");
     CU(cudaSetDevice(c->device));
     return report_async(c, stream ? (cudaStream_t)stream : c->stream, out, out_cap, hdr);
+}
+
+/* arguments of the full-capacity report path (scratch carved by report_async) */
+struct arep_args {
+    uint64_t *lo0, *lo1, *hi0, *hi1;
+    uint32_t *ix0, *ix1, *head, *pos;
+    void *tmp;
+    hr_race *out;
+    uint32_t out_cap;
+    uint32_t *hdr;
+    int lo_bits, hi_bits;
+};
+
+static uint32_t arep_body_launches(const arep_args &a)
+{
+    /* keys, sort (onesweep: histogram + scan + one pass per 8 bits), hi keys, sort,
+     * heads, scan (2), emit */
+    return 1u + (2u + (a.lo_bits + 7) / 8) + 1u + (2u + (a.hi_bits + 7) / 8) + 1u + 2u + 1u;
+}
+
+/* The full-capacity path: sort the whole ring (entries past the tail as the
+ * largest keys), flag and scan the run heads, emit. */
+static hr_status arep_enqueue_sort(hr_ctx *c, cudaStream_t s, const arep_args &a)
+{
+    const uint32_t cap = c->cfg.ring_capacity;
+    const unsigned g = (cap + 255) / 256;
+    size_t tb = c->arep_tmp_bytes;
+    hr_arep_keys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, cap, a.lo0, a.ix0);
+    CU(cudaGetLastError());
+    CU(cub::DeviceRadixSort::SortPairs(a.tmp, tb, a.lo0, a.lo1, a.ix0, a.ix1, (int)cap, 0, a.lo_bits, s));
+    hr_arep_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, a.ix1, cap, a.hi0);
+    CU(cudaGetLastError());
+    tb = c->arep_tmp_bytes;
+    CU(cub::DeviceRadixSort::SortPairs(a.tmp, tb, a.hi0, a.hi1, a.ix1, a.ix0, (int)cap, 0, a.hi_bits, s));
+    hr_arep_heads_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, a.ix0, cap, a.head);
+    CU(cudaGetLastError());
+    tb = c->arep_tmp_bytes;
+    CU(cub::DeviceScan::ExclusiveSum(a.tmp, tb, a.head, a.pos, (int)cap, s));
+    hr_arep_emit_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, a.ix0, a.head, a.pos, cap, a.out, a.out_cap, a.hdr);
+    CU(cudaGetLastError());
+    return HR_OK;
+}
+
+/* (Re)build the report graph for these arguments: a kernel node (the small-set
+ * kernel, which sets the IF condition when the ring holds more than
+ * HR_AREP_SMALL records) followed by a conditional IF node whose body is the
+ * full-capacity path, captured from arep_enqueue_sort. */
+static hr_status arep_graph_build(hr_ctx *c, const arep_args &a)
+{
+    const uint32_t cap = c->cfg.ring_capacity;
+    if (c->arep_exec && c->arep_key.out == a.out && c->arep_key.hdr == a.hdr &&
+        c->arep_key.scratch == c->arep_scratch && c->arep_key.ring == c->ring && c->arep_key.out_cap == a.out_cap &&
+        c->arep_key.cap == cap &&
+        c->arep_key.lo_bits == a.lo_bits && c->arep_key.hi_bits == a.hi_bits)
+        return HR_OK;
+    if (c->arep_exec) { cudaGraphExecDestroy(c->arep_exec); c->arep_exec = nullptr; }
+    if (c->arep_graph) { cudaGraphDestroy(c->arep_graph); c->arep_graph = nullptr; }
+    if (!c->arep_cap) CU(cudaStreamCreateWithFlags(&c->arep_cap, cudaStreamNonBlocking));
+    if (!c->arep_big) {
+        CU(cudaMalloc(&c->arep_big, sizeof(unsigned long long)));
+        CU(cudaMemset(c->arep_big, 0, sizeof(unsigned long long)));
+    }
+    CU(cudaFuncSetAttribute(hr_arep_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)HR_AREP_SMALL_SMEM));
+    cudaGraph_t g = nullptr;
+    CU(cudaGraphCreate(&g, 0));
+    c->arep_graph = g;
+    cudaGraphConditionalHandle big;
+    CU(cudaGraphConditionalHandleCreate(&big, g, 0u, cudaGraphCondAssignDefault));
+    const hr_race *ring = c->ring;
+    const unsigned int *tail = c->tail;
+    hr_race *out = a.out;
+    uint32_t out_cap = a.out_cap, capv = cap, body = arep_body_launches(a);
+    uint32_t *hdr = a.hdr;
+    unsigned long long *bigc = c->arep_big;
+    void *kargs[] = {(void *)&ring, (void *)&tail, (void *)&capv, (void *)&out, (void *)&out_cap,
+                     (void *)&hdr, (void *)&big, (void *)&bigc, (void *)&body};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void *)hr_arep_small_kernel;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(HR_AREP_SMALL_THREADS);
+    kp.sharedMemBytes = (unsigned)HR_AREP_SMALL_SMEM;
+    kp.kernelParams = kargs;
+    cudaGraphNode_t kn = nullptr, cn = nullptr;
+    CU(cudaGraphAddKernelNode(&kn, g, nullptr, 0, &kp));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = big;
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    CU(cudaGraphAddNode(&cn, g, &kn, 1, &np));
+    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+    CU(cudaStreamBeginCaptureToGraph(c->arep_cap, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const hr_status st = arep_enqueue_sort(c, c->arep_cap, a);
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->arep_cap, &captured);
+    if (st) return st;
+    CU(ec);
+    CU(cudaGraphInstantiate(&c->arep_exec, g, 0));
+    c->arep_key.out = a.out;
+    c->arep_key.hdr = a.hdr;
+    c->arep_key.scratch = c->arep_scratch;
+    c->arep_key.ring = c->ring;
+    c->arep_key.out_cap = a.out_cap;
+    c->arep_key.cap = cap;
+    c->arep_key.lo_bits = a.lo_bits;
+    c->arep_key.hi_bits = a.hi_bits;
+    return HR_OK;
 }
 
 /* a13 on the device (hr_report_async / hr_report_async_to): enqueue on `s` the
@@ -1712,11 +1935,6 @@ static hr_status report_async(hr_ctx *c, cudaStream_t s, hr_race *out, uint32_t 
     uint32_t *ix0 = (uint32_t *)(b + off[4]), *ix1 = (uint32_t *)(b + off[5]);
     uint32_t *head = (uint32_t *)(b + off[6]), *pos = (uint32_t *)(b + off[7]);
     void *tmp = b + off[8];
-    const unsigned g = (cap + 255) / 256;
-    size_t tb = c->arep_tmp_bytes;
-    c->launches++;
-    hr_arep_keys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, cap, lo0, ix0);
-    CU(cudaGetLastError());
     /* only the key bits that can be set: words < max(global end, shared words),
      * hi = kernel << 33 | space << 32 | block with kernel <= last_kernel; the
      * padding keys (~0) stay the largest within the range, and the sorts are
@@ -1725,24 +1943,20 @@ static hr_status report_async(hr_ctx *c, cudaStream_t s, hr_race *out, uint32_t 
     int lo_bits = std::max(1, std::min(64, bits_of(std::max<uint64_t>(c->gbase + c->gwords, c->smem_words_max))));
     int hi_bits = std::min(64, 33 + bits_of((uint64_t)std::max(c->max_kernel, c->last_kernel) + 1));
     if (c->online_used) lo_bits = hi_bits = 64;  /* online kernels: caller-chosen ids and instance sizes */
-    c->launches += 2 + (lo_bits + 7) / 8;        /* onesweep: histogram + scan + one pass per 8 bits */
-    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, lo0, lo1, ix0, ix1, (int)cap, 0, lo_bits, s));
-    c->launches++;
-    hr_arep_hikeys_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix1, cap, hi0);
-    CU(cudaGetLastError());
-    tb = c->arep_tmp_bytes;
-    c->launches += 2 + (hi_bits + 7) / 8;
-    CU(cub::DeviceRadixSort::SortPairs(tmp, tb, hi0, hi1, ix1, ix0, (int)cap, 0, hi_bits, s));
-    c->launches++;
-    hr_arep_heads_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, cap, head);
-    CU(cudaGetLastError());
-    tb = c->arep_tmp_bytes;
-    c->launches += 2;
-    CU(cub::DeviceScan::ExclusiveSum(tmp, tb, head, pos, (int)cap, s));
-    c->launches++;
-    hr_arep_emit_kernel<<<g, 256, 0, s>>>(c->ring, c->tail, ix0, head, pos, cap, out, out_cap, hdr);
-    CU(cudaGetLastError());
-    return HR_OK;
+    const arep_args a = {lo0, lo1, hi0, hi1, ix0, ix1, head, pos, tmp, out, out_cap, hdr, lo_bits, hi_bits};
+    if (!c->arep_no_graph) {
+        const hr_status st = arep_graph_build(c, a);
+        if (st == HR_OK) {
+            c->launches++;                             /* the small-set kernel; the IF body counts itself */
+            CU(cudaGraphLaunch(c->arep_exec, s));
+            return HR_OK;
+        }
+        if (st != HR_E_CUDA) return st;
+        cudaGetLastError();
+        c->arep_no_graph = true;                   /* e.g. a driver without conditional nodes */
+    }
+    c->launches += arep_body_launches(a);
+    return arep_enqueue_sort(c, s, a);
 }
 
 extern "C" hr_status hr_report_collect(hr_ctx *c, hr_race *out, size_t cap, size_t *n_out, uint32_t *flags_out)
@@ -1984,7 +2198,14 @@ extern "C" hr_status hr_replay_timing(hr_ctx *c, double *reset_ms, uint64_t *n_r
 extern "C" hr_status hr_launch_count(hr_ctx *c, uint64_t *n)
 {
     if (!c || !n) return HR_E_ARG;
-    *n = c->launches;
+    uint64_t big = 0;
+    if (c->arep_big) {                          /* kernels the report graph's IF body ran */
+        CU(cudaSetDevice(c->device));
+        CU(cudaDeviceSynchronize());
+        CU(cudaMemcpy(&big, c->arep_big, sizeof big, cudaMemcpyDeviceToHost));
+        CU(cudaMemset(c->arep_big, 0, sizeof big));
+    }
+    *n = c->launches + big;
     c->launches = 0;
     return HR_OK;
 }
@@ -2032,6 +2253,10 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->arep_hdr_host) cudaFreeHost(c->arep_hdr_host);
     if (c->arep_scratch) cudaFree(c->arep_scratch);
     if (c->arep_ev) cudaEventDestroy(c->arep_ev);
+    if (c->arep_exec) cudaGraphExecDestroy(c->arep_exec);
+    if (c->arep_graph) cudaGraphDestroy(c->arep_graph);
+    if (c->arep_cap) cudaStreamDestroy(c->arep_cap);
+    if (c->arep_big) cudaFree(c->arep_big);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (auto &pr : c->ev_kernel) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

@@ -277,7 +277,10 @@ __host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint
 #ifndef HR_ROW_NARROW_REGS
 #define HR_ROW_NARROW_REGS 48
 #endif
-#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : ((POOL) ? 32 : HR_ROW_NARROW_REGS))
+#ifndef HR_POOL_NARROW_REGS
+#define HR_POOL_NARROW_REGS 32
+#endif
+#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : ((POOL) ? HR_POOL_NARROW_REGS : HR_ROW_NARROW_REGS))
 #endif
 template <bool POOL, bool WIDE, bool ABL, typename SRC>
 __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
@@ -388,6 +391,32 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
                 for (uint32_t j = 0; j < CH; j++) insert(vs[j], xs[j]);
                 j0 = rows;
             }
+        }
+        if (POOL && !WIDE && !ABL && SRC::C32 && split_log2 == 0u && (d.shard_log2 == 0u || d.owned_only)) {
+            /* C32 rows into the pool, nothing to filter but the thread's enables (no
+             * helper split, no owner hash: the trace is this shard's alone): the raw
+             * (word, op | space << 2) pair of each lane, one barrier vote, one insert.
+             * Lanes beyond the grid read the NOP record of the table copy. */
+            uint32_t pw = active ? buf + lane * 4u : t.fsm + HR_FSM_NOP_OFF;
+            uint32_t pb = active ? buf + CH * 128u + lane : t.fsm + HR_FSM_NOP_OFF + 4u;
+            const uint32_t dw = active ? 128u : 0u, db = active ? 32u : 0u;
+            /* bit s: accesses of space s are checked (t.off changes only at barriers) */
+            uint32_t en = (t.off & 1u) ? 0u : ((t.off & 2u) ? 1u : 3u);
+            for (uint32_t j = 0; j < rows; j++, pw += dw, pb += db) {
+                uint32_t w32, ob;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w32) : "r"(pw) : "memory");
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(ob) : "r"(pb) : "memory");
+                const bool ctl = (ob & 3u) == 3u;
+                const uint64_t x = ((uint64_t)(ob & 3u) << 62) | ((uint64_t)((ob >> 2) & 1u) << 61) | w32;
+                if (__any_sync(0xffffffffu, ctl && w32 != 0u)) {
+                    if (cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); cnt = 0; __syncwarp(); }
+                    hr__barrier_row(d, t, x, lane_mask);
+                    en = (t.off & 1u) ? 0u : ((t.off & 2u) ? 1u : 3u);
+                    continue;
+                }
+                insert(!ctl && ((en >> ((ob >> 2) & 1u)) & 1u), x);
+            }
+            j0 = rows;
         }
         if (!POOL && !ABL && SRC::C32) {
             /* C32 rows read undecoded: barrier test, then the shared-row fast path

@@ -566,6 +566,65 @@ def test_report_async_c5_planted_repeated():
     assert [(int(r["word"]), int(r["scope"])) for r in raw] == c5.planted(lb)
 
 
+@pytest.mark.parametrize("lb", [10, 12, 15])
+def test_report_async_graph_paths(lb):
+    """hr_report_async is one CUDA graph: up to 8192 ring records take the
+    one-CTA small-set kernel, more take the conditional full-capacity sort (C5
+    at 2^lb blocks plants 2^lb racy words, with one or two ring records each:
+    2^12 fit the small path, 2^15 do not).  Both equal the
+    synchronous report byte for byte and the planted set (closed form); the
+    launch count shows which path ran."""
+    from tracegen import c5
+    h = hr()
+    rec, woff, kd = c5.gpu_trace(lb)
+    dt = h.DeviceTrace(rec, woff, kd)
+    ck = h.Checker(c5.total_words(lb), 0, ring_capacity=1 << 16, options=h.HR_OPT_LAZY_RESET)
+    launches = []
+    for _ in range(2):
+        ck.reset(); ck.replay(dt)
+        h.hr_launch_count(ck.ctx)
+        ck.report_async()
+        a_raw, a_fl = ck.collect_raw()
+        launches.append(h.hr_launch_count(ck.ctx))
+    s_raw, s_fl = ck.report_raw()
+    ck.close()
+    assert a_raw.tobytes() == s_raw.tobytes() and a_fl == s_fl == 0
+    assert [(int(r["word"]), int(r["scope"])) for r in a_raw] == c5.planted(lb)
+    # spill scan + small-set kernel; the IF body adds its keys / sort / heads / scan / emit kernels
+    assert launches[0] == launches[1]
+    assert (launches[0] == 2) == (lb <= 12), launches
+
+
+def test_report_async_small_out_cap_and_runs():
+    """Small-set path with several records per address (scope upgrades across
+    kernels of one ctx are separate addresses; within a kernel RACE_BLOCK then
+    RACE_GRID records merge to the widest scope) and an hr_report_async_to
+    buffer smaller than the set: hdr[0] is the full count, the first out_cap
+    records are the sorted prefix."""
+    import torch
+    h = hr()
+    tr = _random_batch(77, 60, max_blocks=6, max_warps=8, max_lanes=32, max_slots=12, n_words=24,
+                       spaces=(0, 1), p_barrier=0.2, p_skip=0.3)
+    want = oracle_set(tr)[0]
+    assert len(want) > 8
+    gmax, smem = h.trace_extent(tr)
+    ck = h.Checker(gmax, smem)
+    dt = h.DeviceTrace.from_trace(tr)
+    ck.reset(); ck.replay(dt); ck.report_async()
+    a_raw, _ = ck.collect_raw()
+    assert [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"]))
+            for r in a_raw] == want
+    cap = 5
+    out = torch.zeros(cap * 24, dtype=torch.uint8, device="cuda")
+    hdr = torch.zeros(4, dtype=torch.int32, device="cuda")
+    h.hr_report_async_to(ck.ctx, out.data_ptr(), cap, hdr.data_ptr())
+    torch.cuda.synchronize()
+    got = np.frombuffer(out.cpu().numpy().tobytes(), dtype=a_raw.dtype)
+    assert int(hdr[0]) == len(want)
+    assert got.tobytes() == a_raw[:cap].tobytes()
+    ck.close()
+
+
 # ---- HR_OPT_BSERIAL: block-serial pooled replay (hr_bserial.cuh) ----
 BS = 16384 | 32                                      # forced, with the pooled kernel choice
 
