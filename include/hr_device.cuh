@@ -760,12 +760,14 @@ __device__ __forceinline__ uint32_t hr__min1(uint32_t v)
     return r;
 }
 
-__device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind)
+/* (wcb, wsh, tl) = d.wc_bits, d.wc_lsh, d.tile_log2, passed in so that a row loop
+ * can keep them in registers instead of reloading them per row */
+__device__ __forceinline__ void hr__check_shared_row_k(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind,
+                                                       uint32_t wcb, uint32_t wsh, uint32_t tl)
 {
     const uint32_t sa = t.sshadow + (word << 3);
     const uint32_t lo = (uint32_t)t.meta, tid_lo = (uint32_t)(t.meta >> HR_TID_SHIFT) & 1023u;
     const uint32_t kcol = t.fsm + (kind << 4);
-    const uint32_t wsh = d.wc_lsh;                                        /* 32 - wc_bits */
     unsigned long long old = hr__ld_s(sa);
     uint32_t os = 0, cur = 0;
     bool racy = false;
@@ -782,8 +784,8 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
          * relation to Us (fsm/generate.py), and an INIT word ignores the label.
          * Each 0/1 term as a min (one VIMNMX) so the index folds into LEA/IADD3. */
         const uint32_t dlo = (uint32_t)old ^ lo;
-        const uint32_t idx = (os << 6) + (hr__min1(dlo >> d.wc_bits) << 3) + (hr__min1(dlo << wsh) << 2) +
-                             hr__min1(x) + hr__min1(x >> d.tile_log2);        /* + rel: Self / Warp / Block */
+        const uint32_t idx = (os << 6) + (hr__min1(dlo >> wcb) << 3) + (hr__min1(dlo << wsh) << 2) +
+                             hr__min1(x) + hr__min1(x >> tl);                 /* + rel: Self / Warp / Block */
         cur = hr__lds_u8(kcol + idx);
         const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
         /* a7 (iii) only: a RACE word stays RACE (the stored tid is diagnostic).  (i), the
@@ -803,6 +805,11 @@ __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_t
     if (racy)
         hr__emit_shared_x(d.ring, d.ring_tail, d.ring_cap, d.kernel_id, t.fsm, t.tid(), word,
                           HR_EI_EMIT | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u));
+}
+
+__device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind)
+{
+    hr__check_shared_row_k(d, t, word, kind, d.wc_bits, d.wc_lsh, d.tile_log2);
 }
 
 /* The test for hr__check_shared_row (warp-uniform result). */

@@ -98,11 +98,14 @@ struct hr_ctx {
     /* the report as one CUDA graph: the one-CTA small-set kernel, then an IF node
      * (set by that kernel) around the full-capacity CUB path; rebuilt when its
      * arguments change.  arep_big: kernels the IF body launched (hr_launch_count). */
-    cudaGraph_t arep_graph = nullptr;
-    cudaGraphExec_t arep_exec = nullptr;
+    struct arep_key_t { const void *out, *hdr, *scratch, *ring; uint32_t out_cap, cap; int lo_bits, hi_bits; };
+    /* two cached graphs (hr_report_async into the ctx's pinned buffer and
+     * hr_report_async_to into a caller's may alternate); slot arep_lru is replaced next */
+    struct { cudaGraph_t graph; cudaGraphExec_t exec; arep_key_t key; } arep_g[2] = {};
+    int arep_lru = 0;
+    cudaGraphExec_t arep_exec = nullptr;          /* the graph of the current call */
     cudaStream_t arep_cap = nullptr;              /* capture stream of the IF body */
     unsigned long long *arep_big = nullptr;
-    struct { const void *out, *hdr, *scratch, *ring; uint32_t out_cap, cap; int lo_bits, hi_bits; } arep_key = {};
     bool arep_no_graph = false;                   /* graph build failed once: direct launches */
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_reset, ev_kernel;
@@ -1841,13 +1844,21 @@ static hr_status arep_enqueue_sort(hr_ctx *c, cudaStream_t s, const arep_args &a
 static hr_status arep_graph_build(hr_ctx *c, const arep_args &a)
 {
     const uint32_t cap = c->cfg.ring_capacity;
-    if (c->arep_exec && c->arep_key.out == a.out && c->arep_key.hdr == a.hdr &&
-        c->arep_key.scratch == c->arep_scratch && c->arep_key.ring == c->ring && c->arep_key.out_cap == a.out_cap &&
-        c->arep_key.cap == cap &&
-        c->arep_key.lo_bits == a.lo_bits && c->arep_key.hi_bits == a.hi_bits)
-        return HR_OK;
-    if (c->arep_exec) { cudaGraphExecDestroy(c->arep_exec); c->arep_exec = nullptr; }
-    if (c->arep_graph) { cudaGraphDestroy(c->arep_graph); c->arep_graph = nullptr; }
+    const hr_ctx::arep_key_t key = {a.out, a.hdr, c->arep_scratch, c->ring, a.out_cap, cap, a.lo_bits, a.hi_bits};
+    for (int i = 0; i < 2; i++) {
+        const hr_ctx::arep_key_t &k = c->arep_g[i].key;
+        if (c->arep_g[i].exec && k.out == key.out && k.hdr == key.hdr && k.scratch == key.scratch &&
+            k.ring == key.ring && k.out_cap == key.out_cap && k.cap == key.cap && k.lo_bits == key.lo_bits &&
+            k.hi_bits == key.hi_bits) {
+            c->arep_exec = c->arep_g[i].exec;
+            c->arep_lru = 1 - i;
+            return HR_OK;
+        }
+    }
+    const int slot = c->arep_lru;
+    c->arep_exec = nullptr;
+    if (c->arep_g[slot].exec) { cudaGraphExecDestroy(c->arep_g[slot].exec); c->arep_g[slot].exec = nullptr; }
+    if (c->arep_g[slot].graph) { cudaGraphDestroy(c->arep_g[slot].graph); c->arep_g[slot].graph = nullptr; }
     if (!c->arep_cap) CU(cudaStreamCreateWithFlags(&c->arep_cap, cudaStreamNonBlocking));
     if (!c->arep_big) {
         CU(cudaMalloc(&c->arep_big, sizeof(unsigned long long)));
@@ -1857,7 +1868,7 @@ static hr_status arep_graph_build(hr_ctx *c, const arep_args &a)
                             (int)HR_AREP_SMALL_SMEM));
     cudaGraph_t g = nullptr;
     CU(cudaGraphCreate(&g, 0));
-    c->arep_graph = g;
+    c->arep_g[slot].graph = g;
     cudaGraphConditionalHandle big;
     CU(cudaGraphConditionalHandleCreate(&big, g, 0u, cudaGraphCondAssignDefault));
     const hr_race *ring = c->ring;
@@ -1889,15 +1900,10 @@ static hr_status arep_graph_build(hr_ctx *c, const arep_args &a)
     const cudaError_t ec = cudaStreamEndCapture(c->arep_cap, &captured);
     if (st) return st;
     CU(ec);
-    CU(cudaGraphInstantiate(&c->arep_exec, g, 0));
-    c->arep_key.out = a.out;
-    c->arep_key.hdr = a.hdr;
-    c->arep_key.scratch = c->arep_scratch;
-    c->arep_key.ring = c->ring;
-    c->arep_key.out_cap = a.out_cap;
-    c->arep_key.cap = cap;
-    c->arep_key.lo_bits = a.lo_bits;
-    c->arep_key.hi_bits = a.hi_bits;
+    CU(cudaGraphInstantiate(&c->arep_g[slot].exec, g, 0));
+    c->arep_g[slot].key = key;
+    c->arep_exec = c->arep_g[slot].exec;
+    c->arep_lru = 1 - slot;
     return HR_OK;
 }
 
@@ -2253,8 +2259,10 @@ extern "C" void hr_destroy(hr_ctx *c)
     if (c->arep_hdr_host) cudaFreeHost(c->arep_hdr_host);
     if (c->arep_scratch) cudaFree(c->arep_scratch);
     if (c->arep_ev) cudaEventDestroy(c->arep_ev);
-    if (c->arep_exec) cudaGraphExecDestroy(c->arep_exec);
-    if (c->arep_graph) cudaGraphDestroy(c->arep_graph);
+    for (auto &ag : c->arep_g) {
+        if (ag.exec) cudaGraphExecDestroy(ag.exec);
+        if (ag.graph) cudaGraphDestroy(ag.graph);
+    }
     if (c->arep_cap) cudaStreamDestroy(c->arep_cap);
     if (c->arep_big) cudaFree(c->arep_big);
     for (auto &pr : c->ev_reset) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }

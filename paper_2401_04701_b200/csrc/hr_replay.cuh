@@ -35,6 +35,15 @@
  * lane walking a hub's adjacency list, shard-filtered rows) are packed 32 per
  * step instead of one.
  */
+template <bool B> struct hr_bool { static constexpr bool value = B; };
+
+/* a warp-uniform value the compiler keeps in a vector register (a SHFL result is
+ * not provably uniform, so it is not re-read from the parameter bank in a loop) */
+__device__ __forceinline__ uint32_t hr__reg(uint32_t v)
+{
+    return __shfl_sync(0xffffffffu, v, 0);
+}
+
 struct hr_pool_smem {
     uint64_t rec[32];       /* pooled records */
     uint8_t src[32];        /* simulated lane of each pooled record */
@@ -267,9 +276,12 @@ __host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint
  * POOL = true, WIDE = true: pooled at up to 64 registers, no spills (a few
  *   very long warps, e.g. power-law BFS hubs: per-warp latency decides).
  * Rows reach the warp through its TMA staging ring (hr_records.cuh). */
+#ifndef HR_ROW_WIDE_REGS
+#define HR_ROW_WIDE_REGS 64
+#endif
 #ifdef HR_ROW_REGS
 /* register-cap experiments: the narrow kernels get __maxnreg__(HR_ROW_REGS) instead */
-#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : HR_ROW_REGS)
+#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? HR_ROW_WIDE_REGS : HR_ROW_REGS)
 #else
 /* narrow row kernel at 48 registers: on C5 (dense, random-DRAM bound) it beats both the
  * 64-register kernel (fewer warps) and the 32-register one (spills): 88.6 vs 90.2 ms,
@@ -280,7 +292,7 @@ __host__ __device__ __forceinline__ uint32_t hr_stage_bytes(uint32_t warps, uint
 #ifndef HR_POOL_NARROW_REGS
 #define HR_POOL_NARROW_REGS 32
 #endif
-#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? 64 : ((POOL) ? HR_POOL_NARROW_REGS : HR_ROW_NARROW_REGS))
+#define HR_REPLAY_BOUNDS(POOL, WIDE) __maxnreg__((WIDE) ? HR_ROW_WIDE_REGS : ((POOL) ? HR_POOL_NARROW_REGS : HR_ROW_NARROW_REGS))
 #endif
 template <bool POOL, bool WIDE, bool ABL, typename SRC>
 __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
@@ -420,37 +432,49 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
         }
         if (!POOL && !ABL && SRC::C32) {
             /* C32 rows read undecoded: barrier test, then the shared-row fast path
-             * (hr__check_shared_row) on the raw (word, op | space << 2) pair */
-            /* the shared-row word limit: 0 while this lane is off (t.off changes only at barriers) */
-            uint32_t swl = (t.off & 3u) ? 0u : t.swords;
-            /* this lane's word / op byte; lanes beyond the grid read the NOP record of
-             * the table copy (HR_FSM_NOP_OFF) on every row */
-            uint32_t pw = active ? buf + lane * 4u : t.fsm + HR_FSM_NOP_OFF;
-            uint32_t pb = active ? buf + CH * 128u + lane : t.fsm + HR_FSM_NOP_OFF + 4u;
-            const uint32_t dw = active ? 128u : 0u, db = active ? 32u : 0u;
-            const uint32_t l0 = lane == 0u ? 1u : 0u;
-            for (uint32_t j = 0; j < rows; j++, pw += dw, pb += db) {
-                uint32_t w32, ob;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w32) : "r"(pw) : "memory");
-                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(ob) : "r"(pb) : "memory");
-                const bool ctl = (ob & 3u) == 3u;
-                /* one vote classifies a shared row: every lane a shared-space access
-                 * (op | space << 2 in 4..6; a byte with other bits set takes the general
-                 * path, which masks them) to strictly increasing in-range words (lane 0
-                 * compares with itself: + 1) */
-                const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
-                if (__all_sync(0xffffffffu, (ob - 4u < 3u) & (w32 < swl) & (w32 + l0 > wprev))) {
-                    hr__check_shared_row(d, t, w32, ob & 3u);
-                    continue;
+             * (hr__check_shared_row) on the raw (word, op | space << 2) pair.  FULL (wide
+             * kernel): every lane is in the grid (constant row strides); otherwise lanes
+             * beyond the grid
+             * read the NOP record of the table copy (HR_FSM_NOP_OFF) on every row. */
+            auto c32_rows = [&](auto full) {
+                constexpr bool FULL = decltype(full)::value;
+                /* the shared-row word limit: 0 while this lane is off (t.off changes only at barriers) */
+                uint32_t swl = (t.off & 3u) ? 0u : t.swords;
+                const bool in = FULL || active;
+                uint32_t pw = in ? buf + lane * 4u : t.fsm + HR_FSM_NOP_OFF;
+                uint32_t pb = in ? buf + CH * 128u + lane : t.fsm + HR_FSM_NOP_OFF + 4u;
+                const uint32_t dw = FULL ? 128u : (active ? 128u : 0u), db = FULL ? 32u : (active ? 32u : 0u);
+                const uint32_t l0 = lane == 0u ? 1u : 0u;
+                /* kept in registers (an opaque copy: not re-read from the parameter bank per row) */
+                const uint32_t wcb = WIDE ? hr__reg(d.wc_bits) : d.wc_bits, wsh = WIDE ? hr__reg(d.wc_lsh) : d.wc_lsh,
+                               tl = WIDE ? hr__reg(d.tile_log2) : d.tile_log2;
+                for (uint32_t j = 0; j < rows; j++, pw += dw, pb += db) {
+                    uint32_t w32, ob;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w32) : "r"(pw) : "memory");
+                    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(ob) : "r"(pb) : "memory");
+                    const bool ctl = (ob & 3u) == 3u;
+                    /* one vote classifies a shared row: every lane a shared-space access
+                     * (op | space << 2 in 4..6; a byte with other bits set takes the general
+                     * path, which masks them) to strictly increasing in-range words (lane 0
+                     * compares with itself: + 1) */
+                    const uint32_t wprev = __shfl_up_sync(0xffffffffu, w32, 1);
+                    if (__all_sync(0xffffffffu, (ob - 4u < 3u) & (w32 < swl) & (w32 + l0 > wprev))) {
+                        hr__check_shared_row_k(d, t, w32, ob & 3u, wcb, wsh, tl);
+                        continue;
+                    }
+                    if (__any_sync(0xffffffffu, ctl && w32 != 0u)) {
+                        hr__barrier_row(d, t, ((uint64_t)(ob & 3u) << 62) | ((uint64_t)((ob >> 2) & 1u) << 61) | w32,
+                                        lane_mask);
+                        swl = (t.off & 3u) ? 0u : t.swords;
+                        continue;
+                    }
+                    hr_check_lanes<false, ABL>(d, t, 0xffffffffu, !ctl, (ob >> 2) & 1u, w32, ob & 3u);
                 }
-                if (__any_sync(0xffffffffu, ctl && w32 != 0u)) {
-                    hr__barrier_row(d, t, ((uint64_t)(ob & 3u) << 62) | ((uint64_t)((ob >> 2) & 1u) << 61) | w32,
-                                    lane_mask);
-                    swl = (t.off & 3u) ? 0u : t.swords;
-                    continue;
-                }
-                hr_check_lanes<false, ABL>(d, t, 0xffffffffu, !ctl, (ob >> 2) & 1u, w32, ob & 3u);
-            }
+            };
+            /* (the 48-register kernel keeps one copy: the dense global traces it runs
+             * rarely take the shared-row path, and a second copy costs it registers) */
+            if (WIDE && lanes >= 32u) c32_rows(hr_bool<true>{});
+            else c32_rows(hr_bool<false>{});
             j0 = rows;
         }
         for (uint32_t j = j0; j < rows; j++) {

@@ -617,11 +617,16 @@ def test_report_async_small_out_cap_and_runs():
     cap = 5
     out = torch.zeros(cap * 24, dtype=torch.uint8, device="cuda")
     hdr = torch.zeros(4, dtype=torch.int32, device="cuda")
-    h.hr_report_async_to(ck.ctx, out.data_ptr(), cap, hdr.data_ptr())
-    torch.cuda.synchronize()
-    got = np.frombuffer(out.cpu().numpy().tobytes(), dtype=a_raw.dtype)
-    assert int(hdr[0]) == len(want)
-    assert got.tobytes() == a_raw[:cap].tobytes()
+    for _ in range(3):                     # alternating targets: both cached report graphs
+        out.zero_(); hdr.zero_()
+        h.hr_report_async_to(ck.ctx, out.data_ptr(), cap, hdr.data_ptr())
+        torch.cuda.synchronize()
+        got = np.frombuffer(out.cpu().numpy().tobytes(), dtype=a_raw.dtype)
+        assert int(hdr[0]) == len(want)
+        assert got.tobytes() == a_raw[:cap].tobytes()
+        ck.report_async()
+        b_raw, _ = ck.collect_raw()
+        assert b_raw.tobytes() == a_raw.tobytes()
     ck.close()
 
 
@@ -729,3 +734,60 @@ def test_representatives_suite():
     for c in suite.suite()[::5]:
         g = [tuple(r) for r in hr().check_trace(c.trace, representatives=(2, 2))[0]]
         assert g == oracle_set(_only_representatives(c.trace, 2, 2))[0], c.name
+
+
+# ---- shared rows (hr__check_shared_row: wide and narrow row kernels, C32 and u64 records) ----
+def _shared_rows_trace(seed, n_kernels=6, n_rows=40, smem=1024, private=False):
+    """Full warps whose rows are mostly "shared rows" (32 strictly increasing
+    shared words, any kinds), with repeated rows (the same word twice in a row
+    per lane), block barriers at common row indices, and some global or
+    non-increasing rows in between (pairs broken off).  private: each shared
+    word belongs to one lane of one warp (race-free shared space)."""
+    rng = np.random.default_rng(seed)
+    kernels = []
+    for _ in range(n_kernels):
+        blocks, warps = int(rng.integers(1, 5)), int(rng.integers(1, 9))
+        kinds = rng.choice([0, 1, 2, 3], size=n_rows, p=[0.72, 0.1, 0.08, 0.1])   # shared / global / shuffled / barrier
+        rows = np.zeros((blocks * warps, n_rows, 32), dtype=np.uint64)
+        for w in range(blocks * warps):
+            prev = None
+            for i in range(n_rows):
+                if kinds[i] == 3:
+                    rows[w, i, :] = tf.SYNCTHREADS
+                    prev = None
+                    continue
+                if prev is not None and rng.random() < 0.3:
+                    words = prev                                           # same words as the last row
+                elif private:
+                    words = (w % warps) * 128 + 32 * int(rng.integers(0, 4)) + np.arange(32)
+                else:
+                    s = int(rng.integers(1, 4))
+                    words = int(rng.integers(0, smem - 32 * s)) + s * np.arange(32)
+                if kinds[i] == 2 and not private:
+                    words = rng.permutation(words)                         # not increasing: general path
+                ops = rng.choice([0, 1, 2], size=32, p=[0.7, 0.2, 0.1])
+                space = 0 if kinds[i] == 1 else 1
+                rows[w, i, :] = [tf.encode(int(o), space, int(x)) for o, x in zip(ops, words)]
+                if private and kinds[i] == 2:
+                    rows[w, i, rng.random(32) < 0.3] = tf.NOP           # partial row: general path
+                prev = words if kinds[i] == 0 else None
+        kernels.append(tf.kernel_from_rows(blocks, warps, 32, rows, smem_words=smem))
+    return tf.make_trace(kernels)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("options", [0, 512, 65536])
+def test_shared_rows_paired(seed, options):
+    """Runs of shared rows (the specialised shared-row check) in the wide and
+    the narrow row kernel = the oracle: racy and race-free words, the same
+    words in consecutive rows, runs broken by barriers, global rows, shuffled
+    or partial rows (general path)."""
+    tr = _shared_rows_trace(900 + seed)
+    o = oracle_set(tr)
+    assert gpu_set(tr, compact=True, options=options) == o
+    assert gpu_set(tr, options=options) == o
+    assert len(o[0]) > 0
+    tr = _shared_rows_trace(950 + seed, private=True)
+    o = oracle_set(tr)
+    assert gpu_set(tr, compact=True, options=options) == o
+    assert all(r[1] == 0 for r in o[0])                 # only the global rows race
