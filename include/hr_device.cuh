@@ -716,10 +716,12 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
  *     bc > oBC (an INIT word ignores relation and sync, any value indexes
  *     the same table row);
  *   - no epoch tag (the instance is zeroed at block start), no probe;
- *   - a7: RACE_BLOCK under a non-Global relation (iii) — always non-Global
- *     here; (ii)'s insensitive states are GREAD, GATOMIC, RACE_GRID, which
- *     need another block and never occur; the unchanged word (i) goes to the
- *     CAS, which rewrites the same value.
+ *   - a7 is left out: its exits only save a write.  (ii)'s insensitive states
+ *     (GREAD, GATOMIC, RACE_GRID) need another block and never occur; (iii),
+ *     RACE_BLOCK under a non-Global relation, maps to itself for every label
+ *     in the generated table, so committing it rewrites only the diagnostic
+ *     tid and clocks; the unchanged word (i) rewrites the same value.  One
+ *     CAS per access, no exit test on the common path.
  */
 /* The racy lanes of a shared row that arrive together share one ring
  * reservation (warp-aggregated over __activemask); a full ring drops the
@@ -769,10 +771,10 @@ __device__ __forceinline__ void hr__check_shared_row_k(const hr_dev &d, const hr
     const uint32_t lo = (uint32_t)t.meta, tid_lo = (uint32_t)(t.meta >> HR_TID_SHIFT) & 1023u;
     const uint32_t kcol = t.fsm + (kind << 4);
     unsigned long long old = hr__ld_s(sa);
-    uint32_t os = 0, cur = 0;
-    bool racy = false;
+    uint32_t os, cur;
+    bool done;
     HR_COUNT(d, 0);
-    while (true) {
+    do {
         const uint32_t ohi = (uint32_t)(old >> 32);
         os = ohi >> (HR_STATE_SHIFT - 32);
         const uint32_t x = (tid_lo ^ ohi) & 1023u;
@@ -787,22 +789,18 @@ __device__ __forceinline__ void hr__check_shared_row_k(const hr_dev &d, const hr
         const uint32_t idx = (os << 6) + (hr__min1(dlo >> wcb) << 3) + (hr__min1(dlo << wsh) << 2) +
                              hr__min1(x) + hr__min1(x >> tl);                 /* + rel: Self / Warp / Block */
         cur = hr__lds_u8(kcol + idx);
-        const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta;
-        /* a7 (iii) only: a RACE word stays RACE (the stored tid is diagnostic).  (i), the
-         * unchanged word, is left to the CAS, which then writes the same value: in a
-         * shared row the clocks or the tid nearly always differ (C3: never equal) */
-        if (cur == os && os >= HR_RACE_BLOCK) { HR_COUNT(d, 2); break; }
-        const unsigned long long prev = hr__cas_s(sa, old, nw);
-        if (prev == old) {                                                /* a8 committed */
-            HR_COUNT(d, 3);
-            racy = cur >= HR_RACE_BLOCK && cur != os;
-            break;
-        }
-        HR_COUNT(d, 1);
+        /* no a7 exit: every access commits its word with one CAS.  Inside one block's
+         * instance the relation is never Global, so a RACE_BLOCK word stays RACE_BLOCK
+         * and rewriting it only refreshes the diagnostic tid and clocks (no second
+         * record: the emit test below needs a state change) */
+        const unsigned long long prev = hr__cas_s(sa, old, ((unsigned long long)cur << HR_STATE_SHIFT) | t.meta);
+        done = prev == old;                                               /* a8 committed */
+        if (!done) HR_COUNT(d, 1);
         old = prev;
-    }
+    } while (!done);
+    HR_COUNT(d, 3);
     /* a9: rare here, so no warp vote on the common path and the emit out of line */
-    if (racy)
+    if (cur >= HR_RACE_BLOCK && cur != os)
         hr__emit_shared_x(d.ring, d.ring_tail, d.ring_cap, d.kernel_id, t.fsm, t.tid(), word,
                           HR_EI_EMIT | (kind << 24) | (os << 19) | (cur == HR_RACE_GRID ? 1u : 0u));
 }
