@@ -131,6 +131,13 @@ enum {
                                     shadow RMWs hit L2.  Opt-in: exact, but measured slower than the
                                     row replay on C5 (161 vs 90 ms, DESIGN.md §5 item 17) */
     HR_OPT_NO_BINNED = 524288u,  /* never use the binned replay (the default) */
+    HR_OPT_HYBRID = 1048576u,    /* hybrid binned replay (csrc/hr_hybrid.cuh) for row-replayed kernels
+                                    without warp tiles: shadow buckets of 32 MB whose accesses arrive
+                                    mostly scattered are binned — the row replay appends their accesses
+                                    to (bucket, block) runs in happens-before order and a bucket-major
+                                    pass checks them with the bucket's shadow in L2 — the rest is
+                                    checked by the row replay as usual */
+    HR_OPT_BIN_ALL = 2097152u,   /* with HR_OPT_HYBRID: bin every touched bucket (tests) */
     HR_OPT_NO_STREAMS = 131072u, /* long-tailed barrier-free kernels without shared shadow: use the
                                     per-block compacted replay instead of the stream-scheduled one
                                     (hr_streams.cuh: hub warps fanned out over helper streams that

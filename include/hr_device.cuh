@@ -88,7 +88,21 @@ struct hr_dev {
     uint32_t epoch_tag;           /* HR_OPT_LAZY_RESET: kernel epoch tag 1..15 in bits [31:28] of the
                                      shadow's clock word; a global word with another tag is INIT.
                                      0 = off (the shadow is zeroed at every kernel boundary) */
+    /* hybrid binned replay (HR_OPT_BINNED, csrc/hr_hybrid.cuh): the row replay appends
+     * the global accesses of the shadow buckets set in hy_map as entries (run of
+     * (bucket, block) at hy_off[bucket * hy_nb + block]) instead of checking them */
+    const uint32_t *hy_map;       /* bitmap over 2^HR_HY_BITS-word buckets; nullptr = off */
+    const unsigned long long *hy_off;
+    unsigned long long *hy_ent;
+    uint32_t hy_nb, hy_nbk;       /* blocks of the launch, buckets */
+    uint32_t hy_sa_off;           /* per-bucket write positions (u64) at this offset past the FSM copy */
 };
+
+/* hybrid entry: [63:42] word offset in the bucket | [41:40] kind | [39:13] packed tid
+ * | [12:6] bc | [5:0] wc */
+#define HR_HY_BITS 22u
+#define HR_HY_BC_MAX 127u
+#define HR_HY_WC_MAX 63u
 
 /* Per-thread registers. */
 struct hr_thr {
@@ -661,6 +675,24 @@ __device__ __forceinline__ unsigned hr__group(const hr_dev &d, const hr_thr &t, 
  * access is committed (the final ballot is the warp's convergence point), so a
  * lane never runs ahead of an access folded into another lane (program order).
  */
+/* Hybrid binned replay: an access to a binned bucket becomes one entry of its
+ * (bucket, block) run, in this thread's program order and epoch order (the
+ * position counter is the block's, in shared memory, and the row replay's real
+ * barriers separate the epochs), checked later by hr_hy_replay_kernel. */
+__device__ __forceinline__ bool hr__hy_append(const hr_dev &d, const hr_thr &t, uint64_t local, uint32_t kind)
+{
+    const uint32_t bk = (uint32_t)(local >> HR_HY_BITS);
+    if (!((__ldg(d.hy_map + (bk >> 5)) >> (bk & 31u)) & 1u)) return false;
+    const uint32_t lo = (uint32_t)t.meta & 0x0fffffffu;
+    const uint32_t bc = lo >> d.wc_bits, wc = lo & ((1u << d.wc_bits) - 1u);
+    const uint64_t e = ((local & ((1ull << HR_HY_BITS) - 1u)) << 42) | ((uint64_t)kind << 40) |
+                       ((uint64_t)t.tid() << 13) | ((uint64_t)bc << 6) | (uint64_t)wc;
+    unsigned long long slot;
+    asm volatile("atom.shared.add.u64 %0, [%1], 1;" : "=l"(slot) : "r"(t.fsm + d.hy_sa_off + 8u * bk) : "memory");
+    __stcs(reinterpret_cast<unsigned long long *>(d.hy_ent) + slot, (unsigned long long)e);
+    return true;
+}
+
 __device__ __forceinline__ void hr__check_shared_row(const hr_dev &d, const hr_thr &t, uint32_t word, uint32_t kind);
 __device__ __forceinline__ bool hr__shared_row_ok(const hr_thr &t, uint32_t op, uint32_t space, uint64_t word);
 
@@ -678,6 +710,7 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
     const bool is_shared = space != 0u;
     uint64_t local = 0;
     valid = valid && !(t.off & 1u) && hr__locate(d, t, space, word, local);
+    if (!ONLINE && d.hy_map != nullptr && valid && !is_shared) valid = !hr__hy_append(d, t, local, kind);
     if (valid) HR_COUNT(d, 0);
     /* match key: 0 = no access on this lane (filtered lanes must not alias owned words) */
     const uint64_t key = valid ? ((local << 2) | (is_shared ? 2u : 0u) | 1u) : 0ull;

@@ -234,6 +234,7 @@ __device__ __forceinline__ void hr__bn_check(const hr_dev &d, const hr_thr &t, u
             uint32_t rinfo = (cur >= HR_RACE_BLOCK && cur != os) ? (HR_EI_EMIT | (lane << 26) | (kind << 24) | (os << 19))
                                                                  : 0u;
             uint32_t ptid = tid, plo = lo;
+            bool anyg = rel == 3u;                /* a Global label anywhere in the fold */
             unsigned r = peers & ~(1u << lane);
             while (r) {
                 const uint32_t j = __ffs(r) - 1;
@@ -243,9 +244,11 @@ __device__ __forceinline__ void hr__bn_check(const hr_dev &d, const hr_thr &t, u
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ej) : "r"(pool_sa + 8u * j) : "memory");
                 hr__bn_decode(ej, hr__lds_u32(pool_sa + 256u + 4u * j), tag_hi, d.wc_bits, tj, lj, kj);
                 const uint32_t rj = hr__rel(tj, ptid, d.tile_log2);
+                anyg = anyg || rj == 3u;
                 const uint32_t sj = hr__sync(rj, lj, plo, d.wc_bits);
                 const uint32_t nx = hr__lds_u8(t.fsm + ((cur << 6) | (kj << 4) | (sj << 2) | rj));
-                if (nx >= HR_RACE_BLOCK && cur < HR_RACE_BLOCK && !rinfo)
+                /* entering RACE, or (a member from another block) RACE_BLOCK -> RACE_GRID */
+                if (nx >= HR_RACE_BLOCK && nx != cur && !rinfo)
                     rinfo = HR_EI_EMIT | (j << 26) | (kj << 24) | (cur << 19);
                 cur = nx;
                 ptid = tj;
@@ -254,7 +257,9 @@ __device__ __forceinline__ void hr__bn_check(const hr_dev &d, const hr_thr &t, u
             const unsigned long long nw = ((unsigned long long)cur << HR_STATE_SHIFT) | nmeta;
             if (fastexit && cur == os && fresh != HR_OLD_GUESS) {
                 const uint32_t f = hr__lds_u8(t.fsm + HR_FSM_BYTES + os);
-                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && rel != 3u && fresh == HR_OLD_FRESH))
+                /* (iii) needs every label of the fold non-Global: members of a pool can
+                 * come from other blocks (a RACE_BLOCK word they touch becomes RACE_GRID) */
+                if ((f & HR_FLAG_INSENSITIVE) || ((f & HR_FLAG_BLOCK_ONLY) && !anyg && fresh == HR_OLD_FRESH))
                     break;
             }
             if (nw == old) {

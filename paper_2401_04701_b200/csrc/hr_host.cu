@@ -30,6 +30,7 @@
 #include "hr_bserial.cuh"
 #include "hr_streams.cuh"
 #include "hr_binned.cuh"
+#include "hr_hybrid.cuh"
 #include "fsm_table.inc"
 #include "fsm_classes.inc"
 
@@ -792,6 +793,90 @@ static hr_status launch_binned(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src
     return HR_OK;
 }
 
+/* Hybrid binned replay (HR_OPT_HYBRID, hr_hybrid.cuh), first half: count the
+ * (bucket, block) runs of kernel k's blocks [b0, b1), choose the binned buckets,
+ * lay the runs out bucket-major and point d at them (d.hy_*: the row replay
+ * then appends those buckets' accesses).  One synchronous read sizes the
+ * entries.  d is left untouched (plain row replay) if nothing is binned or the
+ * clocks do not fit an entry. */
+template <typename SRC>
+static hr_status hybrid_prepare(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const uint64_t *woff, cudaStream_t s,
+                                uint64_t b0, uint64_t b1, hr_dev &d)
+{
+    const uint64_t *kd = t->kdesc + 8ull * k;
+    const uint64_t warps = kd[1], lanes = kd[2], woi = kd[4];
+    const uint32_t nb = (uint32_t)(b1 - b0);
+    const uint32_t nbk = (uint32_t)((c->glocal + (1ull << HR_HY_BITS) - 1) >> HR_HY_BITS);
+    if (nbk == 0 || nbk > HR_HY_MAXBK || nb == 0) return HR_OK;
+    const uint64_t nruns = (uint64_t)nbk * nb;
+    hr_status st;
+    if ((st = reserve(c, 22, (size_t)(nruns + 1) * 8)) || (st = reserve(c, 23, (size_t)(nruns + 1) * 8)) ||
+        (st = reserve(c, 20, (size_t)nbk * 16 + 512)))
+        return st;
+    unsigned long long *cnt = (unsigned long long *)c->stage[22];
+    unsigned long long *off = (unsigned long long *)c->stage[23];
+    unsigned long long *stat = (unsigned long long *)c->stage[20];
+    uint32_t *map = (uint32_t *)((char *)c->stage[20] + (size_t)nbk * 16);
+    unsigned int *clk = (unsigned int *)((char *)c->stage[20] + (size_t)nbk * 16 + 128);
+    CU(cudaMemsetAsync(c->stage[20], 0, (size_t)nbk * 16 + 512, s));
+    CU(cudaMemsetAsync(cnt + nruns, 0, 8, s));
+    c->launches++;
+    hr_hy_count_kernel<SRC><<<nb, (unsigned)(warps * 32), (size_t)nbk * 8, s>>>(
+        d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes, nbk, nb, cnt, stat, clk);
+    CU(cudaGetLastError());
+    const bool all = (c->cfg.options & HR_OPT_BIN_ALL) != 0;
+    c->launches += 2;
+    if (all) {
+        hr_hy_decide_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(stat, nbk, map, 0ull);
+        /* every touched bucket: a bucket with no access contributes no run */
+        CU(cudaMemsetAsync(map, 0xff, (nbk + 31) / 32 * 4, s));
+    } else {
+        hr_hy_decide_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(stat, nbk, map, 1ull << 16);
+    }
+    CU(cudaGetLastError());
+    hr_hy_mask_kernel<<<1024, 256, 0, s>>>(cnt, nruns, nb, map);
+    CU(cudaGetLastError());
+    size_t tmp = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int64_t)(nruns + 1), s));
+    if ((st = reserve(c, 5, tmp ? tmp : 1))) return st;
+    c->launches += 2;
+    CU(cub::DeviceScan::ExclusiveSum(c->stage[5], tmp, cnt, off, (int64_t)(nruns + 1), s));
+    unsigned long long total = 0;
+    unsigned int hclk[2] = {0, 0};
+    CU(cudaMemcpyAsync(&total, off + nruns, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hclk, clk, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    /* exact counts need clocks that never overflow (a thread past its limit stops
+     * checking) and that fit an entry */
+    if (total == 0 || hclk[0] > HR_HY_BC_MAX || hclk[0] >= d.bc_max || hclk[1] > HR_HY_WC_MAX || hclk[1] >= d.wc_max)
+        return HR_OK;
+    if ((st = reserve(c, 21, (size_t)total * 8))) return st;
+    d.hy_map = map;
+    d.hy_off = off;
+    d.hy_ent = (unsigned long long *)c->stage[21];
+    d.hy_nb = nb;
+    d.hy_nbk = nbk;
+    return HR_OK;
+}
+
+/* second half: check the binned runs bucket by bucket (after the row replay) */
+static hr_status hybrid_replay(hr_ctx *c, const hr_dev &d, cudaStream_t s)
+{
+    hr_status st;
+    if ((st = reserve(c, 20, (size_t)d.hy_nbk * 16 + 512))) return st;
+    unsigned long long *next = (unsigned long long *)((char *)c->stage[20] + (size_t)d.hy_nbk * 16 + 256);
+    CU(cudaMemsetAsync(next, 0, 8, s));
+    const size_t rsm = hr_hy_replay_smem(d.hy_nbk);
+    if (rsm > 48 * 1024) CU(cudaFuncSetAttribute(hr_hy_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->launches++;
+    hr_hy_replay_kernel<<<(unsigned)(dev_sms * 2), HR_HY_WARPS * 32, rsm, s>>>(d, d.hy_ent, d.hy_off, d.hy_nb, d.hy_nbk,
+                                                                             next);
+    CU(cudaGetLastError());
+    return HR_OK;
+}
+
 /* Binned replay (HR_OPT_BINNED) for kernels without shared shadow and at most
  * HR_BN_MAXBK shadow buckets. */
 static bool use_binned(const hr_ctx *c, int kind, uint64_t smem_words)
@@ -912,6 +997,16 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
         return HR_OK;
     }
     size_t smem = (size_t)hr_stage_offset(pool, nhw, smem_u64(c, smem_words)) + hr_stage_bytes(nhw, nb, ch, SRC::ROW_BYTES);
+    bool timing = c->cfg.options & HR_OPT_TIMING;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }   /* the hybrid passes included */
+    if ((c->cfg.options & HR_OPT_HYBRID) && !pool && !tiles && !abl && c->shadow_bytes == 8 && c->gshadow) {
+        if (hr_status st = hybrid_prepare(c, t, k, src, woff, s, b0, b1, d)) return st;
+        if (d.hy_map) {
+            d.hy_sa_off = (uint32_t)smem;               /* the block's run positions after the staging */
+            smem += (size_t)d.hy_nbk * 8;
+        }
+    }
     if (smem > 227 * 1024)
         return fail(c, HR_E_ARG, "kernel %u: %zu bytes of shared memory per block (shadow %llu words + staging)", k, smem,
                     (unsigned long long)smem_words);
@@ -924,13 +1019,12 @@ static hr_status launch(hr_ctx *c, const hr_trace *t, uint32_t k, SRC src, const
                     : (wide ? hr_replay_kernel<false, true, false, SRC> : hr_replay_kernel<false, false, false, SRC>);
     const uint32_t stage_off = hr_stage_offset(pool, nhw, smem_u64(c, smem_words));
     if (smem > 48 * 1024) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    bool timing = c->cfg.options & HR_OPT_TIMING;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (timing) { e0 = get_event(c); e1 = get_event(c); CU(cudaEventRecord(e0, s)); }
     c->launches++;
     kern<<<(unsigned)(b1 - b0), nhw * 32u, smem, s>>>(d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes,
                                                        (uint32_t)smem_words, stage_off, split);
     CU(cudaGetLastError());
+    if (d.hy_map)
+        if (hr_status st = hybrid_replay(c, d, s)) return st;
     if (timing) { CU(cudaEventRecord(e1, s)); c->ev_kernel.push_back({e0, e1}); }
     note_kernel(c, kid);
     return HR_OK;

@@ -320,6 +320,12 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
     const uint32_t cta = blockIdx.x;
 #endif
 
+    if (!POOL && d.hy_map != nullptr) {
+        /* hybrid binned replay: this block's write position in each (bucket, block) run */
+        unsigned long long *pos = reinterpret_cast<unsigned long long *>(hr_smem + d.hy_sa_off);
+        for (uint32_t i = threadIdx.x; i < d.hy_nbk; i += blockDim.x) pos[i] = d.hy_off[(uint64_t)i * d.hy_nb + cta];
+        __syncthreads();
+    }
     constexpr uint32_t NB = hr_stage_cfg<WIDE, POOL, SRC::ROW_BYTES>::NB;
     constexpr uint32_t CH = hr_stage_cfg<WIDE, POOL, SRC::ROW_BYTES>::CH;
     constexpr uint32_t CHB = CH * SRC::ROW_BYTES;

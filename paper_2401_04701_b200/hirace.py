@@ -39,6 +39,8 @@ HR_OPT_ROW_NARROW = 65536
 HR_OPT_NO_STREAMS = 131072
 HR_OPT_BINNED = 262144
 HR_OPT_NO_BINNED = 524288
+HR_OPT_HYBRID = 1048576
+HR_OPT_BIN_ALL = 2097152
 EXPORTS = ("hr_init", "hr_set_shard", "hr_set_shard_ex", "hr_set_representatives", "hr_set_warp_tile", "hr_shadow_alloc", "hr_kernel_begin", "hr_replay_trace",
            "hr_replay_trace_host", "hr_pack_trace", "hr_unpack_trace", "hr_pool_trace", "hr_report", "hr_report_async",
            "hr_report_async_to",
