@@ -96,11 +96,16 @@ struct hr_dev {
     unsigned long long *hy_ent;
     uint32_t hy_nb, hy_nbk;       /* blocks of the launch, buckets */
     uint32_t hy_sa_off;           /* per-bucket write positions (u64) at this offset past the FSM copy */
+    uint64_t glocal_words;        /* words of the local global shadow (gshadow[0, glocal_words)) */
 };
 
 /* hybrid entry: [63:42] word offset in the bucket | [41:40] kind | [39:13] packed tid
  * | [12:6] bc | [5:0] wc */
+#ifdef HR_HY_BITS_OVERRIDE
+#define HR_HY_BITS HR_HY_BITS_OVERRIDE
+#else
 #define HR_HY_BITS 22u
+#endif
 #define HR_HY_BC_MAX 127u
 #define HR_HY_WC_MAX 63u
 
@@ -710,7 +715,10 @@ __device__ __forceinline__ void hr_check_lanes(const hr_dev &d, const hr_thr &t,
     const bool is_shared = space != 0u;
     uint64_t local = 0;
     valid = valid && !(t.off & 1u) && hr__locate(d, t, space, word, local);
-    if (!ONLINE && d.hy_map != nullptr && valid && !is_shared) valid = !hr__hy_append(d, t, local, kind);
+    if (!ONLINE && d.hy_map != nullptr) {
+        if (valid && !is_shared) valid = !hr__hy_append(d, t, local, kind);
+        if (!__any_sync(mask, valid)) return;                       /* a row of binned accesses only */
+    }
     if (valid) HR_COUNT(d, 0);
     /* match key: 0 = no access on this lane (filtered lanes must not alias owned words) */
     const uint64_t key = valid ? ((local << 2) | (is_shared ? 2u : 0u) | 1u) : 0ull;

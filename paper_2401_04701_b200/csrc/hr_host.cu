@@ -173,6 +173,7 @@ static hr_dev make_dev(hr_ctx *c, uint32_t kernel_id)
     d.gshadow = c->gshadow;
     d.gbase = c->gbase;
     d.gwords = c->gwords;
+    d.glocal_words = c->glocal;
     d.ring = c->ring;
     d.ring_tail = c->tail;
     d.flags = c->tail + 1;
@@ -820,21 +821,22 @@ static hr_status hybrid_prepare(hr_ctx *c, const hr_trace *t, uint32_t k, SRC sr
     unsigned int *clk = (unsigned int *)((char *)c->stage[20] + (size_t)nbk * 16 + 128);
     CU(cudaMemsetAsync(c->stage[20], 0, (size_t)nbk * 16 + 512, s));
     CU(cudaMemsetAsync(cnt + nruns, 0, 8, s));
-    c->launches++;
-    hr_hy_count_kernel<SRC><<<nb, (unsigned)(warps * 32), (size_t)nbk * 8, s>>>(
-        d, src, woff + woi + b0 * warps, (uint32_t)warps, (uint32_t)lanes, nbk, nb, cnt, stat, clk);
-    CU(cudaGetLastError());
-    const bool all = (c->cfg.options & HR_OPT_BIN_ALL) != 0;
-    c->launches += 2;
-    if (all) {
-        hr_hy_decide_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(stat, nbk, map, 0ull);
-        /* every touched bucket: a bucket with no access contributes no run */
-        CU(cudaMemsetAsync(map, 0xff, (nbk + 31) / 32 * 4, s));
+    const uint64_t *wk = woff + woi + b0 * warps;
+    if (c->cfg.options & HR_OPT_BIN_ALL) {
+        CU(cudaMemsetAsync(map, 0xff, (nbk + 31) / 32 * 4, s));           /* every bucket (tests) */
     } else {
-        hr_hy_decide_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(stat, nbk, map, 1ull << 16);
+        /* the choice from a sample of 1 in 64 blocks: >= 2^16 accesses scaled, >= half scattered */
+        const uint32_t stride = nb >= 4096 ? 64u : 1u;
+        c->launches += 2;
+        hr_hy_count_kernel<true, SRC><<<(nb + stride - 1) / stride, (unsigned)(warps * 32), (size_t)nbk * 8, s>>>(
+            d, src, wk, (uint32_t)warps, (uint32_t)lanes, nbk, nb, stride, map, cnt, stat, clk);
+        CU(cudaGetLastError());
+        hr_hy_decide_kernel<<<(nbk + 255) / 256, 256, 0, s>>>(stat, nbk, map, std::max<unsigned long long>(1ull, (1ull << 16) / stride));
+        CU(cudaGetLastError());
     }
-    CU(cudaGetLastError());
-    hr_hy_mask_kernel<<<1024, 256, 0, s>>>(cnt, nruns, nb, map);
+    c->launches++;
+    hr_hy_count_kernel<false, SRC><<<nb, (unsigned)(warps * 32), (size_t)nbk * 4, s>>>(
+        d, src, wk, (uint32_t)warps, (uint32_t)lanes, nbk, nb, 1u, map, cnt, stat, clk);
     CU(cudaGetLastError());
     size_t tmp = 0;
     CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int64_t)(nruns + 1), s));
@@ -871,7 +873,7 @@ static hr_status hybrid_replay(hr_ctx *c, const hr_dev &d, cudaStream_t s)
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     c->launches++;
-    hr_hy_replay_kernel<<<(unsigned)(dev_sms * 2), HR_HY_WARPS * 32, rsm, s>>>(d, d.hy_ent, d.hy_off, d.hy_nb, d.hy_nbk,
+    hr_hy_replay_kernel<<<(unsigned)(dev_sms * 3), HR_HY_WARPS * 32, rsm, s>>>(d, d.hy_ent, d.hy_off, d.hy_nb, d.hy_nbk,
                                                                              next);
     CU(cudaGetLastError());
     return HR_OK;

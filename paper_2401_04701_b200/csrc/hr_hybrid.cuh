@@ -10,23 +10,26 @@
  * changes.  Words are independent FSMs, so each word's
  * commit order only has to stay a linear extension of happens-before.
  *
- *   count   one CTA per simulated block counts, per 2^HR_HY_BITS-word shadow
- *           bucket, the block's global accesses (its (bucket, block) run) and
- *           how many of them arrive scattered (at most 4 lanes of a row in the
- *           bucket).  A bucket whose accesses are mostly scattered and
- *           numerous is BINNED; the others (coalesced own-row rows, hot sets
- *           that live in L2) stay with the row replay.  Every word belongs to
- *           one bucket, so each word is checked by exactly one of the two.
+ *   choose  a sample of the blocks (1 in 64) counts, per 2^HR_HY_BITS-word
+ *           shadow bucket, the accesses and how many arrive scattered (at
+ *           most 4 lanes of a row in the bucket).  A bucket whose accesses
+ *           are mostly scattered and numerous is BINNED; the others
+ *           (coalesced own-row rows, hot sets that live in L2) stay with the
+ *           row replay.  Every word belongs to one bucket, so each word is
+ *           checked by exactly one of the two.
+ *   count   one CTA per simulated block counts its accesses to each binned
+ *           bucket: the length of its (bucket, block) run.
  *   row     the normal row replay, with real barriers; an access to a binned
  *           bucket becomes an entry of its (bucket, block) run (hr__hy_append)
  *           at the block's next position: a thread's entries follow its
  *           program order, and epochs are separated by the barriers, so each
  *           run is in happens-before order.
  *   replay  a persistent grid checks the runs bucket by bucket (the SMs work
- *           in one or two 32 MB buckets at a time, whose shadow stays in L2),
- *           each run by one warp in order, 32 entries per pool; same-word
- *           entries of a pool are folded in entry order with their own
- *           (tid, bc, wc) labels.  Runs of different blocks are unordered.
+ *           in one or two 32 MB buckets at a time, whose shadow is streamed
+ *           into L2 ahead), each run by one warp in order, 32 entries per
+ *           pool; same-word entries of a pool are folded in entry order with
+ *           their own (tid, bc, wc) labels.  Runs of different blocks are
+ *           unordered.
  *
  * Used only when the count is exact (no clock can overflow, no warp tiles)
  * and the clocks fit an entry (bc <= 127, wc <= 63); otherwise the host
@@ -41,18 +44,23 @@
 #define HR_HY_MAXBK 1024u
 #define HR_HY_ROWS 8u                 /* rows loaded per batch by the count walk (ILP) */
 
-/* counts [nbk * nb + 1] (u64, bucket-major: run (bk, b) at bk * nb + b),
- * stat [2 * nbk] (accesses, scattered accesses), clk [2] (max __syncthreads /
- * __syncwarp rows of a warp) */
-template <typename SRC>
+/* The count walk, one CTA per simulated block (SAMPLE: every stride-th block).
+ * SAMPLE: per bucket, accesses and scattered accesses (at most 4 lanes of a row
+ * in the bucket) into stat [2 * nbk] — the binning decision is a heuristic, so
+ * a sample suffices.  Otherwise: the block's accesses to each binned bucket (map)
+ * into counts [nbk * nb + 1] (u64, bucket-major: run (bk, b) at bk * nb + b;
+ * exact: the row replay appends exactly these), and clk [2] = the most
+ * __syncthreads / __syncwarp rows of a warp. */
+template <bool SAMPLE, typename SRC>
 __global__ void hr_hy_count_kernel(hr_dev d, SRC src, const uint64_t *__restrict__ woff, uint32_t warps, uint32_t lanes,
-                                   uint32_t nbk, uint32_t nb, unsigned long long *__restrict__ cnt,
-                                   unsigned long long *__restrict__ stat, unsigned int *__restrict__ clk)
+                                   uint32_t nbk, uint32_t nb, uint32_t stride, const uint32_t *__restrict__ map,
+                                   unsigned long long *__restrict__ cnt, unsigned long long *__restrict__ stat,
+                                   unsigned int *__restrict__ clk)
 {
     extern __shared__ uint32_t hy_sm[];                           /* [nbk] accesses, [nbk] scattered */
-    for (uint32_t i = threadIdx.x; i < 2u * nbk; i += blockDim.x) hy_sm[i] = 0u;
+    for (uint32_t i = threadIdx.x; i < (SAMPLE ? 2u : 1u) * nbk; i += blockDim.x) hy_sm[i] = 0u;
     __syncthreads();
-    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, cta = blockIdx.x;
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, cta = SAMPLE ? blockIdx.x * stride : blockIdx.x;
     const uint32_t block = d.block_base + cta;
     const bool rep = !(hr__thread_off(d, block, w) & 1u);
     const bool active = lane < lanes;
@@ -70,8 +78,10 @@ __global__ void hr_hy_count_kernel(hr_dev d, SRC src, const uint64_t *__restrict
             /* a row holding any control record is a barrier row: the row replay checks
              * none of its accesses (hr__barrier_row) */
             if (__any_sync(0xffffffffu, op == 3u && wd != 0u)) {
-                nbar += __any_sync(0xffffffffu, op == 3u && wd == 1u) ? 1u : 0u;
-                nws += __any_sync(0xffffffffu, op == 3u && wd == 2u) ? 1u : 0u;
+                if (!SAMPLE) {
+                    nbar += __any_sync(0xffffffffu, op == 3u && wd == 1u) ? 1u : 0u;
+                    nws += __any_sync(0xffffffffu, op == 3u && wd == 2u) ? 1u : 0u;
+                }
                 continue;
             }
             bool v = rep && op != 3u && !((x >> 61) & 1u);
@@ -84,27 +94,35 @@ __global__ void hr_hy_count_kernel(hr_dev d, SRC src, const uint64_t *__restrict
                     const uint64_t local = ((gran >> d.shard_log2) << d.gran_log2) | (g & ((1ull << d.gran_log2) - 1u));
                     v = d.owned_only || hr_shard_owner(gran, d.shard_log2) == d.shard_rank;
                     bk = (uint32_t)(local >> HR_HY_BITS);
+                    if (!SAMPLE) v = v && ((__ldg(map + (bk >> 5)) >> (bk & 31u)) & 1u);
                 }
             }
-            const unsigned grp = __match_any_sync(0xffffffffu, v ? bk : 0xffffffffu);
-            if (v && (__ffs(grp) - 1) == (int)lane) {
-                const uint32_t n = __popc(grp);
-                atomicAdd(&hy_sm[bk], n);
-                if (n <= 4u) atomicAdd(&hy_sm[nbk + bk], n);
+            if (SAMPLE) {
+                const unsigned grp = __match_any_sync(0xffffffffu, v ? bk : 0xffffffffu);
+                if (v && (__ffs(grp) - 1) == (int)lane) {
+                    const uint32_t n = __popc(grp);
+                    atomicAdd(&hy_sm[bk], n);
+                    if (n <= 4u) atomicAdd(&hy_sm[nbk + bk], n);
+                }
+            } else if (v) {
+                atomicAdd(&hy_sm[bk], 1u);
             }
         }
     }
-    if (lane == 0) {
+    if (!SAMPLE && lane == 0) {
         atomicMax(&clk[0], nbar);
         atomicMax(&clk[1], nws);
     }
     __syncthreads();
     for (uint32_t bk = threadIdx.x; bk < nbk; bk += blockDim.x) {
         const uint32_t n = hy_sm[bk];
-        cnt[(uint64_t)bk * nb + cta] = n;
-        if (n) {
-            atomicAdd(&stat[2u * bk], (unsigned long long)n);
-            atomicAdd(&stat[2u * bk + 1u], (unsigned long long)hy_sm[nbk + bk]);
+        if (SAMPLE) {
+            if (n) {
+                atomicAdd(&stat[2u * bk], (unsigned long long)n);
+                atomicAdd(&stat[2u * bk + 1u], (unsigned long long)hy_sm[nbk + bk]);
+            }
+        } else {
+            cnt[(uint64_t)bk * nb + cta] = n;
         }
     }
 }
@@ -117,28 +135,6 @@ __global__ void hr_hy_decide_kernel(const unsigned long long *__restrict__ stat,
     const bool binned = bk < nbk && stat[2u * bk] >= min_acc && 2ull * stat[2u * bk + 1u] >= stat[2u * bk];
     const unsigned m = __ballot_sync(0xffffffffu, binned);
     if ((threadIdx.x & 31u) == 0u && bk < nbk) map[bk >> 5] = m;
-}
-
-/* runs of buckets left to the row replay hold no entries */
-__global__ void hr_hy_mask_kernel(unsigned long long *__restrict__ cnt, uint64_t n, uint32_t nb,
-                                  const uint32_t *__restrict__ map)
-{
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t bk = (uint32_t)(i / nb);
-        if (!((map[bk >> 5] >> (bk & 31u)) & 1u)) cnt[i] = 0ull;
-    }
-}
-
-/* first index i in [0, n] with off[i] >= v (off non-decreasing) */
-__device__ __forceinline__ uint64_t hr__hy_lower(const unsigned long long *__restrict__ off, uint64_t n, uint64_t v)
-{
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (off[mid] < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
 }
 
 /* One pool of up to 32 entries: a3 grouping by word, the leader folds its
@@ -251,25 +247,54 @@ __device__ __forceinline__ void hr__hy_check(const hr_dev &d, const hr_thr &t, b
     }
 }
 
-/* Persistent replay of the runs, bucket-major.  A warp takes chunk k of the
- * entry range and checks every run that STARTS in it, to the run's end (so a
- * run is never split between warps); 32 entries per pool.  The bucket of an
- * entry is found from the buckets' first entries (SMEM). */
+/* Stream one bucket's shadow (2^HR_HY_BITS words = 32 MB) into L2: the warp's
+ * lanes issue 64 KB bulk prefetches (cp.async.bulk.prefetch.L2), clipped to the
+ * shadow's end. */
+__device__ __forceinline__ void hr__hy_prefetch(const unsigned long long *p, const unsigned long long *end, uint32_t lane)
+{
+    const char *b = reinterpret_cast<const char *>(p), *e = reinterpret_cast<const char *>(end);
+    for (uint32_t i = lane; i < ((8u << HR_HY_BITS) >> 16); i += 32u) {
+        const char *a = b + ((size_t)i << 16);
+        if (a >= e) break;
+        const uint32_t n = (uint32_t)min((size_t)(e - a), (size_t)65536) & ~15u;
+        if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    }
+}
+
+/* Persistent replay of the runs, bucket-major over the binned buckets only.  A
+ * warp takes HR_HY_GRAB consecutive runs (runs are never split, so each is
+ * checked by one warp in order) and checks their concatenated entries 32 at a
+ * time.  The warp that takes a bucket's first runs streams the next
+ * binned bucket's shadow into L2. */
 #define HR_HY_WARPS 16u
-#define HR_HY_CHUNK 1024u
-__global__ void __launch_bounds__(HR_HY_WARPS * 32, 2) hr_hy_replay_kernel(
+#define HR_HY_GRAB 32u
+__global__ void __launch_bounds__(HR_HY_WARPS * 32, 3) hr_hy_replay_kernel(
     hr_dev d, const unsigned long long *__restrict__ ent, const unsigned long long *__restrict__ off, uint32_t nb,
     uint32_t nbk, unsigned long long *__restrict__ next)
 {
     extern __shared__ __align__(16) unsigned char hr_smem[];
     for (uint32_t i = threadIdx.x; i < HR_FSM_SMEM_BYTES / 16; i += blockDim.x)
         reinterpret_cast<uint4 *>(hr_smem)[i] = reinterpret_cast<const uint4 *>(d.fsm)[i];
-    /* bucket starts: bst[b] = first entry of bucket b, bst[nbk] = total */
-    unsigned long long *bst = reinterpret_cast<unsigned long long *>(hr_smem + ((HR_FSM_SMEM_BYTES + 15u) & ~15u));
-    const uint64_t nruns = (uint64_t)nbk * nb;
-    for (uint32_t b = threadIdx.x; b <= nbk; b += blockDim.x) bst[b] = off[(uint64_t)b * nb];
+    /* the binned buckets in order (from the map), and how many */
+    uint16_t *bins = reinterpret_cast<uint16_t *>(hr_smem + ((HR_FSM_SMEM_BYTES + 15u) & ~15u));
+    __shared__ uint32_t nbin_s;
+    if (threadIdx.x < 32u) {
+        uint32_t n = 0;
+        for (uint32_t w0 = 0; w0 < nbk; w0 += 32u) {
+            const uint32_t bk = w0 + threadIdx.x;
+            const bool on = bk < nbk && ((d.hy_map[bk >> 5] >> (bk & 31u)) & 1u);
+            const unsigned m = __ballot_sync(0xffffffffu, on);
+            if (on) bins[n + __popc(m & ((1u << threadIdx.x) - 1u))] = (uint16_t)bk;
+            n += __popc(m);
+        }
+        if (threadIdx.x == 0) nbin_s = n;
+    }
     __syncthreads();
-    const uint64_t total = bst[nbk];
+    const uint32_t nbin = nbin_s;
+    /* virtual runs (binned bucket i, block b) at i * nbp + b, each bucket padded to whole
+     * grabs so that a grab never crosses a bucket */
+    const uint32_t nbp = (nb + HR_HY_GRAB - 1u) / HR_HY_GRAB * HR_HY_GRAB;
+    const uint64_t nv = (uint64_t)nbin * nbp;
     const uint32_t lane = threadIdx.x & 31u;
     hr_thr t;
     t.meta = 0;
@@ -277,49 +302,44 @@ __global__ void __launch_bounds__(HR_HY_WARPS * 32, 2) hr_hy_replay_kernel(
     t.swords = 0;
     t.fsm = (uint32_t)__cvta_generic_to_shared(hr_smem);
     t.off = 0;
-    const uint32_t pool_sa = t.fsm + ((HR_FSM_SMEM_BYTES + 15u) & ~15u) + (nbk + 1u) * 8u + (threadIdx.x >> 5) * 384u;
+    const uint32_t pool_sa = t.fsm + ((HR_FSM_SMEM_BYTES + 15u) & ~15u) + 2048u + (threadIdx.x >> 5) * 384u;
     const uint32_t tag_hi = d.epoch_tag << 28;
+    /* grabs from one counter, in bucket order (measured: dealing them round-robin
+     * over the warps was slower at 2^32 accesses, 128 vs 94.6 ms per step) */
     while (true) {
-        unsigned long long k = 0;
-        if (lane == 0) k = atomicAdd(next, 1ull);
-        k = __shfl_sync(0xffffffffu, k, 0);
-        const uint64_t c0 = k * HR_HY_CHUNK;
-        if (c0 >= total) break;
-        /* the runs starting in [c0, c0 + CHUNK): entries [e0, e1) */
-        uint64_t e0 = 0, e1 = 0;
-        if (lane == 0) {
-            e0 = off[hr__hy_lower(off, nruns, c0)];
-            e1 = c0 + HR_HY_CHUNK >= total ? total : off[hr__hy_lower(off, nruns, c0 + HR_HY_CHUNK)];
-        }
-        e0 = __shfl_sync(0xffffffffu, e0, 0);
-        e1 = __shfl_sync(0xffffffffu, e1, 0);
-        if (e0 >= e1) continue;
-        /* bucket of e0 (largest b with bst[b] <= e0) */
-        uint32_t lo_b = 0, hi_b = nbk;
-        while (lo_b + 1 < hi_b) {
-            const uint32_t mid = (lo_b + hi_b) >> 1;
-            if (bst[mid] <= e0) lo_b = mid;
-            else hi_b = mid;
-        }
+        unsigned long long v0 = 0;
+        if (lane == 0) v0 = atomicAdd(next, (unsigned long long)HR_HY_GRAB);
+        v0 = __shfl_sync(0xffffffffu, v0, 0);
+        if (v0 >= nv) break;
+        const uint32_t bi = (uint32_t)(v0 / nbp), b0 = (uint32_t)(v0 % nbp);
+        if (b0 >= nb) continue;                                    /* padding */
+        const uint32_t bk = bins[bi];
+        /* runs [b0, b0 + n) of bucket bk */
+        const uint32_t n = min(HR_HY_GRAB, nb - b0);
+        const uint64_t sr = (uint64_t)bk * nb + b0;
+        const uint64_t e0 = off[sr], e1 = off[sr + n];
+        if (b0 == 0 && bi + 1u < nbin)
+            hr__hy_prefetch(d.gshadow + ((uint64_t)bins[bi + 1u] << HR_HY_BITS), d.gshadow + d.glocal_words, lane);
+        const uint64_t lbase = (uint64_t)bk << HR_HY_BITS;
+        uint64_t xn = e0 + lane < e1 ? __ldcs(ent + e0 + lane) : 0ull;   /* next pool's entry, loaded ahead */
         for (uint64_t p = e0; p < e1; p += 32u) {
             const uint64_t e = p + lane;
             const bool valid = e < e1;
-            const uint64_t x = valid ? __ldcs(ent + e) : 0ull;
-            uint32_t bk = lo_b;
-            while (bk + 1u < nbk && bst[bk + 1u] <= e) bk++;
-            const uint64_t local = ((uint64_t)bk << HR_HY_BITS) | (x >> 42);
+            const uint64_t x = xn;
+            xn = e + 32u < e1 ? __ldcs(ent + e + 32u) : 0ull;
+            const uint64_t local = lbase | (x >> 42);
             const uint32_t kind = (uint32_t)(x >> 40) & 3u;
             const uint32_t tid = (uint32_t)(x >> 13) & 0x7ffffffu;
             const uint32_t lo = tag_hi | ((((uint32_t)x >> 6) & 127u) << d.wc_bits) | ((uint32_t)x & 63u);
             hr__hy_check(d, t, valid, local, tid, lo, kind, pool_sa);
-            lo_b = __shfl_sync(0xffffffffu, bk, 31);
         }
     }
 }
 
 __host__ __forceinline__ size_t hr_hy_replay_smem(uint32_t nbk)
 {
-    return ((HR_FSM_SMEM_BYTES + 15u) & ~15u) + (size_t)(nbk + 1u) * 8u + HR_HY_WARPS * 384u;
+    (void)nbk;
+    return ((HR_FSM_SMEM_BYTES + 15u) & ~15u) + 2048u + HR_HY_WARPS * 384u;
 }
 
 #endif /* HR_HYBRID_CUH_ */
