@@ -873,7 +873,7 @@ static hr_status hybrid_replay(hr_ctx *c, const hr_dev &d, cudaStream_t s)
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     c->launches++;
-    hr_hy_replay_kernel<<<(unsigned)(dev_sms * 3), HR_HY_WARPS * 32, rsm, s>>>(d, d.hy_ent, d.hy_off, d.hy_nb, d.hy_nbk,
+    hr_hy_replay_kernel<<<(unsigned)(dev_sms * HR_HY_MINB), HR_HY_WARPS * 32, rsm, s>>>(d, d.hy_ent, d.hy_off, d.hy_nb, d.hy_nbk,
                                                                              next);
     CU(cudaGetLastError());
     return HR_OK;

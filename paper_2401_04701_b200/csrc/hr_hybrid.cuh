@@ -268,7 +268,10 @@ __device__ __forceinline__ void hr__hy_prefetch(const unsigned long long *p, con
  * binned bucket's shadow into L2. */
 #define HR_HY_WARPS 16u
 #define HR_HY_GRAB 32u
-__global__ void __launch_bounds__(HR_HY_WARPS * 32, 3) hr_hy_replay_kernel(
+#ifndef HR_HY_MINB
+#define HR_HY_MINB 3
+#endif
+__global__ void __launch_bounds__(HR_HY_WARPS * 32, HR_HY_MINB) hr_hy_replay_kernel(
     hr_dev d, const unsigned long long *__restrict__ ent, const unsigned long long *__restrict__ off, uint32_t nb,
     uint32_t nbk, unsigned long long *__restrict__ next)
 {
