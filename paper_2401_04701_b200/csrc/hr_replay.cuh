@@ -440,8 +440,8 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
             /* C32 rows read undecoded: barrier test, then the shared-row fast path
              * (hr__check_shared_row) on the raw (word, op | space << 2) pair.  FULL (wide
              * kernel): every lane is in the grid (constant row strides); otherwise lanes
-             * beyond the grid
-             * read the NOP record of the table copy (HR_FSM_NOP_OFF) on every row. */
+             * beyond the grid read the NOP record of the table copy (HR_FSM_NOP_OFF) on
+             * every row. */
             auto c32_rows = [&](auto full) {
                 constexpr bool FULL = decltype(full)::value;
                 /* the shared-row word limit: 0 while this lane is off (t.off changes only at barriers) */
