@@ -208,7 +208,10 @@ enum {
  *                                k-bit delta at bits [l*k, l*k+k) (little-endian)
  * A nibble is op | x << 2: for op 0..2 (access) x = space and the word is
  * base + lane (affine), base + delta_l, or base (k == 0); for op 3 (control)
- * x = the control word (0..2) and no word bits are used.  k == 63 means the
+ * x = the control word (0..2) and no word bits are used.  Exception: an affine
+ * row with k = 1 or 2 (affine rows carry no deltas) holds every lane as a read
+ * or write of space k - 1, and its nibbles are one u32 bit mask instead (bit l
+ * set = lane l writes): body = mask, base (12 bytes).  k == 63 means the
  * row has no access lanes (no base).  Rows a nibble cannot express (a control
  * record with word > 2 or the space bit set) use the raw form.  The decoder
  * reads up to 8 bytes past a segment's last body; allocate `packed` with 16

@@ -5,8 +5,9 @@
  * records so that hr_replay_trace_host moves fewer PCIe bytes.
  * Frame-of-reference per warp-row: a nibble per lane (op | space or control
  * word), one base word, and either word = base + lane (a coalesced row),
- * word = base (a broadcast), or k-bit deltas.  C5's own-row rows shrink from
- * 160 B (C32) to 25 B, its random gathers to 137 B.
+ * word = base (a broadcast), or k-bit deltas; a coalesced row of reads and
+ * writes of one space keeps one bit per lane instead of a nibble.  C5's own-row
+ * rows shrink from 160 B (C32) to 13 B, its random gathers to 137 B.
  *
  * Both directions run one CUDA warp per segment (one trace warp's rows).
  * The decoder writes U64 rows that the unchanged replay kernels then read.
@@ -23,12 +24,21 @@
 #define HR_PACK_SLACK 16u
 #define HR_PACK_WORD_MASK ((1ull << 61) - 1)
 
+/* An affine row whose lanes are all reads or writes of one space: the nibbles
+ * are one u32 bit mask (bit l = lane l writes), k = 1 + space (affine rows have
+ * no deltas, so these k values are otherwise unused). */
+__host__ __device__ __forceinline__ bool hr_pack_is_rwmask(uint32_t h)
+{
+    const uint32_t k = h & 63u;
+    return (h & HR_PACK_AFFINE) && (k == 1u || k == 2u);
+}
+
 /* Body bytes of a row with header byte h. */
 __host__ __device__ __forceinline__ uint32_t hr_pack_body_bytes(uint32_t h)
 {
     const uint32_t k = h & 63u;
     if (k == HR_PACK_RAW) return 256u;
-    uint32_t b = (h & HR_PACK_UNIFORM) ? 4u : 16u;
+    uint32_t b = ((h & HR_PACK_UNIFORM) || hr_pack_is_rwmask(h)) ? 4u : 16u;
     if (k != HR_PACK_NOWORD) b += 8u + ((h & HR_PACK_AFFINE) ? 0u : 4u * k);
     return b;
 }
@@ -77,6 +87,12 @@ __device__ __forceinline__ hr_pack_row hr__pack_decide(uint64_t x, uint32_t lane
     const uint64_t base_a = hr__shfl64(w, l0) - (uint64_t)l0;
     if (__all_sync(0xffffffffu, !acc || w == base_a + lane)) {
         r.base = base_a;
+        /* every lane a read or write of one space, not all the same op: a bit mask */
+        const uint32_t sp0 = (uint32_t)__shfl_sync(0xffffffffu, (int)sp, 0);
+        if (!uniform && amask == 0xffffffffu && __all_sync(0xffffffffu, op <= 1u && sp == sp0)) {
+            r.h = HR_PACK_AFFINE | (1u + sp0);
+            return r;
+        }
         r.h = h | HR_PACK_AFFINE;
         return r;
     }
@@ -152,7 +168,11 @@ __global__ void __launch_bounds__(256) hr_pack_write_kernel(const uint64_t *__re
             continue;
         }
         uint32_t nw;
-        if (h & HR_PACK_UNIFORM) {
+        if (hr_pack_is_rwmask(h)) {
+            const unsigned m = __ballot_sync(0xffffffffu, ((x >> 62) & 1u) != 0u);
+            if (lane == 0) body[0] = m;
+            nw = 1;
+        } else if (h & HR_PACK_UNIFORM) {
             if (lane == 0) body[0] = pr.nib;
             nw = 1;
         } else {
@@ -192,6 +212,11 @@ __device__ __forceinline__ uint64_t hr__unpack_lane(const uint32_t *__restrict__
 {
     const uint32_t k = h & 63u;
     if (k == HR_PACK_RAW) return (uint64_t)body[2 * lane] | ((uint64_t)body[2 * lane + 1] << 32);
+    if (hr_pack_is_rwmask(h)) {
+        const uint64_t base = (uint64_t)body[1] | ((uint64_t)body[2] << 32);
+        return ((uint64_t)((body[0] >> lane) & 1u) << 62) | ((uint64_t)(k - 1u) << 61) |
+               ((base + lane) & HR_PACK_WORD_MASK);
+    }
     uint32_t nib;
     uint32_t nw;
     if (h & HR_PACK_UNIFORM) {
