@@ -29,5 +29,20 @@ ck.report_raw(); ck.close()
 d3 = torch.zeros(2 * 64 * 64, dtype=torch.int32, device="cuda")
 ck = hr.Checker(2 * 64 * 64, 648)
 on.c3(ck.ctx, d3, True, n=64, sweeps=6, removed=None if rf else 2); ck.report_raw(); ck.close()
+# round 2: the report graph (small-set kernel and the conditional sort path), the
+# hybrid binned replay, the PACKED read/write mask, an owned address shard
+for tr, n_ring in ((tp.listing2(2, 2, 32), 1 << 12), (tp.listing2(64, 8, 32), 1 << 14)):
+    gmax, smem = hr.trace_extent(tr)
+    ck = hr.Checker(gmax, smem, ring_capacity=n_ring)
+    ck.reset(); ck.replay(hr.DeviceTrace.from_trace(tr)); ck.report_async()
+    raw, fl = ck.collect_raw()
+    want = oracle.check(tr)
+    assert [(int(r["kernel"]), int(r["space"]), int(r["block"]), int(r["word"]), int(r["scope"])) for r in raw] == \
+        [tuple(r) for r in want.races]
+    ck.close()
+same(tp.listing2(4, 4, 32), options=hr.HR_OPT_HYBRID | hr.HR_OPT_BIN_ALL)
+same(tp.listing4(2, 2, 32, 60), options=hr.HR_OPT_HYBRID | hr.HR_OPT_BIN_ALL, compact=True)
+same(tp.c1_tree_reduction(removed=16), packed=True)
+same(c5.cpu_trace(2), packed=True)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
