@@ -63,7 +63,8 @@ enum {
     HR_F_BARRIER_DIVERGENCE = 8u,  /* barrier record not uniform across a warp's lanes */
     HR_F_UNMONITORED = 16u,        /* global access outside the registered shadow region */
     HR_F_INCOMPLETE = 32u          /* overflow recovery failed: the spill store was full, or (as
-                                      HR_E_INCOMPLETE) a dropped shared record was never spilled */
+                                      HR_E_INCOMPLETE) a dropped shared record was never spilled;
+                                      or (HR_OPT_HYBRID) a run's appends disagreed with its count */
 };
 
 /* Shadow word layout ("5 bits ... 8 bytes of memory per address"):

@@ -508,6 +508,17 @@ __global__ void HR_REPLAY_BOUNDS(POOL, WIDE) hr_replay_kernel(hr_dev d, SRC src,
         }
     }
     if (POOL && cnt) { __syncwarp(); hr__check_pool<ABL>(d, t, ps, cnt); __syncwarp(); }
+    if (!POOL && d.hy_map != nullptr) {
+        /* hybrid: every run must end exactly where the count put the next one; a
+         * mismatch (a count that disagrees with the appends) would corrupt a
+         * neighbouring run, so it marks the result incomplete */
+        __syncthreads();
+        const unsigned long long *pos = reinterpret_cast<const unsigned long long *>(hr_smem + d.hy_sa_off);
+        bool bad = false;
+        for (uint32_t i = threadIdx.x; i < d.hy_nbk; i += blockDim.x)
+            bad = bad || pos[i] != d.hy_off[(uint64_t)i * d.hy_nb + cta + 1u];
+        if (bad) hr__set_flag(d, HR_F_INCOMPLETE);
+    }
     hr_thread_end(d, t);                                             /* a9: spill a dropped shared race */
 }
 
