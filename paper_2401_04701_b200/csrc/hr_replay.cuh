@@ -247,11 +247,16 @@ __device__ __forceinline__ bool hr__pool_owned(const hr_dev &d, const hr_thr &t,
 #ifndef HR_STAGE_NB_ROW
 #define HR_STAGE_NB_ROW 2u
 #endif
+#ifndef HR_WIDE_C32_CH
+/* C3 (wide kernel, C32): 16-row chunks at 64 registers 0.226 ms; 8-row chunks at
+ * 64 / 48 / 40 registers (more CTAs per SM) 0.244 / 0.252 / 0.254 ms */
+#define HR_WIDE_C32_CH 16u
+#endif
 template <bool WIDE, bool POOL = false, uint32_t ROW_BYTES = 256u> struct hr_stage_cfg {
     static constexpr uint32_t NB = WIDE ? HR_STAGE_NB_WIDE : HR_STAGE_NB_ROW;
     /* the 64-register row kernel on C32 rows (160 B): 16-row chunks, which halve the
      * per-chunk refill work of the issue-bound shared-shadow traces (C3) */
-    static constexpr uint32_t CH = WIDE ? ((!POOL && ROW_BYTES == 160u) ? 16u : 8u) : 4u;
+    static constexpr uint32_t CH = WIDE ? ((!POOL && ROW_BYTES == 160u) ? HR_WIDE_C32_CH : 8u) : 4u;
 };
 
 /* Dynamic shared memory of a replay launch: FSM table, warp pools, the shared
