@@ -7,7 +7,8 @@
  * word), one base word, and either word = base + lane (a coalesced row),
  * word = base (a broadcast), or k-bit deltas; a coalesced row of reads and
  * writes of one space keeps one bit per lane instead of a nibble.  C5's own-row
- * rows shrink from 160 B (C32) to 13 B, its random gathers to 137 B.
+ * rows shrink from 160 B (C32) to 13 B, its random gathers to 133 B (a base
+ * below 2^32 takes 4 bytes).
  *
  * Both directions run one CUDA warp per segment (one trace warp's rows).
  * The decoder writes U64 rows that the unchanged replay kernels then read.
@@ -33,12 +34,22 @@ __host__ __device__ __forceinline__ bool hr_pack_is_rwmask(uint32_t h)
     return (h & HR_PACK_AFFINE) && (k == 1u || k == 2u);
 }
 
+/* A delta row (k >= 3 bits) whose base fits 32 bits stores it in one u32; the
+ * affine bit marks it (affine rows carry no deltas, so affine with k >= 3 is
+ * otherwise unused; k = 62 / 63 keep their meaning). */
+__host__ __device__ __forceinline__ bool hr_pack_is_short(uint32_t h)
+{
+    const uint32_t k = h & 63u;
+    return (h & HR_PACK_AFFINE) && k >= 3u && k < HR_PACK_RAW;
+}
+
 /* Body bytes of a row with header byte h. */
 __host__ __device__ __forceinline__ uint32_t hr_pack_body_bytes(uint32_t h)
 {
     const uint32_t k = h & 63u;
     if (k == HR_PACK_RAW) return 256u;
     uint32_t b = ((h & HR_PACK_UNIFORM) || hr_pack_is_rwmask(h)) ? 4u : 16u;
+    if (hr_pack_is_short(h)) return b + 4u + 4u * k;
     if (k != HR_PACK_NOWORD) b += 8u + ((h & HR_PACK_AFFINE) ? 0u : 4u * k);
     return b;
 }
@@ -110,7 +121,9 @@ __device__ __forceinline__ hr_pack_row hr__pack_decide(uint64_t x, uint32_t lane
     }
     r.base = mn;
     r.delta = acc ? w - mn : 0ull;
-    r.h = h | (mx ? (uint32_t)(64 - __clzll((long long)mx)) : 0u);
+    const uint32_t k = mx ? (uint32_t)(64 - __clzll((long long)mx)) : 0u;
+    r.h = h | k;
+    if (k >= 3u && mn < (1ull << 32)) r.h |= HR_PACK_AFFINE;      /* 4-byte base */
     return r;
 }
 
@@ -185,12 +198,13 @@ __global__ void __launch_bounds__(256) hr_pack_write_kernel(const uint64_t *__re
         }
         body += nw;
         if (k == HR_PACK_NOWORD) continue;
+        const bool shb = hr_pack_is_short(h);
         if (lane == 0) {
             body[0] = (uint32_t)pr.base;
-            body[1] = (uint32_t)(pr.base >> 32);
+            if (!shb) body[1] = (uint32_t)(pr.base >> 32);
         }
-        body += 2;
-        if ((h & HR_PACK_AFFINE) || k == 0) continue;
+        body += shb ? 1 : 2;
+        if (((h & HR_PACK_AFFINE) && !shb) || k == 0) continue;
         sb[lane] = 0;
         sb[lane + 32] = 0;
         __syncwarp();
@@ -228,14 +242,15 @@ __device__ __forceinline__ uint64_t hr__unpack_lane(const uint32_t *__restrict__
     }
     const uint64_t op = nib & 3u, x2 = nib >> 2;
     if (op == 3u) return (3ull << 62) | x2;
-    const uint64_t base = (uint64_t)body[nw] | ((uint64_t)body[nw + 1] << 32);
+    const bool shb = hr_pack_is_short(h);
+    const uint64_t base = shb ? (uint64_t)body[nw] : ((uint64_t)body[nw] | ((uint64_t)body[nw + 1] << 32));
     uint64_t d;
-    if (h & HR_PACK_AFFINE) {
+    if ((h & HR_PACK_AFFINE) && !shb) {
         d = lane;
     } else if (k == 0) {
         d = 0;
     } else {
-        const uint32_t *dw = body + nw + 2;
+        const uint32_t *dw = body + nw + (shb ? 1u : 2u);
         const uint32_t p = lane * k, q = p >> 5, s = p & 31u;
         uint64_t lo = dw[q];
         if (s + k > 32) lo |= (uint64_t)dw[q + 1] << 32;

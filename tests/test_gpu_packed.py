@@ -70,6 +70,8 @@ def _rows(rng: np.random.Generator, n: int) -> np.ndarray:
         else:                                            # deltas of width k, some NOP / control lanes
             k = int(rng.integers(0, 62))
             base = int(rng.integers(0, M - (1 << k) + 1)) if k < 61 else 0
+            if kind in (5, 6) and k < 32:                # bases below 2^32 (the 4-byte base form)
+                base = int(rng.integers(0, (1 << 32) - (1 << k) + 1))
             d = rng.integers(0, 1 << k, 32, dtype=np.uint64) if k else np.zeros(32, np.uint64)
             ops = rng.integers(0, 3, 32).astype(np.uint64)
             sp = rng.integers(0, 2, 32).astype(np.uint64)
@@ -122,7 +124,9 @@ def test_row_sizes():
          4 + 4 + 8),                                                             # shared-space R/W affine: mask
         ((lanes % np.uint64(3)) << np.uint64(62) | (np.uint64(4096) + lanes), 4 + 16 + 8),   # R/W/A affine: nibbles
         (np.full(32, 77, np.uint64), 4 + 4 + 8),                                  # broadcast read, k = 0
-        (np.uint64(5) * lanes, 4 + 4 + 8 + 4 * 8),                                # reads, max delta 155 -> k = 8
+        (np.uint64(5) * lanes, 4 + 4 + 4 + 4 * 8),                                # reads, max delta 155 -> k = 8, u32 base
+        (np.uint64(1 << 40) + np.uint64(5) * lanes, 4 + 4 + 8 + 4 * 8),           # the same above 2^32: u64 base
+        (np.uint64(7) + (lanes % np.uint64(2)), 4 + 4 + 8 + 4 * 1),               # k = 1 keeps the u64 base
         (np.full(32, (3 << 62) | 5, np.uint64), 4 + 256),                         # unknown control word -> raw
     ]
     for row, size in cases:
