@@ -212,7 +212,9 @@ enum {
  * x = the control word (0..2) and no word bits are used.  Exception: an affine
  * row with k = 1 or 2 (affine rows carry no deltas) holds every lane as a read
  * or write of space k - 1, and its nibbles are one u32 bit mask instead (bit l
- * set = lane l writes): body = mask, base (12 bytes); and an affine row with
+ * set = lane l writes): body = mask, base (12 bytes; 8 with the uniform bit set,
+ * which a mask row otherwise never has: a base below 2^32 in one u32); and an
+ * affine row with
  * 3 <= k <= 61 is a k-bit delta row whose base fits 32 bits: the base is one
  * u32 (nibbles, base u32, deltas).  k == 63 means the
  * row has no access lanes (no base).  Rows a nibble cannot express (a control

@@ -7,7 +7,7 @@
  * word), one base word, and either word = base + lane (a coalesced row),
  * word = base (a broadcast), or k-bit deltas; a coalesced row of reads and
  * writes of one space keeps one bit per lane instead of a nibble.  C5's own-row
- * rows shrink from 160 B (C32) to 13 B, its random gathers to 133 B (a base
+ * rows shrink from 160 B (C32) to 9 B, its random gathers to 133 B (a base
  * below 2^32 takes 4 bytes).
  *
  * Both directions run one CUDA warp per segment (one trace warp's rows).
@@ -27,7 +27,8 @@
 
 /* An affine row whose lanes are all reads or writes of one space: the nibbles
  * are one u32 bit mask (bit l = lane l writes), k = 1 + space (affine rows have
- * no deltas, so these k values are otherwise unused). */
+ * no deltas, so these k values are otherwise unused); the uniform bit (a mask
+ * row is never uniform) marks a base below 2^32 stored in one u32. */
 __host__ __device__ __forceinline__ bool hr_pack_is_rwmask(uint32_t h)
 {
     const uint32_t k = h & 63u;
@@ -48,7 +49,8 @@ __host__ __device__ __forceinline__ uint32_t hr_pack_body_bytes(uint32_t h)
 {
     const uint32_t k = h & 63u;
     if (k == HR_PACK_RAW) return 256u;
-    uint32_t b = ((h & HR_PACK_UNIFORM) || hr_pack_is_rwmask(h)) ? 4u : 16u;
+    if (hr_pack_is_rwmask(h)) return (h & HR_PACK_UNIFORM) ? 8u : 12u;
+    uint32_t b = (h & HR_PACK_UNIFORM) ? 4u : 16u;
     if (hr_pack_is_short(h)) return b + 4u + 4u * k;
     if (k != HR_PACK_NOWORD) b += 8u + ((h & HR_PACK_AFFINE) ? 0u : 4u * k);
     return b;
@@ -101,7 +103,7 @@ __device__ __forceinline__ hr_pack_row hr__pack_decide(uint64_t x, uint32_t lane
         /* every lane a read or write of one space, not all the same op: a bit mask */
         const uint32_t sp0 = (uint32_t)__shfl_sync(0xffffffffu, (int)sp, 0);
         if (!uniform && amask == 0xffffffffu && __all_sync(0xffffffffu, op <= 1u && sp == sp0)) {
-            r.h = HR_PACK_AFFINE | (1u + sp0);
+            r.h = HR_PACK_AFFINE | (1u + sp0) | (base_a < (1ull << 32) ? HR_PACK_UNIFORM : 0u);
             return r;
         }
         r.h = h | HR_PACK_AFFINE;
@@ -183,8 +185,13 @@ __global__ void __launch_bounds__(256) hr_pack_write_kernel(const uint64_t *__re
         uint32_t nw;
         if (hr_pack_is_rwmask(h)) {
             const unsigned m = __ballot_sync(0xffffffffu, ((x >> 62) & 1u) != 0u);
-            if (lane == 0) body[0] = m;
-            nw = 1;
+            if (lane == 0) {
+                body[0] = m;
+                body[1] = (uint32_t)pr.base;
+                if (!(h & HR_PACK_UNIFORM)) body[2] = (uint32_t)(pr.base >> 32);
+            }
+            body += (h & HR_PACK_UNIFORM) ? 2 : 3;
+            continue;
         } else if (h & HR_PACK_UNIFORM) {
             if (lane == 0) body[0] = pr.nib;
             nw = 1;
@@ -227,7 +234,7 @@ __device__ __forceinline__ uint64_t hr__unpack_lane(const uint32_t *__restrict__
     const uint32_t k = h & 63u;
     if (k == HR_PACK_RAW) return (uint64_t)body[2 * lane] | ((uint64_t)body[2 * lane + 1] << 32);
     if (hr_pack_is_rwmask(h)) {
-        const uint64_t base = (uint64_t)body[1] | ((uint64_t)body[2] << 32);
+        const uint64_t base = (uint64_t)body[1] | ((h & HR_PACK_UNIFORM) ? 0ull : ((uint64_t)body[2] << 32));
         return ((uint64_t)((body[0] >> lane) & 1u) << 62) | ((uint64_t)(k - 1u) << 61) |
                ((base + lane) & HR_PACK_WORD_MASK);
     }

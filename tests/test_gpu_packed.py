@@ -56,7 +56,7 @@ def _rows(rng: np.random.Generator, n: int) -> np.ndarray:
         if kind == 0:                                    # arbitrary 64-bit garbage -> raw escape
             out[i] = rng.integers(0, 2**64, 32, dtype=np.uint64, endpoint=False)
         elif kind == 1:                                  # coalesced row, mixed R/W (affine: bit mask)
-            base = int(rng.integers(0, 1 << 40))
+            base = int(rng.integers(0, 1 << 40)) if rng.random() < 0.5 else int(rng.integers(0, (1 << 32) - 32))
             ops = rng.integers(0, 2, 32).astype(np.uint64)
             sp = np.uint64(int(rng.integers(0, 2)))
             out[i] = (ops << np.uint64(62)) | (sp << np.uint64(61)) | (np.uint64(base) + lanes)
@@ -119,9 +119,10 @@ def test_row_sizes():
     cases = [
         (np.full(32, tf.SYNCTHREADS, np.uint64), 4 + 4),                         # uniform nibble, no words
         (np.uint64(1 << 62) | (np.uint64(4096) + lanes), 4 + 4 + 8),              # uniform W, affine
-        ((lanes % np.uint64(2)) << np.uint64(62) | (np.uint64(4096) + lanes), 4 + 4 + 8),    # mixed R/W affine: mask
+        ((lanes % np.uint64(2)) << np.uint64(62) | (np.uint64(4096) + lanes), 4 + 4 + 4),    # mixed R/W affine: mask
+        ((lanes % np.uint64(2)) << np.uint64(62) | (np.uint64(1 << 40) + lanes), 4 + 4 + 8),  # the same, u64 base
         ((lanes % np.uint64(3) == 0).astype(np.uint64) << np.uint64(62) | np.uint64(1 << 61) | (np.uint64(64) + lanes),
-         4 + 4 + 8),                                                             # shared-space R/W affine: mask
+         4 + 4 + 4),                                                             # shared-space R/W affine: mask
         ((lanes % np.uint64(3)) << np.uint64(62) | (np.uint64(4096) + lanes), 4 + 16 + 8),   # R/W/A affine: nibbles
         (np.full(32, 77, np.uint64), 4 + 4 + 8),                                  # broadcast read, k = 0
         (np.uint64(5) * lanes, 4 + 4 + 4 + 4 * 8),                                # reads, max delta 155 -> k = 8, u32 base
